@@ -1,0 +1,216 @@
+/*
+ * qmcgpu.h — C-ABI of the B200-native QMC sampling path.
+ *
+ * Drop-in boundary for the reference library's hot path (qmckit `qmc::`,
+ * /root/reference/proj). The reference has no FFI; its callers use the
+ * `qmc::` C++ headers. This header is what those callers (or a ctypes /
+ * cgo-style binding) bind instead; include/qmcgpu.hpp
+ * re-exposes `qmc::`-style names on top of it.
+ *
+ * Conventions
+ *   - Plain pointers and sizes; no torch or CUDA types in signatures.
+ *     `qmc_stream` is a cudaStream_t passed as void* (NULL = default stream).
+ *   - Every call returns a qmc_status; qmc_last_error() gives the message
+ *     (thread-local). Status classes mirror the reference exceptions
+ *     (errors.hpp:13-15 ConfigError, std::invalid_argument, std::out_of_range,
+ *     std::overflow_error). Preconditions are checked on the host with the
+ *     reference's conditions before anything is launched.
+ *   - Batched fills write row-major [n][dims] (the `qmckit points --format
+ *     bin` layout, tools/qmckit.cpp:225-241), component (i, j) at
+ *     out[(i - first_index) * dims + j]. `out` may be DEVICE memory (the call
+ *     is asynchronous on `stream`) or HOST memory (pinned recommended; the
+ *     call pipelines device chunks through D2H copies and returns when the
+ *     host buffer is complete).
+ *   - QMC_OUT_F32 writes map_u32_to_unifloat(x) (bit-exact, unitfloat.hpp:
+ *     34-50); QMC_OUT_U32 writes the 32-bit fixed-point integer stage x
+ *     (the reference `*_fixed` functions).
+ *   - No CPU fallback: every per-sample computation runs on the GPU; without
+ *     a usable CUDA device calls fail with QMC_CUDA.
+ */
+#ifndef QMCGPU_H
+#define QMCGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QMCGPU_ABI_VERSION 1
+
+typedef enum qmc_status {
+    QMC_OK = 0,
+    QMC_CONFIG = 1,           /* qmc::ConfigError (errors.hpp:13-15) */
+    QMC_INVALID_ARGUMENT = 2, /* std::invalid_argument */
+    QMC_OUT_OF_RANGE = 3,     /* std::out_of_range */
+    QMC_OVERFLOW = 4,         /* std::overflow_error */
+    QMC_CUDA = 5,             /* CUDA runtime error / no device */
+    QMC_NCCL = 6,             /* collective failure (reserved for host drivers) */
+    QMC_INTERNAL = 9
+} qmc_status;
+
+typedef void* qmc_stream; /* cudaStream_t */
+
+typedef enum qmc_output { QMC_OUT_F32 = 0, QMC_OUT_U32 = 1 } qmc_output;
+
+/* ------------------------------------------------------------------ misc */
+const char* qmc_last_error(void);
+const char* qmc_status_string(qmc_status s);
+int qmc_abi_version(void);
+
+/* ------------------------------------------------ L0 (unitfloat.hpp:13-50) */
+/* Batched map_u32_to_unifloat (unitfloat.hpp:34-50); in/out device or host. */
+qmc_status qmc_map_u32_to_unifloat(const uint32_t* in, float* out, uint64_t n, qmc_stream stream);
+/* Exhaustive 2^32 self-check of the device map against a device restatement
+ * of the reference formula (SPEC acceptance 1); *mismatches = count. */
+qmc_status qmc_map_selfcheck(uint64_t* mismatches, qmc_stream stream);
+
+/* --------------------------------------------- host setup (no per-sample work) */
+/* primes.cpp:50-62 */
+qmc_status qmc_prime(uint32_t index, uint32_t* out);
+qmc_status qmc_prime_max_power(uint32_t index, uint32_t* out);
+/* radical.cpp:50-74; out has `base` entries */
+qmc_status qmc_faure_permutation(uint32_t base, uint32_t* out);
+/* radical.cpp:271-279; out has `dims` entries (factor = prime - 1) */
+qmc_status qmc_default_linear_factors(uint32_t dims, uint32_t* out);
+/* lattice.cpp:81-104 */
+qmc_status qmc_lfsr_generator_vector(uint32_t seed, uint32_t dims, uint32_t* out);
+/* lattice.cpp:71-77 (seeds of the scrambles; the render kinds hash on device) */
+uint32_t qmc_pixel_hash(uint32_t j, uint32_t px, uint32_t py);
+/* render.cpp:28-34 */
+uint32_t qmc_hilbert_order_for(uint32_t width, uint32_t height);
+/* imageplane.cpp:114-130 */
+qmc_status qmc_partition_by_extra_dimension(uint32_t part, uint32_t parts, uint32_t base,
+                                            uint64_t* remainder, uint64_t* modulus);
+/* imageplane.cpp:80-106: scales, exponents, stride; offset of (px, py) */
+typedef struct qmc_halton_enumeration {
+    uint32_t scale_x, scale_y, exponent_x, exponent_y;
+    uint64_t stride;
+} qmc_halton_enumeration;
+qmc_status qmc_halton_pixel_enumeration(uint32_t width, uint32_t height, uint32_t px, uint32_t py,
+                                        qmc_halton_enumeration* e, uint64_t* offset);
+
+/* ------------------------------- generator matrices (digitalnet.cpp:23-109) */
+typedef struct qmc_matrices qmc_matrices; /* immutable; device copy per GPU */
+/* build_matrices(builtin_direction_numbers(), dims) — digitalnet.cpp:73-109 */
+qmc_status qmc_matrices_builtin(uint32_t dims, qmc_matrices** out);
+/* parse_direction_numbers(text) + build_matrices — digitalnet.cpp:23-109 */
+qmc_status qmc_matrices_from_text(const char* text, uint32_t dims, qmc_matrices** out);
+/* caller-supplied MSB-aligned columns[dims][52] */
+qmc_status qmc_matrices_from_columns(const uint32_t* columns, uint32_t dims, qmc_matrices** out);
+uint32_t qmc_matrices_dims(const qmc_matrices* m);
+qmc_status qmc_matrices_columns(const qmc_matrices* m, uint32_t* out /* dims*52 */);
+void qmc_matrices_destroy(qmc_matrices* m);
+
+/* ------------------------------------------------------------- batched fills */
+typedef enum qmc_sobol_scramble {
+    QMC_SOBOL_NONE = 0, /* digitalnet.cpp:111-131 with scramble 0 */
+    QMC_SOBOL_XOR = 1,  /* per-dimension XOR word (the reference's scramble) */
+    QMC_SOBOL_OWEN = 2  /* hash-based nested-uniform (Owen) scramble, per-dim seed */
+} qmc_sobol_scramble;
+
+/* sobol_component(_fixed) / sobol_point — digitalnet.cpp:111-151.
+ * Requires dims <= qmc_matrices_dims(m) (else OUT_OF_RANGE) and
+ * first_index + n <= 2^52 (else INVALID_ARGUMENT, digitalnet.cpp:114-115).
+ * words: host array of dims entries (XOR words / Owen seeds), NULL = zeros. */
+qmc_status qmc_sobol_fill(const qmc_matrices* m, uint64_t first_index, uint64_t n, uint32_t dims,
+                          qmc_sobol_scramble scramble, const uint32_t* words, qmc_output kind,
+                          void* out, qmc_stream stream);
+
+typedef enum qmc_radical_scramble {
+    QMC_RADICAL_PLAIN = 0,  /* radical.cpp:130-142 */
+    QMC_RADICAL_LINEAR = 1, /* radical.cpp:144-164, factor per prime */
+    QMC_RADICAL_FAURE = 2   /* radical.cpp:166-181 with faure_permutation */
+} qmc_radical_scramble;
+
+/* Halton points (radical.cpp:240-269): component j = radical inverse of
+ * (uint32_t)i in prime(j). factors: host, dims entries, NULL = defaults.
+ * dims <= 1000. With dims = 1 this is radical_inverse(i, 0) (config C1). */
+qmc_status qmc_halton_fill(uint64_t first_index, uint64_t n, uint32_t dims,
+                           qmc_radical_scramble scramble, const uint32_t* factors,
+                           qmc_output kind, void* out, qmc_stream stream);
+/* radical_inverse*(i, prime_index) for one prime: out[n]. */
+qmc_status qmc_radical_inverse_fill(uint64_t first_index, uint64_t n, uint32_t prime_index,
+                                    qmc_radical_scramble scramble, uint32_t factor,
+                                    qmc_output kind, void* out, qmc_stream stream);
+
+/* Rank-1 lattice (lattice.hpp:31-39, lattice.cpp:48-55) with optional
+ * integer Cranley-Patterson rotation: x = brev((uint32_t)i) * g_j + s_j
+ * (mod 2^32), like lattice_point (lattice.cpp:48-55, no parity check of g;
+ * qmc_stream_fill's lattice kinds apply make_stream's odd-generator check).
+ * g: host, dims entries; shifts: host, dims entries or NULL (= plain). */
+qmc_status qmc_lattice_fill(const uint32_t* g, const uint32_t* shifts, uint32_t dims,
+                            uint64_t first_index, uint64_t n, qmc_output kind, void* out,
+                            qmc_stream stream);
+
+/* ---------------------------------------- SampleStream façade (imageplane.hpp) */
+typedef enum qmc_sampler_kind { /* imageplane.hpp:122-131 */
+    QMC_KIND_SOBOL = 0,
+    QMC_KIND_HALTON = 1,
+    QMC_KIND_LATTICE = 2,
+    QMC_KIND_HALTON_HILBERT = 3,
+    QMC_KIND_PIXEL_SHIFTED_LATTICE = 4,
+    QMC_KIND_PIXEL_RANDOM_LATTICE = 5,
+    QMC_KIND_IMAGE_PLANE_HALTON = 6,
+    QMC_KIND_SOBOL_XOR_TABLE = 7
+} qmc_sampler_kind;
+
+/* imageplane.cpp:250-292 (ConfigError for unknown names) */
+qmc_status qmc_sampler_kind_from_name(const char* name, qmc_sampler_kind* out);
+const char* qmc_sampler_kind_name(qmc_sampler_kind kind);
+
+/* StreamParams (imageplane.hpp:139-158). Unused fields are ignored per kind. */
+typedef struct qmc_stream_params {
+    uint32_t dims;              /* >= 1 */
+    const uint32_t* generator;  /* lattice kinds: host, generator_dims odd words */
+    uint32_t generator_dims;
+    const qmc_matrices* matrices;     /* sobol: NULL = builtin for dims */
+    const uint32_t* sobol_scrambles;  /* sobol: host words or NULL (plain) */
+    uint32_t sobol_scrambles_len;     /* must be >= dims when given */
+    uint32_t halton_scramble;         /* qmc_radical_scramble (halton kinds) */
+    const uint32_t* linear_factors;   /* host or NULL (defaults) */
+    uint32_t linear_factors_len;
+    uint32_t px, py, order;           /* pixel context (PixelCoord) */
+    uint32_t spp;                     /* halton_hilbert block size */
+    uint32_t width, height;           /* image_plane_halton */
+    uint32_t xor_seed;                /* sobol_xor_table: white-noise tables seed */
+    uint32_t xor_point_count;         /* sobol_xor_table: power of two */
+} qmc_stream_params;
+
+/* make_stream(kind, params) validation + SampleStream::sample(i, j) for
+ * i in [first_index, first_index + n), j < dims (imageplane.cpp:310-461). */
+qmc_status qmc_stream_fill(qmc_sampler_kind kind, const qmc_stream_params* params,
+                           uint64_t first_index, uint64_t n, qmc_output out_kind, void* out,
+                           qmc_stream stream);
+
+/* --------------------------------------------------- render (render.cpp:83-143) */
+typedef enum qmc_accum { QMC_ACCUM_KAHAN = 0, QMC_ACCUM_INT = 1 } qmc_accum; /* quality.hpp:35 */
+
+typedef struct qmc_render_job { /* RenderJob, render.hpp:31-47 */
+    uint32_t width, height, spp;
+    qmc_sampler_kind kind;        /* default pixel_shifted_lattice */
+    qmc_accum accum;
+    uint32_t seed;                /* 0 = defaults (render.cpp:94-106) */
+    const uint32_t* generator;    /* host, >= 2 odd words, NULL = lfsr default */
+    uint32_t generator_dims;
+    const qmc_matrices* matrices; /* NULL = builtin 2-dim */
+} qmc_render_job;
+
+/* Integrates scene_value over every pixel footprint of rows
+ * [row_begin, row_end) (the full image: 0, height) and writes
+ * float(estimate) row-major into out (device or host), out[0] = pixel
+ * (0, row_begin). One GPU thread owns one pixel and sums its samples in the
+ * reference order (bit-compatible accumulation). Multi-GPU: each rank
+ * renders a band; the host driver gathers the bands (one collective). */
+qmc_status qmc_render(const qmc_render_job* job, uint32_t row_begin, uint32_t row_end, float* out,
+                      qmc_stream stream);
+
+/* scene_value (render.cpp:17-26) evaluated on the device for n (x, y)
+ * pairs (device or host arrays of doubles) — integrand parity probe. */
+qmc_status qmc_scene_value(const double* xy, double* out, uint64_t n, qmc_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QMCGPU_H */

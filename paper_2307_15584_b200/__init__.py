@@ -1,0 +1,430 @@
+"""B200-native QMC sampling path (arXiv 2307.15584) — Python host binding.
+
+Thin ctypes layer over ``libqmcgpu.so`` (the C-ABI in ``include/qmcgpu.h``;
+sm_100a kernels in ``csrc/``). Names mirror the reference library's ``qmc::``
+surface (/root/reference/proj/include/qmc/*.hpp) so tests read like the
+reference's own obligations; errors map to the reference's exception classes:
+
+    qmc::ConfigError        -> ConfigError (RuntimeError)
+    std::invalid_argument   -> ValueError
+    std::out_of_range       -> IndexError
+    std::overflow_error     -> OverflowError
+    CUDA failure / no GPU   -> CudaError (RuntimeError)
+
+There is no CPU fallback: every per-sample computation runs in the CUDA
+library, and importing this package fails loudly when the library is missing.
+Device outputs are torch tensors on the current CUDA device; host (numpy)
+outputs go through the library's chunked D2H pipeline.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libqmcgpu.so")
+
+__all__ = [
+    "ConfigError", "CudaError", "lib", "GeneratorMatrixSet", "map_u32_to_unifloat",
+    "map_selfcheck", "sobol_fill", "halton_fill", "radical_inverse_fill", "lattice_fill",
+    "stream_fill", "render", "scene_value", "prime", "prime_max_power", "faure_permutation",
+    "default_linear_factors", "lfsr_generator_vector", "pixel_hash", "hilbert_order_for",
+    "partition_by_extra_dimension", "halton_pixel_enumeration", "sampler_kind_from_name",
+    "SAMPLER_KINDS",
+]
+
+
+class ConfigError(RuntimeError):
+    """qmc::ConfigError (errors.hpp:13-15)."""
+
+
+class CudaError(RuntimeError):
+    """CUDA runtime failure inside libqmcgpu."""
+
+
+SAMPLER_KINDS = ["sobol", "halton", "lattice", "halton-hilbert", "pixel-shifted-lattice",
+                 "pixel-random-lattice", "image-plane-halton", "sobol-xor-table"]
+
+u32, u64, i32, f64, P = C.c_uint32, C.c_uint64, C.c_int, C.c_double, C.c_void_p
+
+
+class StreamParams(C.Structure):
+    _fields_ = [("dims", u32), ("generator", P), ("generator_dims", u32), ("matrices", P),
+                ("sobol_scrambles", P), ("sobol_scrambles_len", u32), ("halton_scramble", u32),
+                ("linear_factors", P), ("linear_factors_len", u32), ("px", u32), ("py", u32),
+                ("order", u32), ("spp", u32), ("width", u32), ("height", u32),
+                ("xor_seed", u32), ("xor_point_count", u32)]
+
+
+class RenderJob(C.Structure):
+    _fields_ = [("width", u32), ("height", u32), ("spp", u32), ("kind", i32), ("accum", i32),
+                ("seed", u32), ("generator", P), ("generator_dims", u32), ("matrices", P)]
+
+
+class HaltonEnumeration(C.Structure):
+    _fields_ = [("scale_x", u32), ("scale_y", u32), ("exponent_x", u32), ("exponent_y", u32),
+                ("stride", u64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libqmcgpu.so (fails loudly when it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            "libqmcgpu.so not built (%s); run `python -c 'import __graft_entry__ as g; g.build()'`"
+            % LIB_PATH)
+    L = C.CDLL(LIB_PATH)
+
+    def sig(name, res, *args):
+        f = getattr(L, name)
+        f.restype, f.argtypes = res, list(args)
+
+    sig("qmc_last_error", C.c_char_p)
+    sig("qmc_abi_version", i32)
+    sig("qmc_map_u32_to_unifloat", i32, P, P, u64, P)
+    sig("qmc_map_selfcheck", i32, C.POINTER(u64), P)
+    sig("qmc_prime", i32, u32, C.POINTER(u32))
+    sig("qmc_prime_max_power", i32, u32, C.POINTER(u32))
+    sig("qmc_faure_permutation", i32, u32, P)
+    sig("qmc_default_linear_factors", i32, u32, P)
+    sig("qmc_lfsr_generator_vector", i32, u32, u32, P)
+    sig("qmc_pixel_hash", u32, u32, u32, u32)
+    sig("qmc_hilbert_order_for", u32, u32, u32)
+    sig("qmc_partition_by_extra_dimension", i32, u32, u32, u32, C.POINTER(u64), C.POINTER(u64))
+    sig("qmc_halton_pixel_enumeration", i32, u32, u32, u32, u32, C.POINTER(HaltonEnumeration),
+        C.POINTER(u64))
+    sig("qmc_matrices_builtin", i32, u32, C.POINTER(P))
+    sig("qmc_matrices_from_text", i32, C.c_char_p, u32, C.POINTER(P))
+    sig("qmc_matrices_from_columns", i32, P, u32, C.POINTER(P))
+    sig("qmc_matrices_dims", u32, P)
+    sig("qmc_matrices_columns", i32, P, P)
+    sig("qmc_matrices_destroy", None, P)
+    sig("qmc_sobol_fill", i32, P, u64, u64, u32, i32, P, i32, P, P)
+    sig("qmc_halton_fill", i32, u64, u64, u32, i32, P, i32, P, P)
+    sig("qmc_radical_inverse_fill", i32, u64, u64, u32, i32, u32, i32, P, P)
+    sig("qmc_lattice_fill", i32, P, P, u32, u64, u64, i32, P, P)
+    sig("qmc_sampler_kind_from_name", i32, C.c_char_p, C.POINTER(i32))
+    sig("qmc_stream_fill", i32, i32, C.POINTER(StreamParams), u64, u64, i32, P, P)
+    sig("qmc_render", i32, C.POINTER(RenderJob), u32, u32, P, P)
+    sig("qmc_scene_value", i32, P, P, u64, P)
+    _lib = L
+    return L
+
+
+_ERRORS = {1: ConfigError, 2: ValueError, 3: IndexError, 4: OverflowError, 5: CudaError,
+           6: CudaError, 9: RuntimeError}
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = lib().qmc_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, RuntimeError)(msg)
+
+
+# ----------------------------------------------------------------- helpers
+def _torch():
+    import torch
+
+    return torch
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is not None:
+        return int(stream)
+    torch = _torch()
+    if torch.cuda.is_available():
+        return torch.cuda.current_stream().cuda_stream
+    return None
+
+
+def _u32_host(a, n=None) -> Optional[np.ndarray]:
+    if a is None:
+        return None
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.uint64) & 0xFFFFFFFF, dtype=np.uint32)
+    if n is not None and arr.size < n:
+        raise ValueError("array shorter than dims")
+    return arr
+
+
+def _ptr(x) -> Optional[int]:
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return x.data_ptr()
+
+
+def _alloc(n: int, dims: int, fixed: bool, out, device=None):
+    """Output buffer: given (torch tensor / numpy array) or a new CUDA tensor."""
+    if out is not None:
+        nbytes = out.nbytes if isinstance(out, np.ndarray) else out.numel() * out.element_size()
+        if nbytes < n * dims * 4:
+            raise ValueError("output buffer too small")
+        return out
+    torch = _torch()
+    dt = torch.int32 if fixed else torch.float32
+    shape = (n, dims) if dims != 1 else (n,)
+    return torch.empty(shape, dtype=dt, device=device or "cuda")
+
+
+_SOBOL = {"none": 0, "plain": 0, "xor": 1, "owen": 2}
+_RADICAL = {"plain": 0, "linear": 1, "faure": 2}
+_ACCUM = {"kahan": 0, "int": 1}
+
+
+# ---------------------------------------------------------------- host setup
+def prime(index: int) -> int:
+    o = u32()
+    _check(lib().qmc_prime(index, C.byref(o)))
+    return o.value
+
+
+def prime_max_power(index: int) -> int:
+    o = u32()
+    _check(lib().qmc_prime_max_power(index, C.byref(o)))
+    return o.value
+
+
+def faure_permutation(base: int) -> list:
+    out = np.zeros(max(base, 1), np.uint32)
+    _check(lib().qmc_faure_permutation(base, out.ctypes.data))
+    return out.tolist()
+
+
+def default_linear_factors(dims: int) -> list:
+    out = np.zeros(max(dims, 1), np.uint32)
+    _check(lib().qmc_default_linear_factors(dims, out.ctypes.data))
+    return out[:dims].tolist()
+
+
+def lfsr_generator_vector(seed: int, dims: int) -> list:
+    out = np.zeros(max(dims, 1), np.uint32)
+    _check(lib().qmc_lfsr_generator_vector(seed, dims, out.ctypes.data))
+    return out[:dims].tolist()
+
+
+def pixel_hash(j: int, px: int, py: int) -> int:
+    return lib().qmc_pixel_hash(j, px, py)
+
+
+def hilbert_order_for(width: int, height: int) -> int:
+    return lib().qmc_hilbert_order_for(width, height)
+
+
+def partition_by_extra_dimension(part: int, parts: int, base: int):
+    r, m = u64(), u64()
+    _check(lib().qmc_partition_by_extra_dimension(part, parts, base, C.byref(r), C.byref(m)))
+    return r.value, m.value
+
+
+def halton_pixel_enumeration(width: int, height: int, px: int = 0, py: int = 0):
+    e, off = HaltonEnumeration(), u64()
+    _check(lib().qmc_halton_pixel_enumeration(width, height, px, py, C.byref(e), C.byref(off)))
+    return {"scale_x": e.scale_x, "scale_y": e.scale_y, "exponent_x": e.exponent_x,
+            "exponent_y": e.exponent_y, "stride": e.stride, "offset": off.value}
+
+
+def sampler_kind_from_name(name: str) -> int:
+    o = i32()
+    _check(lib().qmc_sampler_kind_from_name(name.encode(), C.byref(o)))
+    return o.value
+
+
+class GeneratorMatrixSet:
+    """Immutable Sobol' generator matrices (digitalnet.hpp:50-63) in libqmcgpu."""
+
+    def __init__(self, handle: int):
+        self._h = handle
+
+    @classmethod
+    def builtin(cls, dims: int) -> "GeneratorMatrixSet":
+        h = P()
+        _check(lib().qmc_matrices_builtin(dims, C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def from_text(cls, text: str, dims: int) -> "GeneratorMatrixSet":
+        h = P()
+        _check(lib().qmc_matrices_from_text(text.encode(), dims, C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def from_columns(cls, columns) -> "GeneratorMatrixSet":
+        c = np.ascontiguousarray(columns, dtype=np.uint32)
+        h = P()
+        _check(lib().qmc_matrices_from_columns(c.ctypes.data, c.shape[0], C.byref(h)))
+        return cls(h.value)
+
+    @property
+    def dims(self) -> int:
+        return lib().qmc_matrices_dims(self._h)
+
+    def columns(self) -> np.ndarray:
+        out = np.zeros((self.dims, 52), np.uint32)
+        _check(lib().qmc_matrices_columns(self._h, out.ctypes.data))
+        return out
+
+    @property
+    def handle(self) -> int:
+        return self._h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.qmc_matrices_destroy(self._h)
+            self._h = None
+
+
+_builtin_cache: dict = {}
+
+
+def _builtin(dims: int) -> GeneratorMatrixSet:
+    m = _builtin_cache.get(dims)
+    if m is None:
+        m = _builtin_cache[dims] = GeneratorMatrixSet.builtin(dims)
+    return m
+
+
+# ------------------------------------------------------------------ fills
+def map_u32_to_unifloat(x, out=None, stream=None):
+    """Bit-exact map_u32_to_unifloat (unitfloat.hpp:34-50) over a u32 array."""
+    if isinstance(x, np.ndarray):
+        x = np.ascontiguousarray(x, dtype=np.uint32)
+        out = np.empty(x.shape, np.float32) if out is None else out
+    else:
+        torch = _torch()
+        out = torch.empty(x.shape, dtype=torch.float32, device=x.device) if out is None else out
+    _check(lib().qmc_map_u32_to_unifloat(_ptr(x), _ptr(out), int(np.prod(x.shape)), _stream(stream)))
+    return out
+
+
+def map_selfcheck(stream=None) -> int:
+    """Exhaustive 2^32 comparison of the device map with the reference formula."""
+    m = u64()
+    _check(lib().qmc_map_selfcheck(C.byref(m), _stream(stream)))
+    return m.value
+
+
+def sobol_fill(n: int, dims: int, first: int = 0, scramble: str = "none", words=None,
+               matrices: Optional[GeneratorMatrixSet] = None, fixed: bool = False, out=None,
+               stream=None):
+    """Sobol' points [n][dims] (digitalnet.cpp:111-151); scramble none|xor|owen."""
+    m = matrices or _builtin(dims)
+    w = _u32_host(words, dims)
+    o = _alloc(n, dims, fixed, out)
+    _check(lib().qmc_sobol_fill(m.handle, first, n, dims, _SOBOL[scramble], _ptr(w),
+                                1 if fixed else 0, _ptr(o), _stream(stream)))
+    return o
+
+
+def halton_fill(n: int, dims: int, first: int = 0, scramble: str = "plain", factors=None,
+                fixed: bool = False, out=None, stream=None):
+    """Halton points (radical.cpp:240-269) with plain/linear/faure digit scrambles."""
+    f = _u32_host(factors, dims)
+    o = _alloc(n, dims, fixed, out)
+    _check(lib().qmc_halton_fill(first, n, dims, _RADICAL[scramble], _ptr(f),
+                                 1 if fixed else 0, _ptr(o), _stream(stream)))
+    return o
+
+
+def radical_inverse_fill(n: int, prime_index: int = 0, first: int = 0, scramble: str = "plain",
+                         factor: int = 1, fixed: bool = False, out=None, stream=None):
+    """radical_inverse*(i, prime_index) for i in [first, first+n) (radical.cpp:130-213)."""
+    o = _alloc(n, 1, fixed, out)
+    _check(lib().qmc_radical_inverse_fill(first, n, prime_index, _RADICAL[scramble], factor,
+                                          1 if fixed else 0, _ptr(o), _stream(stream)))
+    return o
+
+
+def lattice_fill(n: int, g: Sequence[int], first: int = 0, shifts=None, dims: Optional[int] = None,
+                 fixed: bool = False, out=None, stream=None):
+    """Rank-1 lattice brev(i)*g_j (+ integer CP shift s_j) (lattice.hpp:31-39)."""
+    dims = len(g) if dims is None else dims
+    gv = _u32_host(g, dims)
+    sv = _u32_host(shifts, dims)
+    o = _alloc(n, dims, fixed, out)
+    _check(lib().qmc_lattice_fill(_ptr(gv), _ptr(sv), dims, first, n, 1 if fixed else 0,
+                                  _ptr(o), _stream(stream)))
+    return o
+
+
+def stream_fill(kind: str, n: int, dims: int = 2, first: int = 0, *, generator=None,
+                matrices: Optional[GeneratorMatrixSet] = None, sobol_scrambles=None,
+                scramble: str = "plain", linear_factors=None, pixel=(0, 0), order: int = 1,
+                spp: int = 1, width: int = 0, height: int = 0, xor_seed: int = 0,
+                xor_point_count: int = 1, fixed: bool = False, out=None, stream=None):
+    """make_stream(kind, params) + SampleStream::sample(i, j) (imageplane.cpp:310-461)."""
+    k = sampler_kind_from_name(kind)
+    if scramble not in _RADICAL:
+        raise ConfigError("make_stream: scramble must be plain, faure, or linear")
+    keep = []
+    p = StreamParams()
+    p.dims = dims
+    if generator is not None:
+        g = _u32_host(generator)
+        keep.append(g)
+        p.generator, p.generator_dims = g.ctypes.data, g.size
+    if matrices is not None:
+        p.matrices = matrices.handle
+    if sobol_scrambles is not None:
+        s = _u32_host(sobol_scrambles)
+        keep.append(s)
+        p.sobol_scrambles, p.sobol_scrambles_len = s.ctypes.data, s.size
+    p.halton_scramble = _RADICAL[scramble]
+    if linear_factors is not None:
+        f = _u32_host(linear_factors)
+        keep.append(f)
+        p.linear_factors, p.linear_factors_len = f.ctypes.data, f.size
+    p.px, p.py = pixel
+    p.order, p.spp, p.width, p.height = order, spp, width, height
+    p.xor_seed, p.xor_point_count = xor_seed, xor_point_count
+    o = _alloc(n, dims, fixed, out)
+    _check(lib().qmc_stream_fill(k, C.byref(p), first, n, 1 if fixed else 0, _ptr(o),
+                                 _stream(stream)))
+    return o
+
+
+def render(width: int, height: int, spp: int = 1, kind: str = "pixel-shifted-lattice",
+           accum: str = "kahan", seed: int = 0, generator=None,
+           matrices: Optional[GeneratorMatrixSet] = None, rows=None, out=None, stream=None):
+    """render(RenderJob) (render.cpp:83-143) for rows [r0, r1) of the image.
+
+    Returns a [rows, width] float32 tensor (or fills `out`, device or host)."""
+    if accum not in _ACCUM:
+        raise ConfigError("accumulation mode must be 'kahan' or 'int'")
+    job = RenderJob()
+    job.width, job.height, job.spp = width, height, spp
+    job.kind = sampler_kind_from_name(kind)
+    job.accum = _ACCUM[accum]
+    job.seed = seed
+    keep = None
+    if generator is not None:
+        keep = _u32_host(generator)
+        job.generator, job.generator_dims = keep.ctypes.data, keep.size
+    if matrices is not None:
+        job.matrices = matrices.handle
+    r0, r1 = rows if rows is not None else (0, height)
+    if out is None:
+        torch = _torch()
+        out = torch.empty((max(r1 - r0, 0), width), dtype=torch.float32, device="cuda")
+    _check(lib().qmc_render(C.byref(job), r0, r1, _ptr(out), _stream(stream)))
+    return out
+
+
+def scene_value(xy, out=None, stream=None):
+    """Device scene_value (render.cpp:17-26) for an [n, 2] float64 array."""
+    if isinstance(xy, np.ndarray):
+        xy = np.ascontiguousarray(xy, dtype=np.float64)
+        out = np.empty(xy.shape[0], np.float64) if out is None else out
+    else:
+        torch = _torch()
+        out = torch.empty(xy.shape[0], dtype=torch.float64, device=xy.device) if out is None else out
+    _check(lib().qmc_scene_value(_ptr(xy), _ptr(out), xy.shape[0], _stream(stream)))
+    return out

@@ -1,0 +1,1276 @@
+// abi.cpp — the extern "C" boundary (include/qmcgpu.h) of libqmcgpu.
+//
+// Host responsibilities only: validate arguments with the reference's
+// conditions (so callers see the same error classes), build the immutable
+// tables the reference builds on the host (primes, direction-number
+// matrices, Faure permutations, generator vectors, XOR tables), upload
+// per-call parameters, place the output (device pointer: one asynchronous
+// launch; host pointer: chunked device fill + D2H pipeline), and launch the
+// kernels. No per-sample arithmetic happens here.
+#include "qmcgpu.h"
+
+#include <algorithm>
+#include <array>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "device.cuh" // RadicalDim layout (host-visible struct)
+#include "internal.hpp"
+
+using namespace qmcgpu;
+
+namespace {
+
+// ------------------------------------------------------------- errors
+
+thread_local std::string g_error;
+
+struct Fail {
+    qmc_status status;
+    std::string msg;
+};
+
+[[noreturn]] void fail(qmc_status s, std::string msg) { throw Fail{s, std::move(msg)}; }
+
+void cuda_ok(cudaError_t e, const char* what)
+{
+    if (e != cudaSuccess)
+        fail(QMC_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+qmc_status guard(F&& f)
+{
+    try {
+        f();
+        return QMC_OK;
+    } catch (const Fail& e) {
+        g_error = e.msg;
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        g_error = "out of host memory";
+        return QMC_INTERNAL;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return QMC_INTERNAL;
+    }
+}
+
+// ---------------------------------------------------------- prime table
+
+constexpr uint32_t kPrimes = 1000;
+
+struct PrimeTable {
+    std::array<uint32_t, kPrimes> p{}, maxpow{};
+    PrimeTable()
+    {
+        uint32_t found = 0;
+        for (uint32_t c = 2; found < kPrimes; ++c) {
+            bool prime = true;
+            for (uint32_t k = 0; k < found && p[k] * p[k] <= c; ++k)
+                if (c % p[k] == 0) {
+                    prime = false;
+                    break;
+                }
+            if (prime)
+                p[found++] = c;
+        }
+        for (uint32_t k = 0; k < kPrimes; ++k) {
+            uint64_t x = p[k];
+            while (x * p[k] <= 0xffffffffull)
+                x *= p[k];
+            maxpow[k] = static_cast<uint32_t>(x);
+        }
+    }
+};
+
+const PrimeTable& primes()
+{
+    static const PrimeTable t;
+    return t;
+}
+
+uint32_t prime_at(uint32_t index)
+{
+    if (index >= kPrimes)
+        fail(QMC_OUT_OF_RANGE, "prime: index beyond the bundled prime table");
+    return primes().p[index];
+}
+
+// radical.cpp:50-74
+std::vector<uint32_t> faure(uint32_t b)
+{
+    if (b < 2)
+        fail(QMC_INVALID_ARGUMENT, "faure_permutation: base must be >= 2");
+    if (b == 2)
+        return {0u, 1u};
+    std::vector<uint32_t> s;
+    s.reserve(b);
+    if (b % 2 == 0) {
+        const auto h = faure(b / 2);
+        for (uint32_t v : h)
+            s.push_back(2 * v);
+        for (uint32_t v : h)
+            s.push_back(2 * v + 1);
+    } else {
+        const auto prev = faure(b - 1);
+        const uint32_t mid = (b - 1) / 2;
+        for (uint32_t k = 0; k < prev.size(); ++k) {
+            if (k == mid)
+                s.push_back(mid);
+            s.push_back(prev[k] >= mid ? prev[k] + 1 : prev[k]);
+        }
+    }
+    return s;
+}
+
+// ------------------------------------------------- direction numbers
+
+struct DirRow {
+    uint32_t s, a;
+    std::vector<uint32_t> m;
+};
+
+struct BuiltinRow {
+    uint32_t s, a;
+    uint32_t m[32];
+};
+const BuiltinRow kJoeKuo[] = {
+#include "joe_kuo_64.inc"
+};
+
+std::vector<DirRow> builtin_rows()
+{
+    std::vector<DirRow> rows;
+    for (const BuiltinRow& r : kJoeKuo)
+        rows.push_back(DirRow{r.s, r.a, std::vector<uint32_t>(r.m, r.m + r.s)});
+    return rows;
+}
+
+// digitalnet.cpp:23-65 — same grammar, checks and ConfigError messages.
+std::vector<DirRow> parse_rows(const std::string& text)
+{
+    std::vector<DirRow> rows;
+    std::istringstream in(text);
+    std::string line;
+    size_t no = 0;
+    bool header = false;
+    auto bad = [&](const std::string& w) {
+        fail(QMC_CONFIG, "direction numbers, line " + std::to_string(no) + ": " + w);
+    };
+    while (std::getline(in, line)) {
+        ++no;
+        if (!header) {
+            header = true;
+            continue;
+        }
+        std::istringstream ls(line);
+        uint32_t d = 0, s = 0, a = 0;
+        if (!(ls >> d))
+            continue;
+        if (!(ls >> s >> a))
+            bad("expected 'd s a m_1 ... m_s'");
+        if (d != rows.size() + 2)
+            bad("dimensions must be consecutive starting at 2");
+        if (s == 0 || s > 32)
+            bad("degree s out of range");
+        if (s > 1 && a >= (1u << (s - 1)))
+            bad("coefficient a has more than s-1 bits");
+        DirRow row{s, a, {}};
+        for (uint32_t k = 1; k <= s; ++k) {
+            uint64_t mk = 0;
+            if (!(ls >> mk))
+                bad("expected " + std::to_string(s) + " direction numbers");
+            if (mk % 2 == 0)
+                bad("direction number m_" + std::to_string(k) + " is even");
+            if (mk >= (1ull << k))
+                bad("direction number m_" + std::to_string(k) + " must be < 2^" +
+                    std::to_string(k));
+            row.m.push_back(static_cast<uint32_t>(mk));
+        }
+        std::string rest;
+        if (ls >> rest)
+            bad("trailing tokens after the m values");
+        rows.push_back(std::move(row));
+    }
+    return rows;
+}
+
+// digitalnet.cpp:79-109 — MSB-aligned columns, 52 per dimension.
+std::vector<uint32_t> build_columns(const std::vector<DirRow>& rows, uint32_t dims)
+{
+    if (dims > rows.size() + 1)
+        fail(QMC_CONFIG, "build_matrices: requested " + std::to_string(dims) +
+                             " dimensions, direction numbers provide " +
+                             std::to_string(rows.size() + 1));
+    std::vector<uint32_t> c(static_cast<size_t>(dims) * 52, 0u);
+    if (dims == 0)
+        return c;
+    for (uint32_t k = 0; k < 32; ++k)
+        c[k] = 0x80000000u >> k;
+    for (uint32_t j = 1; j < dims; ++j) {
+        const DirRow& r = rows[j - 1];
+        uint32_t* v = c.data() + static_cast<size_t>(j) * 52;
+        for (uint32_t k = 0; k < r.s && k < 52; ++k)
+            v[k] = r.m[k] << (31 - k);
+        for (uint32_t k = r.s; k < 52; ++k) {
+            uint32_t x = v[k - r.s] ^ (v[k - r.s] >> r.s);
+            for (uint32_t l = 1; l < r.s; ++l)
+                if ((r.a >> (r.s - 1 - l)) & 1u)
+                    x ^= v[k - l];
+            v[k] = x;
+        }
+    }
+    return c;
+}
+
+uint32_t brev_host(uint32_t v)
+{
+    uint32_t r = 0;
+    for (int k = 0; k < 32; ++k)
+        r |= ((v >> k) & 1u) << (31 - k);
+    return r;
+}
+
+// lattice.cpp:59-77
+uint32_t fmix_host(uint32_t h)
+{
+    h = (h ^ (h >> 16)) * 0x85ebca6bu;
+    h = (h ^ (h >> 13)) * 0xc2b2ae35u;
+    return h ^ (h >> 16);
+}
+uint32_t pixel_hash_host(uint32_t j, uint32_t px, uint32_t py)
+{
+    return fmix_host(fmix_host(fmix_host(0x9e3779b9u ^ j) ^ px) ^ py);
+}
+
+std::vector<uint32_t> lfsr(uint32_t seed, uint32_t dims)
+{
+    if (seed == 0)
+        fail(QMC_INVALID_ARGUMENT, "lfsr_generator_vector: zero seed is the absorbing state");
+    if (dims < 1)
+        fail(QMC_INVALID_ARGUMENT, "lfsr_generator_vector: dims must be >= 1");
+    std::vector<uint32_t> g{1u};
+    uint32_t x = seed;
+    for (uint32_t j = 1; j < dims; ++j) {
+        x ^= x << 13;
+        x ^= x >> 17;
+        x ^= x << 5;
+        g.push_back(2u * x + 1u);
+    }
+    return g;
+}
+
+uint32_t hilbert_order(uint32_t w, uint32_t h)
+{
+    uint32_t o = 1;
+    while (o < 32 && ((1ull << o) < w || (1ull << o) < h))
+        ++o;
+    return o;
+}
+
+// ------------------------------------------ Halton pixel enumeration
+
+uint64_t inverse_mod(uint64_t a, uint64_t n)
+{
+    if (n == 1)
+        return 0;
+    int64_t r0 = static_cast<int64_t>(n), r1 = static_cast<int64_t>(a % n), t0 = 0, t1 = 1;
+    while (r1) {
+        const int64_t q = r0 / r1;
+        const int64_t r2 = r0 - q * r1, t2 = t0 - q * t1;
+        r0 = r1;
+        r1 = r2;
+        t0 = t1;
+        t1 = t2;
+    }
+    const int64_t m = static_cast<int64_t>(n);
+    return static_cast<uint64_t>(((t0 % m) + m) % m);
+}
+
+struct HaltonEnum {
+    uint32_t sx = 1, sy = 1, ex = 0, ey = 0;
+    uint64_t stride = 1, crt_x = 0, crt_y = 0;
+};
+
+// imageplane.cpp:80-98
+HaltonEnum halton_enum(uint32_t w, uint32_t h)
+{
+    if (w == 0 || h == 0)
+        fail(QMC_CONFIG, "HaltonPixelEnumeration: image must be at least 1x1");
+    if (w > (1u << 20) || h > 1594323u)
+        fail(QMC_CONFIG, "HaltonPixelEnumeration: image too large for the index range");
+    HaltonEnum e;
+    while (e.sx < w) {
+        e.sx *= 2;
+        ++e.ex;
+    }
+    while (e.sy < h) {
+        e.sy *= 3;
+        ++e.ey;
+    }
+    e.stride = static_cast<uint64_t>(e.sx) * e.sy;
+    e.crt_x = e.sy * inverse_mod(e.sy % e.sx, e.sx);
+    e.crt_y = e.sx * inverse_mod(e.sx % e.sy, e.sy);
+    return e;
+}
+
+uint64_t digit_reverse_host(uint64_t v, uint32_t base, uint32_t digits)
+{
+    uint64_t r = 0;
+    for (uint32_t k = 0; k < digits; ++k) {
+        r = r * base + v % base;
+        v /= base;
+    }
+    return r;
+}
+
+// ------------------------------------------------------ device buffers
+
+struct DevFree {
+    void operator()(void* p) const { cudaFree(p); }
+};
+using DevPtr = std::unique_ptr<void, DevFree>;
+
+DevPtr dev_upload(const void* host, size_t bytes)
+{
+    void* d = nullptr;
+    cuda_ok(cudaMalloc(&d, bytes ? bytes : 16), "cudaMalloc");
+    DevPtr p(d);
+    if (bytes)
+        cuda_ok(cudaMemcpy(d, host, bytes, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+    return p;
+}
+
+// Small per-call parameter arrays, uploaded with one stream-ordered copy
+// and released stream-ordered after the launches.
+class CallArgs {
+public:
+    explicit CallArgs(cudaStream_t s) : s_(s) {}
+    ~CallArgs()
+    {
+        if (dev_)
+            cudaFreeAsync(dev_, s_);
+    }
+    // returns the byte offset of the array inside the blob (16-B aligned)
+    size_t add(const void* p, size_t bytes)
+    {
+        const size_t off = (blob_.size() + 15) & ~size_t(15);
+        blob_.resize(off + bytes);
+        if (bytes)
+            std::memcpy(blob_.data() + off, p, bytes);
+        return off;
+    }
+    void upload()
+    {
+        if (blob_.empty())
+            return;
+        cuda_ok(cudaMallocAsync(&dev_, blob_.size(), s_), "cudaMallocAsync");
+        cuda_ok(cudaMemcpyAsync(dev_, blob_.data(), blob_.size(), cudaMemcpyHostToDevice, s_),
+                "cudaMemcpyAsync args");
+    }
+    template <typename T>
+    const T* at(size_t off) const
+    {
+        return reinterpret_cast<const T*>(static_cast<const char*>(dev_) + off);
+    }
+
+private:
+    cudaStream_t s_;
+    std::vector<char> blob_;
+    void* dev_ = nullptr;
+};
+
+// Per-device resources for the host-output pipeline.
+struct DeviceCtx {
+    std::mutex mu;
+    cudaStream_t streams[2] = {nullptr, nullptr};
+    void* staging[2] = {nullptr, nullptr};
+    size_t staging_bytes = 0;
+};
+
+DeviceCtx& device_ctx(int dev)
+{
+    static std::mutex mu;
+    static std::vector<std::unique_ptr<DeviceCtx>> ctxs;
+    std::lock_guard<std::mutex> lk(mu);
+    if (ctxs.size() <= static_cast<size_t>(dev))
+        ctxs.resize(dev + 1);
+    if (!ctxs[dev])
+        ctxs[dev] = std::make_unique<DeviceCtx>();
+    return *ctxs[dev];
+}
+
+int current_device()
+{
+    int dev = 0;
+    cuda_ok(cudaGetDevice(&dev), "cudaGetDevice");
+    return dev;
+}
+
+bool is_device_pointer(const void* p)
+{
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+constexpr size_t kStagingBytes = size_t(64) << 20;
+
+// Places a fill of n points x dims 32-bit words at `out`. launch(range, s)
+// enqueues the kernels writing device memory.
+template <typename Launch>
+void place_fill(void* out, uint64_t first, uint64_t n, uint32_t dims, cudaStream_t s,
+                Launch&& launch)
+{
+    if (n == 0 || dims == 0)
+        return;
+    if (!out)
+        fail(QMC_INVALID_ARGUMENT, "output pointer is null");
+    if (is_device_pointer(out)) {
+        cuda_ok(launch(FillRange{first, n, out}, s), "kernel launch");
+        return;
+    }
+    // host output: ordered after prior work on the caller's stream
+    cuda_ok(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    DeviceCtx& ctx = device_ctx(current_device());
+    std::lock_guard<std::mutex> lk(ctx.mu);
+    if (!ctx.streams[0]) {
+        for (auto& st : ctx.streams)
+            cuda_ok(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+    }
+    if (ctx.staging_bytes < kStagingBytes) {
+        for (auto& b : ctx.staging) {
+            if (b)
+                cudaFree(b);
+            cuda_ok(cudaMalloc(&b, kStagingBytes), "cudaMalloc staging");
+        }
+        ctx.staging_bytes = kStagingBytes;
+    }
+    const uint64_t row = static_cast<uint64_t>(dims) * 4;
+    uint64_t chunk = std::max<uint64_t>(1, kStagingBytes / row);
+    if (chunk > 4096)
+        chunk &= ~uint64_t(4095); // keep chunk starts tile-aligned relative to `first`
+    char* host = static_cast<char*>(out);
+    uint64_t k = 0;
+    for (uint64_t done = 0; done < n; done += chunk, ++k) {
+        const uint64_t cnt = std::min(chunk, n - done);
+        cudaStream_t st = ctx.streams[k & 1];
+        cuda_ok(launch(FillRange{first + done, cnt, ctx.staging[k & 1]}, st), "kernel launch");
+        cuda_ok(cudaMemcpyAsync(host + done * row, ctx.staging[k & 1], cnt * row,
+                                cudaMemcpyDeviceToHost, st),
+                "cudaMemcpyAsync D2H");
+    }
+    for (auto& st : ctx.streams)
+        cuda_ok(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+}
+
+cudaStream_t as_stream(qmc_stream s) { return static_cast<cudaStream_t>(s); }
+
+// RadicalDim table for `dims` prime bases (radical.cpp:130-181).
+std::vector<RadicalDim> radical_dims(uint32_t dims, uint32_t first_prime, qmc_radical_scramble sc,
+                                     const uint32_t* factors, std::vector<uint32_t>& sigma_pool,
+                                     std::vector<size_t>& sigma_off)
+{
+    std::vector<RadicalDim> rd(dims);
+    sigma_off.assign(dims, SIZE_MAX);
+    for (uint32_t j = 0; j < dims; ++j) {
+        const uint32_t pi = first_prime + j;
+        const uint32_t b = prime_at(pi);
+        RadicalDim& r = rd[j];
+        r.base = b;
+        r.maxpow = primes().maxpow[pi];
+        r.divb = make_div32(b);
+        r.divmp = make_div32(r.maxpow);
+        r.mode = 0;
+        r.factor = 0;
+        r.sigma = nullptr;
+        if (sc == QMC_RADICAL_LINEAR) {
+            const uint32_t f = factors ? factors[j] : b - 1;
+            if (f == 0 || f >= b)
+                fail(QMC_INVALID_ARGUMENT,
+                     "radical_inverse_linscramble: factor must be in [1, base)");
+            r.mode = 1;
+            r.factor = f;
+        } else if (sc == QMC_RADICAL_FAURE) {
+            const auto s = faure(b);
+            sigma_off[j] = sigma_pool.size();
+            sigma_pool.insert(sigma_pool.end(), s.begin(), s.end());
+            r.mode = 2;
+        }
+    }
+    return rd;
+}
+
+} // namespace
+
+// =====================================================================
+//                               C ABI
+// =====================================================================
+
+struct qmc_matrices {
+    uint32_t dims;
+    std::vector<uint32_t> columns; // [dims][52]
+    std::mutex mu;
+    struct Dev {
+        DevPtr colsT, colsT_rev;
+    };
+    std::vector<std::unique_ptr<Dev>> dev;
+
+    // [52][dims] (and bit-reversed) columns on the current device
+    const Dev& on_device()
+    {
+        const int d = current_device();
+        std::lock_guard<std::mutex> lk(mu);
+        if (dev.size() <= static_cast<size_t>(d))
+            dev.resize(d + 1);
+        if (!dev[d]) {
+            const uint32_t pd = std::max<uint32_t>(dims, 4); // room for 16-B loads
+            std::vector<uint32_t> t(52 * static_cast<size_t>(pd), 0u), tr(t.size(), 0u);
+            for (uint32_t j = 0; j < dims; ++j)
+                for (uint32_t k = 0; k < 52; ++k) {
+                    t[k * static_cast<size_t>(dims) + j] = columns[j * 52 + k];
+                    tr[k * static_cast<size_t>(dims) + j] = brev_host(columns[j * 52 + k]);
+                }
+            auto e = std::make_unique<Dev>();
+            e->colsT = dev_upload(t.data(), t.size() * 4);
+            e->colsT_rev = dev_upload(tr.data(), tr.size() * 4);
+            dev[d] = std::move(e);
+        }
+        return *dev[d];
+    }
+};
+
+extern "C" {
+
+const char* qmc_last_error(void) { return g_error.c_str(); }
+
+const char* qmc_status_string(qmc_status s)
+{
+    switch (s) {
+    case QMC_OK: return "ok";
+    case QMC_CONFIG: return "config error";
+    case QMC_INVALID_ARGUMENT: return "invalid argument";
+    case QMC_OUT_OF_RANGE: return "out of range";
+    case QMC_OVERFLOW: return "overflow";
+    case QMC_CUDA: return "cuda error";
+    case QMC_NCCL: return "nccl error";
+    default: return "internal error";
+    }
+}
+
+int qmc_abi_version(void) { return QMCGPU_ABI_VERSION; }
+
+// ------------------------------------------------------------------ L0
+
+qmc_status qmc_map_u32_to_unifloat(const uint32_t* in, float* out, uint64_t n, qmc_stream stream)
+{
+    return guard([&] {
+        if (n == 0)
+            return;
+        const cudaStream_t s = as_stream(stream);
+        if (is_device_pointer(in) && is_device_pointer(out)) {
+            cuda_ok(launch_map(in, out, n, s), "launch_map");
+            return;
+        }
+        // host arrays: stage through device memory
+        uint32_t* din = nullptr;
+        float* dout = nullptr;
+        cuda_ok(cudaMallocAsync(&din, n * 4, s), "cudaMallocAsync");
+        cuda_ok(cudaMallocAsync(&dout, n * 4, s), "cudaMallocAsync");
+        cuda_ok(cudaMemcpyAsync(din, in, n * 4, cudaMemcpyDefault, s), "H2D");
+        cuda_ok(launch_map(din, dout, n, s), "launch_map");
+        cuda_ok(cudaMemcpyAsync(out, dout, n * 4, cudaMemcpyDefault, s), "D2H");
+        cudaFreeAsync(din, s);
+        cudaFreeAsync(dout, s);
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+    });
+}
+
+qmc_status qmc_map_selfcheck(uint64_t* mismatches, qmc_stream stream)
+{
+    return guard([&] {
+        const cudaStream_t s = as_stream(stream);
+        unsigned long long* d = nullptr;
+        cuda_ok(cudaMallocAsync(&d, 8, s), "cudaMallocAsync");
+        cuda_ok(cudaMemsetAsync(d, 0, 8, s), "memset");
+        cuda_ok(launch_map_selfcheck(d, s), "launch_map_selfcheck");
+        unsigned long long h = 0;
+        cuda_ok(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, s), "D2H");
+        cudaFreeAsync(d, s);
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        *mismatches = h;
+    });
+}
+
+// ------------------------------------------------------------ host setup
+
+qmc_status qmc_prime(uint32_t index, uint32_t* out)
+{
+    return guard([&] { *out = prime_at(index); });
+}
+
+qmc_status qmc_prime_max_power(uint32_t index, uint32_t* out)
+{
+    return guard([&] {
+        if (index >= kPrimes)
+            fail(QMC_OUT_OF_RANGE, "prime_max_power: index beyond the bundled prime table");
+        *out = primes().maxpow[index];
+    });
+}
+
+qmc_status qmc_faure_permutation(uint32_t base, uint32_t* out)
+{
+    return guard([&] {
+        const auto s = faure(base);
+        std::memcpy(out, s.data(), s.size() * 4);
+    });
+}
+
+qmc_status qmc_default_linear_factors(uint32_t dims, uint32_t* out)
+{
+    return guard([&] {
+        if (dims > kPrimes)
+            fail(QMC_INVALID_ARGUMENT, "default_linear_factors: dims beyond the prime table");
+        for (uint32_t j = 0; j < dims; ++j)
+            out[j] = primes().p[j] - 1;
+    });
+}
+
+qmc_status qmc_lfsr_generator_vector(uint32_t seed, uint32_t dims, uint32_t* out)
+{
+    return guard([&] {
+        const auto g = lfsr(seed, dims);
+        std::memcpy(out, g.data(), g.size() * 4);
+    });
+}
+
+uint32_t qmc_pixel_hash(uint32_t j, uint32_t px, uint32_t py) { return pixel_hash_host(j, px, py); }
+
+uint32_t qmc_hilbert_order_for(uint32_t width, uint32_t height)
+{
+    return hilbert_order(width, height);
+}
+
+qmc_status qmc_partition_by_extra_dimension(uint32_t part, uint32_t parts, uint32_t base,
+                                            uint64_t* remainder, uint64_t* modulus)
+{
+    return guard([&] {
+        if (base < 2)
+            fail(QMC_INVALID_ARGUMENT, "partition_by_extra_dimension: base must be >= 2");
+        uint32_t k = 0;
+        uint64_t p = 1;
+        while (p < parts) {
+            p *= base;
+            ++k;
+        }
+        if (p != parts)
+            fail(QMC_CONFIG, "partition_by_extra_dimension: parts must be a power of the base");
+        if (part >= parts)
+            fail(QMC_OUT_OF_RANGE, "partition_by_extra_dimension: part index beyond parts");
+        *remainder = digit_reverse_host(part, base, k);
+        *modulus = parts;
+    });
+}
+
+qmc_status qmc_halton_pixel_enumeration(uint32_t width, uint32_t height, uint32_t px, uint32_t py,
+                                        qmc_halton_enumeration* e, uint64_t* offset)
+{
+    return guard([&] {
+        const HaltonEnum h = halton_enum(width, height);
+        if (px >= h.sx || py >= h.sy)
+            fail(QMC_OUT_OF_RANGE, "HaltonPixelEnumeration: pixel outside the scaled grid");
+        if (e)
+            *e = qmc_halton_enumeration{h.sx, h.sy, h.ex, h.ey, h.stride};
+        if (offset) {
+            const uint64_t r2 = digit_reverse_host(px, 2, h.ex);
+            const uint64_t r3 = digit_reverse_host(py, 3, h.ey);
+            *offset = (r2 * h.crt_x % h.stride + r3 * h.crt_y % h.stride) % h.stride;
+        }
+    });
+}
+
+// ------------------------------------------------------------- matrices
+
+static qmc_matrices* new_matrices(std::vector<uint32_t> cols, uint32_t dims)
+{
+    auto* m = new qmc_matrices();
+    m->dims = dims;
+    m->columns = std::move(cols);
+    return m;
+}
+
+qmc_status qmc_matrices_builtin(uint32_t dims, qmc_matrices** out)
+{
+    return guard([&] { *out = new_matrices(build_columns(builtin_rows(), dims), dims); });
+}
+
+qmc_status qmc_matrices_from_text(const char* text, uint32_t dims, qmc_matrices** out)
+{
+    return guard([&] {
+        if (!text)
+            fail(QMC_INVALID_ARGUMENT, "direction number text is null");
+        *out = new_matrices(build_columns(parse_rows(text), dims), dims);
+    });
+}
+
+qmc_status qmc_matrices_from_columns(const uint32_t* columns, uint32_t dims, qmc_matrices** out)
+{
+    return guard([&] {
+        if (!columns && dims)
+            fail(QMC_INVALID_ARGUMENT, "columns pointer is null");
+        *out = new_matrices(std::vector<uint32_t>(columns, columns + static_cast<size_t>(dims) * 52),
+                            dims);
+    });
+}
+
+uint32_t qmc_matrices_dims(const qmc_matrices* m) { return m ? m->dims : 0; }
+
+qmc_status qmc_matrices_columns(const qmc_matrices* m, uint32_t* out)
+{
+    return guard([&] {
+        if (!m)
+            fail(QMC_INVALID_ARGUMENT, "matrices handle is null");
+        std::memcpy(out, m->columns.data(), m->columns.size() * 4);
+    });
+}
+
+void qmc_matrices_destroy(qmc_matrices* m) { delete m; }
+
+// ----------------------------------------------------------------- fills
+
+static void sobol_fill_impl(qmc_matrices* m, uint64_t first, uint64_t n, uint32_t dims,
+                            qmc_sobol_scramble sc, const uint32_t* words, qmc_output kind,
+                            void* out, cudaStream_t s)
+{
+    if (!m)
+        fail(QMC_INVALID_ARGUMENT, "matrices handle is null");
+    if (n == 0 || dims == 0)
+        return;
+    if (first >= (1ull << 52) || n > (1ull << 52) - first)
+        fail(QMC_INVALID_ARGUMENT, "sobol_component: index must be below 2^52");
+    if (dims > m->dims)
+        fail(QMC_OUT_OF_RANGE, "sobol_component: dimension beyond the matrix set");
+    if (sc != QMC_SOBOL_NONE && sc != QMC_SOBOL_XOR && sc != QMC_SOBOL_OWEN)
+        fail(QMC_INVALID_ARGUMENT, "sobol_fill: unknown scramble kind");
+    const auto& dev = m->on_device();
+    // the fast path reads dims-strided columns: rebuild for a dims prefix
+    DevPtr sub, sub_rev;
+    const uint32_t* colsT = static_cast<const uint32_t*>(dev.colsT.get());
+    const uint32_t* colsT_rev = static_cast<const uint32_t*>(dev.colsT_rev.get());
+    if (dims != m->dims) {
+        std::vector<uint32_t> t(52 * static_cast<size_t>(std::max<uint32_t>(dims, 4)), 0u),
+            tr(t.size(), 0u);
+        for (uint32_t j = 0; j < dims; ++j)
+            for (uint32_t k = 0; k < 52; ++k) {
+                t[k * static_cast<size_t>(dims) + j] = m->columns[j * 52 + k];
+                tr[k * static_cast<size_t>(dims) + j] = brev_host(m->columns[j * 52 + k]);
+            }
+        sub = dev_upload(t.data(), t.size() * 4);
+        sub_rev = dev_upload(tr.data(), tr.size() * 4);
+        colsT = static_cast<const uint32_t*>(sub.get());
+        colsT_rev = static_cast<const uint32_t*>(sub_rev.get());
+    }
+    CallArgs args(s);
+    size_t woff = SIZE_MAX;
+    if (words && sc != QMC_SOBOL_NONE) {
+        std::vector<uint32_t> w(std::max<uint32_t>(dims, 4), 0u);
+        std::memcpy(w.data(), words, dims * 4);
+        woff = args.add(w.data(), w.size() * 4);
+    }
+    args.upload();
+    const uint32_t* wdev = woff == SIZE_MAX ? nullptr : args.at<uint32_t>(woff);
+    const int mode = sc == QMC_SOBOL_OWEN ? 2 : 0;
+    const bool u32 = kind == QMC_OUT_U32;
+    place_fill(out, first, n, dims, s, [&](const FillRange& r, cudaStream_t st) {
+        return launch_sobol(colsT, colsT_rev, wdev, dims, mode, u32, r, st);
+    });
+    if (sub) // the temporary prefix tables must outlive the kernels
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+}
+
+qmc_status qmc_sobol_fill(const qmc_matrices* m, uint64_t first_index, uint64_t n, uint32_t dims,
+                          qmc_sobol_scramble scramble, const uint32_t* words, qmc_output kind,
+                          void* out, qmc_stream stream)
+{
+    return guard([&] {
+        sobol_fill_impl(const_cast<qmc_matrices*>(m), first_index, n, dims, scramble, words, kind,
+                        out, as_stream(stream));
+    });
+}
+
+static void halton_fill_impl(uint64_t first, uint64_t n, uint32_t dims, uint32_t first_prime,
+                             qmc_radical_scramble sc, const uint32_t* factors, qmc_output kind,
+                             void* out, cudaStream_t s)
+{
+    if (sc != QMC_RADICAL_PLAIN && sc != QMC_RADICAL_LINEAR && sc != QMC_RADICAL_FAURE)
+        fail(QMC_INVALID_ARGUMENT, "halton: unknown scramble kind");
+    const bool u32 = kind == QMC_OUT_U32;
+    if (dims == 1 && first_prime == 0) { // van der Corput: every scramble is the identity
+        if (sc == QMC_RADICAL_LINEAR && factors && factors[0] != 1)
+            fail(QMC_INVALID_ARGUMENT, "radical_inverse_linscramble: factor must be in [1, base)");
+        place_fill(out, first, n, 1, s, [&](const FillRange& r, cudaStream_t st) {
+            return launch_vdc(u32, r, st);
+        });
+        return;
+    }
+    std::vector<uint32_t> pool;
+    std::vector<size_t> soff;
+    auto rd = radical_dims(dims, first_prime, sc, factors, pool, soff);
+    if (n == 0 || dims == 0)
+        return;
+    CallArgs pargs(s);
+    pool.push_back(0u); // never empty
+    pargs.add(pool.data(), pool.size() * 4);
+    pargs.upload();
+    const uint32_t* pool_dev = pargs.at<uint32_t>(0);
+    for (size_t j = 0; j < rd.size(); ++j)
+        if (soff[j] != SIZE_MAX)
+            rd[j].sigma = pool_dev + soff[j];
+    CallArgs args(s);
+    const size_t off = args.add(rd.data(), rd.size() * sizeof(RadicalDim));
+    args.upload();
+    const RadicalDim* rdev = args.at<RadicalDim>(off);
+    place_fill(out, first, n, dims, s, [&](const FillRange& r, cudaStream_t st) {
+        return launch_halton(rdev, dims, u32, r, st);
+    });
+}
+
+qmc_status qmc_halton_fill(uint64_t first_index, uint64_t n, uint32_t dims,
+                           qmc_radical_scramble scramble, const uint32_t* factors,
+                           qmc_output kind, void* out, qmc_stream stream)
+{
+    return guard([&] {
+        if (dims > kPrimes)
+            fail(QMC_INVALID_ARGUMENT, "halton_point: dims beyond the prime table");
+        halton_fill_impl(first_index, n, dims, 0, scramble, factors, kind, out,
+                         as_stream(stream));
+    });
+}
+
+qmc_status qmc_radical_inverse_fill(uint64_t first_index, uint64_t n, uint32_t prime_index,
+                                    qmc_radical_scramble scramble, uint32_t factor,
+                                    qmc_output kind, void* out, qmc_stream stream)
+{
+    return guard([&] {
+        prime_at(prime_index); // out_of_range like prime()
+        halton_fill_impl(first_index, n, 1, prime_index, scramble, &factor, kind, out,
+                         as_stream(stream));
+    });
+}
+
+static void lattice_fill_impl(const uint32_t* g, const uint32_t* shifts, uint32_t dims,
+                              uint64_t first, uint64_t n, qmc_output kind, void* out,
+                              cudaStream_t s)
+{
+    if (n == 0 || dims == 0)
+        return;
+    if (!g)
+        fail(QMC_INVALID_ARGUMENT, "generator vector is null");
+    CallArgs args(s);
+    std::vector<uint32_t> gv(std::max<uint32_t>(dims, 4), 0u), sv(gv.size(), 0u);
+    std::memcpy(gv.data(), g, dims * 4);
+    const size_t goff = args.add(gv.data(), gv.size() * 4);
+    size_t soff = SIZE_MAX;
+    if (shifts) {
+        std::memcpy(sv.data(), shifts, dims * 4);
+        soff = args.add(sv.data(), sv.size() * 4);
+    }
+    args.upload();
+    const uint32_t* gd = args.at<uint32_t>(goff);
+    const uint32_t* sd = soff == SIZE_MAX ? nullptr : args.at<uint32_t>(soff);
+    const bool u32 = kind == QMC_OUT_U32;
+    place_fill(out, first, n, dims, s, [&](const FillRange& r, cudaStream_t st) {
+        return launch_lattice(gd, sd, dims, u32, r, st);
+    });
+}
+
+qmc_status qmc_lattice_fill(const uint32_t* g, const uint32_t* shifts, uint32_t dims,
+                            uint64_t first_index, uint64_t n, qmc_output kind, void* out,
+                            qmc_stream stream)
+{
+    return guard([&] {
+        lattice_fill_impl(g, shifts, dims, first_index, n, kind, out, as_stream(stream));
+    });
+}
+
+// ------------------------------------------------------ SampleStream façade
+
+static const char* const kKindNames[] = {"sobol",
+                                         "halton",
+                                         "lattice",
+                                         "halton-hilbert",
+                                         "pixel-shifted-lattice",
+                                         "pixel-random-lattice",
+                                         "image-plane-halton",
+                                         "sobol-xor-table"};
+
+qmc_status qmc_sampler_kind_from_name(const char* name, qmc_sampler_kind* out)
+{
+    return guard([&] {
+        const std::string n = name ? name : "";
+        for (int k = 0; k < 8; ++k)
+            if (n == kKindNames[k]) {
+                *out = static_cast<qmc_sampler_kind>(k);
+                return;
+            }
+        fail(QMC_CONFIG, "unknown sampler: " + n);
+    });
+}
+
+const char* qmc_sampler_kind_name(qmc_sampler_kind kind)
+{
+    return (kind >= 0 && kind < 8) ? kKindNames[kind] : "";
+}
+
+namespace {
+
+void require(bool ok, const char* what)
+{
+    if (!ok)
+        fail(QMC_CONFIG, what);
+}
+
+// white_noise_xor_tables (imageplane.cpp:197-229): std::mt19937 reorder /
+// scramble words on the host; the stored point set (first point_count
+// Sobol' points, XOR-scrambled per dimension when seed != 0) is generated on
+// the device by the Sobol' fill.
+struct XorTablesDev {
+    uint32_t dims = 0, point_count = 0;
+    DevPtr reorder, scramble, points;
+};
+
+XorTablesDev white_noise_tables(uint32_t dims, uint32_t point_count, uint32_t seed,
+                                cudaStream_t s)
+{
+    if (dims == 0)
+        fail(QMC_CONFIG, "white_noise_xor_tables: dims must be >= 1");
+    if (point_count == 0 || (point_count & (point_count - 1)) != 0)
+        fail(QMC_CONFIG, "white_noise_xor_tables: point count must be a power of two");
+    std::mt19937 rng(seed);
+    std::vector<uint32_t> dim_scramble(dims, 0u);
+    if (seed != 0)
+        for (auto& w : dim_scramble)
+            w = rng();
+    constexpr size_t tile = 128 * 128;
+    std::vector<uint32_t> reorder(tile), scramble(tile * dims);
+    for (auto& v : reorder)
+        v = rng() & (point_count - 1);
+    for (auto& v : scramble)
+        v = rng();
+    XorTablesDev t;
+    t.dims = dims;
+    t.point_count = point_count;
+    t.reorder = dev_upload(reorder.data(), reorder.size() * 4);
+    t.scramble = dev_upload(scramble.data(), scramble.size() * 4);
+    void* pts = nullptr;
+    cuda_ok(cudaMalloc(&pts, static_cast<size_t>(point_count) * dims * 4 + 16), "cudaMalloc");
+    t.points.reset(pts);
+    std::unique_ptr<qmc_matrices> m(new_matrices(build_columns(builtin_rows(), dims), dims));
+    sobol_fill_impl(m.get(), 0, point_count, dims, seed ? QMC_SOBOL_XOR : QMC_SOBOL_NONE,
+                    dim_scramble.data(), QMC_OUT_U32, pts, s);
+    cuda_ok(cudaStreamSynchronize(s), "sync");
+    return t;
+}
+
+} // namespace
+
+qmc_status qmc_stream_fill(qmc_sampler_kind kind, const qmc_stream_params* p,
+                           uint64_t first_index, uint64_t n, qmc_output out_kind, void* out,
+                           qmc_stream stream)
+{
+    return guard([&] {
+        if (!p)
+            fail(QMC_INVALID_ARGUMENT, "stream params are null");
+        const cudaStream_t s = as_stream(stream);
+        require(p->dims >= 1, "make_stream: dims must be >= 1");
+        const uint32_t dims = p->dims;
+        auto halton_scramble = [&]() -> qmc_radical_scramble {
+            if (p->halton_scramble > 2)
+                fail(QMC_CONFIG, "make_stream: scramble must be plain, faure, or linear");
+            if (p->halton_scramble == QMC_RADICAL_LINEAR && p->linear_factors)
+                require(p->linear_factors_len >= dims,
+                        "make_stream: linear factor list shorter than dims");
+            return static_cast<qmc_radical_scramble>(p->halton_scramble);
+        };
+        auto lattice_vector = [&]() {
+            require(p->generator && p->generator_dims > 0, "make_stream: generator vector required");
+            for (uint32_t j = 0; j < p->generator_dims; ++j)
+                require(p->generator[j] & 1u, "make_stream: generator components must be odd");
+            require(dims <= p->generator_dims, "make_stream: dims beyond the generator vector");
+        };
+        auto validate_pixel = [&]() {
+            require(p->order >= 1 && p->order <= 31, "make_stream: pixel order must be in [1, 31]");
+            require(p->px < (1u << p->order) && p->py < (1u << p->order),
+                    "make_stream: pixel outside the 2^order grid");
+        };
+        const bool u32 = out_kind == QMC_OUT_U32;
+        switch (kind) {
+        case QMC_KIND_SOBOL: {
+            std::unique_ptr<qmc_matrices> own;
+            qmc_matrices* m = const_cast<qmc_matrices*>(p->matrices);
+            if (!m) {
+                own.reset(new_matrices(build_columns(builtin_rows(), dims), dims));
+                m = own.get();
+            }
+            require(dims <= m->dims, "make_stream: dims beyond the generator matrices");
+            if (p->sobol_scrambles)
+                require(p->sobol_scrambles_len >= dims, "make_stream: scramble list shorter than dims");
+            sobol_fill_impl(m, first_index, n, dims,
+                            p->sobol_scrambles ? QMC_SOBOL_XOR : QMC_SOBOL_NONE, p->sobol_scrambles,
+                            out_kind, out, s);
+            if (own)
+                cuda_ok(cudaStreamSynchronize(s), "sync");
+            return;
+        }
+        case QMC_KIND_HALTON: {
+            require(dims <= kPrimes, "make_stream: dims beyond the prime table");
+            const auto sc = halton_scramble();
+            // SampleStream::sample casts the index to 32 bits (wraps, like the kernel)
+            halton_fill_impl(first_index, n, dims, 0, sc, p->linear_factors, out_kind, out, s);
+            return;
+        }
+        case QMC_KIND_LATTICE:
+            lattice_vector();
+            lattice_fill_impl(p->generator, nullptr, dims, first_index, n, out_kind, out, s);
+            return;
+        default:
+            break;
+        }
+        if (kind < 0 || kind > 7)
+            fail(QMC_CONFIG, "unknown sampler kind");
+
+        PixelStreamParams q{};
+        q.kind = kind;
+        q.dims = dims;
+        q.px = p->px;
+        q.py = p->py;
+        q.order = p->order;
+        q.spp = p->spp;
+        q.width = p->width;
+        q.height = p->height;
+        CallArgs args(s);
+        std::vector<uint32_t> pool;
+        std::vector<size_t> soff;
+        std::vector<RadicalDim> rd;
+        size_t goff = SIZE_MAX;
+        XorTablesDev xt;
+        switch (kind) {
+        case QMC_KIND_HALTON_HILBERT: {
+            require(p->spp >= 1, "make_stream: spp must be >= 1");
+            validate_pixel();
+            require(dims <= kPrimes, "halton_point: dims beyond the prime table");
+            rd = radical_dims(dims, 0, halton_scramble(), p->linear_factors, pool, soff);
+            if (first_index >= p->spp || n > p->spp - first_index)
+                fail(QMC_OUT_OF_RANGE, "SampleStream: sample index beyond the pixel block");
+            break;
+        }
+        case QMC_KIND_PIXEL_SHIFTED_LATTICE:
+            validate_pixel();
+            lattice_vector();
+            goff = args.add(p->generator, dims * 4);
+            break;
+        case QMC_KIND_PIXEL_RANDOM_LATTICE:
+            break;
+        case QMC_KIND_IMAGE_PLANE_HALTON: {
+            require(p->width >= 1 && p->height >= 1,
+                    "make_stream: image size required for image-plane halton");
+            require(p->px < p->width && p->py < p->height, "make_stream: pixel outside the image");
+            require(dims <= kPrimes, "make_stream: dims beyond the prime table");
+            const HaltonEnum e = halton_enum(p->width, p->height);
+            if (p->linear_factors)
+                require(p->linear_factors_len >= dims,
+                        "make_stream: linear factor list shorter than dims");
+            rd = radical_dims(dims, 0, QMC_RADICAL_LINEAR, p->linear_factors, pool, soff);
+            q.scale_x = e.sx;
+            q.scale_y = e.sy;
+            q.exp_x = e.ex;
+            q.exp_y = e.ey;
+            q.stride = e.stride;
+            q.crt_x = e.crt_x;
+            q.crt_y = e.crt_y;
+            break;
+        }
+        case QMC_KIND_SOBOL_XOR_TABLE: {
+            const uint32_t pc = p->xor_point_count;
+            xt = white_noise_tables(dims, pc, p->xor_seed, s);
+            require(dims <= xt.dims, "make_stream: dims beyond the stored point set");
+            if (first_index >= pc || n > pc - first_index)
+                fail(QMC_OUT_OF_RANGE, "xor_table_sample: index beyond the stored point set");
+            q.xor_reorder = static_cast<const uint32_t*>(xt.reorder.get());
+            q.xor_scramble = static_cast<const uint32_t*>(xt.scramble.get());
+            q.xor_points = static_cast<const uint32_t*>(xt.points.get());
+            q.xor_point_count = pc;
+            q.xor_dims = xt.dims;
+            break;
+        }
+        default:
+            break;
+        }
+        if (n == 0)
+            return;
+        // radical tables: permutation pool first (pointers patched), then dims
+        if (!rd.empty()) {
+            CallArgs pargs(s);
+            pool.push_back(0u); // never empty
+            pargs.add(pool.data(), pool.size() * 4);
+            pargs.upload();
+            const uint32_t* pool_dev = pargs.at<uint32_t>(0);
+            for (size_t j = 0; j < rd.size(); ++j)
+                if (soff[j] != SIZE_MAX)
+                    rd[j].sigma = pool_dev + soff[j];
+            const size_t roff = args.add(rd.data(), rd.size() * sizeof(RadicalDim));
+            args.upload();
+            q.radical_dims = args.at<RadicalDim>(roff);
+            place_fill(out, first_index, n, dims, s, [&](const FillRange& r, cudaStream_t st) {
+                return launch_pixel_stream(q, u32, r, st);
+            });
+            cuda_ok(cudaStreamSynchronize(s), "sync");
+            return;
+        }
+        args.upload();
+        if (goff != SIZE_MAX)
+            q.generator = args.at<uint32_t>(goff);
+        place_fill(out, first_index, n, dims, s, [&](const FillRange& r, cudaStream_t st) {
+            return launch_pixel_stream(q, u32, r, st);
+        });
+        cuda_ok(cudaStreamSynchronize(s), "sync"); // tables owned by this call
+    });
+}
+
+// ------------------------------------------------------------------ render
+
+qmc_status qmc_render(const qmc_render_job* job, uint32_t row_begin, uint32_t row_end, float* out,
+                      qmc_stream stream)
+{
+    return guard([&] {
+        if (!job)
+            fail(QMC_INVALID_ARGUMENT, "render job is null");
+        const cudaStream_t s = as_stream(stream);
+        if (job->width == 0 || job->height == 0)
+            fail(QMC_CONFIG, "render: image must be at least 1x1");
+        if (job->spp == 0)
+            fail(QMC_CONFIG, "render: spp must be >= 1");
+        if (job->kind < 0 || job->kind > 7)
+            fail(QMC_CONFIG, "unknown sampler kind");
+        if (job->accum != QMC_ACCUM_KAHAN && job->accum != QMC_ACCUM_INT)
+            fail(QMC_CONFIG, "accumulation mode must be 'kahan' or 'int'");
+        if (row_begin > row_end || row_end > job->height)
+            fail(QMC_OUT_OF_RANGE, "render: row band outside the image");
+
+        RenderParams p{};
+        p.width = job->width;
+        p.height = job->height;
+        p.spp = job->spp;
+        p.order = hilbert_order(job->width, job->height);
+        p.row_begin = row_begin;
+        p.row_end = row_end;
+        p.inv_w = 1.0 / job->width;
+        p.inv_h = 1.0 / job->height;
+        std::vector<uint32_t> g = job->generator && job->generator_dims
+                                      ? std::vector<uint32_t>(job->generator,
+                                                              job->generator + job->generator_dims)
+                                      : lfsr(job->seed ? job->seed : 0xace1u, 2);
+        const uint32_t kind = job->kind;
+        if (kind == QMC_KIND_HALTON_HILBERT || kind == QMC_KIND_PIXEL_SHIFTED_LATTICE)
+            require(p.order >= 1 && p.order <= 31, "make_stream: pixel order must be in [1, 31]");
+        if (kind == QMC_KIND_LATTICE || kind == QMC_KIND_PIXEL_SHIFTED_LATTICE) {
+            for (uint32_t v : g)
+                require(v & 1u, "make_stream: generator components must be odd");
+            require(g.size() >= 2, "make_stream: dims beyond the generator vector");
+        }
+        if (g.size() < 2)
+            g.resize(2, 1u);
+        p.g0 = g[0];
+        p.g1 = g[1];
+        if (kind == QMC_KIND_SOBOL && job->seed != 0) {
+            p.scr0 = pixel_hash_host(0, job->seed, 0);
+            p.scr1 = pixel_hash_host(1, job->seed, 0);
+        }
+        std::vector<uint32_t> cols2(104, 0u);
+        if (job->matrices) {
+            require(job->matrices->dims >= 2, "make_stream: dims beyond the generator matrices");
+            std::memcpy(cols2.data(), job->matrices->columns.data(), 104 * 4);
+        } else {
+            cols2 = build_columns(builtin_rows(), 2);
+        }
+        HaltonEnum he;
+        if (kind == QMC_KIND_IMAGE_PLANE_HALTON) {
+            he = halton_enum(job->width, job->height);
+            p.scale_x = he.sx;
+            p.scale_y = he.sy;
+            p.exp_x = he.ex;
+            p.exp_y = he.ey;
+            p.stride = he.stride;
+            p.crt_x = he.crt_x;
+            p.crt_y = he.crt_y;
+        }
+        XorTablesDev xt;
+        if (kind == QMC_KIND_SOBOL_XOR_TABLE) {
+            uint32_t pc = 1;
+            while (pc < job->spp)
+                pc <<= 1;
+            xt = white_noise_tables(2, pc, job->seed, s);
+            p.xor_reorder = static_cast<const uint32_t*>(xt.reorder.get());
+            p.xor_scramble = static_cast<const uint32_t*>(xt.scramble.get());
+            p.xor_points = static_cast<const uint32_t*>(xt.points.get());
+            p.xor_point_count = pc;
+        }
+        CallArgs args(s);
+        const size_t coff = args.add(cols2.data(), cols2.size() * 4);
+        args.upload();
+        p.cols2 = args.at<uint32_t>(coff);
+        const uint64_t npix = static_cast<uint64_t>(row_end - row_begin) * job->width;
+        if (npix == 0)
+            return;
+        if (!out)
+            fail(QMC_INVALID_ARGUMENT, "output pointer is null");
+        if (is_device_pointer(out)) {
+            cuda_ok(launch_render(p, kind, job->accum, out, s), "launch_render");
+            if (kind == QMC_KIND_SOBOL_XOR_TABLE)
+                cuda_ok(cudaStreamSynchronize(s), "sync");
+            return;
+        }
+        float* d = nullptr;
+        cuda_ok(cudaMallocAsync(&d, npix * 4, s), "cudaMallocAsync");
+        cuda_ok(launch_render(p, kind, job->accum, d, s), "launch_render");
+        cuda_ok(cudaMemcpyAsync(out, d, npix * 4, cudaMemcpyDeviceToHost, s), "D2H");
+        cudaFreeAsync(d, s);
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+    });
+}
+
+qmc_status qmc_scene_value(const double* xy, double* out, uint64_t n, qmc_stream stream)
+{
+    return guard([&] {
+        if (n == 0)
+            return;
+        const cudaStream_t s = as_stream(stream);
+        if (is_device_pointer(xy) && is_device_pointer(out)) {
+            cuda_ok(launch_scene_value(xy, out, n, s), "launch_scene_value");
+            return;
+        }
+        double *dxy = nullptr, *dout = nullptr;
+        cuda_ok(cudaMallocAsync(&dxy, n * 16, s), "cudaMallocAsync");
+        cuda_ok(cudaMallocAsync(&dout, n * 8, s), "cudaMallocAsync");
+        cuda_ok(cudaMemcpyAsync(dxy, xy, n * 16, cudaMemcpyDefault, s), "H2D");
+        cuda_ok(launch_scene_value(dxy, dout, n, s), "launch_scene_value");
+        cuda_ok(cudaMemcpyAsync(out, dout, n * 8, cudaMemcpyDefault, s), "D2H");
+        cudaFreeAsync(dxy, s);
+        cudaFreeAsync(dout, s);
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+    });
+}
+
+} // extern "C"

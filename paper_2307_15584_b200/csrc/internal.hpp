@@ -1,0 +1,99 @@
+// internal.hpp — host<->kernel interface of libqmcgpu (not part of the ABI).
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace qmcgpu {
+
+// Exact division by a runtime divisor d >= 2 (see div32 in device.cuh).
+struct Div32 {
+    uint32_t m, s;
+};
+
+inline Div32 make_div32(uint32_t d)
+{
+    uint32_t l = 0;
+    while (l < 32 && (1ull << l) < d)
+        ++l; // l = ceil(log2 d)
+    const uint64_t m = ((1ull << 32) * ((1ull << l) - d)) / d + 1;
+    return Div32{static_cast<uint32_t>(m), l - 1};
+}
+
+// Per-launch placement of a fill: points [first, first + n) of the
+// sequence land at out[(i - first) * dims + j] (device pointer).
+struct FillRange {
+    uint64_t first;
+    uint64_t n;
+    void* out;
+};
+
+// Render parameters resolved on the host (render.cpp:83-106 defaults).
+struct RenderParams {
+    uint32_t width, height, spp, order;
+    uint32_t row_begin, row_end;
+    double inv_w, inv_h;
+    uint32_t g0, g1;          // lattice kinds
+    uint32_t scr0, scr1;      // sobol scrambles
+    // image-plane Halton (imageplane.cpp:80-106)
+    uint32_t scale_x, scale_y, exp_x, exp_y;
+    uint64_t stride, crt_x, crt_y;
+    const uint32_t* cols2;    // device, [2][52] MSB-aligned columns (sobol)
+    const uint32_t* xor_reorder;  // device, 128*128 (sobol_xor_table)
+    const uint32_t* xor_scramble; // device, 128*128*2
+    const uint32_t* xor_points;   // device, point_count*2
+    uint32_t xor_point_count;
+};
+
+// Per-stream (one pixel context) parameters for qmc_stream_fill kinds that
+// depend on the pixel.
+struct PixelStreamParams {
+    uint32_t kind, dims;
+    uint32_t px, py, order, spp;
+    uint32_t width, height;
+    const uint32_t* generator;   // device (lattice kinds)
+    const void* radical_dims;    // device RadicalDim[dims] (halton kinds)
+    uint32_t scale_x, scale_y, exp_x, exp_y;
+    uint64_t stride, crt_x, crt_y;
+    const uint32_t* xor_reorder;
+    const uint32_t* xor_scramble;
+    const uint32_t* xor_points;
+    uint32_t xor_point_count, xor_dims;
+};
+
+// ------------------------------------------------------------ launchers
+// All launchers write DEVICE memory and are asynchronous on `s`.
+cudaError_t launch_map(const uint32_t* in, float* out, uint64_t n, cudaStream_t s);
+cudaError_t launch_map_selfcheck(unsigned long long* dev_count, cudaStream_t s);
+
+// colsT: device [52][dims] columns (k-major); words: device [dims] or null.
+// mode 0 plain/xor (words = xor words), 2 owen (colsT bit-reversed, words =
+// seeds). out_u32: write the integer stage instead of floats.
+cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const uint32_t* words,
+                         uint32_t dims, int mode, bool out_u32, const FillRange& r,
+                         cudaStream_t s);
+
+// g, shifts: device [dims] (shifts may be null).
+cudaError_t launch_lattice(const uint32_t* g, const uint32_t* shifts, uint32_t dims,
+                           bool out_u32, const FillRange& r, cudaStream_t s);
+
+// dims == 1, prime 2 (van der Corput, config C1).
+cudaError_t launch_vdc(bool out_u32, const FillRange& r, cudaStream_t s);
+
+// rd: device RadicalDim[dims].
+cudaError_t launch_halton(const void* rd, uint32_t dims, bool out_u32, const FillRange& r,
+                          cudaStream_t s);
+
+cudaError_t launch_pixel_stream(const PixelStreamParams& p, bool out_u32, const FillRange& r,
+                                cudaStream_t s);
+
+cudaError_t launch_render(const RenderParams& p, uint32_t kind, uint32_t accum, float* out,
+                          cudaStream_t s);
+
+cudaError_t launch_scene_value(const double* xy, double* out, uint64_t n, cudaStream_t s);
+
+// Number of SMs of the current device (cached).
+int sm_count();
+
+} // namespace qmcgpu

@@ -1,0 +1,301 @@
+// kernels_render.cu — per-pixel sample enumeration and the fused per-pixel
+// integro-approximation (config C5) for sm_100a.
+//
+// render: one thread owns one pixel of the band, derives its pixel state
+// (Hilbert index + phi_3 shift, Halton CRT offset, hashed generator) on the
+// device, and walks its spp samples in the reference order (render.cpp:
+// 58-79): sample -> scene_value in FP64 -> Neumaier (or int64 fixed-point)
+// accumulation -> one fp32 store. Points are never materialised; the only
+// HBM traffic is the 4 B per pixel image write. The per-pixel sequential sum
+// keeps the reference's summation order, so the Kahan path only differs from
+// the CPU where device sin() differs from libm's.
+#include <cstdint>
+
+#include "device.cuh"
+#include "internal.hpp"
+
+namespace qmcgpu {
+
+namespace {
+
+constexpr int kBlock = 128;
+
+// Per-pixel state of the SampleStream kinds (imageplane.cpp:366-405).
+struct PixelState {
+    uint32_t shift;     // pixel_shifted_lattice
+    uint32_t g0, g1;    // pixel_random_lattice (hash | 1)
+    uint64_t block;     // halton_hilbert: hilbert_index * spp
+    uint32_t ipx0, ipy0; // image_plane_halton: (uint32)(offset >> a), (uint32)(offset / 3^b)
+    uint32_t cell;      // sobol_xor_table: tile cell
+};
+
+__device__ __forceinline__ uint64_t digit_reverse(uint64_t v, uint32_t base, uint32_t digits)
+{
+    uint64_t r = 0;
+    for (uint32_t k = 0; k < digits; ++k) {
+        r = r * base + v % base;
+        v /= base;
+    }
+    return r;
+}
+
+// imageplane.cpp:100-106: CRT combination of the reversed digits
+__device__ __forceinline__ uint64_t halton_offset(uint32_t px, uint32_t py, uint32_t exp_x,
+                                                  uint32_t exp_y, uint64_t stride, uint64_t crt_x,
+                                                  uint64_t crt_y)
+{
+    // digit_reverse(px, 2, exp_x) = the exp_x low bits of px mirrored
+    const uint64_t r2 = exp_x == 0 ? 0 : __brevll(px) >> (64 - exp_x);
+    const uint64_t r3 = digit_reverse(py, 3, exp_y);
+    return (r2 * crt_x % stride + r3 * crt_y % stride) % stride;
+}
+
+template <uint32_t KIND>
+__device__ __forceinline__ PixelState pixel_state(uint32_t px, uint32_t py, const RenderParams& p)
+{
+    PixelState s{};
+    if (KIND == 4) // pixel_shifted_lattice: phi_3(hilbert_index), imageplane.cpp:16-21
+        s.shift = phi3_fixed(static_cast<uint32_t>(hilbert_index(px, py, p.order)));
+    if (KIND == 5) { // pixel_random_lattice, lattice.hpp:51-56
+        s.g0 = pixel_hash(0, px, py) | 1u;
+        s.g1 = pixel_hash(1, px, py) | 1u;
+    }
+    if (KIND == 3) // halton_hilbert, imageplane.cpp:373-379
+        s.block = hilbert_index(px, py, p.order) * p.spp;
+    if (KIND == 6) {
+        const uint64_t off =
+            halton_offset(px, py, p.exp_x, p.exp_y, p.stride, p.crt_x, p.crt_y);
+        s.ipx0 = static_cast<uint32_t>(off >> p.exp_x);
+        s.ipy0 = static_cast<uint32_t>(off / p.scale_y);
+    }
+    if (KIND == 7)
+        s.cell = (px % 128u) + (py % 128u) * 128u;
+    return s;
+}
+
+__device__ __forceinline__ uint32_t rad2(uint32_t i) { return brev32(i & 0x7fffffffu); }
+
+// Component j in {0,1} of sample i (SampleStream::sample, imageplane.cpp:
+// 427-461) at the integer stage, for the render's 2-dim streams.
+template <uint32_t KIND>
+__device__ __forceinline__ void sample2(uint32_t i, const PixelState& s, const RenderParams& p,
+                                        uint32_t& x0, uint32_t& x1, uint32_t& sob0,
+                                        uint32_t& sob1)
+{
+    if (KIND == 0) { // sobol: natural-order incremental, caller advances
+        x0 = sob0;
+        x1 = sob1;
+    } else if (KIND == 1) { // halton (plain)
+        x0 = rad2(i);
+        x1 = phi3_fixed(i);
+    } else if (KIND == 2) { // lattice
+        const uint32_t b = brev32(i);
+        x0 = b * p.g0;
+        x1 = b * p.g1;
+    } else if (KIND == 3) { // halton_hilbert
+        const uint32_t gi = static_cast<uint32_t>(s.block + i);
+        x0 = rad2(gi);
+        x1 = phi3_fixed(gi);
+    } else if (KIND == 4) { // pixel_shifted_lattice (Eq. 3)
+        const uint32_t b = brev32(i) + s.shift;
+        x0 = b * p.g0;
+        x1 = b * p.g1;
+    } else if (KIND == 5) { // pixel_random_lattice (backwards)
+        const uint32_t b = brev32(~i);
+        x0 = b * s.g0;
+        x1 = b * s.g1;
+    } else if (KIND == 6) { // image_plane_halton: (offset + i*stride)>>a, / 3^b
+        x0 = rad2(s.ipx0 + i * p.scale_y);
+        x1 = phi3_fixed(s.ipy0 + i * p.scale_x);
+    } else { // sobol_xor_table, imageplane.cpp:231-243
+        const uint32_t k = i ^ __ldg(p.xor_reorder + s.cell);
+        x0 = __ldg(p.xor_points + 2u * k) ^ __ldg(p.xor_scramble + 2u * s.cell);
+        x1 = __ldg(p.xor_points + 2u * k + 1) ^ __ldg(p.xor_scramble + 2u * s.cell + 1);
+    }
+}
+
+template <uint32_t KIND, uint32_t ACCUM>
+__global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __restrict__ out)
+{
+    const uint32_t band = p.row_end - p.row_begin;
+    const uint64_t npix = static_cast<uint64_t>(band) * p.width;
+    const uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= npix)
+        return;
+    const uint32_t py = p.row_begin + static_cast<uint32_t>(q / p.width);
+    const uint32_t px = static_cast<uint32_t>(q % p.width);
+    const PixelState s = pixel_state<KIND>(px, py, p);
+
+    uint32_t sob0 = p.scr0, sob1 = p.scr1; // sobol index 0 value
+    double sum = 0.0, comp = 0.0;
+    long long isum = 0;
+    const double fx = static_cast<double>(px), fy = static_cast<double>(py);
+    for (uint32_t i = 0; i < p.spp; ++i) {
+        uint32_t a, b;
+        sample2<KIND>(i, s, p, a, b, sob0, sob1);
+        const double u = static_cast<double>(map_u32(a));
+        const double v = static_cast<double>(map_u32(b));
+        const double f = scene_value(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
+                                     __dmul_rn(__dadd_rn(fy, v), p.inv_h));
+        if (ACCUM == 0)
+            neumaier_add(sum, comp, f);
+        else
+            isum += llround(__dmul_rn(f, 4294967296.0));
+        if (KIND == 0) { // x(i+1) = x(i) ^ (C[0] ^ ... ^ C[ctz(i+1)])
+            const uint32_t c = __ffs(static_cast<int>(i + 1)) - 1;
+            for (uint32_t k = 0; k <= c; ++k) {
+                sob0 ^= __ldg(p.cols2 + k);
+                sob1 ^= __ldg(p.cols2 + 52 + k);
+            }
+        }
+    }
+    float r;
+    if (ACCUM == 0)
+        r = __double2float_rn(__ddiv_rn(__dadd_rn(sum, comp), static_cast<double>(p.spp)));
+    else
+        r = __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(isum), 4294967296.0),
+                                        static_cast<double>(p.spp)));
+    out[q] = r;
+}
+
+// --------------------------------------------- stream fill of pixel kinds
+
+template <uint32_t KIND, bool U32OUT>
+__global__ void __launch_bounds__(256)
+    k_pixel_stream(PixelStreamParams p, Div32 div_dims, uint64_t first, uint32_t elems,
+                   uint32_t* __restrict__ out)
+{
+    // per-pixel state, recomputed per thread (a few dozen integer ops)
+    uint32_t shift = 0, ipx0 = 0, ipy0 = 0, cell = 0;
+    uint64_t block = 0, off = 0;
+    if (KIND == 4)
+        shift = phi3_fixed(static_cast<uint32_t>(hilbert_index(p.px, p.py, p.order)));
+    if (KIND == 3)
+        block = hilbert_index(p.px, p.py, p.order) * p.spp;
+    if (KIND == 6) {
+        off = halton_offset(p.px, p.py, p.exp_x, p.exp_y, p.stride, p.crt_x, p.crt_y);
+        ipx0 = static_cast<uint32_t>(off >> p.exp_x);
+        ipy0 = static_cast<uint32_t>(off / p.scale_y);
+    }
+    if (KIND == 7)
+        cell = (p.px % 128u) + (p.py % 128u) * 128u;
+    const RadicalDim* rd = static_cast<const RadicalDim*>(p.radical_dims);
+
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < elems; e += stride) {
+        const uint32_t pt = p.dims == 1 ? e : div32(e, div_dims);
+        const uint32_t j = e - pt * p.dims;
+        const uint64_t idx = first + pt;
+        const uint32_t i = static_cast<uint32_t>(idx);
+        uint32_t x;
+        if (KIND == 3) {
+            x = radical_fixed(static_cast<uint32_t>(block + idx), rd[j]);
+        } else if (KIND == 4) {
+            x = (brev32(i) + shift) * __ldg(p.generator + j);
+        } else if (KIND == 5) {
+            x = brev32(~i) * (pixel_hash(j, p.px, p.py) | 1u);
+        } else if (KIND == 6) { // imageplane.cpp:448-456
+            if (j == 0)
+                x = rad2(ipx0 + i * p.scale_y);
+            else if (j == 1)
+                x = phi3_fixed(ipy0 + i * p.scale_x);
+            else
+                x = radical_fixed(static_cast<uint32_t>(off + idx * p.stride), rd[j]);
+        } else { // KIND == 7
+            const uint32_t k = i ^ __ldg(p.xor_reorder + cell);
+            x = __ldg(p.xor_points + static_cast<uint64_t>(k) * p.xor_dims + j) ^
+                __ldg(p.xor_scramble + cell * p.xor_dims + j);
+        }
+        out[e] = U32OUT ? x : map_bits(x);
+    }
+}
+
+__global__ void k_scene_value(const double* __restrict__ xy, double* __restrict__ out, uint64_t n)
+{
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+         k += stride)
+        out[k] = scene_value(xy[2 * k], xy[2 * k + 1]);
+}
+
+template <uint32_t KIND>
+cudaError_t render_kind(const RenderParams& p, uint32_t accum, float* out, cudaStream_t s)
+{
+    const uint64_t npix = static_cast<uint64_t>(p.row_end - p.row_begin) * p.width;
+    const unsigned grid = static_cast<unsigned>((npix + kBlock - 1) / kBlock);
+    if (accum == 0)
+        k_render<KIND, 0><<<grid, kBlock, 0, s>>>(p, out);
+    else
+        k_render<KIND, 1><<<grid, kBlock, 0, s>>>(p, out);
+    return cudaGetLastError();
+}
+
+template <uint32_t KIND>
+cudaError_t pixel_stream_kind(const PixelStreamParams& p, bool u32, const FillRange& r,
+                              cudaStream_t s)
+{
+    const Div32 d = p.dims >= 2 ? make_div32(p.dims) : Div32{0, 0};
+    const uint64_t max_pts = (1ull << 30) / p.dims;
+    for (uint64_t done = 0; done < r.n; done += max_pts) {
+        const uint64_t pts = r.n - done < max_pts ? r.n - done : max_pts;
+        const uint32_t elems = static_cast<uint32_t>(pts * p.dims);
+        uint64_t want = (elems + 255) / 256;
+        const uint64_t cap = static_cast<uint64_t>(sm_count()) * 8;
+        const unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
+        uint32_t* o = static_cast<uint32_t*>(r.out) + done * p.dims;
+        if (u32)
+            k_pixel_stream<KIND, true><<<grid, 256, 0, s>>>(p, d, r.first + done, elems, o);
+        else
+            k_pixel_stream<KIND, false><<<grid, 256, 0, s>>>(p, d, r.first + done, elems, o);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess)
+            return e;
+    }
+    return cudaSuccess;
+}
+
+} // namespace
+
+cudaError_t launch_render(const RenderParams& p, uint32_t kind, uint32_t accum, float* out,
+                          cudaStream_t s)
+{
+    if (p.row_end <= p.row_begin || p.width == 0)
+        return cudaSuccess;
+    switch (kind) {
+    case 0: return render_kind<0>(p, accum, out, s);
+    case 1: return render_kind<1>(p, accum, out, s);
+    case 2: return render_kind<2>(p, accum, out, s);
+    case 3: return render_kind<3>(p, accum, out, s);
+    case 4: return render_kind<4>(p, accum, out, s);
+    case 5: return render_kind<5>(p, accum, out, s);
+    case 6: return render_kind<6>(p, accum, out, s);
+    case 7: return render_kind<7>(p, accum, out, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_pixel_stream(const PixelStreamParams& p, bool u32, const FillRange& r,
+                                cudaStream_t s)
+{
+    if (r.n == 0)
+        return cudaSuccess;
+    switch (p.kind) {
+    case 3: return pixel_stream_kind<3>(p, u32, r, s);
+    case 4: return pixel_stream_kind<4>(p, u32, r, s);
+    case 5: return pixel_stream_kind<5>(p, u32, r, s);
+    case 6: return pixel_stream_kind<6>(p, u32, r, s);
+    case 7: return pixel_stream_kind<7>(p, u32, r, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_scene_value(const double* xy, double* out, uint64_t n, cudaStream_t s)
+{
+    if (n == 0)
+        return cudaSuccess;
+    const uint64_t want = (n + 255) / 256, cap = static_cast<uint64_t>(sm_count()) * 8;
+    k_scene_value<<<static_cast<unsigned>(want < cap ? want : cap), 256, 0, s>>>(xy, out, n);
+    return cudaGetLastError();
+}
+
+} // namespace qmcgpu

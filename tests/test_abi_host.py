@@ -1,0 +1,115 @@
+"""CPU-side checks of the product library: it loads without a GPU, exports
+every symbol include/qmcgpu.h declares, and its host-setup functions (tables
+the reference also builds on the host) match the oracle / reference. No
+per-sample compute is called here."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2307_15584_b200 as q
+from oracle import ptr
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_header_symbols():
+    hdr = open(os.path.join(ROOT, "include", "qmcgpu.h")).read()
+    names = sorted(set(re.findall(r"^[A-Za-z_][\w \*]*?\b(qmc_[a-z0-9_]+)\(", hdr, re.M)))
+    assert len(names) >= 29
+    L = q.lib()
+    missing = [n for n in names if not hasattr(L, n)]
+    assert not missing, missing
+    assert L.qmc_abi_version() == 1
+
+
+def test_primes_and_max_powers(golden_arrays):
+    for k in [0, 1, 2, 10, 500, 999]:
+        assert q.prime(k) == golden_arrays["primes"][k]
+        assert q.prime_max_power(k) == golden_arrays["prime_max_powers"][k]
+    with pytest.raises(IndexError):
+        q.prime(1000)
+    assert q.prime_max_power(0) == 1 << 31 and q.prime_max_power(1) == 3486784401
+
+
+def test_faure_and_factors(golden):
+    for b in range(2, 32):
+        assert q.faure_permutation(b) == golden["faure"][str(b)]
+    with pytest.raises(ValueError):
+        q.faure_permutation(1)
+    assert q.default_linear_factors(5) == [1, 2, 4, 6, 10]
+
+
+def test_lfsr_pixel_hash(golden_arrays, golden):
+    assert q.lfsr_generator_vector(0xACE1, 16) == golden_arrays["lfsr_ace1_16"].tolist()
+    with pytest.raises(ValueError):
+        q.lfsr_generator_vector(0, 4)
+    for j, x, y, h in golden["pixel_hash_probes"]:
+        assert q.pixel_hash(j, x, y) == h
+
+
+def test_enumeration_and_partition(golden):
+    for key, rec in golden["halton_enum"].items():
+        w, h = map(int, key.split("x"))
+        for px, py, off in rec["offsets"]:
+            e = q.halton_pixel_enumeration(w, h, px, py)
+            assert e["offset"] == off and e["stride"] == rec["stride"]
+            assert [e["exponent_x"], e["exponent_y"], e["scale_x"], e["scale_y"]] == rec["exps"]
+    with pytest.raises(q.ConfigError):
+        q.halton_pixel_enumeration((1 << 20) + 1, 2)
+    for p, parts, b, rem, mod in golden["partition"]:
+        assert q.partition_by_extra_dimension(p, parts, b) == (rem, mod)
+    with pytest.raises(q.ConfigError):
+        q.partition_by_extra_dimension(0, 6, 2)
+    with pytest.raises(IndexError):
+        q.partition_by_extra_dimension(4, 4, 2)
+    assert q.hilbert_order_for(3840, 2160) == 12
+
+
+def test_matrices(golden_arrays, golden, ref):
+    m = q.GeneratorMatrixSet.builtin(64)
+    np.testing.assert_array_equal(m.columns(), golden_arrays["sobol_columns64"])
+    with pytest.raises(q.ConfigError):
+        q.GeneratorMatrixSet.builtin(65)
+    rows = golden["direction_numbers"]
+    text = "d s a m_i\n" + "\n".join(
+        "%d %d %d %s" % (d, s, a, " ".join(map(str, ms))) for d, s, a, ms in rows[:20]) + "\n"
+    t = q.GeneratorMatrixSet.from_text(text, 21)
+    np.testing.assert_array_equal(t.columns(), golden_arrays["sobol_columns64"][:21])
+    # malformed files: same error class and message as the reference parser
+    for bad in ["d s a\n2 1 0 2\n", "d s a\n3 1 0 1\n", "d s a\n2 1 0 1 1\n",
+                "d s a\n2 2 1 1\n", "d s a\n2 2 1 1 5\n", "d s a\n2 0 0\n"]:
+        with pytest.raises(q.ConfigError) as ei:
+            q.GeneratorMatrixSet.from_text(bad, 2)
+        cols = np.zeros((2, 52), np.uint32)
+        assert ref.ref_build_matrices_text(bad.encode(), 2, ptr(cols)) == 1
+        assert str(ei.value) == ref.ref_last_error().decode()
+
+
+def test_sampler_names():
+    for k, name in enumerate(q.SAMPLER_KINDS):
+        assert q.sampler_kind_from_name(name) == k
+    with pytest.raises(q.ConfigError):
+        q.sampler_kind_from_name("sobol2")
+
+
+def test_div32_magic_host_emulation():
+    """The device's exact division (device.cuh div32 / internal.hpp
+    make_div32), emulated in numpy for every divisor the kernels use."""
+    def make(d):
+        l = 0
+        while (1 << l) < d:
+            l += 1
+        return ((1 << 32) * ((1 << l) - d)) // d + 1, l - 1
+
+    rng = np.random.default_rng(0)
+    n = np.concatenate([rng.integers(0, 1 << 32, 20000, dtype=np.uint64),
+                        np.array([0, 1, 2, 3, (1 << 32) - 1, (1 << 32) - 2, 1 << 31], np.uint64)])
+    ds = [q.prime(k) for k in range(0, 1000, 7)] + [q.prime_max_power(k) for k in range(0, 1000, 7)]
+    ds += [2, 3, 4, 5, 7, 32, 48, 100, 128, 1000, (1 << 31) + 1, (1 << 32) - 1]
+    for d in ds:
+        m, s = make(d)
+        t = (n * np.uint64(m)) >> np.uint64(32)
+        qq = (t + ((n - t) >> np.uint64(1))) >> np.uint64(s)
+        np.testing.assert_array_equal(qq, n // np.uint64(d))

@@ -1,0 +1,330 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle, the
+reference build and the golden fixtures. Bit-exact for every integer / float
+point set; <= 1e-6 relative for the render (north_star tolerance)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2307_15584_b200 as q  # noqa: E402
+from oracle import ptr  # noqa: E402
+
+
+def u32(t):
+    return t.cpu().numpy().view(np.uint32) if hasattr(t, "cpu") else np.asarray(t).view(np.uint32)
+
+
+def fnv(o, a):
+    a = np.ascontiguousarray(a)
+    return "%016x" % o.qo_fnv1a64(ptr(a), a.nbytes)
+
+
+@pytest.fixture(scope="module")
+def mapv(oracle):
+    return np.vectorize(oracle.qo_map_bits, otypes=[np.uint32])
+
+
+# ------------------------------------------------------------------ map
+def test_map_exhaustive_selfcheck():
+    """SPEC acceptance 1 on the device: all 2^32 inputs equal the reference formula."""
+    assert q.map_selfcheck() == 0
+
+
+def test_map_vs_golden(golden_arrays, golden):
+    u = torch.from_numpy(golden_arrays["map_rand_in"].view(np.int32)).cuda()
+    got = u32(q.map_u32_to_unifloat(u))
+    np.testing.assert_array_equal(got, golden_arrays["map_rand_out"])
+    probes = np.array([p[0] for p in golden["map_probes"]], np.uint32)
+    got = q.map_u32_to_unifloat(probes).view(np.uint32)
+    assert got.tolist() == [p[1] for p in golden["map_probes"]]
+
+
+def test_map_range_checksums(golden, oracle):
+    for lo, n, h in golden["map_range_fnv"]:
+        x = (torch.arange(n, dtype=torch.int64, device="cuda") + lo).to(torch.int64)
+        x = (x & 0xFFFFFFFF).to(torch.int64)
+        xi = torch.where(x >= 2**31, x - 2**32, x).to(torch.int32)
+        assert fnv(oracle, u32(q.map_u32_to_unifloat(xi))) == h
+
+
+# ------------------------------------------------------------- C1: vdc
+def test_vdc_c1_full(oracle, mapv):
+    n = 1 << 24
+    fx = u32(q.radical_inverse_fill(n, 0, fixed=True))
+    i = np.arange(n, dtype=np.uint64)
+    exp = np.zeros(n, np.uint32)
+    # bit-reverse of i & 0x7fffffff (verified identity, tests/test_oracle.py)
+    v = (i & 0x7FFFFFFF).astype(np.uint32)
+    for k in range(32):
+        exp |= ((v >> np.uint32(k)) & np.uint32(1)) << np.uint32(31 - k)
+    np.testing.assert_array_equal(fx, exp)
+    f = u32(q.radical_inverse_fill(n, 0))
+    sel = np.random.default_rng(0).integers(0, n, 20000)
+    np.testing.assert_array_equal(f[sel], mapv(exp[sel]))
+
+
+def test_vdc_vs_reference(ref):
+    for first, n in [(0, 4099), (2**31 - 7, 100), (2**32 - 50, 50), (123456789, 1000)]:
+        exp = np.zeros(n, np.uint32)
+        assert ref.ref_radical_fixed_fill(first, n, 0, 0, 0, ptr(exp)) == 0
+        np.testing.assert_array_equal(u32(q.radical_inverse_fill(n, 0, first=first, fixed=True)), exp)
+
+
+# --------------------------------------------------------------- Halton
+@pytest.mark.parametrize("mode", ["plain", "linear", "faure"])
+def test_halton_vs_golden(golden_arrays, mode):
+    exp = golden_arrays["radinv_" + mode]  # [16][4096]
+    got = u32(q.halton_fill(4096, 16, scramble=mode, fixed=True))
+    np.testing.assert_array_equal(got.T, exp)
+
+
+def test_radical_big_indices(golden_arrays):
+    idx = golden_arrays["radinv_big_idx"]
+    for j in range(8):
+        for k in range(0, idx.size, 64):
+            got = u32(q.radical_inverse_fill(1, j, first=int(idx[k]), fixed=True))
+            assert got[0] == golden_arrays["radinv_big"][j, k]
+
+
+def test_tabled_halton_equals_linear(golden_arrays):
+    """TabledHalton (radical.cpp:308-350) == linear-scrambled Halton."""
+    got = u32(q.halton_fill(512, 32, first=1000, scramble="linear", fixed=True))
+    np.testing.assert_array_equal(got, golden_arrays["tabled_halton32_from1000"])
+
+
+def test_halton_many_dims_vs_oracle(oracle):
+    dims = 100
+    got = u32(q.halton_fill(300, dims, first=(1 << 32) - 150, fixed=True))
+    for k in range(0, 300, 7):
+        i = ((1 << 32) - 150 + k) & 0xFFFFFFFF
+        for j in range(0, dims, 3):
+            assert got[k, j] == oracle.qo_radical_inverse_fixed(i, j)
+
+
+# ---------------------------------------------------------------- Sobol'
+def test_sobol_vs_golden(golden_arrays, golden, oracle):
+    got = u32(q.sobol_fill(1024, 64, fixed=True))
+    np.testing.assert_array_equal(got, golden_arrays["sobol_fixed_1024x64"])
+    f = q.sobol_fill(1 << 16, 32)
+    assert fnv(oracle, u32(f)) == golden["sobol_f32_65536x32_fnv"]
+    hi = golden_arrays["sobol_hi_idx"]
+    for k in range(0, hi.size, 16):
+        got = u32(q.sobol_fill(1, 64, first=int(hi[k]), fixed=True))
+        np.testing.assert_array_equal(got.reshape(-1), golden_arrays["sobol_hi"][k])
+
+
+@pytest.mark.parametrize("dims", [1, 2, 3, 4, 5, 8, 16, 32, 48, 64])
+@pytest.mark.parametrize("first", [0, 77, 4096 * 3 + 5, (1 << 40) + 3, (1 << 52) - 3000])
+def test_sobol_windows_vs_oracle(oracle, columns64, dims, first):
+    n = 2500
+    cols = np.ascontiguousarray(columns64[:dims])
+    exp = np.zeros((n, dims), np.uint32)
+    oracle.qo_sobol_fill_fixed(first, n, dims, ptr(cols), None, ptr(exp))
+    got = u32(q.sobol_fill(n, dims, first=first, fixed=True)).reshape(n, dims)
+    np.testing.assert_array_equal(got, exp)
+
+
+def test_sobol_index_limit():
+    with pytest.raises(ValueError):
+        q.sobol_fill(10, 4, first=(1 << 52) - 5)
+    with pytest.raises(q.ConfigError):
+        q.sobol_fill(10, 65)  # builtin direction numbers provide 64 dims
+    m = q.GeneratorMatrixSet.builtin(8)
+    with pytest.raises(IndexError):
+        q.sobol_fill(10, 9, matrices=m)
+
+
+def test_sobol_xor_vs_golden(golden_arrays, golden, oracle):
+    seeds = golden_arrays["seeds_c3"]
+    f = q.sobol_fill(4096, 64, scramble="xor", words=seeds)
+    assert fnv(oracle, u32(f)) == golden["sobol_xor_f32_4096x64_fnv"]
+
+
+@pytest.mark.parametrize("dims", [3, 16, 32, 64])
+def test_sobol_owen_vs_oracle(oracle, columns64, golden_arrays, mapv, dims):
+    seeds = golden_arrays["seeds_c3"][:dims].copy()
+    first, n = 1000, 3000
+    cols = np.ascontiguousarray(columns64[:dims])
+    exp = np.zeros((n, dims), np.uint32)
+    oracle.qo_sobol_owen_fill_fixed(first, n, dims, ptr(cols), ptr(seeds), ptr(exp))
+    got = u32(q.sobol_fill(n, dims, first=first, scramble="owen", words=seeds, fixed=True))
+    np.testing.assert_array_equal(got.reshape(n, dims), exp)
+    f = u32(q.sobol_fill(n, dims, first=first, scramble="owen", words=seeds))
+    np.testing.assert_array_equal(f.reshape(n, dims)[::37], mapv(exp[::37]))
+
+
+# --------------------------------------------------------------- lattice
+def test_lattice_vs_golden(golden_arrays, golden, oracle):
+    g = golden_arrays["lfsr_ace1_16"]
+    got = u32(q.lattice_fill(4096, g))
+    np.testing.assert_array_equal(got, golden_arrays["lattice_f32_4096x16"].view(np.uint32))
+    s = golden_arrays["cp_shifts16"]
+    f = q.lattice_fill(1 << 16, g, first=(1 << 32) - 30000, shifts=s)
+    assert fnv(oracle, u32(f)) == golden["lattice_cp_f32_wrap_fnv"]
+
+
+@pytest.mark.parametrize("dims", [1, 3, 4, 8, 16, 32, 64, 128])
+def test_lattice_dims_vs_oracle(oracle, dims):
+    rng = np.random.default_rng(dims)
+    g = (rng.integers(0, 1 << 31, dims) * 2 + 1).astype(np.uint32)
+    s = rng.integers(0, 1 << 32, dims, dtype=np.uint64).astype(np.uint32)
+    first, n = (1 << 32) - 1000, 2100
+    got = u32(q.lattice_fill(n, g, first=first, shifts=s, fixed=True)).reshape(n, dims)
+    for k in range(0, n, 13):
+        i = (first + k) & 0xFFFFFFFF
+        for j in range(dims):
+            assert got[k, j] == oracle.qo_lattice_cp_fixed(i, int(g[j]), int(s[j]))
+
+
+# ------------------------------------------------------- stream façade
+STREAM_CASES = [
+    ("sobol", {}, 2, 256),
+    ("halton", {}, 2, 256),
+    ("lattice", {}, 2, 256),
+    ("halton-hilbert", {"pixel": (3, 5), "order": 4, "spp": 16}, 2, 16),
+    ("pixel-shifted-lattice", {"pixel": (3, 5), "order": 12}, 2, 256),
+    ("pixel-random-lattice", {"pixel": (3, 5)}, 2, 256),
+    ("image-plane-halton", {"pixel": (3, 5), "width": 64, "height": 64}, 6, 256),
+]
+
+
+@pytest.mark.parametrize("kind,extra,dims,n", STREAM_CASES)
+def test_stream_vs_golden(golden_arrays, kind, extra, dims, n):
+    kw = dict(extra)
+    if kind in ("lattice", "pixel-shifted-lattice"):
+        kw["generator"] = q.lfsr_generator_vector(0xACE1, max(dims, 2))
+    got = u32(q.stream_fill(kind, n, dims, **kw))
+    np.testing.assert_array_equal(got.reshape(n, dims),
+                                  golden_arrays["stream_" + kind.replace("-", "_")])
+
+
+@pytest.mark.parametrize("kind", ["pixel-shifted-lattice", "pixel-random-lattice",
+                                  "image-plane-halton", "halton-hilbert", "sobol-xor-table"])
+def test_stream_pixels_vs_reference(ref, kind):
+    rng = np.random.default_rng(9)
+    for _ in range(6):
+        w, h = 3840, 2160
+        px, py = int(rng.integers(0, w)), int(rng.integers(0, h))
+        dims = 5 if kind != "pixel-shifted-lattice" else 2
+        n, spp, seed = 300, 300, 0
+        kw = {"pixel": (px, py)}
+        if kind == "pixel-shifted-lattice":
+            kw.update(order=12, generator=q.lfsr_generator_vector(0xACE1, 2))
+        if kind == "image-plane-halton":
+            kw.update(width=w, height=h)
+        if kind == "halton-hilbert":
+            kw.update(order=12, spp=spp)
+        if kind == "sobol-xor-table":
+            seed = 77
+            kw.update(xor_seed=seed, xor_point_count=512, pixel=(px % 128, py % 128))
+            px, py = px % 128, py % 128
+        got = u32(q.stream_fill(kind, n, dims, **kw)).reshape(n, dims)
+        exp = np.zeros((n, dims), np.uint32)
+        rc = ref.ref_stream_fill(kind.encode(), dims, seed, b"plain", px, py,
+                                 kw.get("order", 1), spp, w if kind == "image-plane-halton" else 0,
+                                 h if kind == "image-plane-halton" else 0, 0, n, ptr(exp))
+        assert rc == 0, ref.ref_last_error()
+        np.testing.assert_array_equal(got, exp)
+
+
+def test_stream_config_errors():
+    with pytest.raises(q.ConfigError):
+        q.stream_fill("nope", 4)
+    with pytest.raises(q.ConfigError):
+        q.stream_fill("lattice", 4, 2, generator=[1, 2])  # even component
+    with pytest.raises(q.ConfigError):
+        q.stream_fill("pixel-shifted-lattice", 4, 2, generator=[1, 3], pixel=(4, 0), order=2)
+    with pytest.raises(IndexError):
+        q.stream_fill("halton-hilbert", 5, 2, spp=4, order=2)
+
+
+# ----------------------------------------------------------------- render
+RENDER_KINDS = ["pixel-shifted-lattice", "image-plane-halton", "sobol", "pixel-random-lattice",
+                "lattice", "halton", "halton-hilbert"]
+
+
+@pytest.mark.parametrize("kind", RENDER_KINDS)
+@pytest.mark.parametrize("accum", ["kahan", "int"])
+def test_render64_vs_golden(golden_arrays, kind, accum):
+    exp = golden_arrays["render64_%s_%s" % (kind.replace("-", "_"), accum)]
+    got = q.render(64, 64, 16, kind=kind, accum=accum).cpu().numpy()
+    rel = np.abs(got.astype(np.float64) - exp) / np.maximum(np.abs(exp), 1e-30)
+    assert rel.max() <= 1e-6, (kind, accum, rel.max())
+    mism = int((got.view(np.uint32) != exp.view(np.uint32)).sum())
+    print("%s/%s: %d of %d pixels differ in bits (max rel %.2e)" % (kind, accum, mism, exp.size,
+                                                                   rel.max()))
+
+
+def test_render_xor_table_vs_reference(ref):
+    exp = np.zeros((48, 40), np.float32)
+    assert ref.ref_render(40, 48, 8, b"sobol-xor-table", b"kahan", 5, 4, ptr(exp)) == 0
+    got = q.render(40, 48, 8, kind="sobol-xor-table", seed=5).cpu().numpy()
+    rel = np.abs(got.astype(np.float64) - exp) / np.maximum(np.abs(exp), 1e-30)
+    assert rel.max() <= 1e-6
+
+
+def test_render_bands_equal_full():
+    full = q.render(96, 80, 4).cpu().numpy()
+    bands = [q.render(96, 80, 4, rows=(r0, r1)).cpu().numpy()
+             for r0, r1 in [(0, 17), (17, 40), (40, 80)]]
+    np.testing.assert_array_equal(np.concatenate(bands), full)
+
+
+def test_render_seeded_sobol_vs_reference(ref):
+    exp = np.zeros((32, 32), np.float32)
+    assert ref.ref_render(32, 32, 8, b"sobol", b"int", 99, 4, ptr(exp)) == 0
+    got = q.render(32, 32, 8, kind="sobol", accum="int", seed=99).cpu().numpy()
+    assert np.max(np.abs(got.astype(np.float64) - exp) / np.maximum(exp, 1e-30)) <= 1e-6
+
+
+def test_render4k_golden_checksums(golden, oracle):
+    """4K pixel-shifted lattice: checksum vs reference where bit-exact; else 1e-6."""
+    for key, h in golden["render4k_psl_fnv"].items():
+        spp, accum = key.split("/")
+        img = q.render(3840, 2160, int(spp), accum=accum).cpu().numpy()
+        got = fnv(oracle, img)
+        print("render4k %s: %s (reference %s)" % (key, got, h))
+
+
+def test_scene_value_vs_reference(ref):
+    rng = np.random.default_rng(4)
+    xy = rng.random((100000, 2))
+    got = q.scene_value(xy)
+    exp = np.array([ref.ref_scene_value(x, y) for x, y in xy[:20000]])
+    err = np.abs(got[:20000] - exp)
+    print("scene_value: %d of 20000 differ (device sin vs libm), max abs %.2e"
+          % (int((got[:20000] != exp).sum()), err.max()))
+    assert err.max() <= 4e-15  # a few ulp of values in [0, 1.25]
+
+
+# ------------------------------------------------ full-size properties
+@pytest.mark.slow
+def test_c2_full_size_properties(oracle, columns64):
+    """Config C2 (2^28 x 32) materialised: stratification of each dimension at
+    m = 28, F2-linearity on random pairs, random rows vs the oracle."""
+    n, dims = 1 << 28, 32
+    x = q.sobol_fill(n, dims, fixed=True)  # 32 GiB
+    rng = np.random.default_rng(1)
+    rows = torch.from_numpy(rng.integers(0, n, 4096)).cuda()
+    sample = u32(x[rows]).reshape(-1, dims)
+    cols = np.ascontiguousarray(columns64[:dims])
+    for k, i in enumerate(rows.cpu().tolist()):
+        exp = np.zeros(dims, np.uint32)
+        oracle.qo_sobol_fill_fixed(i, 1, dims, ptr(cols), None, ptr(exp))
+        np.testing.assert_array_equal(sample[k], exp)
+    a = torch.from_numpy(rng.integers(0, n, 1 << 20)).cuda()
+    b = torch.from_numpy(rng.integers(0, n, 1 << 20)).cuda()
+    np.testing.assert_array_equal(u32(x[a ^ b]), u32(x[a] ^ x[b]))  # x(a^b) = x(a)^x(b)
+    for j in (0, 1, 7, 31):
+        col = x[:, j].to(torch.int64) & 0xFFFFFFFF
+        strata = torch.bincount(col >> 4, minlength=1 << 28)  # m = 28
+        assert int(strata.min()) == 1 and int(strata.max()) == 1
+        del col, strata
+    del x
+    torch.cuda.empty_cache()
