@@ -262,6 +262,10 @@ def run_ours(args):
         torch.cuda.synchronize()
     clk = clocks.stop()
 
+    # write-only streaming ceiling on the same buffer (diagnostic denominator)
+    wp_ms = time_steps(lambda: q.write_probe(out), 5, stream)
+    write_probe_gbs = N_POINTS * DIMS * 4 / (sum(wp_ms) / len(wp_ms) * 1e-3) / 1e9
+
     ms_per_step = total_ms / args.steps
     samples = N_POINTS * DIMS
     value = samples * world / (ms_per_step * 1e-3) / 1e9
@@ -332,6 +336,8 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_src,
+                         "write_probe_gbs": write_probe_gbs,
+                         "frac_of_write_probe": achieved / write_probe_gbs,
                          "algorithmic_bytes_per_launch": samples * 4},
             "gpu_launches": args.steps,
             "clocks": clk,

@@ -614,6 +614,16 @@ qmc_status qmc_map_selfcheck(uint64_t* mismatches, qmc_stream stream)
     });
 }
 
+qmc_status qmc_write_probe(void* device_buffer, uint64_t bytes, qmc_stream stream)
+{
+    return guard([&] {
+        if (!is_device_pointer(device_buffer))
+            fail(QMC_INVALID_ARGUMENT, "write probe needs a device buffer");
+        cuda_ok(launch_write_probe(device_buffer, bytes & ~uint64_t(15), as_stream(stream)),
+                "launch_write_probe");
+    });
+}
+
 // ------------------------------------------------------------ host setup
 
 qmc_status qmc_prime(uint32_t index, uint32_t* out)

@@ -93,6 +93,9 @@ cudaError_t launch_render(const RenderParams& p, uint32_t kind, uint32_t accum, 
 
 cudaError_t launch_scene_value(const double* xy, double* out, uint64_t n, cudaStream_t s);
 
+// Write-only 128-bit streaming store probe over `bytes` (diagnostic).
+cudaError_t launch_write_probe(void* out, uint64_t bytes, cudaStream_t s);
+
 // Number of SMs of the current device (cached).
 int sm_count();
 

@@ -403,7 +403,26 @@ cudaError_t lattice_fast_dispatch(const uint32_t* g, const uint32_t* sh, bool u3
                : launch_tiled(k_lattice_fast<LOG_PPS, false>, LOG_TP, r, s, g, sh);
 }
 
+// Write-only streaming probe: the ceiling a pure 128-bit store stream reaches
+// on this GPU (same grid shape and store hint as the fills). Diagnostic for
+// the roofline denominator, not part of any fill.
+__global__ void __launch_bounds__(kBlock) k_write_probe(uint4* __restrict__ out, uint64_t n16)
+{
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const uint4 v = make_uint4(blockIdx.x, threadIdx.x, 0x3f000000u, 0u);
+    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n16;
+         k += stride)
+        store4(out + k, v);
+}
+
 } // namespace
+
+cudaError_t launch_write_probe(void* out, uint64_t bytes, cudaStream_t s)
+{
+    const unsigned grid = static_cast<unsigned>(sm_count() * blocks_per_sm(k_write_probe));
+    k_write_probe<<<grid, kBlock, 0, s>>>(static_cast<uint4*>(out), bytes / 16);
+    return cudaGetLastError();
+}
 
 int sm_count()
 {

@@ -1,0 +1,79 @@
+"""Multi-GPU host driver: one process per GPU, torch.distributed for plumbing.
+
+Two partitionings:
+
+* Materialised fills (configs C1-C4) shard contiguous index ranges; rank r
+  owns [first + r*n/G, first + (r+1)*n/G) and writes its slab of the
+  row-major array through the fill's `first_index`. No collective: the points
+  stay resident on their GPU (`index_shard`).
+* The fused render (config C5) splits the image into row bands; every pixel
+  is computed by exactly one GPU with the single-GPU summation order, so the
+  gathered image is bit-identical to the 1-GPU render. One collective — an
+  all-gather of the fp32 bands (NCCL over NVLink on a GPU box, gloo in the
+  CPU tests) — assembles the image (`render_distributed`).
+
+The sample-partition alternative of the paper (`partition_by_extra_dimension`,
+imageplane.cpp:114-130; PAPER §2.5.1) is exposed for integration-style
+splits as `sample_partition`.
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional, Tuple
+
+import torch
+import torch.distributed as dist
+
+
+def index_shard(first: int, n: int, world: int, rank: int) -> Tuple[int, int]:
+    """Contiguous index range [start, start + count) of `rank` (balanced)."""
+    lo = first + n * rank // world
+    hi = first + n * (rank + 1) // world
+    return lo, hi - lo
+
+
+def row_bands(height: int, world: int):
+    """Row bands [(r0, r1)] per rank, sizes differing by at most one row."""
+    return [(height * r // world, height * (r + 1) // world) for r in range(world)]
+
+
+def sample_partition(part: int, parts: int, base: int = 2) -> Tuple[int, int]:
+    """(remainder, modulus) of the indices owned by `part` (imageplane.cpp:114-130)."""
+    from . import partition_by_extra_dimension
+
+    return partition_by_extra_dimension(part, parts, base)
+
+
+def gather_bands(band: torch.Tensor, height: int, width: int, group=None) -> torch.Tensor:
+    """All-gather the per-rank row bands into the full [height, width] image.
+
+    Bands are padded to the largest band so one all_gather_into_tensor moves
+    everything in a single collective."""
+    world = dist.get_world_size(group)
+    bands = row_bands(height, world)
+    rows = max(r1 - r0 for r0, r1 in bands)
+    pad = torch.zeros((rows, width), dtype=band.dtype, device=band.device)
+    pad[: band.shape[0]] = band
+    full = torch.empty((world * rows, width), dtype=band.dtype, device=band.device)
+    dist.all_gather_into_tensor(full, pad, group=group)
+    parts = [full[r * rows: r * rows + (r1 - r0)] for r, (r0, r1) in enumerate(bands)]
+    return torch.cat(parts, 0)
+
+
+def render_distributed(width: int, height: int, spp: int, kind: str = "pixel-shifted-lattice",
+                       accum: str = "kahan", seed: int = 0, group=None,
+                       band_renderer: Optional[Callable] = None) -> torch.Tensor:
+    """Render rank's row band on its GPU, then one all-gather of the bands.
+
+    `band_renderer(r0, r1) -> [r1-r0, width] tensor` defaults to the CUDA
+    render (libqmcgpu qmc_render); tests inject a stand-in to exercise the
+    partition/gather logic on CPU ranks."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    r0, r1 = row_bands(height, world)[rank]
+    if band_renderer is None:
+        from . import render
+
+        band = render(width, height, spp, kind=kind, accum=accum, seed=seed, rows=(r0, r1))
+    else:
+        band = band_renderer(r0, r1)
+    return gather_bands(band, height, width, group)

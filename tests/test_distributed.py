@@ -1,0 +1,66 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2 and 3): index-range shards
+cover the sequence exactly once, and the row-band all-gather reassembles the
+image the single-process render produces (bands from the oracle)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2307_15584_b200.distributed import index_shard, row_bands
+
+
+def test_index_shards_partition():
+    for first, n, world in [(0, 1 << 28, 8), (5, 1001, 3), (7, 3, 4)]:
+        spans = [index_shard(first, n, world, r) for r in range(world)]
+        assert spans[0][0] == first
+        for (a, c), (b, _) in zip(spans, spans[1:]):
+            assert a + c == b
+        assert sum(c for _, c in spans) == n
+
+
+def test_row_bands():
+    for h, w in [(2160, 8), (5, 3), (1, 2)]:
+        b = row_bands(h, w)
+        assert b[0][0] == 0 and b[-1][1] == h
+        assert all(r1 - r0 in (h // w, h // w + 1) for r0, r1 in b)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, w, h, spp, expect_path, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2307_15584_b200.distributed import render_distributed
+
+    full = torch.from_numpy(np.load(expect_path))
+    img = render_distributed(w, h, spp, band_renderer=lambda r0, r1: full[r0:r1].clone())
+    if rank == 0:
+        np.save(out_path, img.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_render_band_gather_gloo(tmp_path, oracle, columns64, world):
+    from oracle import ptr
+
+    w, h, spp = 40, 23, 4
+    img = np.zeros((h, w), np.float32)
+    cols2 = np.ascontiguousarray(columns64[:2])
+    assert oracle.qo_render(w, h, spp, 4, 0, 0, ptr(cols2), ptr(img)) == 0
+    exp_path, out_path = str(tmp_path / "exp.npy"), str(tmp_path / "out.npy")
+    np.save(exp_path, img)
+    mp.spawn(_worker, args=(world, _free_port(), w, h, spp, exp_path, out_path), nprocs=world,
+             join=True)
+    np.testing.assert_array_equal(np.load(out_path), img)
