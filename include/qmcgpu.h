@@ -66,9 +66,12 @@ qmc_status qmc_map_u32_to_unifloat(const uint32_t* in, float* out, uint64_t n, q
  * of the reference formula (SPEC acceptance 1); *mismatches = count. */
 qmc_status qmc_map_selfcheck(uint64_t* mismatches, qmc_stream stream);
 
-/* Diagnostic: write-only 128-bit streaming stores over a device buffer (the
- * HBM write ceiling the fills are compared against in bench.py). */
-qmc_status qmc_write_probe(void* device_buffer, uint64_t bytes, qmc_stream stream);
+/* Diagnostic: write-only store streams over a device buffer (the HBM write
+ * ceiling the fills are compared against in bench.py). mode 0: 128-bit
+ * streaming stores, grid-stride; 1: 128-bit write-back stores; 2: 256-bit
+ * streaming stores; 3: 128-bit streaming, contiguous chunk per warp;
+ * 4: cudaMemsetAsync. */
+qmc_status qmc_write_probe(void* device_buffer, uint64_t bytes, int mode, qmc_stream stream);
 
 /* --------------------------------------------- host setup (no per-sample work) */
 /* primes.cpp:50-62 */

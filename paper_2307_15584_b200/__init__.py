@@ -91,7 +91,7 @@ def lib():
     sig("qmc_abi_version", i32)
     sig("qmc_map_u32_to_unifloat", i32, P, P, u64, P)
     sig("qmc_map_selfcheck", i32, C.POINTER(u64), P)
-    sig("qmc_write_probe", i32, P, u64, P)
+    sig("qmc_write_probe", i32, P, u64, i32, P)
     sig("qmc_prime", i32, u32, C.POINTER(u32))
     sig("qmc_prime_max_power", i32, u32, C.POINTER(u32))
     sig("qmc_faure_permutation", i32, u32, P)
@@ -313,9 +313,10 @@ def map_selfcheck(stream=None) -> int:
     return m.value
 
 
-def write_probe(buf, stream=None) -> None:
-    """Write-only streaming stores over a device tensor (roofline diagnostic)."""
-    _check(lib().qmc_write_probe(_ptr(buf), buf.numel() * buf.element_size(), _stream(stream)))
+def write_probe(buf, mode: int = 0, stream=None) -> None:
+    """Write-only store stream over a device tensor (roofline diagnostic)."""
+    _check(lib().qmc_write_probe(_ptr(buf), buf.numel() * buf.element_size(), mode,
+                                 _stream(stream)))
 
 
 def sobol_fill(n: int, dims: int, first: int = 0, scramble: str = "none", words=None,

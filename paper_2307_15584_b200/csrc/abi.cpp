@@ -352,6 +352,8 @@ DevPtr dev_upload(const void* host, size_t bytes)
 
 // Small per-call parameter arrays, uploaded with one stream-ordered copy
 // and released stream-ordered after the launches.
+void pool_keep_memory();
+
 class CallArgs {
 public:
     explicit CallArgs(cudaStream_t s) : s_(s) {}
@@ -373,6 +375,7 @@ public:
     {
         if (blob_.empty())
             return;
+        pool_keep_memory();
         cuda_ok(cudaMallocAsync(&dev_, blob_.size(), s_), "cudaMallocAsync");
         cuda_ok(cudaMemcpyAsync(dev_, blob_.data(), blob_.size(), cudaMemcpyHostToDevice, s_),
                 "cudaMemcpyAsync args");
@@ -388,6 +391,36 @@ private:
     std::vector<char> blob_;
     void* dev_ = nullptr;
 };
+
+// Fills SmallArgs array `which` (0 = a, 1 = b) by value when it fits the
+// parameter space, else stages a device copy through `args` (patched in
+// finish_small after the upload).
+void set_small(SmallArgs& sa, int which, const uint32_t* host, uint32_t n, CallArgs& args)
+{
+    uint32_t* dst = which ? sa.b : sa.a;
+    if (n <= kSmall) {
+        std::memcpy(dst, host, n * 4);
+        (which ? sa.has_b : sa.has_a) = 1;
+        return;
+    }
+    std::vector<uint32_t> pad(std::max<uint32_t>(n, 8) + 8, 0u);
+    std::memcpy(pad.data(), host, n * 4);
+    const size_t off = args.add(pad.data(), pad.size() * 4);
+    (which ? sa.has_b : sa.has_a) = static_cast<uint32_t>(off + 1); // patched below
+    (which ? sa.dev_b : sa.dev_a) = reinterpret_cast<const uint32_t*>(uintptr_t(1));
+}
+
+void finish_small(SmallArgs& sa, const CallArgs& args)
+{
+    if (sa.dev_a) {
+        sa.dev_a = args.at<uint32_t>(sa.has_a - 1);
+        sa.has_a = 1;
+    }
+    if (sa.dev_b) {
+        sa.dev_b = args.at<uint32_t>(sa.has_b - 1);
+        sa.has_b = 1;
+    }
+}
 
 // Per-device resources for the host-output pipeline.
 struct DeviceCtx {
@@ -414,6 +447,28 @@ int current_device()
     int dev = 0;
     cuda_ok(cudaGetDevice(&dev), "cudaGetDevice");
     return dev;
+}
+
+// Keep the stream-ordered pool's memory cached across synchronizations, so
+// the per-call argument blobs (cudaMallocAsync) never remap physical memory
+// in a timed loop (the default release threshold of 0 returns it at every
+// sync, which cost milliseconds per call).
+void pool_keep_memory()
+{
+    static std::mutex mu;
+    static std::vector<char> done;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.size() <= static_cast<size_t>(dev))
+        done.resize(dev + 1, 0);
+    if (done[dev])
+        return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done[dev] = 1;
 }
 
 bool is_device_pointer(const void* p)
@@ -614,12 +669,12 @@ qmc_status qmc_map_selfcheck(uint64_t* mismatches, qmc_stream stream)
     });
 }
 
-qmc_status qmc_write_probe(void* device_buffer, uint64_t bytes, qmc_stream stream)
+qmc_status qmc_write_probe(void* device_buffer, uint64_t bytes, int mode, qmc_stream stream)
 {
     return guard([&] {
         if (!is_device_pointer(device_buffer))
             fail(QMC_INVALID_ARGUMENT, "write probe needs a device buffer");
-        cuda_ok(launch_write_probe(device_buffer, bytes & ~uint64_t(15), as_stream(stream)),
+        cuda_ok(launch_write_probe(device_buffer, bytes & ~uint64_t(31), mode, as_stream(stream)),
                 "launch_write_probe");
     });
 }
@@ -793,18 +848,15 @@ static void sobol_fill_impl(qmc_matrices* m, uint64_t first, uint64_t n, uint32_
         colsT_rev = static_cast<const uint32_t*>(sub_rev.get());
     }
     CallArgs args(s);
-    size_t woff = SIZE_MAX;
-    if (words && sc != QMC_SOBOL_NONE) {
-        std::vector<uint32_t> w(std::max<uint32_t>(dims, 4), 0u);
-        std::memcpy(w.data(), words, dims * 4);
-        woff = args.add(w.data(), w.size() * 4);
-    }
+    SmallArgs small{};
+    if (words && sc != QMC_SOBOL_NONE)
+        set_small(small, 0, words, dims, args);
     args.upload();
-    const uint32_t* wdev = woff == SIZE_MAX ? nullptr : args.at<uint32_t>(woff);
+    finish_small(small, args);
     const int mode = sc == QMC_SOBOL_OWEN ? 2 : 0;
     const bool u32 = kind == QMC_OUT_U32;
     place_fill(out, first, n, dims, s, [&](const FillRange& r, cudaStream_t st) {
-        return launch_sobol(colsT, colsT_rev, wdev, dims, mode, u32, r, st);
+        return launch_sobol(colsT, colsT_rev, small, dims, mode, u32, r, st);
     });
     if (sub) // the temporary prefix tables must outlive the kernels
         cuda_ok(cudaStreamSynchronize(s), "sync");
@@ -889,20 +941,15 @@ static void lattice_fill_impl(const uint32_t* g, const uint32_t* shifts, uint32_
     if (!g)
         fail(QMC_INVALID_ARGUMENT, "generator vector is null");
     CallArgs args(s);
-    std::vector<uint32_t> gv(std::max<uint32_t>(dims, 4), 0u), sv(gv.size(), 0u);
-    std::memcpy(gv.data(), g, dims * 4);
-    const size_t goff = args.add(gv.data(), gv.size() * 4);
-    size_t soff = SIZE_MAX;
-    if (shifts) {
-        std::memcpy(sv.data(), shifts, dims * 4);
-        soff = args.add(sv.data(), sv.size() * 4);
-    }
+    SmallArgs small{};
+    set_small(small, 0, g, dims, args);
+    if (shifts)
+        set_small(small, 1, shifts, dims, args);
     args.upload();
-    const uint32_t* gd = args.at<uint32_t>(goff);
-    const uint32_t* sd = soff == SIZE_MAX ? nullptr : args.at<uint32_t>(soff);
+    finish_small(small, args);
     const bool u32 = kind == QMC_OUT_U32;
     place_fill(out, first, n, dims, s, [&](const FillRange& r, cudaStream_t st) {
-        return launch_lattice(gd, sd, dims, u32, r, st);
+        return launch_lattice(small, dims, u32, r, st);
     });
 }
 

@@ -62,21 +62,35 @@ struct PixelStreamParams {
     uint32_t xor_point_count, xor_dims;
 };
 
+// Small per-call arrays (XOR words / Owen seeds, generator vector, CP
+// shifts) passed BY VALUE in the kernel parameter space (read through a
+// __grid_constant__ reference), so a fill is one launch with no per-call
+// device allocation or H2D copy. Arrays longer than kSmall words go through
+// dev_a / dev_b (device copies) instead.
+constexpr uint32_t kSmall = 256;
+struct SmallArgs {
+    const uint32_t* dev_a;
+    const uint32_t* dev_b;
+    uint32_t has_a, has_b;
+    uint32_t a[kSmall];
+    uint32_t b[kSmall];
+};
+
 // ------------------------------------------------------------ launchers
 // All launchers write DEVICE memory and are asynchronous on `s`.
 cudaError_t launch_map(const uint32_t* in, float* out, uint64_t n, cudaStream_t s);
 cudaError_t launch_map_selfcheck(unsigned long long* dev_count, cudaStream_t s);
 
-// colsT: device [52][dims] columns (k-major); words: device [dims] or null.
+// colsT: device [52][dims] columns (k-major); args.a = per-dim words.
 // mode 0 plain/xor (words = xor words), 2 owen (colsT bit-reversed, words =
 // seeds). out_u32: write the integer stage instead of floats.
-cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const uint32_t* words,
+cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const SmallArgs& args,
                          uint32_t dims, int mode, bool out_u32, const FillRange& r,
                          cudaStream_t s);
 
-// g, shifts: device [dims] (shifts may be null).
-cudaError_t launch_lattice(const uint32_t* g, const uint32_t* shifts, uint32_t dims,
-                           bool out_u32, const FillRange& r, cudaStream_t s);
+// args.a = generator vector g, args.b = CP shifts (optional).
+cudaError_t launch_lattice(const SmallArgs& args, uint32_t dims, bool out_u32,
+                           const FillRange& r, cudaStream_t s);
 
 // dims == 1, prime 2 (van der Corput, config C1).
 cudaError_t launch_vdc(bool out_u32, const FillRange& r, cudaStream_t s);
@@ -94,7 +108,7 @@ cudaError_t launch_render(const RenderParams& p, uint32_t kind, uint32_t accum, 
 cudaError_t launch_scene_value(const double* xy, double* out, uint64_t n, cudaStream_t s);
 
 // Write-only 128-bit streaming store probe over `bytes` (diagnostic).
-cudaError_t launch_write_probe(void* out, uint64_t bytes, cudaStream_t s);
+cudaError_t launch_write_probe(void* out, uint64_t bytes, int mode, cudaStream_t s);
 
 // Number of SMs of the current device (cached).
 int sm_count();

@@ -13,7 +13,9 @@
 //     lattice update is one IMAD with a compile-time brev constant;
 //   * the float map is 9 full-rate ops (device.cuh map_u32).
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
+#include <type_traits>
 
 #include "device.cuh"
 #include "internal.hpp"
@@ -98,115 +100,188 @@ __global__ void k_map_selfcheck(unsigned long long* count)
 
 // ------------------------------------------------------------------ Sobol'
 
+// DPL consecutive dimensions per lane (8 -> one 256-bit store per lane,
+// 1 KiB contiguous per warp store; 4 -> 128-bit stores, 512 B per warp).
+template <int DPL>
+__device__ __forceinline__ void load_cols(const uint32_t* p, uint32_t (&v)[DPL])
+{
+#pragma unroll
+    for (int q = 0; q < DPL / 4; ++q) {
+        const uint4 t = __ldg(reinterpret_cast<const uint4*>(p) + q);
+        v[4 * q] = t.x;
+        v[4 * q + 1] = t.y;
+        v[4 * q + 2] = t.z;
+        v[4 * q + 3] = t.w;
+    }
+}
+
+// Array `a` / `b` of the by-value SmallArgs (param space) or its device copy.
+__device__ __forceinline__ const uint32_t* small_a(const SmallArgs& g)
+{
+    return g.dev_a ? g.dev_a : (g.has_a ? g.a : nullptr);
+}
+__device__ __forceinline__ const uint32_t* small_b(const SmallArgs& g)
+{
+    return g.dev_b ? g.dev_b : (g.has_b ? g.b : nullptr);
+}
+
+template <int DPL>
+__device__ __forceinline__ void load_small(const uint32_t* p, uint32_t (&v)[DPL])
+{
+#pragma unroll
+    for (int e = 0; e < DPL; ++e)
+        v[e] = p[e];
+}
+
+template <int DPL>
+__device__ __forceinline__ void store_vec(uint32_t* p, const uint32_t (&v)[DPL])
+{
+    if constexpr (DPL == 8) {
+        asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]),
+                     "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                     : "memory");
+    } else {
+        __stcs(reinterpret_cast<uint4*>(p), make_uint4(v[0], v[1], v[2], v[3]));
+    }
+}
+
 // MODE 0: plain / XOR-scrambled (words = XOR words, folded into the start
 // value since the scramble is linear). MODE 2: hash-Owen, columns and the
 // running value live in the bit-reversed domain; words = per-dim seeds.
-template <int LOG_PPS, int MODE, bool U32OUT>
+template <int DPL, int LOG_PPS, int MODE, bool U32OUT>
 __global__ void __launch_bounds__(kBlock)
-    k_sobol_fast(const uint32_t* __restrict__ colsT, const uint32_t* __restrict__ words,
+    k_sobol_fast(const uint32_t* __restrict__ colsT, const __grid_constant__ SmallArgs args,
                  uint64_t first, uint64_t n, uint64_t tile0, uint64_t ntiles, uint64_t per_warp,
-                 uint4* __restrict__ out)
+                 uint32_t* __restrict__ out)
 {
-    constexpr int PPS = 1 << LOG_PPS; // points per warp store
+    constexpr int PPS = 1 << LOG_PPS;  // points per warp store
     constexpr int LPP = 32 >> LOG_PPS; // lanes per point
-    constexpr int DIMS = 4 * LPP;
+    constexpr int DIMS = DPL * LPP;
     constexpr int LOG_TP = LOG_PPS + 5; // 32 steps per tile
     uint64_t t, tend;
     if (!warp_tiles(tile0, ntiles, per_warp, t, tend))
         return;
     const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t r = lane / LPP; // point within a step
-    const uint32_t dq = lane % LPP; // dims 4*dq .. 4*dq+3
-    const uint4* cols = reinterpret_cast<const uint4*>(colsT) + dq; // cols[k * LPP] = column k
-    auto col = [&](uint32_t k) { return __ldg(cols + k * LPP); };
+    const uint32_t r = lane / LPP;  // point within a step
+    const uint32_t dq = lane % LPP; // dims DPL*dq .. DPL*dq + DPL-1
+    const uint32_t* cols = colsT + dq * DPL; // column k of my dims at cols + k * DIMS
 
     // Step masks: index += PPS flips bits LOG_PPS .. LOG_PPS + ctz(u+1).
-    uint4 D[5];
+    uint32_t D[5][DPL];
     {
-        uint4 acc = make_uint4(0, 0, 0, 0);
+        uint32_t c[DPL];
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
-            acc = xor4(acc, col(LOG_PPS + k));
-            D[k] = acc;
+            load_cols<DPL>(cols + (LOG_PPS + k) * DIMS, c);
+#pragma unroll
+            for (int e = 0; e < DPL; ++e)
+                D[k][e] = k ? D[k - 1][e] ^ c[e] : c[e];
         }
     }
-    uint4 seed = make_uint4(0, 0, 0, 0);
-    uint4 xr = make_uint4(0, 0, 0, 0);
-    if (words) {
-        const uint4 w = __ldg(reinterpret_cast<const uint4*>(words) + dq);
+    uint32_t seed[DPL], xr[DPL], xp[DPL], c[DPL];
+#pragma unroll
+    for (int e = 0; e < DPL; ++e)
+        seed[e] = xr[e] = xp[e] = 0;
+    if (const uint32_t* words = small_a(args)) {
         if (MODE == 2)
-            seed = w;
+            load_small<DPL>(words + dq * DPL, seed);
         else
-            xr = w;
+            load_small<DPL>(words + dq * DPL, xr);
     }
 #pragma unroll
     for (int k = 0; k < LOG_PPS; ++k)
-        if ((r >> k) & 1u)
-            xr = xor4(xr, col(k));
-    // Value of the tile base t << LOG_TP (bits >= LOG_TP).
-    uint4 xp = make_uint4(0, 0, 0, 0);
-    for (uint64_t b = t; b; b &= b - 1)
-        xp = xor4(xp, col(LOG_TP + __ffsll(static_cast<long long>(b)) - 1));
-
-    auto emit = [&](uint4 x) -> uint4 {
-        if (MODE == 2) {
-            x = make_uint4(brev32(owen_lk(x.x, seed.x)), brev32(owen_lk(x.y, seed.y)),
-                           brev32(owen_lk(x.z, seed.z)), brev32(owen_lk(x.w, seed.w)));
+        if ((r >> k) & 1u) {
+            load_cols<DPL>(cols + k * DIMS, c);
+#pragma unroll
+            for (int e = 0; e < DPL; ++e)
+                xr[e] ^= c[e];
         }
-        return U32OUT ? x : map4(x);
-    };
+    // Value of the tile base t << LOG_TP (bits >= LOG_TP).
+    for (uint64_t b = t; b; b &= b - 1) {
+        load_cols<DPL>(cols + (LOG_TP + __ffsll(static_cast<long long>(b)) - 1) * DIMS, c);
+#pragma unroll
+        for (int e = 0; e < DPL; ++e)
+            xp[e] ^= c[e];
+    }
 
     for (;;) {
         const uint64_t p0 = (t << LOG_TP) + r; // this thread's point at step 0
-        uint4 x = xor4(xp, xr);
+        uint32_t x[DPL], y[DPL];
+#pragma unroll
+        for (int e = 0; e < DPL; ++e)
+            x[e] = xp[e] ^ xr[e];
         const uint64_t lo = t << LOG_TP, hi = (t + 1) << LOG_TP;
-        if (lo >= first && hi <= first + n) {
-            uint4* o = out + (p0 - first) * LPP + dq;
+        const bool full = lo >= first && hi <= first + n;
+        uint32_t* o = out + (p0 - first) * DIMS + dq * DPL;
+        // 32 steps as 4 x 8: the inner 8 are unrolled with compile-time
+        // masks (ctz(w+1), w < 7); the step between groups flips bits up to
+        // 3 + ctz(v+1) (v = 0,1,2 -> D[3], D[4], D[3]). Keeps the loop body
+        // ~12 KB of SASS (inside the 32 KB L1.5 I-cache).
+        auto group = [&](uint32_t v, auto check) {
 #pragma unroll
-            for (uint32_t u = 0; u < 32; ++u) {
-                store4(o + u * 32, emit(x));
-                if (u < 31)
-                    x = xor4(x, D[ctz_const(u + 1)]);
+            for (uint32_t w = 0; w < 8; ++w) {
+                const uint32_t u = 8 * v + w;
+#pragma unroll
+                for (int e = 0; e < DPL; ++e) {
+                    uint32_t val = x[e];
+                    if (MODE == 2)
+                        val = brev32(owen_lk(val, seed[e]));
+                    y[e] = U32OUT ? val : map_bits(val);
+                }
+                if (!decltype(check)::value || (p0 + u * PPS) - first < n)
+                    store_vec<DPL>(o + u * 32 * DPL, y);
+                if (w < 7) {
+#pragma unroll
+                    for (int e = 0; e < DPL; ++e)
+                        x[e] ^= D[ctz_const(w + 1)][e];
+                }
             }
+#pragma unroll
+            for (int e = 0; e < DPL; ++e)
+                x[e] ^= (v == 1) ? D[4][e] : D[3][e];
+        };
+        if (full) { // interior tile: no per-store predicate
+#pragma unroll 1
+            for (uint32_t v = 0; v < 4; ++v)
+                group(v, std::false_type{});
         } else {
-#pragma unroll
-            for (uint32_t u = 0; u < 32; ++u) {
-                const uint64_t i = p0 + u * PPS;
-                if (i - first < n)
-                    store4(out + (i - first) * LPP + dq, emit(x));
-                if (u < 31)
-                    x = xor4(x, D[ctz_const(u + 1)]);
-            }
+#pragma unroll 1
+            for (uint32_t v = 0; v < 4; ++v)
+                group(v, std::true_type{});
         }
         if (++t >= tend)
             break;
         // tile t-1 -> t flips bits LOG_TP .. LOG_TP + ctz(t)
-        const int c = __ffsll(static_cast<long long>(t)) - 1;
-        for (int k = 0; k <= c; ++k)
-            xp = xor4(xp, col(LOG_TP + k));
+        const int cz = __ffsll(static_cast<long long>(t)) - 1;
+        for (int k = 0; k <= cz; ++k) {
+            load_cols<DPL>(cols + (LOG_TP + k) * DIMS, c);
+#pragma unroll
+            for (int e = 0; e < DPL; ++e)
+                xp[e] ^= c[e];
+        }
     }
-    (void)DIMS;
 }
 
 // Any dims: one thread per (point, dim) element of a chunk whose element
 // count fits 32 bits; direct per-set-bit evaluation (digitalnet.cpp:111-131).
 template <int MODE, bool U32OUT>
 __global__ void __launch_bounds__(kBlock)
-    k_sobol_generic(const uint32_t* __restrict__ colsT, const uint32_t* __restrict__ words,
+    k_sobol_generic(const uint32_t* __restrict__ colsT, const __grid_constant__ SmallArgs args,
                     uint32_t dims, Div32 div_dims, uint64_t first, uint32_t elems,
                     uint32_t* __restrict__ out)
 {
+    const uint32_t* words = small_a(args);
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < elems; e += stride) {
         const uint32_t p = point_of(e, dims, div_dims);
         const uint32_t j = e - p * dims;
         uint64_t i = first + p;
-        uint32_t x = (MODE == 0 && words) ? __ldg(words + j) : 0u;
+        uint32_t x = (MODE == 0 && words) ? words[j] : 0u;
         for (uint32_t k = 0; i; ++k, i >>= 1)
             if (i & 1u)
                 x ^= __ldg(colsT + k * dims + j);
         if (MODE == 2)
-            x = brev32(owen_lk(brev32(x), words ? __ldg(words + j) : 0u));
+            x = brev32(owen_lk(brev32(x), words ? words[j] : 0u));
         out[e] = U32OUT ? x : map_bits(x);
     }
 }
@@ -217,57 +292,87 @@ __global__ void __launch_bounds__(kBlock)
 // is P | (u << LOG_PPS) | r with disjoint bits, so brev(i) = brev(P | r) +
 // brev5(u) << (27 - LOG_PPS): one IMAD per sample with a compile-time
 // multiplier.
-template <int LOG_PPS, bool U32OUT>
+template <int DPL, int LOG_PPS, bool U32OUT>
 __global__ void __launch_bounds__(kBlock)
-    k_lattice_fast(const uint32_t* __restrict__ g, const uint32_t* __restrict__ shifts,
+    k_lattice_fast(const uint32_t* __restrict__ unused, const __grid_constant__ SmallArgs args,
                    uint64_t first, uint64_t n, uint64_t tile0, uint64_t ntiles, uint64_t per_warp,
-                   uint4* __restrict__ out)
+                   uint32_t* __restrict__ out)
 {
     constexpr int PPS = 1 << LOG_PPS;
     constexpr int LPP = 32 >> LOG_PPS;
+    constexpr int DIMS = DPL * LPP;
     constexpr int LOG_TP = LOG_PPS + 5;
     uint64_t t, tend;
     if (!warp_tiles(tile0, ntiles, per_warp, t, tend))
         return;
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t r = lane / LPP, dq = lane % LPP;
-    const uint4 g4 = __ldg(reinterpret_cast<const uint4*>(g) + dq);
-    const uint4 s4 = shifts ? __ldg(reinterpret_cast<const uint4*>(shifts) + dq)
-                            : make_uint4(0, 0, 0, 0);
-    const uint4 G = make_uint4(g4.x << (27 - LOG_PPS), g4.y << (27 - LOG_PPS),
-                               g4.z << (27 - LOG_PPS), g4.w << (27 - LOG_PPS));
+    uint32_t gv[DPL], sv[DPL], G[DPL];
+    load_small<DPL>(small_a(args) + dq * DPL, gv);
+    const uint32_t* shifts = small_b(args);
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) {
+        sv[e] = 0;
+        G[e] = gv[e] << (27 - LOG_PPS);
+    }
+    if (shifts)
+        load_small<DPL>(shifts + dq * DPL, sv);
     for (; t < tend; ++t) {
         const uint64_t p0 = (t << LOG_TP) + r;
         const uint32_t b = brev32(static_cast<uint32_t>(p0));
-        const uint4 x0 = make_uint4(b * g4.x + s4.x, b * g4.y + s4.y, b * g4.z + s4.z,
-                                    b * g4.w + s4.w);
+        uint32_t x0[DPL], y[DPL];
+#pragma unroll
+        for (int e = 0; e < DPL; ++e)
+            x0[e] = b * gv[e] + sv[e];
         const uint64_t lo = t << LOG_TP, hi = (t + 1) << LOG_TP;
         const bool full = lo >= first && hi <= first + n;
-        uint4* o = out + (p0 - first) * LPP + dq;
+        uint32_t* o = out + (p0 - first) * DIMS + dq * DPL;
+        // u = 8v + w: brev5(u) = brev3(w) << 2 | brev2(v); the v part is
+        // added once per group of 8, the w part is a compile-time multiplier.
+        auto group = [&](uint32_t v, auto check) {
+            const uint32_t cv = ((v & 1u) << 1) | (v >> 1);
+            uint32_t xv[DPL];
 #pragma unroll
-        for (uint32_t u = 0; u < 32; ++u) {
-            const uint32_t c = brev5(u);
-            uint4 x = make_uint4(x0.x + c * G.x, x0.y + c * G.y, x0.z + c * G.z, x0.w + c * G.w);
-            if (!U32OUT)
-                x = map4(x);
-            if (full || (p0 + u * PPS) - first < n)
-                store4(o + u * 32, x);
+            for (int e = 0; e < DPL; ++e)
+                xv[e] = x0[e] + cv * G[e];
+#pragma unroll
+            for (uint32_t w = 0; w < 8; ++w) {
+                const uint32_t u = 8 * v + w;
+                const uint32_t cw = (((w & 1u) << 2) | (w & 2u) | (w >> 2)) << 2;
+#pragma unroll
+                for (int e = 0; e < DPL; ++e) {
+                    const uint32_t xx = xv[e] + cw * G[e];
+                    y[e] = U32OUT ? xx : map_bits(xx);
+                }
+                if (!decltype(check)::value || (p0 + u * PPS) - first < n)
+                    store_vec<DPL>(o + u * 32 * DPL, y);
+            }
+        };
+        if (full) {
+#pragma unroll 1
+            for (uint32_t v = 0; v < 4; ++v)
+                group(v, std::false_type{});
+        } else {
+#pragma unroll 1
+            for (uint32_t v = 0; v < 4; ++v)
+                group(v, std::true_type{});
         }
     }
 }
 
 __global__ void __launch_bounds__(kBlock)
-    k_lattice_generic(const uint32_t* __restrict__ g, const uint32_t* __restrict__ shifts,
-                      uint32_t dims, Div32 div_dims, uint64_t first, uint32_t elems, bool u32out,
-                      uint32_t* __restrict__ out)
+    k_lattice_generic(const __grid_constant__ SmallArgs args, uint32_t dims, Div32 div_dims,
+                      uint64_t first, uint32_t elems, bool u32out, uint32_t* __restrict__ out)
 {
+    const uint32_t* g = small_a(args);
+    const uint32_t* shifts = small_b(args);
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < elems; e += stride) {
         const uint32_t p = point_of(e, dims, div_dims);
         const uint32_t j = e - p * dims;
-        uint32_t x = brev32(static_cast<uint32_t>(first + p)) * __ldg(g + j);
+        uint32_t x = brev32(static_cast<uint32_t>(first + p)) * g[j];
         if (shifts)
-            x += __ldg(shifts + j);
+            x += shifts[j];
         out[e] = u32out ? x : map_bits(x);
     }
 }
@@ -333,7 +438,7 @@ int blocks_per_sm(K kernel)
 // from the occupancy of the kernel (a multiple of the SM count).
 template <typename K>
 cudaError_t launch_tiled(K kernel, int log_tp, const FillRange& r, cudaStream_t s,
-                         const uint32_t* a, const uint32_t* b)
+                         const uint32_t* a, const SmallArgs& b)
 {
     const uint64_t tile0 = r.first >> log_tp;
     const uint64_t tile1 = (r.first + r.n + (1ull << log_tp) - 1) >> log_tp;
@@ -345,7 +450,7 @@ cudaError_t launch_tiled(K kernel, int log_tp, const FillRange& r, cudaStream_t 
     const uint64_t used_warps = (ntiles + per_warp - 1) / per_warp;
     const unsigned grid = static_cast<unsigned>((used_warps * 32 + kBlock - 1) / kBlock);
     kernel<<<grid, kBlock, 0, s>>>(a, b, r.first, r.n, tile0, ntiles, per_warp,
-                                   static_cast<uint4*>(r.out));
+                                   static_cast<uint32_t*>(r.out));
     return cudaGetLastError();
 }
 
@@ -368,10 +473,24 @@ cudaError_t launch_chunked(uint32_t dims, const FillRange& r, F&& f)
     return cudaSuccess;
 }
 
-bool fast_dims(uint32_t dims, const FillRange& r)
+// Fast-path lane width for `dims`: 8 dims per lane (256-bit stores) when
+// dims is a multiple of 8 dividing 256 and the output is 32-B aligned; 4
+// dims per lane (128-bit stores) when dims divides 128 and the output is
+// 16-B aligned; 0 = generic path. The issue-bound Owen kernel keeps 4 dims
+// per lane: at 8 its 128 registers halve occupancy (measured 4.3 vs 4.9
+// TB/s), while the HBM-bound kernels gain ~1.5 % from 256-bit stores.
+int fast_dpl(uint32_t dims, const FillRange& r, bool issue_bound = false)
 {
-    return dims >= 4 && dims <= 128 && (128 % dims) == 0 &&
-           (reinterpret_cast<uintptr_t>(r.out) & 15u) == 0;
+    static const int forced = [] {
+        const char* e = std::getenv("QMCGPU_FAST_DPL"); // experiment knob: 4 or 8
+        return e ? std::atoi(e) : 0;
+    }();
+    const uintptr_t a = reinterpret_cast<uintptr_t>(r.out);
+    if (forced != 4 && !issue_bound && dims >= 8 && dims <= 256 && (256 % dims) == 0 && (a & 31u) == 0)
+        return 8;
+    if (dims >= 4 && dims <= 128 && (128 % dims) == 0 && (a & 15u) == 0)
+        return 4;
+    return 0;
 }
 
 int log2u(uint32_t v)
@@ -382,45 +501,90 @@ int log2u(uint32_t v)
     return l;
 }
 
-template <int LOG_PPS>
-cudaError_t sobol_fast_dispatch(const uint32_t* colsT, const uint32_t* words, int mode,
+template <int DPL, int LOG_PPS>
+cudaError_t sobol_fast_dispatch(const uint32_t* colsT, const SmallArgs& words, int mode,
                                 bool u32, const FillRange& r, cudaStream_t s)
 {
     constexpr int LOG_TP = LOG_PPS + 5;
     if (mode == 2)
-        return u32 ? launch_tiled(k_sobol_fast<LOG_PPS, 2, true>, LOG_TP, r, s, colsT, words)
-                   : launch_tiled(k_sobol_fast<LOG_PPS, 2, false>, LOG_TP, r, s, colsT, words);
-    return u32 ? launch_tiled(k_sobol_fast<LOG_PPS, 0, true>, LOG_TP, r, s, colsT, words)
-               : launch_tiled(k_sobol_fast<LOG_PPS, 0, false>, LOG_TP, r, s, colsT, words);
+        return u32 ? launch_tiled(k_sobol_fast<DPL, LOG_PPS, 2, true>, LOG_TP, r, s, colsT, words)
+                   : launch_tiled(k_sobol_fast<DPL, LOG_PPS, 2, false>, LOG_TP, r, s, colsT, words);
+    return u32 ? launch_tiled(k_sobol_fast<DPL, LOG_PPS, 0, true>, LOG_TP, r, s, colsT, words)
+               : launch_tiled(k_sobol_fast<DPL, LOG_PPS, 0, false>, LOG_TP, r, s, colsT, words);
 }
 
-template <int LOG_PPS>
-cudaError_t lattice_fast_dispatch(const uint32_t* g, const uint32_t* sh, bool u32,
-                                  const FillRange& r, cudaStream_t s)
+template <int DPL, int LOG_PPS>
+cudaError_t lattice_fast_dispatch(const SmallArgs& args, bool u32, const FillRange& r,
+                                  cudaStream_t s)
 {
     constexpr int LOG_TP = LOG_PPS + 5;
-    return u32 ? launch_tiled(k_lattice_fast<LOG_PPS, true>, LOG_TP, r, s, g, sh)
-               : launch_tiled(k_lattice_fast<LOG_PPS, false>, LOG_TP, r, s, g, sh);
+    return u32 ? launch_tiled(k_lattice_fast<DPL, LOG_PPS, true>, LOG_TP, r, s, nullptr, args)
+               : launch_tiled(k_lattice_fast<DPL, LOG_PPS, false>, LOG_TP, r, s, nullptr, args);
 }
 
-// Write-only streaming probe: the ceiling a pure 128-bit store stream reaches
-// on this GPU (same grid shape and store hint as the fills). Diagnostic for
-// the roofline denominator, not part of any fill.
+// dims -> LOG_PPS = log2(32 * DPL / dims) dispatch for both fast kernels.
+template <int DPL, typename F>
+cudaError_t by_log_pps(uint32_t dims, F&& f)
+{
+    switch (log2u(32 * DPL / dims)) {
+    case 0: return f(std::integral_constant<int, 0>{});
+    case 1: return f(std::integral_constant<int, 1>{});
+    case 2: return f(std::integral_constant<int, 2>{});
+    case 3: return f(std::integral_constant<int, 3>{});
+    case 4: return f(std::integral_constant<int, 4>{});
+    case 5: return f(std::integral_constant<int, 5>{});
+    }
+    return cudaErrorInvalidValue;
+}
+
+// Write-only streaming probes: the ceiling pure store streams reach on this
+// GPU (diagnostic for the roofline denominator, not part of any fill).
+// mode 0: st.global.cs.v4 grid-stride; 1: st.global.v4 (write-back) grid-
+// stride; 2: st.global.cs.v8 (256-bit) grid-stride; 3: st.global.cs.v4,
+// contiguous chunk per warp (the fills' pattern).
+template <int MODE>
 __global__ void __launch_bounds__(kBlock) k_write_probe(uint4* __restrict__ out, uint64_t n16)
 {
+    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     const uint4 v = make_uint4(blockIdx.x, threadIdx.x, 0x3f000000u, 0u);
-    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n16;
-         k += stride)
-        store4(out + k, v);
+    if (MODE == 0) {
+        for (uint64_t k = tid; k < n16; k += stride)
+            __stcs(out + k, v);
+    } else if (MODE == 1) {
+        for (uint64_t k = tid; k < n16; k += stride)
+            out[k] = v;
+    } else if (MODE == 2) {
+        const uint64_t n32 = n16 / 2;
+        for (uint64_t k = tid; k < n32; k += stride) {
+            uint4* p = out + 2 * k;
+            asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+                         "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(v.x), "r"(v.y), "r"(v.z),
+                         "r"(v.w)
+                         : "memory");
+        }
+    } else {
+        const uint64_t warps = stride / 32, warp = tid / 32, lane = tid % 32;
+        const uint64_t per = (n16 / 32 + warps - 1) / warps * 32;
+        const uint64_t lo = warp * per, hi = lo + per < n16 ? lo + per : n16;
+        for (uint64_t k = lo + lane; k < hi; k += 32)
+            __stcs(out + k, v);
+    }
 }
 
 } // namespace
 
-cudaError_t launch_write_probe(void* out, uint64_t bytes, cudaStream_t s)
+cudaError_t launch_write_probe(void* out, uint64_t bytes, int mode, cudaStream_t s)
 {
-    const unsigned grid = static_cast<unsigned>(sm_count() * blocks_per_sm(k_write_probe));
-    k_write_probe<<<grid, kBlock, 0, s>>>(static_cast<uint4*>(out), bytes / 16);
+    const unsigned grid = static_cast<unsigned>(sm_count() * blocks_per_sm(k_write_probe<0>));
+    uint4* o = static_cast<uint4*>(out);
+    switch (mode) {
+    case 1: k_write_probe<1><<<grid, kBlock, 0, s>>>(o, bytes / 16); break;
+    case 2: k_write_probe<2><<<grid, kBlock, 0, s>>>(o, bytes / 16); break;
+    case 3: k_write_probe<3><<<grid, kBlock, 0, s>>>(o, bytes / 16); break;
+    case 4: return cudaMemsetAsync(out, 0, bytes, s);
+    default: k_write_probe<0><<<grid, kBlock, 0, s>>>(o, bytes / 16); break;
+    }
     return cudaGetLastError();
 }
 
@@ -452,22 +616,21 @@ cudaError_t launch_map_selfcheck(unsigned long long* count, cudaStream_t s)
     return cudaGetLastError();
 }
 
-cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const uint32_t* words,
+cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const SmallArgs& words,
                          uint32_t dims, int mode, bool u32, const FillRange& r, cudaStream_t s)
 {
     if (r.n == 0)
         return cudaSuccess;
     const uint32_t* cols = mode == 2 ? colsT_rev : colsT;
-    if (fast_dims(dims, r)) {
-        switch (log2u(128 / dims)) {
-        case 0: return sobol_fast_dispatch<0>(cols, words, mode, u32, r, s);
-        case 1: return sobol_fast_dispatch<1>(cols, words, mode, u32, r, s);
-        case 2: return sobol_fast_dispatch<2>(cols, words, mode, u32, r, s);
-        case 3: return sobol_fast_dispatch<3>(cols, words, mode, u32, r, s);
-        case 4: return sobol_fast_dispatch<4>(cols, words, mode, u32, r, s);
-        case 5: return sobol_fast_dispatch<5>(cols, words, mode, u32, r, s);
-        }
-    }
+    const int dpl = fast_dpl(dims, r, mode == 2);
+    if (dpl == 8)
+        return by_log_pps<8>(dims, [&](auto lp) {
+            return sobol_fast_dispatch<8, decltype(lp)::value>(cols, words, mode, u32, r, s);
+        });
+    if (dpl == 4)
+        return by_log_pps<4>(dims, [&](auto lp) {
+            return sobol_fast_dispatch<4, decltype(lp)::value>(cols, words, mode, u32, r, s);
+        });
     // the generic kernel reads columns in the normal domain for both modes
     const Div32 d = dims >= 2 ? make_div32(dims) : Div32{0, 0};
     return launch_chunked(dims, r, [&](unsigned grid, uint64_t first, uint32_t elems, uint32_t* o) {
@@ -480,24 +643,23 @@ cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const
     });
 }
 
-cudaError_t launch_lattice(const uint32_t* g, const uint32_t* shifts, uint32_t dims, bool u32,
-                           const FillRange& r, cudaStream_t s)
+cudaError_t launch_lattice(const SmallArgs& args, uint32_t dims, bool u32, const FillRange& r,
+                           cudaStream_t s)
 {
     if (r.n == 0)
         return cudaSuccess;
-    if (fast_dims(dims, r)) {
-        switch (log2u(128 / dims)) {
-        case 0: return lattice_fast_dispatch<0>(g, shifts, u32, r, s);
-        case 1: return lattice_fast_dispatch<1>(g, shifts, u32, r, s);
-        case 2: return lattice_fast_dispatch<2>(g, shifts, u32, r, s);
-        case 3: return lattice_fast_dispatch<3>(g, shifts, u32, r, s);
-        case 4: return lattice_fast_dispatch<4>(g, shifts, u32, r, s);
-        case 5: return lattice_fast_dispatch<5>(g, shifts, u32, r, s);
-        }
-    }
+    const int dpl = fast_dpl(dims, r);
+    if (dpl == 8)
+        return by_log_pps<8>(dims, [&](auto lp) {
+            return lattice_fast_dispatch<8, decltype(lp)::value>(args, u32, r, s);
+        });
+    if (dpl == 4)
+        return by_log_pps<4>(dims, [&](auto lp) {
+            return lattice_fast_dispatch<4, decltype(lp)::value>(args, u32, r, s);
+        });
     const Div32 d = dims >= 2 ? make_div32(dims) : Div32{0, 0};
     return launch_chunked(dims, r, [&](unsigned grid, uint64_t first, uint32_t elems, uint32_t* o) {
-        k_lattice_generic<<<grid, kBlock, 0, s>>>(g, shifts, dims, d, first, elems, u32, o);
+        k_lattice_generic<<<grid, kBlock, 0, s>>>(args, dims, d, first, elems, u32, o);
     });
 }
 
