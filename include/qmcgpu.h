@@ -191,9 +191,33 @@ qmc_status qmc_stream_fill(qmc_sampler_kind kind, const qmc_stream_params* param
                            uint64_t first_index, uint64_t n, qmc_output out_kind, void* out,
                            qmc_stream stream);
 
-/* --------------------------------------------------- render (render.cpp:83-143) */
+/* ------------------------------ integration (quality.cpp:28-66, :214-282) */
 typedef enum qmc_accum { QMC_ACCUM_KAHAN = 0, QMC_ACCUM_INT = 1 } qmc_accum; /* quality.hpp:35 */
 
+typedef enum qmc_integrand_kind {
+    QMC_PRODUCT_SINE = 0, /* prod_j (pi/2) sin(pi x_j), integral 1 */
+    QMC_PRODUCT_POLY = 1, /* prod_j 3 x_j^2, integral 1 */
+    QMC_INDICATOR = 2     /* prod_j [x_j < 0.7], integral 0.7^s */
+} qmc_integrand_kind;
+
+/* builtin_integrand(name, dims) (quality.cpp:68-74): id and exact integral. */
+qmc_status qmc_builtin_integrand(const char* name, uint32_t dims, qmc_integrand_kind* kind,
+                                 double* exact_integral);
+
+typedef struct qmc_integration_row { /* IntegrationRow, quality.hpp:90-95 */
+    uint64_t n;
+    double estimate, abs_error, seconds;
+} qmc_integration_row;
+
+/* integrate(stream, f, n, mode) (quality.cpp:214-282) over the stream made
+ * from (kind, params): fixed 4096-index chunks, one GPU thread per chunk in
+ * index order, chunk partials combined in chunk order — the reference's
+ * worker-count-independent result. */
+qmc_status qmc_integrate(qmc_sampler_kind kind, const qmc_stream_params* params,
+                         qmc_integrand_kind f, uint32_t f_dims, uint64_t n, qmc_accum mode,
+                         qmc_integration_row* row, qmc_stream stream);
+
+/* --------------------------------------------------- render (render.cpp:83-143) */
 typedef struct qmc_render_job { /* RenderJob, render.hpp:31-47 */
     uint32_t width, height, spp;
     qmc_sampler_kind kind;        /* default pixel_shifted_lattice */

@@ -33,6 +33,7 @@ __all__ = [
     "stream_fill", "render", "scene_value", "prime", "prime_max_power", "faure_permutation",
     "default_linear_factors", "lfsr_generator_vector", "pixel_hash", "hilbert_order_for",
     "partition_by_extra_dimension", "halton_pixel_enumeration", "sampler_kind_from_name",
+    "integrate", "builtin_integrand", "write_probe",
     "SAMPLER_KINDS",
 ]
 
@@ -62,6 +63,10 @@ class StreamParams(C.Structure):
 class RenderJob(C.Structure):
     _fields_ = [("width", u32), ("height", u32), ("spp", u32), ("kind", i32), ("accum", i32),
                 ("seed", u32), ("generator", P), ("generator_dims", u32), ("matrices", P)]
+
+
+class IntegrationRow(C.Structure):
+    _fields_ = [("n", u64), ("estimate", f64), ("abs_error", f64), ("seconds", f64)]
 
 
 class HaltonEnumeration(C.Structure):
@@ -116,6 +121,9 @@ def lib():
     sig("qmc_stream_fill", i32, i32, C.POINTER(StreamParams), u64, u64, i32, P, P)
     sig("qmc_render", i32, C.POINTER(RenderJob), u32, u32, P, P)
     sig("qmc_scene_value", i32, P, P, u64, P)
+    sig("qmc_builtin_integrand", i32, C.c_char_p, u32, C.POINTER(i32), C.POINTER(f64))
+    sig("qmc_integrate", i32, i32, C.POINTER(StreamParams), i32, u32, u64, i32,
+        C.POINTER(IntegrationRow), P)
     _lib = L
     return L
 
@@ -369,6 +377,16 @@ def stream_fill(kind: str, n: int, dims: int = 2, first: int = 0, *, generator=N
                 xor_point_count: int = 1, fixed: bool = False, out=None, stream=None):
     """make_stream(kind, params) + SampleStream::sample(i, j) (imageplane.cpp:310-461)."""
     k = sampler_kind_from_name(kind)
+    p, keep = _stream_params(dims, generator, matrices, sobol_scrambles, scramble, linear_factors,
+                             pixel, order, spp, width, height, xor_seed, xor_point_count)
+    o = _alloc(n, dims, fixed, out)
+    _check(lib().qmc_stream_fill(k, C.byref(p), first, n, 1 if fixed else 0, _ptr(o),
+                                 _stream(stream)))
+    return o
+
+
+def _stream_params(dims, generator, matrices, sobol_scrambles, scramble, linear_factors, pixel,
+                   order, spp, width, height, xor_seed, xor_point_count):
     if scramble not in _RADICAL:
         raise ConfigError("make_stream: scramble must be plain, faure, or linear")
     keep = []
@@ -392,10 +410,40 @@ def stream_fill(kind: str, n: int, dims: int = 2, first: int = 0, *, generator=N
     p.px, p.py = pixel
     p.order, p.spp, p.width, p.height = order, spp, width, height
     p.xor_seed, p.xor_point_count = xor_seed, xor_point_count
-    o = _alloc(n, dims, fixed, out)
-    _check(lib().qmc_stream_fill(k, C.byref(p), first, n, 1 if fixed else 0, _ptr(o),
-                                 _stream(stream)))
-    return o
+    return p, keep
+
+
+_INTEGRANDS = {"product-sine": 0, "product-poly": 1, "indicator": 2}
+
+
+def builtin_integrand(name: str, dims: int):
+    """(id, exact integral) of builtin_integrand(name, dims) (quality.cpp:28-74)."""
+    k, ex = i32(), f64()
+    _check(lib().qmc_builtin_integrand(name.encode(), dims, C.byref(k), C.byref(ex)))
+    return k.value, ex.value
+
+
+def integrate(kind: str, integrand: str, n: int, dims: int, accum: str = "kahan", *,
+              stream_dims: Optional[int] = None, generator=None,
+              matrices: Optional[GeneratorMatrixSet] = None, sobol_scrambles=None,
+              scramble: str = "plain", linear_factors=None, pixel=(0, 0), order: int = 1,
+              spp: int = 1, width: int = 0, height: int = 0, xor_seed: int = 0,
+              xor_point_count: int = 1, stream=None) -> dict:
+    """integrate(make_stream(kind, ...), builtin_integrand(integrand, dims), n, accum)
+    (quality.cpp:214-282); returns the IntegrationRow fields as a dict."""
+    k = sampler_kind_from_name(kind)
+    if accum not in _ACCUM:
+        raise ConfigError("accumulation mode must be 'kahan' or 'int'")
+    if integrand not in _INTEGRANDS:
+        raise ConfigError("unknown integrand: " + integrand)
+    sd = dims if stream_dims is None else stream_dims
+    p, keep = _stream_params(sd, generator, matrices, sobol_scrambles, scramble, linear_factors,
+                             pixel, order, spp, width, height, xor_seed, xor_point_count)
+    row = IntegrationRow()
+    _check(lib().qmc_integrate(k, C.byref(p), _INTEGRANDS[integrand], dims, n, _ACCUM[accum],
+                               C.byref(row), _stream(stream)))
+    return {"n": row.n, "estimate": row.estimate, "abs_error": row.abs_error,
+            "seconds": row.seconds}
 
 
 def render(width: int, height: int, spp: int = 1, kind: str = "pixel-shifted-lattice",

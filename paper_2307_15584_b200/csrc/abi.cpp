@@ -11,6 +11,8 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -1043,166 +1045,312 @@ XorTablesDev white_noise_tables(uint32_t dims, uint32_t point_count, uint32_t se
 
 } // namespace
 
+namespace {
+
+// make_stream (imageplane.cpp:310-416) for one pixel context: validates the
+// parameters with the reference's ConfigError conditions and resolves the
+// device-side state the kernels read. Owns every device resource until it
+// goes out of scope (callers synchronize before that).
+struct ResolvedStream {
+    PixelStreamParams q{};
+    std::unique_ptr<qmc_matrices> own_matrices;
+    qmc_matrices* matrices = nullptr; // sobol
+    std::vector<uint32_t> sobol_words; // sobol scrambles (may be empty)
+    XorTablesDev xt;
+    std::vector<uint32_t> pool;
+    std::vector<size_t> soff;
+    std::vector<RadicalDim> rd;
+    size_t goff = SIZE_MAX, roff = SIZE_MAX, woff = SIZE_MAX;
+    qmc_radical_scramble halton_sc = QMC_RADICAL_PLAIN;
+};
+
+void resolve_stream(qmc_sampler_kind kind, const qmc_stream_params* p, cudaStream_t s,
+                    ResolvedStream& r, CallArgs& args, CallArgs& pargs)
+{
+    if (!p)
+        fail(QMC_INVALID_ARGUMENT, "stream params are null");
+    if (kind < 0 || kind > 7)
+        fail(QMC_CONFIG, "unknown sampler kind");
+    require(p->dims >= 1, "make_stream: dims must be >= 1");
+    const uint32_t dims = p->dims;
+    auto halton_scramble = [&]() -> qmc_radical_scramble {
+        if (p->halton_scramble > 2)
+            fail(QMC_CONFIG, "make_stream: scramble must be plain, faure, or linear");
+        if (p->halton_scramble == QMC_RADICAL_LINEAR && p->linear_factors)
+            require(p->linear_factors_len >= dims,
+                    "make_stream: linear factor list shorter than dims");
+        return static_cast<qmc_radical_scramble>(p->halton_scramble);
+    };
+    auto lattice_vector = [&]() {
+        require(p->generator && p->generator_dims > 0, "make_stream: generator vector required");
+        for (uint32_t j = 0; j < p->generator_dims; ++j)
+            require(p->generator[j] & 1u, "make_stream: generator components must be odd");
+        require(dims <= p->generator_dims, "make_stream: dims beyond the generator vector");
+        r.goff = args.add(p->generator, dims * 4);
+    };
+    auto validate_pixel = [&]() {
+        require(p->order >= 1 && p->order <= 31, "make_stream: pixel order must be in [1, 31]");
+        require(p->px < (1u << p->order) && p->py < (1u << p->order),
+                "make_stream: pixel outside the 2^order grid");
+    };
+    PixelStreamParams& q = r.q;
+    q.kind = kind;
+    q.dims = dims;
+    q.px = p->px;
+    q.py = p->py;
+    q.order = p->order;
+    q.spp = p->spp;
+    q.width = p->width;
+    q.height = p->height;
+    switch (kind) {
+    case QMC_KIND_SOBOL:
+        r.matrices = const_cast<qmc_matrices*>(p->matrices);
+        if (!r.matrices) {
+            r.own_matrices.reset(new_matrices(build_columns(builtin_rows(), dims), dims));
+            r.matrices = r.own_matrices.get();
+        }
+        require(dims <= r.matrices->dims, "make_stream: dims beyond the generator matrices");
+        if (p->sobol_scrambles) {
+            require(p->sobol_scrambles_len >= dims, "make_stream: scramble list shorter than dims");
+            r.sobol_words.assign(p->sobol_scrambles, p->sobol_scrambles + dims);
+            r.woff = args.add(r.sobol_words.data(), dims * 4);
+        }
+        break;
+    case QMC_KIND_HALTON:
+        require(dims <= kPrimes, "make_stream: dims beyond the prime table");
+        r.halton_sc = halton_scramble();
+        r.rd = radical_dims(dims, 0, r.halton_sc, p->linear_factors, r.pool, r.soff);
+        break;
+    case QMC_KIND_LATTICE:
+        lattice_vector();
+        break;
+    case QMC_KIND_HALTON_HILBERT:
+        require(p->spp >= 1, "make_stream: spp must be >= 1");
+        validate_pixel();
+        require(dims <= kPrimes, "halton_point: dims beyond the prime table");
+        r.rd = radical_dims(dims, 0, halton_scramble(), p->linear_factors, r.pool, r.soff);
+        break;
+    case QMC_KIND_PIXEL_SHIFTED_LATTICE:
+        validate_pixel();
+        lattice_vector();
+        break;
+    case QMC_KIND_PIXEL_RANDOM_LATTICE:
+        break;
+    case QMC_KIND_IMAGE_PLANE_HALTON: {
+        require(p->width >= 1 && p->height >= 1,
+                "make_stream: image size required for image-plane halton");
+        require(p->px < p->width && p->py < p->height, "make_stream: pixel outside the image");
+        require(dims <= kPrimes, "make_stream: dims beyond the prime table");
+        const HaltonEnum e = halton_enum(p->width, p->height);
+        if (p->linear_factors)
+            require(p->linear_factors_len >= dims,
+                    "make_stream: linear factor list shorter than dims");
+        r.rd = radical_dims(dims, 0, QMC_RADICAL_LINEAR, p->linear_factors, r.pool, r.soff);
+        q.scale_x = e.sx;
+        q.scale_y = e.sy;
+        q.exp_x = e.ex;
+        q.exp_y = e.ey;
+        q.stride = e.stride;
+        q.crt_x = e.crt_x;
+        q.crt_y = e.crt_y;
+        break;
+    }
+    case QMC_KIND_SOBOL_XOR_TABLE: {
+        r.xt = white_noise_tables(dims, p->xor_point_count, p->xor_seed, s);
+        require(dims <= r.xt.dims, "make_stream: dims beyond the stored point set");
+        q.xor_reorder = static_cast<const uint32_t*>(r.xt.reorder.get());
+        q.xor_scramble = static_cast<const uint32_t*>(r.xt.scramble.get());
+        q.xor_points = static_cast<const uint32_t*>(r.xt.points.get());
+        q.xor_point_count = r.xt.point_count;
+        q.xor_dims = r.xt.dims;
+        break;
+    }
+    }
+    // radical tables: the permutation pool goes first (its device address is
+    // patched into the RadicalDim records), then everything else
+    if (!r.rd.empty()) {
+        r.pool.push_back(0u); // never empty
+        pargs.add(r.pool.data(), r.pool.size() * 4);
+        pargs.upload();
+        const uint32_t* pool_dev = pargs.at<uint32_t>(0);
+        for (size_t j = 0; j < r.rd.size(); ++j)
+            if (r.soff[j] != SIZE_MAX)
+                r.rd[j].sigma = pool_dev + r.soff[j];
+        r.roff = args.add(r.rd.data(), r.rd.size() * sizeof(RadicalDim));
+    }
+    args.upload();
+    if (r.goff != SIZE_MAX)
+        q.generator = args.at<uint32_t>(r.goff);
+    if (r.roff != SIZE_MAX)
+        q.radical_dims = args.at<RadicalDim>(r.roff);
+}
+
+} // namespace
+
 qmc_status qmc_stream_fill(qmc_sampler_kind kind, const qmc_stream_params* p,
                            uint64_t first_index, uint64_t n, qmc_output out_kind, void* out,
                            qmc_stream stream)
 {
     return guard([&] {
+        const cudaStream_t s = as_stream(stream);
         if (!p)
             fail(QMC_INVALID_ARGUMENT, "stream params are null");
-        const cudaStream_t s = as_stream(stream);
-        require(p->dims >= 1, "make_stream: dims must be >= 1");
         const uint32_t dims = p->dims;
-        auto halton_scramble = [&]() -> qmc_radical_scramble {
-            if (p->halton_scramble > 2)
-                fail(QMC_CONFIG, "make_stream: scramble must be plain, faure, or linear");
-            if (p->halton_scramble == QMC_RADICAL_LINEAR && p->linear_factors)
-                require(p->linear_factors_len >= dims,
-                        "make_stream: linear factor list shorter than dims");
-            return static_cast<qmc_radical_scramble>(p->halton_scramble);
-        };
-        auto lattice_vector = [&]() {
-            require(p->generator && p->generator_dims > 0, "make_stream: generator vector required");
-            for (uint32_t j = 0; j < p->generator_dims; ++j)
-                require(p->generator[j] & 1u, "make_stream: generator components must be odd");
-            require(dims <= p->generator_dims, "make_stream: dims beyond the generator vector");
-        };
-        auto validate_pixel = [&]() {
-            require(p->order >= 1 && p->order <= 31, "make_stream: pixel order must be in [1, 31]");
-            require(p->px < (1u << p->order) && p->py < (1u << p->order),
-                    "make_stream: pixel outside the 2^order grid");
-        };
-        const bool u32 = out_kind == QMC_OUT_U32;
-        switch (kind) {
-        case QMC_KIND_SOBOL: {
-            std::unique_ptr<qmc_matrices> own;
-            qmc_matrices* m = const_cast<qmc_matrices*>(p->matrices);
-            if (!m) {
-                own.reset(new_matrices(build_columns(builtin_rows(), dims), dims));
-                m = own.get();
+        // the non-pixel kinds are the batched fills
+        if (kind == QMC_KIND_SOBOL || kind == QMC_KIND_HALTON || kind == QMC_KIND_LATTICE) {
+            CallArgs args(s), pargs(s);
+            ResolvedStream r;
+            resolve_stream(kind, p, s, r, args, pargs);
+            if (kind == QMC_KIND_SOBOL) {
+                sobol_fill_impl(r.matrices, first_index, n, dims,
+                                r.sobol_words.empty() ? QMC_SOBOL_NONE : QMC_SOBOL_XOR,
+                                r.sobol_words.empty() ? nullptr : r.sobol_words.data(), out_kind,
+                                out, s);
+            } else if (kind == QMC_KIND_HALTON) {
+                // SampleStream::sample casts the index to 32 bits (the kernel wraps too)
+                halton_fill_impl(first_index, n, dims, 0, r.halton_sc, p->linear_factors,
+                                 out_kind, out, s);
+            } else {
+                lattice_fill_impl(p->generator, nullptr, dims, first_index, n, out_kind, out, s);
             }
-            require(dims <= m->dims, "make_stream: dims beyond the generator matrices");
-            if (p->sobol_scrambles)
-                require(p->sobol_scrambles_len >= dims, "make_stream: scramble list shorter than dims");
-            sobol_fill_impl(m, first_index, n, dims,
-                            p->sobol_scrambles ? QMC_SOBOL_XOR : QMC_SOBOL_NONE, p->sobol_scrambles,
-                            out_kind, out, s);
-            if (own)
-                cuda_ok(cudaStreamSynchronize(s), "sync");
-            return;
-        }
-        case QMC_KIND_HALTON: {
-            require(dims <= kPrimes, "make_stream: dims beyond the prime table");
-            const auto sc = halton_scramble();
-            // SampleStream::sample casts the index to 32 bits (wraps, like the kernel)
-            halton_fill_impl(first_index, n, dims, 0, sc, p->linear_factors, out_kind, out, s);
-            return;
-        }
-        case QMC_KIND_LATTICE:
-            lattice_vector();
-            lattice_fill_impl(p->generator, nullptr, dims, first_index, n, out_kind, out, s);
-            return;
-        default:
-            break;
-        }
-        if (kind < 0 || kind > 7)
-            fail(QMC_CONFIG, "unknown sampler kind");
-
-        PixelStreamParams q{};
-        q.kind = kind;
-        q.dims = dims;
-        q.px = p->px;
-        q.py = p->py;
-        q.order = p->order;
-        q.spp = p->spp;
-        q.width = p->width;
-        q.height = p->height;
-        CallArgs args(s);
-        std::vector<uint32_t> pool;
-        std::vector<size_t> soff;
-        std::vector<RadicalDim> rd;
-        size_t goff = SIZE_MAX;
-        XorTablesDev xt;
-        switch (kind) {
-        case QMC_KIND_HALTON_HILBERT: {
-            require(p->spp >= 1, "make_stream: spp must be >= 1");
-            validate_pixel();
-            require(dims <= kPrimes, "halton_point: dims beyond the prime table");
-            rd = radical_dims(dims, 0, halton_scramble(), p->linear_factors, pool, soff);
-            if (first_index >= p->spp || n > p->spp - first_index)
-                fail(QMC_OUT_OF_RANGE, "SampleStream: sample index beyond the pixel block");
-            break;
-        }
-        case QMC_KIND_PIXEL_SHIFTED_LATTICE:
-            validate_pixel();
-            lattice_vector();
-            goff = args.add(p->generator, dims * 4);
-            break;
-        case QMC_KIND_PIXEL_RANDOM_LATTICE:
-            break;
-        case QMC_KIND_IMAGE_PLANE_HALTON: {
-            require(p->width >= 1 && p->height >= 1,
-                    "make_stream: image size required for image-plane halton");
-            require(p->px < p->width && p->py < p->height, "make_stream: pixel outside the image");
-            require(dims <= kPrimes, "make_stream: dims beyond the prime table");
-            const HaltonEnum e = halton_enum(p->width, p->height);
-            if (p->linear_factors)
-                require(p->linear_factors_len >= dims,
-                        "make_stream: linear factor list shorter than dims");
-            rd = radical_dims(dims, 0, QMC_RADICAL_LINEAR, p->linear_factors, pool, soff);
-            q.scale_x = e.sx;
-            q.scale_y = e.sy;
-            q.exp_x = e.ex;
-            q.exp_y = e.ey;
-            q.stride = e.stride;
-            q.crt_x = e.crt_x;
-            q.crt_y = e.crt_y;
-            break;
-        }
-        case QMC_KIND_SOBOL_XOR_TABLE: {
-            const uint32_t pc = p->xor_point_count;
-            xt = white_noise_tables(dims, pc, p->xor_seed, s);
-            require(dims <= xt.dims, "make_stream: dims beyond the stored point set");
-            if (first_index >= pc || n > pc - first_index)
-                fail(QMC_OUT_OF_RANGE, "xor_table_sample: index beyond the stored point set");
-            q.xor_reorder = static_cast<const uint32_t*>(xt.reorder.get());
-            q.xor_scramble = static_cast<const uint32_t*>(xt.scramble.get());
-            q.xor_points = static_cast<const uint32_t*>(xt.points.get());
-            q.xor_point_count = pc;
-            q.xor_dims = xt.dims;
-            break;
-        }
-        default:
-            break;
-        }
-        if (n == 0)
-            return;
-        // radical tables: permutation pool first (pointers patched), then dims
-        if (!rd.empty()) {
-            CallArgs pargs(s);
-            pool.push_back(0u); // never empty
-            pargs.add(pool.data(), pool.size() * 4);
-            pargs.upload();
-            const uint32_t* pool_dev = pargs.at<uint32_t>(0);
-            for (size_t j = 0; j < rd.size(); ++j)
-                if (soff[j] != SIZE_MAX)
-                    rd[j].sigma = pool_dev + soff[j];
-            const size_t roff = args.add(rd.data(), rd.size() * sizeof(RadicalDim));
-            args.upload();
-            q.radical_dims = args.at<RadicalDim>(roff);
-            place_fill(out, first_index, n, dims, s, [&](const FillRange& r, cudaStream_t st) {
-                return launch_pixel_stream(q, u32, r, st);
-            });
             cuda_ok(cudaStreamSynchronize(s), "sync");
             return;
         }
-        args.upload();
-        if (goff != SIZE_MAX)
-            q.generator = args.at<uint32_t>(goff);
-        place_fill(out, first_index, n, dims, s, [&](const FillRange& r, cudaStream_t st) {
-            return launch_pixel_stream(q, u32, r, st);
+        CallArgs args(s), pargs(s);
+        ResolvedStream r;
+        resolve_stream(kind, p, s, r, args, pargs);
+        if (kind == QMC_KIND_HALTON_HILBERT && (first_index >= p->spp || n > p->spp - first_index))
+            fail(QMC_OUT_OF_RANGE, "SampleStream: sample index beyond the pixel block");
+        if (kind == QMC_KIND_SOBOL_XOR_TABLE &&
+            (first_index >= r.q.xor_point_count || n > r.q.xor_point_count - first_index))
+            fail(QMC_OUT_OF_RANGE, "xor_table_sample: index beyond the stored point set");
+        if (n == 0)
+            return;
+        const bool u32 = out_kind == QMC_OUT_U32;
+        place_fill(out, first_index, n, dims, s, [&](const FillRange& fr, cudaStream_t st) {
+            return launch_pixel_stream(r.q, u32, fr, st);
         });
         cuda_ok(cudaStreamSynchronize(s), "sync"); // tables owned by this call
+    });
+}
+
+// --------------------------------------------------------------- integrate
+
+static const char* const kIntegrandNames[] = {"product-sine", "product-poly", "indicator"};
+
+qmc_status qmc_builtin_integrand(const char* name, uint32_t dims, qmc_integrand_kind* kind,
+                                 double* exact_integral)
+{
+    return guard([&] {
+        if (dims == 0)
+            fail(QMC_INVALID_ARGUMENT, "builtin_integrands: dims must be >= 1");
+        const std::string n = name ? name : "";
+        for (int k = 0; k < 3; ++k)
+            if (n == kIntegrandNames[k]) {
+                if (kind)
+                    *kind = static_cast<qmc_integrand_kind>(k);
+                if (exact_integral) // quality.cpp:38-66
+                    *exact_integral = k == 2 ? std::pow(0.7, static_cast<double>(dims)) : 1.0;
+                return;
+            }
+        fail(QMC_CONFIG, "unknown integrand: " + n);
+    });
+}
+
+qmc_status qmc_integrate(qmc_sampler_kind kind, const qmc_stream_params* p,
+                         qmc_integrand_kind f, uint32_t f_dims, uint64_t n, qmc_accum mode,
+                         qmc_integration_row* row, qmc_stream stream)
+{
+    return guard([&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        const cudaStream_t s = as_stream(stream);
+        if (f < 0 || f > 2)
+            fail(QMC_CONFIG, "unknown integrand");
+        if (f_dims == 0)
+            fail(QMC_INVALID_ARGUMENT, "builtin_integrands: dims must be >= 1");
+        if (mode != QMC_ACCUM_KAHAN && mode != QMC_ACCUM_INT)
+            fail(QMC_CONFIG, "accumulation mode must be 'kahan' or 'int'");
+        if (n == 0)
+            fail(QMC_INVALID_ARGUMENT, "integrate: n must be >= 1");
+        if (!p)
+            fail(QMC_INVALID_ARGUMENT, "stream params are null");
+        if (p->dims < f_dims)
+            fail(QMC_INVALID_ARGUMENT, "integrate: stream has fewer dimensions than the integrand");
+        if (f_dims > integrate_max_dims())
+            fail(QMC_INVALID_ARGUMENT, "integrate: at most 64 integrand dimensions on the device");
+        CallArgs args(s), pargs(s);
+        ResolvedStream r;
+        resolve_stream(kind, p, s, r, args, pargs);
+        // sample-time preconditions of SampleStream::sample over [0, n)
+        if (kind == QMC_KIND_SOBOL && n > (1ull << 52))
+            fail(QMC_INVALID_ARGUMENT, "sobol_component: index must be below 2^52");
+        if (kind == QMC_KIND_HALTON_HILBERT && n > p->spp)
+            fail(QMC_OUT_OF_RANGE, "SampleStream: sample index beyond the pixel block");
+        if (kind == QMC_KIND_SOBOL_XOR_TABLE && n > r.q.xor_point_count)
+            fail(QMC_OUT_OF_RANGE, "xor_table_sample: index beyond the stored point set");
+        if (kind == QMC_KIND_HALTON || kind == QMC_KIND_HALTON_HILBERT ||
+            kind == QMC_KIND_IMAGE_PLANE_HALTON)
+            for (const RadicalDim& d : r.rd)
+                if (d.mode == 1 && (d.factor == 0 || d.factor >= d.base))
+                    fail(QMC_INVALID_ARGUMENT,
+                         "radical_inverse_linscramble: factor must be in [1, base)");
+
+        IntegrateParams ip{};
+        ip.pix = r.q;
+        ip.fn = f;
+        ip.fdims = f_dims;
+        ip.n = n;
+        if (kind == QMC_KIND_SOBOL) {
+            const auto& dev = r.matrices->on_device();
+            ip.colsT = static_cast<const uint32_t*>(dev.colsT.get());
+            ip.mdims = r.matrices->dims;
+            ip.words = r.woff == SIZE_MAX ? nullptr : args.at<uint32_t>(r.woff);
+        }
+        const uint64_t chunks = (n + 4095) / 4096;
+        double* partial = nullptr;
+        unsigned long long* scal = nullptr; // [0] int sum, [1] first bad index
+        cuda_ok(cudaMallocAsync(&partial, chunks * 8, s), "cudaMallocAsync");
+        cuda_ok(cudaMallocAsync(&scal, 16, s), "cudaMallocAsync");
+        const unsigned long long init[2] = {0ull, ~0ull};
+        cuda_ok(cudaMemcpyAsync(scal, init, 16, cudaMemcpyHostToDevice, s), "H2D");
+        cuda_ok(launch_integrate(ip, mode, partial, scal, scal + 1, s), "launch_integrate");
+        std::vector<double> hp(mode == QMC_ACCUM_KAHAN ? chunks : 0);
+        unsigned long long hs[2] = {0, 0};
+        if (!hp.empty())
+            cuda_ok(cudaMemcpyAsync(hp.data(), partial, chunks * 8, cudaMemcpyDeviceToHost, s),
+                    "D2H");
+        cuda_ok(cudaMemcpyAsync(hs, scal, 16, cudaMemcpyDeviceToHost, s), "D2H");
+        cudaFreeAsync(partial, s);
+        cudaFreeAsync(scal, s);
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        if (hs[1] != ~0ull)
+            fail(QMC_INTERNAL, std::string("integrate: non-finite value of '") +
+                                   kIntegrandNames[f] + "' at index " + std::to_string(hs[1]));
+        double estimate;
+        if (mode == QMC_ACCUM_KAHAN) { // rank-ordered CompensatedSum, quality.cpp:262-267
+            double sum = 0.0, comp = 0.0;
+            for (double v : hp) {
+                const double t = sum + v;
+                if (std::fabs(sum) >= std::fabs(v))
+                    comp += (sum - t) + v;
+                else
+                    comp += (v - t) + sum;
+                sum = t;
+            }
+            estimate = (sum + comp) / static_cast<double>(n);
+        } else { // exact 64-bit sum, quality.cpp:268-272
+            estimate = static_cast<double>(static_cast<long long>(hs[0])) / 4294967296.0 /
+                       static_cast<double>(n);
+        }
+        double exact = 1.0;
+        qmc_builtin_integrand(kIntegrandNames[f], f_dims, nullptr, &exact);
+        if (row) {
+            row->n = n;
+            row->estimate = estimate;
+            row->abs_error = std::fabs(estimate - exact);
+            row->seconds =
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
     });
 }
 

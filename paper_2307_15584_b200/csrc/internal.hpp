@@ -76,6 +76,17 @@ struct SmallArgs {
     uint32_t b[kSmall];
 };
 
+// Fused QMC integration (quality.cpp:214-282): the stream's pixel-context
+// state plus the integrand and (sobol) matrices / scrambles on the device.
+struct IntegrateParams {
+    PixelStreamParams pix; // pix.kind = sampler kind, pix.dims = stream dims
+    uint32_t fn, fdims;    // integrand id, integrand dims (<= stream dims)
+    uint64_t n;
+    const uint32_t* colsT; // sobol: device [52][mdims]
+    uint32_t mdims;
+    const uint32_t* words; // sobol: device XOR scrambles or null
+};
+
 // ------------------------------------------------------------ launchers
 // All launchers write DEVICE memory and are asynchronous on `s`.
 cudaError_t launch_map(const uint32_t* in, float* out, uint64_t n, cudaStream_t s);
@@ -109,6 +120,12 @@ cudaError_t launch_scene_value(const double* xy, double* out, uint64_t n, cudaSt
 
 // Write-only 128-bit streaming store probe over `bytes` (diagnostic).
 cudaError_t launch_write_probe(void* out, uint64_t bytes, int mode, cudaStream_t s);
+
+// partial: device [ceil(n/4096)] chunk sums (kahan); isum: exact int64 sum
+// (int); bad: first index with a non-finite integrand value (~0 if none).
+cudaError_t launch_integrate(const IntegrateParams& p, uint32_t accum, double* partial,
+                             unsigned long long* isum, unsigned long long* bad, cudaStream_t s);
+uint32_t integrate_max_dims();
 
 // Number of SMs of the current device (cached).
 int sm_count();

@@ -229,15 +229,19 @@ def main() -> None:
         bc[k] = "%016x" % cs.value
     G["bench_checksums_65536x32"] = bc
 
-    # ---- integrate (quality.cpp:214-282)
+    # ---- integrate (quality.cpp:214-282); the shim builds the stream like
+    # the CLI: lattice g = lfsr(0xace1, max(dims,2)), sobol scrambles =
+    # pixel_hash(j, seed, 0x5eed) when seed != 0 (qmckit.cpp:110-119)
     integ = []
-    for kind in ["sobol", "lattice"]:
+    for kind, seed in [("sobol", 0), ("sobol", 7), ("lattice", 0), ("halton", 0),
+                       ("pixel-random-lattice", 0)]:
         for f in ["product-sine", "product-poly", "indicator"]:
             for accum in ["kahan", "int"]:
-                e = C.c_double()
-                ok(ref.ref_integrate(kind.encode(), 3, 0, f.encode(), 10000, accum.encode(), 4,
-                                     C.byref(e)))
-                integ.append([kind, f, accum, 3, 10000, e.value])
+                for dims, n in [(3, 10000), (5, (1 << 20) + 5)]:
+                    e = C.c_double()
+                    ok(ref.ref_integrate(kind.encode(), dims, seed, f.encode(), n, accum.encode(),
+                                         8, C.byref(e)))
+                    integ.append([kind, seed, f, accum, dims, n, e.value])
     G["integrate"] = integ
 
     with open(os.path.join(HERE, "golden.json"), "w") as f:

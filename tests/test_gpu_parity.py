@@ -368,3 +368,78 @@ def test_repeated_calls_stay_fast():
         ms.append(a.elapsed_time(b))
     ms = sorted(ms[2:])
     assert ms[-1] < 2.5 * ms[len(ms) // 2], ms
+
+
+def test_host_output_pipeline_matches_device():
+    """HOST outputs (the e2e path: chunked device fill + D2H) equal the
+    device fills, across many 64 MiB chunks, pinned and pageable."""
+    n, dims = (1 << 21) + 77, 64  # ~512 MiB -> 9 chunks
+    dev = u32(q.sobol_fill(n, dims, first=5, scramble="owen", words=list(range(64)), fixed=True))
+    pinned = torch.empty((n, dims), dtype=torch.int32, pin_memory=True).numpy()
+    q.sobol_fill(n, dims, first=5, scramble="owen", words=list(range(64)), fixed=True, out=pinned)
+    np.testing.assert_array_equal(pinned.view(np.uint32), dev.reshape(n, dims))
+    page = np.empty((3001, 16), np.float32)
+    g = q.lfsr_generator_vector(0xACE1, 16)
+    q.lattice_fill(3001, g, first=99, out=page)
+    np.testing.assert_array_equal(page.view(np.uint32), u32(q.lattice_fill(3001, g, first=99)))
+    img = np.empty((40, 64), np.float32)
+    q.render(64, 64, 4, rows=(10, 50), out=img)
+    np.testing.assert_array_equal(img, q.render(64, 64, 4, rows=(10, 50)).cpu().numpy())
+
+
+def test_empty_and_degenerate_fills():
+    out = torch.full((4, 4), 7.0, device="cuda")
+    q.sobol_fill(0, 4, out=out)
+    q.lattice_fill(0, [1, 3, 5, 7], out=out)
+    q.halton_fill(0, 4, out=out)
+    assert float(out.sum()) == 7.0 * 16  # nothing written
+    one = u32(q.sobol_fill(1, 1, first=(1 << 52) - 1, fixed=True))
+    assert one.size == 1
+
+
+# ------------------------------------------------------------- integrate
+def test_integrate_vs_reference_goldens(golden):
+    """integrate() (quality.cpp:214-282) for every recorded (kind, integrand,
+    accum, dims, n): same chunking and combine order as the reference; the
+    estimate agrees to 1e-12 relative (FP64 sin is the only non-bit-exact
+    step) and is reported bit-exact where it is."""
+    exact = 0
+    for kind, seed, f, accum, dims, n, est in golden["integrate"]:
+        kw = {}
+        if kind == "lattice":
+            kw["generator"] = q.lfsr_generator_vector(0xACE1, max(dims, 2))
+        if kind == "sobol" and seed:
+            kw["sobol_scrambles"] = [q.pixel_hash(j, seed, 0x5EED) for j in range(dims)]
+        row = q.integrate(kind, f, n, dims, accum, **kw)
+        assert row["n"] == n
+        rel = abs(row["estimate"] - est) / max(abs(est), 1e-300)
+        assert rel <= 1e-12, (kind, seed, f, accum, dims, n, row["estimate"], est)
+        exact += row["estimate"] == est
+        _, ex = q.builtin_integrand(f, dims)
+        assert row["abs_error"] == abs(row["estimate"] - ex)
+    print("integrate: %d of %d estimates bit-identical to the reference"
+          % (exact, len(golden["integrate"])))
+    assert exact >= len(golden["integrate"]) // 2
+
+
+def test_integrate_errors():
+    with pytest.raises(ValueError):
+        q.integrate("sobol", "product-sine", 0, 3)
+    with pytest.raises(ValueError):
+        q.integrate("sobol", "product-sine", 100, 3, stream_dims=2)
+    with pytest.raises(q.ConfigError):
+        q.integrate("sobol", "nope", 100, 3)
+    with pytest.raises(ValueError):
+        q.builtin_integrand("indicator", 0)
+    assert q.builtin_integrand("indicator", 3)[1] == 0.7 ** 3
+
+
+def test_integrate_pixel_kinds_vs_reference(ref):
+    import ctypes as C
+    for kind in ["halton", "pixel-random-lattice"]:
+        for f in ["product-sine", "product-poly"]:
+            e = C.c_double()
+            assert ref.ref_integrate(kind.encode(), 4, 0, f.encode(), 50000, b"kahan", 4,
+                                     C.byref(e)) == 0
+            row = q.integrate(kind, f, 50000, 4)
+            assert abs(row["estimate"] - e.value) <= 1e-12 * abs(e.value)
