@@ -301,10 +301,13 @@ def run_ours(args):
         del host, hn
 
     extra = {}
-    if not args.no_extra and rank == 0:
+    if not args.no_extra:
         del out
         torch.cuda.empty_cache()
-        extra = run_extra(q, stream, peak, args)
+        if world > 1:
+            extra["c5_render_4k_distributed"] = run_render_distributed(q, world, stream)
+        if rank == 0:
+            extra.update(run_extra(q, stream, peak, args))
 
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -351,6 +354,33 @@ def run_ours(args):
 
         dist.destroy_process_group()
     return 0
+
+
+def run_render_distributed(q, world, stream):
+    """C5 across ranks: row bands + one NCCL all-gather (bit-identical to the
+    1-GPU image); device time, max over ranks."""
+    import torch
+
+    from paper_2307_15584_b200.distributed import render_distributed
+
+    res = {}
+    for spp in (16, 256):
+        fn = lambda: render_distributed(3840, 2160, spp)  # noqa: E731
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        barrier(world)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(3):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms = max_over_ranks(a.elapsed_time(b) / 3, world)
+        res["pixel-shifted-lattice/spp%d" % spp] = {
+            "value": 3840 * 2160 * spp / (ms * 1e-3) / 1e9, "unit": "G pixel-samples/s",
+            "ms_per_step": ms, "n_gpus": world, "collective": "all_gather_into_tensor (NCCL)"}
+    return res
 
 
 def run_extra(q, stream, peak, args):
@@ -405,6 +435,16 @@ def run_extra(q, stream, peak, args):
                 "value": 3840 * 2160 * spp / (avg * 1e-3) / 1e9, "unit": "G pixel-samples/s",
                 "ms_per_step": avg}
     res["c5_render_4k"] = c5
+    # next row: fused QMC integration (quality.cpp:214-282), Sobol' 8 dims
+    ni = 1 << 26
+    fn = lambda: q.integrate("sobol", "product-sine", ni, 8, "kahan")  # noqa: E731
+    fn()
+    t0 = time.perf_counter()
+    row = fn()
+    sec = time.perf_counter() - t0
+    res["integrate_sobol_product_sine_2^26x8"] = {
+        "value": ni * 8 / sec / 1e9, "unit": "Gsamples/s (host-timed call incl. D2H combine)",
+        "estimate": row["estimate"], "abs_error": row["abs_error"]}
     return res
 
 

@@ -6,5 +6,6 @@ import json; d=json.loads(open('gpurun_out/bench_q.json').read())
 print('C2', round(d['value'],1), round(d['roofline']['frac'],4), 'probe', round(d['roofline']['write_probe_gbs']), d['clocks'])
 for k,v in d['configs'].items():
     if 'roofline' in v: print(k, round(v['value'],1), round(v['roofline']['frac'],4))
+    elif 'value' in v: print(k, round(v['value'],1), v.get('unit'))
     else: print(k, {kk: round(vv['value'],1) for kk,vv in v.items()})
 PY
