@@ -287,18 +287,18 @@ void qo_sobol_fill_fixed(uint64_t first, uint64_t n, uint32_t dims, const uint32
  * (SPEC.md:271 lists Owen trees as a non-goal). The 32-bit
  * fixed-point value v is bit-reversed, so digit k (from the most significant
  * end) sits at bit k; then a hash whose every step keeps "output bit k =
- * input bit k XOR f(input bits < k, seed)" (add, and x ^= x*even) flips each
- * digit as a function of the seed and all preceding digits, which is the
- * nested-uniform (Owen) structure; finally reversed back. Constants: Burley,
- * "Practical Hash-based Owen Scrambling", JCGT 9(4) 2020 (LK-style hash). */
+ * input bit k XOR f(input bits < k, seed)" (x ^= x*even, x += c, x *= odd)
+ * flips each digit as a function of the seed and all preceding digits, which
+ * is the nested-uniform (Owen) structure; finally reversed back. Constants:
+ * Vegdahl, "Building a Better LK Hash" (2021), an improved Laine-Karras hash. */
 uint32_t qo_owen_scramble(uint32_t v, uint32_t seed)
 {
     uint32_t x = qo_brev32(v);
+    x ^= x * 0x3d20adeau;
     x += seed;
-    x ^= x * 0x6c50b47cu;
-    x ^= x * 0xb82f1e52u;
-    x ^= x * 0xc7afe638u;
-    x ^= x * 0x8d22f6e6u;
+    x *= (seed >> 16) | 1u;
+    x ^= x * 0x05526c56u;
+    x ^= x * 0x53a22864u;
     return qo_brev32(x);
 }
 

@@ -26,11 +26,6 @@ namespace {
 
 constexpr int kBlock = 256;
 
-__device__ __forceinline__ uint4 xor4(uint4 a, uint4 b)
-{
-    return make_uint4(a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w);
-}
-
 __host__ __device__ constexpr uint32_t ctz_const(uint32_t v)
 {
     uint32_t c = 0;
@@ -41,17 +36,6 @@ __host__ __device__ constexpr uint32_t ctz_const(uint32_t v)
     return c;
 }
 
-__host__ __device__ constexpr uint32_t brev5(uint32_t u)
-{
-    return ((u & 1u) << 4) | ((u & 2u) << 2) | (u & 4u) | ((u & 8u) >> 2) | ((u & 16u) >> 4);
-}
-
-__device__ __forceinline__ uint4 map4(uint4 x)
-{
-    return make_uint4(map_bits(x.x), map_bits(x.y), map_bits(x.z), map_bits(x.w));
-}
-
-__device__ __forceinline__ void store4(uint4* p, uint4 v) { __stcs(p, v); }
 
 // element e of a row-major [points][dims] chunk -> point (dims == 1 needs no
 // division; div32 requires a divisor >= 2)
