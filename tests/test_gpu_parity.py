@@ -443,3 +443,20 @@ def test_integrate_pixel_kinds_vs_reference(ref):
                                      C.byref(e)) == 0
             row = q.integrate(kind, f, 50000, 4)
             assert abs(row["estimate"] - e.value) <= 1e-12 * abs(e.value)
+
+
+@pytest.mark.parametrize("scramble", ["plain", "faure", "linear"])
+@pytest.mark.parametrize("kind", ["halton", "halton-hilbert"])
+def test_halton_streams_scrambles_vs_reference(ref, kind, scramble):
+    dims, n = 7, 200
+    kw = {"scramble": scramble}
+    px = py = 0
+    order, spp = 1, 1
+    if kind == "halton-hilbert":
+        px, py, order, spp = 5, 9, 5, n
+        kw.update(pixel=(px, py), order=order, spp=spp)
+    got = u32(q.stream_fill(kind, n, dims, **kw)).reshape(n, dims)
+    exp = np.zeros((n, dims), np.uint32)
+    assert ref.ref_stream_fill(kind.encode(), dims, 0, scramble.encode(), px, py, order, spp, 0,
+                               0, 0, n, ptr(exp)) == 0, ref.ref_last_error()
+    np.testing.assert_array_equal(got, exp)
