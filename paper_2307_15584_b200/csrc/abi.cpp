@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <array>
+#include <map>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -583,31 +584,55 @@ struct qmc_matrices {
     struct Dev {
         DevPtr colsT, colsT_rev;
     };
-    std::vector<std::unique_ptr<Dev>> dev;
+    // per (device, dims prefix): the k-major column tables the kernels read
+    std::map<std::pair<int, uint32_t>, std::unique_ptr<Dev>> dev;
 
-    // [52][dims] (and bit-reversed) columns on the current device
-    const Dev& on_device()
+    // [52][prefix] (and bit-reversed) columns of the first `prefix`
+    // dimensions on the current device; built once, then cached.
+    const Dev& on_device(uint32_t prefix)
     {
         const int d = current_device();
         std::lock_guard<std::mutex> lk(mu);
-        if (dev.size() <= static_cast<size_t>(d))
-            dev.resize(d + 1);
-        if (!dev[d]) {
-            const uint32_t pd = std::max<uint32_t>(dims, 4); // room for 16-B loads
+        auto& slot = dev[{d, prefix}];
+        if (!slot) {
+            const uint32_t pd = std::max<uint32_t>(prefix, 8); // room for 32-B loads
             std::vector<uint32_t> t(52 * static_cast<size_t>(pd), 0u), tr(t.size(), 0u);
-            for (uint32_t j = 0; j < dims; ++j)
+            for (uint32_t j = 0; j < prefix; ++j)
                 for (uint32_t k = 0; k < 52; ++k) {
-                    t[k * static_cast<size_t>(dims) + j] = columns[j * 52 + k];
-                    tr[k * static_cast<size_t>(dims) + j] = brev_host(columns[j * 52 + k]);
+                    t[k * static_cast<size_t>(prefix) + j] = columns[j * 52 + k];
+                    tr[k * static_cast<size_t>(prefix) + j] = brev_host(columns[j * 52 + k]);
                 }
             auto e = std::make_unique<Dev>();
             e->colsT = dev_upload(t.data(), t.size() * 4);
             e->colsT_rev = dev_upload(tr.data(), tr.size() * 4);
-            dev[d] = std::move(e);
+            slot = std::move(e);
         }
-        return *dev[d];
+        return *slot;
     }
+    const Dev& on_device() { return on_device(dims); }
 };
+
+namespace {
+
+// build_matrices(builtin_direction_numbers(), dims), built once per dims
+// and kept for the process (the reference's builtin_direction_numbers() is
+// likewise a function-local static, digitalnet.cpp:73-77).
+qmc_matrices* builtin_matrices(uint32_t dims)
+{
+    static std::mutex mu;
+    static std::map<uint32_t, std::unique_ptr<qmc_matrices>> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto& m = cache[dims];
+    if (!m) {
+        auto cols = build_columns(builtin_rows(), dims); // ConfigError beyond 64
+        m = std::make_unique<qmc_matrices>();
+        m->dims = dims;
+        m->columns = std::move(cols);
+    }
+    return m.get();
+}
+
+} // namespace
 
 extern "C" {
 
@@ -831,24 +856,10 @@ static void sobol_fill_impl(qmc_matrices* m, uint64_t first, uint64_t n, uint32_
         fail(QMC_OUT_OF_RANGE, "sobol_component: dimension beyond the matrix set");
     if (sc != QMC_SOBOL_NONE && sc != QMC_SOBOL_XOR && sc != QMC_SOBOL_OWEN)
         fail(QMC_INVALID_ARGUMENT, "sobol_fill: unknown scramble kind");
-    const auto& dev = m->on_device();
-    // the fast path reads dims-strided columns: rebuild for a dims prefix
-    DevPtr sub, sub_rev;
+    // the kernels read dims-strided columns: tables for this dims prefix
+    const auto& dev = m->on_device(dims);
     const uint32_t* colsT = static_cast<const uint32_t*>(dev.colsT.get());
     const uint32_t* colsT_rev = static_cast<const uint32_t*>(dev.colsT_rev.get());
-    if (dims != m->dims) {
-        std::vector<uint32_t> t(52 * static_cast<size_t>(std::max<uint32_t>(dims, 4)), 0u),
-            tr(t.size(), 0u);
-        for (uint32_t j = 0; j < dims; ++j)
-            for (uint32_t k = 0; k < 52; ++k) {
-                t[k * static_cast<size_t>(dims) + j] = m->columns[j * 52 + k];
-                tr[k * static_cast<size_t>(dims) + j] = brev_host(m->columns[j * 52 + k]);
-            }
-        sub = dev_upload(t.data(), t.size() * 4);
-        sub_rev = dev_upload(tr.data(), tr.size() * 4);
-        colsT = static_cast<const uint32_t*>(sub.get());
-        colsT_rev = static_cast<const uint32_t*>(sub_rev.get());
-    }
     CallArgs args(s);
     SmallArgs small{};
     if (words && sc != QMC_SOBOL_NONE)
@@ -860,8 +871,6 @@ static void sobol_fill_impl(qmc_matrices* m, uint64_t first, uint64_t n, uint32_
     place_fill(out, first, n, dims, s, [&](const FillRange& r, cudaStream_t st) {
         return launch_sobol(colsT, colsT_rev, small, dims, mode, u32, r, st);
     });
-    if (sub) // the temporary prefix tables must outlive the kernels
-        cuda_ok(cudaStreamSynchronize(s), "sync");
 }
 
 qmc_status qmc_sobol_fill(const qmc_matrices* m, uint64_t first_index, uint64_t n, uint32_t dims,
@@ -1036,8 +1045,7 @@ XorTablesDev white_noise_tables(uint32_t dims, uint32_t point_count, uint32_t se
     void* pts = nullptr;
     cuda_ok(cudaMalloc(&pts, static_cast<size_t>(point_count) * dims * 4 + 16), "cudaMalloc");
     t.points.reset(pts);
-    std::unique_ptr<qmc_matrices> m(new_matrices(build_columns(builtin_rows(), dims), dims));
-    sobol_fill_impl(m.get(), 0, point_count, dims, seed ? QMC_SOBOL_XOR : QMC_SOBOL_NONE,
+    sobol_fill_impl(builtin_matrices(dims), 0, point_count, dims, seed ? QMC_SOBOL_XOR : QMC_SOBOL_NONE,
                     dim_scramble.data(), QMC_OUT_U32, pts, s);
     cuda_ok(cudaStreamSynchronize(s), "sync");
     return t;
@@ -1105,10 +1113,8 @@ void resolve_stream(qmc_sampler_kind kind, const qmc_stream_params* p, cudaStrea
     switch (kind) {
     case QMC_KIND_SOBOL:
         r.matrices = const_cast<qmc_matrices*>(p->matrices);
-        if (!r.matrices) {
-            r.own_matrices.reset(new_matrices(build_columns(builtin_rows(), dims), dims));
-            r.matrices = r.own_matrices.get();
-        }
+        if (!r.matrices)
+            r.matrices = builtin_matrices(dims);
         require(dims <= r.matrices->dims, "make_stream: dims beyond the generator matrices");
         if (p->sobol_scrambles) {
             require(p->sobol_scrambles_len >= dims, "make_stream: scramble list shorter than dims");
@@ -1295,15 +1301,16 @@ qmc_status qmc_integrate(qmc_sampler_kind kind, const qmc_stream_params* p,
                     fail(QMC_INVALID_ARGUMENT,
                          "radical_inverse_linscramble: factor must be in [1, base)");
 
+        const uint32_t dims_of_integrand = p->dims; // stream dims (>= f_dims)
         IntegrateParams ip{};
         ip.pix = r.q;
         ip.fn = f;
         ip.fdims = f_dims;
         ip.n = n;
         if (kind == QMC_KIND_SOBOL) {
-            const auto& dev = r.matrices->on_device();
+            const auto& dev = r.matrices->on_device(dims_of_integrand);
             ip.colsT = static_cast<const uint32_t*>(dev.colsT.get());
-            ip.mdims = r.matrices->dims;
+            ip.mdims = dims_of_integrand;
             ip.words = r.woff == SIZE_MAX ? nullptr : args.at<uint32_t>(r.woff);
         }
         const uint64_t chunks = (n + 4095) / 4096;

@@ -1,14 +1,13 @@
 // kernels_integrate.cu — fused QMC integration (reference
 // integrate(), quality.cpp:214-282, with builtin_integrands, :28-66).
 //
-// One thread owns one fixed 4096-index chunk (quality.cpp:178) and walks it
-// in index order: sample every integrand dimension at the integer stage ->
-// bit-exact float map -> the integrand in FP64 with the reference's
-// operation order (explicit _rn intrinsics, no FMA contraction) -> Neumaier
-// (kahan) or llround(v * 2^32) (int) accumulation. Chunk partials are
-// written per chunk and combined in chunk order on the host (Kahan: the
-// reference's rank-ordered CompensatedSum, quality.cpp:262-267) or summed
-// with exact 64-bit atomics on the device (int: associative, :268-272).
+// Fixed 4096-index chunks (quality.cpp:178), one CTA each: sample every
+// integrand dimension at the integer stage -> bit-exact float map -> the
+// integrand in FP64 with the reference's operation order (explicit _rn
+// intrinsics, no FMA contraction) -> Neumaier in index order (kahan) or
+// llround(v * 2^32) (int). Chunk partials are combined in chunk order on the
+// host (Kahan: the reference's rank-ordered CompensatedSum,
+// quality.cpp:262-267) or summed with exact 64-bit atomics (int, :268-272).
 #include <cstdint>
 
 #include "device.cuh"
@@ -51,17 +50,27 @@ __device__ __forceinline__ bool factor(float xs, double& v)
     return true;
 }
 
+// One CTA per 4096-index chunk. Phase 1: the 128 threads evaluate the
+// integrand at indices begin + t + 128*m (m < 32) into shared memory — all
+// the sampling and FP64 math, fully parallel. Phase 2 (kahan): one thread
+// runs the reference's sequential Neumaier sum over the 4096 values in index
+// order, so the chunk partial is bit-identical to chunk_sum_kahan
+// (quality.cpp:180-194); (int) the llround(v*2^32) terms are exactly
+// associative, so the CTA reduces them in any order (quality.cpp:196-210).
 template <uint32_t KIND, uint32_t FN, uint32_t ACCUM>
 __global__ void __launch_bounds__(kBlock)
     k_integrate(IntegrateParams p, double* __restrict__ partial,
                 unsigned long long* __restrict__ isum, unsigned long long* __restrict__ bad)
 {
-    const uint64_t chunk = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    __shared__ double vals[4096];
+    __shared__ uint32_t E[5][kMaxDims]; // sobol: XOR of columns 7..7+c
+    __shared__ uint32_t XB[kMaxDims];   // sobol: value of `begin` (scramble included)
+    __shared__ long long red[kBlock / 32];
+    const uint64_t chunk = blockIdx.x;
     const uint64_t begin = chunk * 4096;
-    if (begin >= p.n)
-        return;
-    const uint64_t end = begin + 4096 < p.n ? begin + 4096 : p.n;
+    const uint32_t count = static_cast<uint32_t>(p.n - begin < 4096 ? p.n - begin : 4096);
     const uint32_t dims = p.fdims;
+    const uint32_t t = threadIdx.x;
     const PixelStreamParams& q = p.pix;
 
     // per-stream pixel state (imageplane.cpp:366-405)
@@ -82,70 +91,106 @@ __global__ void __launch_bounds__(kBlock)
         cell = (q.px % 128u) + (q.py % 128u) * 128u;
     const RadicalDim* rd = static_cast<const RadicalDim*>(q.radical_dims);
 
-    // Sobol' state: value of index `begin`, then natural-order updates
+    // Sobol' state: x(begin + t + 128 m) = XB ^ X(t) ^ X(128 m); m advances
+    // with x ^= E[ctz(m+1)].
     uint32_t sob[kMaxDims];
     if (KIND == 0) {
-        for (uint32_t j = 0; j < dims; ++j) {
+        for (uint32_t j = t; j < dims; j += kBlock) {
             uint32_t x = p.words ? p.words[j] : 0u;
             uint64_t b = begin;
             for (uint32_t k = 0; b; ++k, b >>= 1)
                 if (b & 1u)
                     x ^= __ldg(p.colsT + k * p.mdims + j);
+            XB[j] = x;
+            uint32_t e = 0;
+            for (uint32_t c = 0; c < 5; ++c) {
+                e ^= __ldg(p.colsT + (7 + c) * p.mdims + j);
+                E[c][j] = e;
+            }
+        }
+        __syncthreads();
+        for (uint32_t j = 0; j < dims; ++j) {
+            uint32_t x = XB[j];
+            for (uint32_t k = 0; k < 7; ++k)
+                if ((t >> k) & 1u)
+                    x ^= __ldg(p.colsT + k * p.mdims + j);
             sob[j] = x;
         }
     }
 
-    double sum = 0.0, comp = 0.0;
+    bool finite = true;
     long long acc = 0;
-    for (uint64_t idx = begin; idx < end; ++idx) {
-        const uint32_t i = static_cast<uint32_t>(idx);
-        double v = 1.0;
-        bool alive = true;
-        for (uint32_t j = 0; j < dims && alive; ++j) {
-            uint32_t x;
-            if (KIND == 0)
-                x = sob[j];
-            else if (KIND == 1)
-                x = radical_fixed(i, rd[j]);
-            else if (KIND == 2)
-                x = brev32(i) * __ldg(q.generator + j);
-            else if (KIND == 3)
-                x = radical_fixed(static_cast<uint32_t>(block + idx), rd[j]);
-            else if (KIND == 4)
-                x = (brev32(i) + shift) * __ldg(q.generator + j);
-            else if (KIND == 5)
-                x = brev32(~i) * (pixel_hash(j, q.px, q.py) | 1u);
-            else if (KIND == 6)
-                x = j == 0   ? rad2(ipx0 + i * q.scale_y)
-                    : j == 1 ? phi3_fixed(ipy0 + i * q.scale_x)
-                             : radical_fixed(static_cast<uint32_t>(off + idx * q.stride), rd[j]);
-            else {
-                const uint32_t k = i ^ __ldg(q.xor_reorder + cell);
-                x = __ldg(q.xor_points + static_cast<uint64_t>(k) * q.xor_dims + j) ^
-                    __ldg(q.xor_scramble + cell * q.xor_dims + j);
+    for (uint32_t m = 0; m < 32; ++m) {
+        const uint32_t local = t + 128 * m;
+        if (local < count) {
+            const uint64_t idx = begin + local;
+            const uint32_t i = static_cast<uint32_t>(idx);
+            double v = 1.0;
+            bool alive = true;
+            for (uint32_t j = 0; j < dims && alive; ++j) {
+                uint32_t x;
+                if (KIND == 0)
+                    x = sob[j];
+                else if (KIND == 1)
+                    x = radical_fixed(i, rd[j]);
+                else if (KIND == 2)
+                    x = brev32(i) * __ldg(q.generator + j);
+                else if (KIND == 3)
+                    x = radical_fixed(static_cast<uint32_t>(block + idx), rd[j]);
+                else if (KIND == 4)
+                    x = (brev32(i) + shift) * __ldg(q.generator + j);
+                else if (KIND == 5)
+                    x = brev32(~i) * (pixel_hash(j, q.px, q.py) | 1u);
+                else if (KIND == 6)
+                    x = j == 0   ? rad2(ipx0 + i * q.scale_y)
+                        : j == 1 ? phi3_fixed(ipy0 + i * q.scale_x)
+                                 : radical_fixed(static_cast<uint32_t>(off + idx * q.stride), rd[j]);
+                else {
+                    const uint32_t k = i ^ __ldg(q.xor_reorder + cell);
+                    x = __ldg(q.xor_points + static_cast<uint64_t>(k) * q.xor_dims + j) ^
+                        __ldg(q.xor_scramble + cell * q.xor_dims + j);
+                }
+                alive = factor<FN>(map_u32(x), v);
             }
-            alive = factor<FN>(map_u32(x), v);
+            if (FN == 2)
+                v = alive ? 1.0 : 0.0;
+            if (!isfinite(v)) {
+                finite = false;
+                atomicMin(bad, static_cast<unsigned long long>(idx));
+            }
+            if (ACCUM == 0)
+                vals[local] = v;
+            else
+                acc += llround(__dmul_rn(v, 4294967296.0));
         }
-        if (FN == 2)
-            v = alive ? 1.0 : 0.0;
-        if (!isfinite(v))
-            atomicMin(bad, static_cast<unsigned long long>(idx));
-        if (ACCUM == 0)
-            neumaier_add(sum, comp, v);
-        else
-            acc += llround(__dmul_rn(v, 4294967296.0));
-        if (KIND == 0) { // x(i+1) = x(i) ^ C[0] ^ ... ^ C[ctz(i+1)]
-            const uint64_t nx = idx + 1;
-            const uint32_t c = static_cast<uint32_t>(__ffsll(static_cast<long long>(nx)) - 1);
-            for (uint32_t k = 0; k <= c && k < 52; ++k)
-                for (uint32_t j = 0; j < dims; ++j)
-                    sob[j] ^= __ldg(p.colsT + k * p.mdims + j);
+        if (KIND == 0 && m < 31) {
+            const uint32_t c = __ffs(static_cast<int>(m + 1)) - 1;
+            for (uint32_t j = 0; j < dims; ++j)
+                sob[j] ^= E[c][j];
         }
     }
-    if (ACCUM == 0)
-        partial[chunk] = __dadd_rn(sum, comp);
-    else
-        atomicAdd(isum, static_cast<unsigned long long>(acc));
+    (void)finite;
+    if (ACCUM == 0) {
+        __syncthreads();
+        if (t == 0) { // chunk_sum_kahan's sequential Neumaier, index order
+            double sum = 0.0, comp = 0.0;
+            for (uint32_t k = 0; k < count; ++k)
+                neumaier_add(sum, comp, vals[k]);
+            partial[chunk] = __dadd_rn(sum, comp);
+        }
+    } else {
+        for (int o = 16; o; o >>= 1)
+            acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if ((t & 31) == 0)
+            red[t >> 5] = acc;
+        __syncthreads();
+        if (t == 0) {
+            long long s = 0;
+            for (int w = 0; w < kBlock / 32; ++w)
+                s += red[w];
+            atomicAdd(isum, static_cast<unsigned long long>(s));
+        }
+    }
 }
 
 template <uint32_t KIND, uint32_t FN>
@@ -153,7 +198,9 @@ cudaError_t integrate_kind_fn(const IntegrateParams& p, uint32_t accum, double* 
                               unsigned long long* isum, unsigned long long* bad, cudaStream_t s)
 {
     const uint64_t chunks = (p.n + 4095) / 4096;
-    const unsigned grid = static_cast<unsigned>((chunks + kBlock - 1) / kBlock);
+    if (chunks > 0x7fffffffull)
+        return cudaErrorInvalidValue;
+    const unsigned grid = static_cast<unsigned>(chunks);
     if (accum == 0)
         k_integrate<KIND, FN, 0><<<grid, kBlock, 0, s>>>(p, partial, isum, bad);
     else
