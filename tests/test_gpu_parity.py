@@ -460,3 +460,60 @@ def test_halton_streams_scrambles_vs_reference(ref, kind, scramble):
     assert ref.ref_stream_fill(kind.encode(), dims, 0, scramble.encode(), px, py, order, spp, 0,
                                0, 0, n, ptr(exp)) == 0, ref.ref_last_error()
     np.testing.assert_array_equal(got, exp)
+
+
+def _strata_ok(col_i32, m):
+    """Every one of the 2^m equal strata holds exactly one value."""
+    v = (col_i32.to(torch.int64) & 0xFFFFFFFF) >> (32 - m)
+    c = torch.bincount(v, minlength=1 << m)
+    return int(c.min()) == 1 and int(c.max()) == 1
+
+
+@pytest.mark.slow
+def test_c3_owen_full_size_properties(oracle, columns64, golden_arrays):
+    """Config C3 (Owen, 2^28 x 64) at full size: random rows equal the oracle
+    and every dimension keeps one-point-per-stratum at m = 28 (Owen
+    scrambling preserves the (0,m)-net property of each coordinate)."""
+    n, dims = 1 << 28, 64
+    seeds = golden_arrays["seeds_c3"]
+    x = q.sobol_fill(n, dims, scramble="owen", words=seeds, fixed=True)  # 64 GiB
+    rng = np.random.default_rng(3)
+    rows = rng.integers(0, n, 2048)
+    got = u32(x[torch.from_numpy(rows).cuda()]).reshape(-1, dims)
+    exp = np.zeros((1, dims), np.uint32)
+    for k, i in enumerate(rows.tolist()):
+        oracle.qo_sobol_owen_fill_fixed(i, 1, dims, ptr(columns64), ptr(seeds), ptr(exp))
+        np.testing.assert_array_equal(got[k], exp[0])
+    for j in (0, 5, 33, 63):
+        assert _strata_ok(x[:, j], 28), j
+    del x
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+def test_c4_lattice_cp_full_size_properties(oracle, golden_arrays):
+    """Config C4 (2^30 x 16 + CP rotation) at full size: random rows equal
+    the oracle; the first 2^26 points of every dimension are stratified at
+    m = 26 (a shifted rank-1 lattice with odd g); the block identity
+    x(i + k 2^m) = x(i) + Delta_k holds (lattice.cpp:157-170)."""
+    n, dims = 1 << 30, 16
+    g = golden_arrays["lfsr_ace1_16"]
+    s = golden_arrays["cp_shifts16"]
+    x = q.lattice_fill(n, g, shifts=s, fixed=True)  # 64 GiB
+    rng = np.random.default_rng(4)
+    rows = rng.integers(0, n, 2048)
+    got = u32(x[torch.from_numpy(rows).cuda()]).reshape(-1, dims)
+    for k, i in enumerate(rows.tolist()):
+        for j in range(dims):
+            assert got[k, j] == oracle.qo_lattice_cp_fixed(i, int(g[j]), int(s[j]))
+    for j in range(0, dims, 5):
+        assert _strata_ok(x[: 1 << 26, j], 26), j
+    m, kk = 20, 37
+    delta = np.zeros(dims, np.uint32)
+    assert oracle.qo_lattice_shift_fixed(kk, m, ptr(g), dims, ptr(delta)) == 0
+    a = u32(x[: 1 << 16]).astype(np.uint64)
+    b = u32(x[kk << m: (kk << m) + (1 << 16)]).astype(np.uint64)
+    np.testing.assert_array_equal(((a + delta[None, :]) & 0xFFFFFFFF).astype(np.uint32),
+                                  b.astype(np.uint32))
+    del x
+    torch.cuda.empty_cache()
