@@ -217,6 +217,23 @@ qmc_status qmc_integrate(qmc_sampler_kind kind, const qmc_stream_params* params,
                          qmc_integrand_kind f, uint32_t f_dims, uint64_t n, qmc_accum mode,
                          qmc_integration_row* row, qmc_stream stream);
 
+/* ------------------------------- quality metrics (quality.cpp:76-156) */
+/* Warnock's L2-star discrepancy of a row-major [n][dims] float point set
+ * (device or host). Per-term products follow the reference's operation order;
+ * the pair terms are summed per row with compensated tree sums (result within
+ * ~1e-15 relative of the reference's sequential sum). dims <= 256. */
+qmc_status qmc_l2_star_discrepancy(const float* points, uint64_t n, uint32_t dims, double* out,
+                                   qmc_stream stream);
+/* Minimum pairwise toroidal distance (order-free: bit-identical). */
+qmc_status qmc_min_toroidal_distance(const float* points, uint64_t n, uint32_t dims, double* out,
+                                     qmc_stream stream);
+/* check_1d_stratification(make_stream(kind, params), j, m): *ok = every one
+ * of the 2^m dyadic intervals holds exactly one of the first 2^m values of
+ * dimension j; histogram (host, 2^m words) optional. */
+qmc_status qmc_check_1d_stratification(qmc_sampler_kind kind, const qmc_stream_params* params,
+                                       uint32_t j, uint32_t m, int* ok, uint32_t* histogram,
+                                       qmc_stream stream);
+
 /* --------------------------------------------------- render (render.cpp:83-143) */
 typedef struct qmc_render_job { /* RenderJob, render.hpp:31-47 */
     uint32_t width, height, spp;

@@ -29,6 +29,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -421,6 +422,39 @@ int ref_integrate(const char* kind, std::uint32_t dims, std::uint32_t seed, cons
         const auto f = qmc::builtin_integrand(integrand, dims);
         *estimate =
             qmc::integrate(s, f, n, qmc::accum_mode_from_name(accum), workers).estimate;
+    });
+}
+int ref_l2_star(const float* pts, std::uint64_t n, std::uint32_t dims, double* out)
+{
+    return guard([&] {
+        *out = qmc::l2_star_discrepancy(std::span<const float>(pts, n * dims), n, dims);
+    });
+}
+int ref_min_toroidal(const float* pts, std::uint64_t n, std::uint32_t dims, double* out)
+{
+    return guard([&] {
+        *out = qmc::min_toroidal_distance(std::span<const float>(pts, n * dims), n, dims);
+    });
+}
+// check_1d_stratification over the stream built as in ref_stream_fill.
+int ref_stratification(const char* kind, std::uint32_t dims, std::uint32_t seed, std::uint32_t j,
+                       std::uint32_t m, int* ok)
+{
+    return guard([&] {
+        const qmc::SamplerKind k = qmc::sampler_kind_from_name(kind);
+        qmc::StreamParams p;
+        p.dims = dims;
+        if (k == qmc::SamplerKind::lattice || k == qmc::SamplerKind::pixel_shifted_lattice)
+            p.generator = qmc::lfsr_generator_vector(seed ? seed : qmc::kDefaultGeneratorSeed,
+                                                     std::max(dims, 2u));
+        if (k == qmc::SamplerKind::sobol) {
+            p.matrices = builtin_matrices(dims);
+            if (seed)
+                for (std::uint32_t d = 0; d < dims; ++d)
+                    p.sobol_scrambles.push_back(qmc::pixel_hash(d, seed, 0x5eedu));
+        }
+        const qmc::SampleStream s = qmc::make_stream(k, std::move(p));
+        *ok = qmc::check_1d_stratification(s, j, m).ok ? 1 : 0;
     });
 }
 double ref_neumaier(const double* v, std::uint64_t n)

@@ -33,7 +33,8 @@ __all__ = [
     "stream_fill", "render", "scene_value", "prime", "prime_max_power", "faure_permutation",
     "default_linear_factors", "lfsr_generator_vector", "pixel_hash", "hilbert_order_for",
     "partition_by_extra_dimension", "halton_pixel_enumeration", "sampler_kind_from_name",
-    "integrate", "builtin_integrand", "write_probe",
+    "integrate", "builtin_integrand", "write_probe", "l2_star_discrepancy",
+    "min_toroidal_distance", "check_1d_stratification",
     "SAMPLER_KINDS",
 ]
 
@@ -121,6 +122,10 @@ def lib():
     sig("qmc_stream_fill", i32, i32, C.POINTER(StreamParams), u64, u64, i32, P, P)
     sig("qmc_render", i32, C.POINTER(RenderJob), u32, u32, P, P)
     sig("qmc_scene_value", i32, P, P, u64, P)
+    sig("qmc_l2_star_discrepancy", i32, P, u64, u32, C.POINTER(f64), P)
+    sig("qmc_min_toroidal_distance", i32, P, u64, u32, C.POINTER(f64), P)
+    sig("qmc_check_1d_stratification", i32, i32, C.POINTER(StreamParams), u32, u32,
+        C.POINTER(i32), P, P)
     sig("qmc_builtin_integrand", i32, C.c_char_p, u32, C.POINTER(i32), C.POINTER(f64))
     sig("qmc_integrate", i32, i32, C.POINTER(StreamParams), i32, u32, u64, i32,
         C.POINTER(IntegrationRow), P)
@@ -411,6 +416,42 @@ def _stream_params(dims, generator, matrices, sobol_scrambles, scramble, linear_
     p.order, p.spp, p.width, p.height = order, spp, width, height
     p.xor_seed, p.xor_point_count = xor_seed, xor_point_count
     return p, keep
+
+
+def l2_star_discrepancy(points, stream=None) -> float:
+    """Warnock L2-star discrepancy of an [n, dims] float32 point set (quality.cpp:76-114)."""
+    pts = np.ascontiguousarray(points, dtype=np.float32) if isinstance(points, np.ndarray) \
+        else points.contiguous()
+    out = f64()
+    _check(lib().qmc_l2_star_discrepancy(_ptr(pts), pts.shape[0], pts.shape[1], C.byref(out),
+                                         _stream(stream)))
+    return out.value
+
+
+def min_toroidal_distance(points, stream=None) -> float:
+    """Minimum pairwise wrap-around distance (quality.cpp:116-136)."""
+    pts = np.ascontiguousarray(points, dtype=np.float32) if isinstance(points, np.ndarray) \
+        else points.contiguous()
+    out = f64()
+    _check(lib().qmc_min_toroidal_distance(_ptr(pts), pts.shape[0], pts.shape[1], C.byref(out),
+                                           _stream(stream)))
+    return out.value
+
+
+def check_1d_stratification(kind: str, j: int, m: int, dims: int = 2, *, generator=None,
+                            matrices: Optional[GeneratorMatrixSet] = None, sobol_scrambles=None,
+                            scramble: str = "plain", linear_factors=None, pixel=(0, 0),
+                            order: int = 1, spp: int = 1, width: int = 0, height: int = 0,
+                            xor_seed: int = 0, xor_point_count: int = 1, stream=None):
+    """(ok, histogram) of check_1d_stratification(make_stream(kind, ...), j, m)."""
+    k = sampler_kind_from_name(kind)
+    p, keep = _stream_params(dims, generator, matrices, sobol_scrambles, scramble, linear_factors,
+                             pixel, order, spp, width, height, xor_seed, xor_point_count)
+    ok = i32()
+    hist = np.zeros(1 << min(m, 20), np.uint32)
+    _check(lib().qmc_check_1d_stratification(k, C.byref(p), j, m, C.byref(ok), hist.ctypes.data,
+                                             _stream(stream)))
+    return bool(ok.value), hist
 
 
 _INTEGRANDS = {"product-sine": 0, "product-poly": 1, "indicator": 2}

@@ -1361,6 +1361,120 @@ qmc_status qmc_integrate(qmc_sampler_kind kind, const qmc_stream_params* p,
     });
 }
 
+// ------------------------------------------------------------ quality metrics
+
+namespace {
+
+// Device copy of a row-major float point set (host arrays are staged).
+struct DevPoints {
+    const float* ptr = nullptr;
+    float* own = nullptr;
+    cudaStream_t s;
+    DevPoints(const float* p, uint64_t count, cudaStream_t st) : s(st)
+    {
+        if (is_device_pointer(p)) {
+            ptr = p;
+            return;
+        }
+        cuda_ok(cudaMallocAsync(&own, count * 4 + 4, s), "cudaMallocAsync");
+        cuda_ok(cudaMemcpyAsync(own, p, count * 4, cudaMemcpyHostToDevice, s), "H2D");
+        ptr = own;
+    }
+    ~DevPoints()
+    {
+        if (own)
+            cudaFreeAsync(own, s);
+    }
+};
+
+double pairwise_metric(const float* points, uint64_t n, uint32_t dims, cudaStream_t s, bool l2)
+{
+    if (dims > quality_max_dims())
+        fail(QMC_INVALID_ARGUMENT, "quality metric: at most 256 dimensions on the device");
+    if (n > 0x7fffffffull)
+        fail(QMC_INVALID_ARGUMENT, "quality metric: at most 2^31 - 1 points");
+    pool_keep_memory();
+    DevPoints dp(points, n * dims, s);
+    double* scratch = nullptr;
+    cuda_ok(cudaMallocAsync(&scratch, (2 * n + 1) * 8, s), "cudaMallocAsync");
+    cuda_ok(l2 ? launch_l2star(dp.ptr, n, dims, scratch + 1, scratch, s)
+               : launch_mindist(dp.ptr, n, dims, scratch + 1, scratch, s),
+            "launch quality");
+    double r = 0.0;
+    cuda_ok(cudaMemcpyAsync(&r, scratch, 8, cudaMemcpyDeviceToHost, s), "D2H");
+    cudaFreeAsync(scratch, s);
+    cuda_ok(cudaStreamSynchronize(s), "sync");
+    return r;
+}
+
+} // namespace
+
+qmc_status qmc_l2_star_discrepancy(const float* points, uint64_t n, uint32_t dims, double* out,
+                                   qmc_stream stream)
+{
+    return guard([&] {
+        if (n == 0 || dims == 0)
+            fail(QMC_INVALID_ARGUMENT, "l2_star_discrepancy: empty point set");
+        if (!points || !out)
+            fail(QMC_INVALID_ARGUMENT, "l2_star_discrepancy: null pointer");
+        *out = pairwise_metric(points, n, dims, as_stream(stream), true);
+    });
+}
+
+qmc_status qmc_min_toroidal_distance(const float* points, uint64_t n, uint32_t dims, double* out,
+                                     qmc_stream stream)
+{
+    return guard([&] {
+        if (n < 2)
+            fail(QMC_INVALID_ARGUMENT, "min_toroidal_distance: need at least two points");
+        if (!points || !out)
+            fail(QMC_INVALID_ARGUMENT, "min_toroidal_distance: null pointer");
+        *out = pairwise_metric(points, n, dims, as_stream(stream), false);
+    });
+}
+
+qmc_status qmc_check_1d_stratification(qmc_sampler_kind kind, const qmc_stream_params* params,
+                                       uint32_t j, uint32_t m, int* ok, uint32_t* histogram,
+                                       qmc_stream stream)
+{
+    return guard([&] {
+        if (m > 20)
+            fail(QMC_INVALID_ARGUMENT, "check_1d_stratification: m must be <= 20");
+        if (!params)
+            fail(QMC_INVALID_ARGUMENT, "stream params are null");
+        if (j >= params->dims)
+            fail(QMC_OUT_OF_RANGE, "SampleStream: dimension beyond the stream");
+        const cudaStream_t s = as_stream(stream);
+        pool_keep_memory();
+        const uint32_t count = 1u << m;
+        float* pts = nullptr;
+        uint32_t* hist = nullptr;
+        unsigned int* bad = nullptr;
+        cuda_ok(cudaMallocAsync(&pts, static_cast<size_t>(count) * params->dims * 4 + 32, s),
+                "cudaMallocAsync");
+        cuda_ok(cudaMallocAsync(&hist, static_cast<size_t>(count) * 4 + 4, s), "cudaMallocAsync");
+        cuda_ok(cudaMemsetAsync(hist, 0, static_cast<size_t>(count) * 4 + 4, s), "memset");
+        const qmc_status st = qmc_stream_fill(kind, params, 0, count, QMC_OUT_F32, pts, stream);
+        if (st != QMC_OK) {
+            cudaFreeAsync(pts, s);
+            cudaFreeAsync(hist, s);
+            fail(st, g_error);
+        }
+        bad = reinterpret_cast<unsigned int*>(hist + count);
+        cuda_ok(launch_stratification(pts, m, params->dims, j, hist, bad, s), "launch");
+        unsigned int hbad = 0;
+        cuda_ok(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, s), "D2H");
+        if (histogram)
+            cuda_ok(cudaMemcpyAsync(histogram, hist, static_cast<size_t>(count) * 4,
+                                    cudaMemcpyDeviceToHost, s),
+                    "D2H");
+        cudaFreeAsync(pts, s);
+        cudaFreeAsync(hist, s);
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        *ok = hbad == 0;
+    });
+}
+
 // ------------------------------------------------------------------ render
 
 qmc_status qmc_render(const qmc_render_job* job, uint32_t row_begin, uint32_t row_end, float* out,

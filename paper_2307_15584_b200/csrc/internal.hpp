@@ -127,6 +127,15 @@ cudaError_t launch_integrate(const IntegrateParams& p, uint32_t accum, double* p
                              unsigned long long* isum, unsigned long long* bad, cudaStream_t s);
 uint32_t integrate_max_dims();
 
+// Quality metrics (quality.cpp:76-156). scratch: device, 2n doubles.
+cudaError_t launch_l2star(const float* pts, uint64_t n, uint32_t dims, double* scratch,
+                          double* out, cudaStream_t s);
+cudaError_t launch_mindist(const float* pts, uint64_t n, uint32_t dims, double* scratch,
+                           double* out, cudaStream_t s);
+cudaError_t launch_stratification(const float* v, uint32_t m, uint32_t dims, uint32_t j,
+                                  uint32_t* hist, unsigned int* bad, cudaStream_t s);
+uint32_t quality_max_dims();
+
 // Number of SMs of the current device (cached).
 int sm_count();
 

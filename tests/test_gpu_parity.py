@@ -517,3 +517,36 @@ def test_c4_lattice_cp_full_size_properties(oracle, golden_arrays):
                                   b.astype(np.uint32))
     del x
     torch.cuda.empty_cache()
+
+
+# --------------------------------------------------------- quality metrics
+def test_quality_metrics_vs_reference(ref):
+    import ctypes as C
+    for dims, n in [(2, 4096), (5, 1000), (1, 17)]:
+        pts = u32(q.sobol_fill(n, dims, first=3)).view(np.float32).reshape(n, dims).copy()
+        e = C.c_double()
+        assert ref.ref_l2_star(ptr(pts), n, dims, C.byref(e)) == 0
+        got = q.l2_star_discrepancy(pts)
+        assert abs(got - e.value) <= 1e-12 * e.value, (got, e.value)
+        if n >= 2:
+            assert ref.ref_min_toroidal(ptr(pts), n, dims, C.byref(e)) == 0
+            assert q.min_toroidal_distance(torch.from_numpy(pts).cuda()) == e.value  # bit-exact
+    one = np.zeros((1, 1), np.float32)
+    assert abs(q.l2_star_discrepancy(one) - (1 / 3) ** 0.5) < 1e-15
+    with pytest.raises(ValueError):
+        q.min_toroidal_distance(one)
+
+
+@pytest.mark.parametrize("kind,dims", [("sobol", 8), ("lattice", 4), ("halton", 3)])
+def test_stratification_vs_reference(ref, kind, dims):
+    import ctypes as C
+    kw = {"generator": q.lfsr_generator_vector(0xACE1, max(dims, 2))} if kind == "lattice" else {}
+    for j in range(dims):
+        for m in (1, 8, 12, 20):
+            ok, hist = q.check_1d_stratification(kind, j, m, dims, **kw)
+            r = C.c_int()
+            assert ref.ref_stratification(kind.encode(), dims, 0, j, m, C.byref(r)) == 0
+            assert ok == bool(r.value), (kind, j, m)
+            assert hist.sum() == 1 << m
+    with pytest.raises(ValueError):
+        q.check_1d_stratification("sobol", 0, 21, 2)
