@@ -167,6 +167,23 @@ typedef enum qmc_sampler_kind { /* imageplane.hpp:122-131 */
 qmc_status qmc_sampler_kind_from_name(const char* name, qmc_sampler_kind* out);
 const char* qmc_sampler_kind_name(qmc_sampler_kind kind);
 
+/* XOR-table sampler data (imageplane.hpp:92-120), immutable handle. */
+typedef struct qmc_xor_tables qmc_xor_tables;
+/* white_noise_xor_tables(dims, point_count, seed) (imageplane.cpp:197-229) */
+qmc_status qmc_xor_tables_white_noise(uint32_t dims, uint32_t point_count, uint32_t seed,
+                                      qmc_xor_tables** out);
+/* load_xor_tables(file, dims, points, point_count) (imageplane.cpp:163-195):
+ * `bytes` = an XQT1 file image; points = host [point_count][dims] words. */
+qmc_status qmc_xor_tables_load(const void* bytes, size_t len, uint32_t dims,
+                               const uint32_t* points, uint32_t point_count,
+                               qmc_xor_tables** out);
+/* write_xor_table_file (imageplane.cpp:154-161); call with bytes = NULL to
+ * get the size in *len. */
+qmc_status qmc_xor_tables_write(const qmc_xor_tables* t, void* bytes, size_t* len);
+uint32_t qmc_xor_tables_dims(const qmc_xor_tables* t);
+uint32_t qmc_xor_tables_point_count(const qmc_xor_tables* t);
+void qmc_xor_tables_destroy(qmc_xor_tables* t);
+
 /* StreamParams (imageplane.hpp:139-158). Unused fields are ignored per kind. */
 typedef struct qmc_stream_params {
     uint32_t dims;              /* >= 1 */
@@ -183,6 +200,8 @@ typedef struct qmc_stream_params {
     uint32_t width, height;           /* image_plane_halton */
     uint32_t xor_seed;                /* sobol_xor_table: white-noise tables seed */
     uint32_t xor_point_count;         /* sobol_xor_table: power of two */
+    const qmc_xor_tables* xor_tables; /* sobol_xor_table: given tables (NULL = white noise
+                                         from xor_seed / xor_point_count) */
 } qmc_stream_params;
 
 /* make_stream(kind, params) validation + SampleStream::sample(i, j) for
@@ -243,6 +262,7 @@ typedef struct qmc_render_job { /* RenderJob, render.hpp:31-47 */
     const uint32_t* generator;    /* host, >= 2 odd words, NULL = lfsr default */
     uint32_t generator_dims;
     const qmc_matrices* matrices; /* NULL = builtin 2-dim */
+    const qmc_xor_tables* tables; /* sobol_xor_table: NULL = white noise (render.cpp:102-104) */
 } qmc_render_job;
 
 /* Integrates scene_value over every pixel footprint of rows

@@ -135,6 +135,8 @@ def load_ref():
         _sig(lib, "ref_l2_star", i32, P, u64, u32, C.POINTER(f64))
         _sig(lib, "ref_min_toroidal", i32, P, u64, u32, C.POINTER(f64))
         _sig(lib, "ref_stratification", i32, cstr, u32, u32, u32, u32, C.POINTER(i32))
+        _sig(lib, "ref_white_noise_xor_file", i32, u32, u32, u32, P, pu64)
+        _sig(lib, "ref_xor_stream_fill", i32, P, u64, u32, u32, u32, u32, u32, u64, u64, P)
         _ref = lib
     return _ref
 

@@ -30,6 +30,7 @@
 #include <memory>
 #include <mutex>
 #include <span>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -455,6 +456,44 @@ int ref_stratification(const char* kind, std::uint32_t dims, std::uint32_t seed,
         }
         const qmc::SampleStream s = qmc::make_stream(k, std::move(p));
         *ok = qmc::check_1d_stratification(s, j, m).ok ? 1 : 0;
+    });
+}
+// write_xor_table_file(white_noise_xor_tables(dims, pc, seed)) into `out`.
+int ref_white_noise_xor_file(std::uint32_t dims, std::uint32_t pc, std::uint32_t seed,
+                             unsigned char* out, std::uint64_t* len)
+{
+    return guard([&] {
+        std::ostringstream os;
+        qmc::write_xor_table_file(os, qmc::white_noise_xor_tables(dims, pc, seed));
+        const std::string b = os.str();
+        if (out && *len >= b.size())
+            std::memcpy(out, b.data(), b.size());
+        *len = b.size();
+    });
+}
+// Tables loaded from an XQT1 image with the CLI's point set (qmckit.cpp:
+// 121-139: Sobol' points, scrambles pixel_hash(j, seed, 0x5eed) when seeded),
+// then SampleStream(sobol_xor_table)::sample — float bits [n][dims].
+int ref_xor_stream_fill(const unsigned char* bytes, std::uint64_t len, std::uint32_t dims,
+                        std::uint32_t seed, std::uint32_t pc, std::uint32_t px, std::uint32_t py,
+                        std::uint64_t first, std::uint64_t n, std::uint32_t* out)
+{
+    return guard([&] {
+        const auto m = builtin_matrices(dims);
+        std::vector<std::uint32_t> pts(static_cast<std::size_t>(pc) * dims);
+        for (std::uint32_t i = 0; i < pc; ++i)
+            for (std::uint32_t j = 0; j < dims; ++j)
+                pts[static_cast<std::size_t>(i) * dims + j] = qmc::sobol_component_fixed(
+                    i, j, *m, seed ? qmc::pixel_hash(j, seed, 0x5eedu) : 0u);
+        std::istringstream in(std::string(reinterpret_cast<const char*>(bytes), len));
+        qmc::StreamParams p;
+        p.dims = dims;
+        p.pixel = qmc::PixelCoord{px, py, 8};
+        p.tables = std::make_shared<qmc::XorTables>(qmc::load_xor_tables(in, dims, pts, pc));
+        const qmc::SampleStream s = qmc::make_stream(qmc::SamplerKind::sobol_xor_table, std::move(p));
+        for (std::uint64_t i = 0; i < n; ++i)
+            for (std::uint32_t j = 0; j < dims; ++j)
+                out[i * dims + j] = std::bit_cast<std::uint32_t>(s.sample(first + i, j));
     });
 }
 double ref_neumaier(const double* v, std::uint64_t n)

@@ -34,7 +34,7 @@ __all__ = [
     "default_linear_factors", "lfsr_generator_vector", "pixel_hash", "hilbert_order_for",
     "partition_by_extra_dimension", "halton_pixel_enumeration", "sampler_kind_from_name",
     "integrate", "builtin_integrand", "write_probe", "l2_star_discrepancy",
-    "min_toroidal_distance", "check_1d_stratification",
+    "min_toroidal_distance", "check_1d_stratification", "XorTables",
     "SAMPLER_KINDS",
 ]
 
@@ -58,12 +58,13 @@ class StreamParams(C.Structure):
                 ("sobol_scrambles", P), ("sobol_scrambles_len", u32), ("halton_scramble", u32),
                 ("linear_factors", P), ("linear_factors_len", u32), ("px", u32), ("py", u32),
                 ("order", u32), ("spp", u32), ("width", u32), ("height", u32),
-                ("xor_seed", u32), ("xor_point_count", u32)]
+                ("xor_seed", u32), ("xor_point_count", u32), ("xor_tables", P)]
 
 
 class RenderJob(C.Structure):
     _fields_ = [("width", u32), ("height", u32), ("spp", u32), ("kind", i32), ("accum", i32),
-                ("seed", u32), ("generator", P), ("generator_dims", u32), ("matrices", P)]
+                ("seed", u32), ("generator", P), ("generator_dims", u32), ("matrices", P),
+                ("tables", P)]
 
 
 class IntegrationRow(C.Structure):
@@ -126,6 +127,12 @@ def lib():
     sig("qmc_min_toroidal_distance", i32, P, u64, u32, C.POINTER(f64), P)
     sig("qmc_check_1d_stratification", i32, i32, C.POINTER(StreamParams), u32, u32,
         C.POINTER(i32), P, P)
+    sig("qmc_xor_tables_white_noise", i32, u32, u32, u32, C.POINTER(P))
+    sig("qmc_xor_tables_load", i32, P, C.c_size_t, u32, P, u32, C.POINTER(P))
+    sig("qmc_xor_tables_write", i32, P, P, C.POINTER(C.c_size_t))
+    sig("qmc_xor_tables_dims", u32, P)
+    sig("qmc_xor_tables_point_count", u32, P)
+    sig("qmc_xor_tables_destroy", None, P)
     sig("qmc_builtin_integrand", i32, C.c_char_p, u32, C.POINTER(i32), C.POINTER(f64))
     sig("qmc_integrate", i32, i32, C.POINTER(StreamParams), i32, u32, u64, i32,
         C.POINTER(IntegrationRow), P)
@@ -296,6 +303,57 @@ class GeneratorMatrixSet:
             self._h = None
 
 
+class XorTables:
+    """XOR-table sampler data (imageplane.hpp:92-120) held by libqmcgpu."""
+
+    def __init__(self, handle: int):
+        self._h = handle
+
+    @classmethod
+    def white_noise(cls, dims: int, point_count: int, seed: int) -> "XorTables":
+        """white_noise_xor_tables (imageplane.cpp:197-229)."""
+        h = P()
+        _check(lib().qmc_xor_tables_white_noise(dims, point_count, seed, C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def load(cls, data: bytes, dims: int, points, point_count: int) -> "XorTables":
+        """load_xor_tables from an XQT1 file image (imageplane.cpp:163-195)."""
+        pts = _u32_host(points)
+        if pts.size != point_count * dims:
+            raise ConfigError("load_xor_tables: point set size does not match point_count * dims")
+        buf = C.create_string_buffer(bytes(data), len(data))
+        h = P()
+        _check(lib().qmc_xor_tables_load(buf, len(data), dims, pts.ctypes.data, point_count,
+                                         C.byref(h)))
+        return cls(h.value)
+
+    def to_bytes(self) -> bytes:
+        """write_xor_table_file (imageplane.cpp:154-161)."""
+        n = C.c_size_t(0)
+        _check(lib().qmc_xor_tables_write(self._h, None, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        _check(lib().qmc_xor_tables_write(self._h, buf, C.byref(n)))
+        return buf.raw[: n.value]
+
+    @property
+    def dims(self) -> int:
+        return lib().qmc_xor_tables_dims(self._h)
+
+    @property
+    def point_count(self) -> int:
+        return lib().qmc_xor_tables_point_count(self._h)
+
+    @property
+    def handle(self) -> int:
+        return self._h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.qmc_xor_tables_destroy(self._h)
+            self._h = None
+
+
 _builtin_cache: dict = {}
 
 
@@ -379,11 +437,13 @@ def stream_fill(kind: str, n: int, dims: int = 2, first: int = 0, *, generator=N
                 matrices: Optional[GeneratorMatrixSet] = None, sobol_scrambles=None,
                 scramble: str = "plain", linear_factors=None, pixel=(0, 0), order: int = 1,
                 spp: int = 1, width: int = 0, height: int = 0, xor_seed: int = 0,
-                xor_point_count: int = 1, fixed: bool = False, out=None, stream=None):
+                xor_point_count: int = 1, xor_tables: Optional["XorTables"] = None,
+                fixed: bool = False, out=None, stream=None):
     """make_stream(kind, params) + SampleStream::sample(i, j) (imageplane.cpp:310-461)."""
     k = sampler_kind_from_name(kind)
     p, keep = _stream_params(dims, generator, matrices, sobol_scrambles, scramble, linear_factors,
-                             pixel, order, spp, width, height, xor_seed, xor_point_count)
+                             pixel, order, spp, width, height, xor_seed, xor_point_count,
+                             xor_tables)
     o = _alloc(n, dims, fixed, out)
     _check(lib().qmc_stream_fill(k, C.byref(p), first, n, 1 if fixed else 0, _ptr(o),
                                  _stream(stream)))
@@ -391,7 +451,7 @@ def stream_fill(kind: str, n: int, dims: int = 2, first: int = 0, *, generator=N
 
 
 def _stream_params(dims, generator, matrices, sobol_scrambles, scramble, linear_factors, pixel,
-                   order, spp, width, height, xor_seed, xor_point_count):
+                   order, spp, width, height, xor_seed, xor_point_count, xor_tables=None):
     if scramble not in _RADICAL:
         raise ConfigError("make_stream: scramble must be plain, faure, or linear")
     keep = []
@@ -415,6 +475,9 @@ def _stream_params(dims, generator, matrices, sobol_scrambles, scramble, linear_
     p.px, p.py = pixel
     p.order, p.spp, p.width, p.height = order, spp, width, height
     p.xor_seed, p.xor_point_count = xor_seed, xor_point_count
+    if xor_tables is not None:
+        p.xor_tables = xor_tables.handle
+        keep.append(xor_tables)
     return p, keep
 
 
@@ -489,7 +552,8 @@ def integrate(kind: str, integrand: str, n: int, dims: int, accum: str = "kahan"
 
 def render(width: int, height: int, spp: int = 1, kind: str = "pixel-shifted-lattice",
            accum: str = "kahan", seed: int = 0, generator=None,
-           matrices: Optional[GeneratorMatrixSet] = None, rows=None, out=None, stream=None):
+           matrices: Optional[GeneratorMatrixSet] = None, tables: Optional[XorTables] = None,
+           rows=None, out=None, stream=None):
     """render(RenderJob) (render.cpp:83-143) for rows [r0, r1) of the image.
 
     Returns a [rows, width] float32 tensor (or fills `out`, device or host)."""
@@ -506,6 +570,8 @@ def render(width: int, height: int, spp: int = 1, kind: str = "pixel-shifted-lat
         job.generator, job.generator_dims = keep.ctypes.data, keep.size
     if matrices is not None:
         job.matrices = matrices.handle
+    if tables is not None:
+        job.tables = tables.handle
     r0, r1 = rows if rows is not None else (0, height)
     if out is None:
         torch = _torch()

@@ -1010,45 +1010,110 @@ void require(bool ok, const char* what)
         fail(QMC_CONFIG, what);
 }
 
-// white_noise_xor_tables (imageplane.cpp:197-229): std::mt19937 reorder /
-// scramble words on the host; the stored point set (first point_count
-// Sobol' points, XOR-scrambled per dimension when seed != 0) is generated on
-// the device by the Sobol' fill.
-struct XorTablesDev {
+} // namespace
+
+// XOR-table sampler data (imageplane.hpp:92-120): 128x128 reorder words,
+// 128x128xdims scramble words and the stored integer-stage point set.
+// Immutable; the device copy is built once per GPU.
+struct qmc_xor_tables {
     uint32_t dims = 0, point_count = 0;
-    DevPtr reorder, scramble, points;
+    std::vector<uint32_t> reorder, scramble; // host
+    std::vector<uint32_t> points;            // host (loaded) — empty for white noise
+    std::vector<uint32_t> dim_scramble;      // white noise: per-dim XOR of the points
+    bool white_noise = false;
+    std::mutex mu;
+    struct Dev {
+        DevPtr reorder, scramble, points;
+    };
+    std::map<int, std::unique_ptr<Dev>> dev;
+
+    const Dev& on_device(cudaStream_t s)
+    {
+        const int d = current_device();
+        std::lock_guard<std::mutex> lk(mu);
+        auto& slot = dev[d];
+        if (!slot) {
+            auto e = std::make_unique<Dev>();
+            e->reorder = dev_upload(reorder.data(), reorder.size() * 4);
+            e->scramble = dev_upload(scramble.data(), scramble.size() * 4);
+            if (white_noise) {
+                // the first point_count Sobol' points at the integer stage,
+                // XOR-scrambled per dimension when seeded (imageplane.cpp:224-227),
+                // generated by the device fill
+                void* pts = nullptr;
+                cuda_ok(cudaMalloc(&pts, static_cast<size_t>(point_count) * dims * 4 + 32),
+                        "cudaMalloc");
+                e->points.reset(pts);
+                const bool scr = std::any_of(dim_scramble.begin(), dim_scramble.end(),
+                                             [](uint32_t w) { return w != 0; });
+                sobol_fill_impl(builtin_matrices(dims), 0, point_count, dims,
+                                scr ? QMC_SOBOL_XOR : QMC_SOBOL_NONE, dim_scramble.data(),
+                                QMC_OUT_U32, pts, s);
+                cuda_ok(cudaStreamSynchronize(s), "sync");
+            } else {
+                e->points = dev_upload(points.data(), points.size() * 4);
+            }
+            slot = std::move(e);
+        }
+        return *slot;
+    }
 };
 
-XorTablesDev white_noise_tables(uint32_t dims, uint32_t point_count, uint32_t seed,
-                                cudaStream_t s)
+namespace {
+
+constexpr size_t kXorTile = 128 * 128;
+
+// white_noise_xor_tables (imageplane.cpp:197-229): std::mt19937 words on the
+// host, in the reference's draw order.
+std::unique_ptr<qmc_xor_tables> make_white_noise(uint32_t dims, uint32_t point_count,
+                                                 uint32_t seed)
 {
     if (dims == 0)
         fail(QMC_CONFIG, "white_noise_xor_tables: dims must be >= 1");
     if (point_count == 0 || (point_count & (point_count - 1)) != 0)
         fail(QMC_CONFIG, "white_noise_xor_tables: point count must be a power of two");
+    auto t = std::make_unique<qmc_xor_tables>();
+    t->dims = dims;
+    t->point_count = point_count;
+    t->white_noise = true;
     std::mt19937 rng(seed);
-    std::vector<uint32_t> dim_scramble(dims, 0u);
+    t->dim_scramble.assign(dims, 0u);
     if (seed != 0)
-        for (auto& w : dim_scramble)
+        for (auto& w : t->dim_scramble)
             w = rng();
-    constexpr size_t tile = 128 * 128;
-    std::vector<uint32_t> reorder(tile), scramble(tile * dims);
-    for (auto& v : reorder)
+    t->reorder.resize(kXorTile);
+    t->scramble.resize(kXorTile * dims);
+    for (auto& v : t->reorder)
         v = rng() & (point_count - 1);
-    for (auto& v : scramble)
+    for (auto& v : t->scramble)
         v = rng();
-    XorTablesDev t;
-    t.dims = dims;
-    t.point_count = point_count;
-    t.reorder = dev_upload(reorder.data(), reorder.size() * 4);
-    t.scramble = dev_upload(scramble.data(), scramble.size() * 4);
-    void* pts = nullptr;
-    cuda_ok(cudaMalloc(&pts, static_cast<size_t>(point_count) * dims * 4 + 16), "cudaMalloc");
-    t.points.reset(pts);
-    sobol_fill_impl(builtin_matrices(dims), 0, point_count, dims, seed ? QMC_SOBOL_XOR : QMC_SOBOL_NONE,
-                    dim_scramble.data(), QMC_OUT_U32, pts, s);
-    cuda_ok(cudaStreamSynchronize(s), "sync");
     return t;
+}
+
+// Device view of the tables a stream / render uses: the caller's handle, or
+// white-noise tables made for this call.
+struct XorTablesDev {
+    uint32_t dims = 0, point_count = 0;
+    const uint32_t *reorder = nullptr, *scramble = nullptr, *points = nullptr;
+    std::unique_ptr<qmc_xor_tables> own;
+};
+
+XorTablesDev xor_view(const qmc_xor_tables* given, uint32_t dims, uint32_t point_count,
+                      uint32_t seed, cudaStream_t s)
+{
+    XorTablesDev v;
+    qmc_xor_tables* t = const_cast<qmc_xor_tables*>(given);
+    if (!t) {
+        v.own = make_white_noise(dims, point_count, seed);
+        t = v.own.get();
+    }
+    const auto& d = t->on_device(s);
+    v.dims = t->dims;
+    v.point_count = t->point_count;
+    v.reorder = static_cast<const uint32_t*>(d.reorder.get());
+    v.scramble = static_cast<const uint32_t*>(d.scramble.get());
+    v.points = static_cast<const uint32_t*>(d.points.get());
+    return v;
 }
 
 } // namespace
@@ -1162,11 +1227,11 @@ void resolve_stream(qmc_sampler_kind kind, const qmc_stream_params* p, cudaStrea
         break;
     }
     case QMC_KIND_SOBOL_XOR_TABLE: {
-        r.xt = white_noise_tables(dims, p->xor_point_count, p->xor_seed, s);
+        r.xt = xor_view(p->xor_tables, dims, p->xor_point_count, p->xor_seed, s);
         require(dims <= r.xt.dims, "make_stream: dims beyond the stored point set");
-        q.xor_reorder = static_cast<const uint32_t*>(r.xt.reorder.get());
-        q.xor_scramble = static_cast<const uint32_t*>(r.xt.scramble.get());
-        q.xor_points = static_cast<const uint32_t*>(r.xt.points.get());
+        q.xor_reorder = r.xt.reorder;
+        q.xor_scramble = r.xt.scramble;
+        q.xor_points = r.xt.points;
         q.xor_point_count = r.xt.point_count;
         q.xor_dims = r.xt.dims;
         break;
@@ -1361,6 +1426,89 @@ qmc_status qmc_integrate(qmc_sampler_kind kind, const qmc_stream_params* p,
     });
 }
 
+// --------------------------------------------------------------- XOR tables
+
+qmc_status qmc_xor_tables_white_noise(uint32_t dims, uint32_t point_count, uint32_t seed,
+                                      qmc_xor_tables** out)
+{
+    return guard([&] { *out = make_white_noise(dims, point_count, seed).release(); });
+}
+
+// load_xor_tables (imageplane.cpp:163-195): "XQT1", 128^2 reorder words (used
+// modulo point_count), then 128^2 * dims scramble words, little-endian.
+qmc_status qmc_xor_tables_load(const void* bytes, size_t len, uint32_t dims,
+                               const uint32_t* points, uint32_t point_count,
+                               qmc_xor_tables** out)
+{
+    return guard([&] {
+        if (dims == 0)
+            fail(QMC_CONFIG, "load_xor_tables: dims must be >= 1");
+        if (point_count == 0 || (point_count & (point_count - 1)) != 0)
+            fail(QMC_CONFIG, "load_xor_tables: point count must be a power of two");
+        if (!points)
+            fail(QMC_CONFIG, "load_xor_tables: point set size does not match point_count * dims");
+        const unsigned char* b = static_cast<const unsigned char*>(bytes);
+        if (!b || len < 4 || std::memcmp(b, "XQT1", 4) != 0)
+            fail(QMC_CONFIG, "xor table file: bad magic, expected XQT1");
+        size_t pos = 4;
+        auto word = [&]() -> uint32_t {
+            if (pos + 4 > len)
+                fail(QMC_CONFIG, "xor table file: truncated");
+            const uint32_t v = static_cast<uint32_t>(b[pos]) | (static_cast<uint32_t>(b[pos + 1]) << 8) |
+                               (static_cast<uint32_t>(b[pos + 2]) << 16) |
+                               (static_cast<uint32_t>(b[pos + 3]) << 24);
+            pos += 4;
+            return v;
+        };
+        auto t = std::make_unique<qmc_xor_tables>();
+        t->dims = dims;
+        t->point_count = point_count;
+        t->reorder.resize(kXorTile);
+        for (auto& v : t->reorder)
+            v = word() & (point_count - 1);
+        t->scramble.resize(kXorTile * dims);
+        for (auto& v : t->scramble)
+            v = word();
+        t->points.assign(points, points + static_cast<size_t>(point_count) * dims);
+        *out = t.release();
+    });
+}
+
+// write_xor_table_file (imageplane.cpp:154-161).
+qmc_status qmc_xor_tables_write(const qmc_xor_tables* t, void* bytes, size_t* len)
+{
+    return guard([&] {
+        if (!t || !len)
+            fail(QMC_INVALID_ARGUMENT, "xor tables: null argument");
+        const size_t need = 4 + 4 * (t->reorder.size() + t->scramble.size());
+        if (!bytes || *len < need) {
+            *len = need;
+            if (bytes)
+                fail(QMC_INVALID_ARGUMENT, "xor tables: output buffer too small");
+            return;
+        }
+        unsigned char* o = static_cast<unsigned char*>(bytes);
+        std::memcpy(o, "XQT1", 4);
+        size_t pos = 4;
+        auto put = [&](uint32_t v) {
+            o[pos] = v & 0xff;
+            o[pos + 1] = (v >> 8) & 0xff;
+            o[pos + 2] = (v >> 16) & 0xff;
+            o[pos + 3] = (v >> 24) & 0xff;
+            pos += 4;
+        };
+        for (uint32_t v : t->reorder)
+            put(v);
+        for (uint32_t v : t->scramble)
+            put(v);
+        *len = need;
+    });
+}
+
+uint32_t qmc_xor_tables_dims(const qmc_xor_tables* t) { return t ? t->dims : 0; }
+uint32_t qmc_xor_tables_point_count(const qmc_xor_tables* t) { return t ? t->point_count : 0; }
+void qmc_xor_tables_destroy(qmc_xor_tables* t) { delete t; }
+
 // ------------------------------------------------------------ quality metrics
 
 namespace {
@@ -1547,11 +1695,13 @@ qmc_status qmc_render(const qmc_render_job* job, uint32_t row_begin, uint32_t ro
             uint32_t pc = 1;
             while (pc < job->spp)
                 pc <<= 1;
-            xt = white_noise_tables(2, pc, job->seed, s);
-            p.xor_reorder = static_cast<const uint32_t*>(xt.reorder.get());
-            p.xor_scramble = static_cast<const uint32_t*>(xt.scramble.get());
-            p.xor_points = static_cast<const uint32_t*>(xt.points.get());
-            p.xor_point_count = pc;
+            xt = xor_view(job->tables, 2, pc, job->seed, s);
+            require(xt.dims >= 2, "make_stream: dims beyond the stored point set");
+            p.xor_reorder = xt.reorder;
+            p.xor_scramble = xt.scramble;
+            p.xor_points = xt.points;
+            p.xor_point_count = xt.point_count;
+            p.xor_dims = xt.dims;
         }
         CallArgs args(s);
         const size_t coff = args.add(cols2.data(), cols2.size() * 4);

@@ -42,8 +42,8 @@ struct RenderParams {
     const uint32_t* cols2;    // device, [2][52] MSB-aligned columns (sobol)
     const uint32_t* xor_reorder;  // device, 128*128 (sobol_xor_table)
     const uint32_t* xor_scramble; // device, 128*128*2
-    const uint32_t* xor_points;   // device, point_count*2
-    uint32_t xor_point_count;
+    const uint32_t* xor_points;   // device, point_count*xor_dims
+    uint32_t xor_point_count, xor_dims;
 };
 
 // Per-stream (one pixel context) parameters for qmc_stream_fill kinds that

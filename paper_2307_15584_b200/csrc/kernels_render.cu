@@ -109,8 +109,10 @@ __device__ __forceinline__ void sample2(uint32_t i, const PixelState& s, const R
         x1 = phi3_fixed(s.ipy0 + i * p.scale_x);
     } else { // sobol_xor_table, imageplane.cpp:231-243
         const uint32_t k = i ^ __ldg(p.xor_reorder + s.cell);
-        x0 = __ldg(p.xor_points + 2u * k) ^ __ldg(p.xor_scramble + 2u * s.cell);
-        x1 = __ldg(p.xor_points + 2u * k + 1) ^ __ldg(p.xor_scramble + 2u * s.cell + 1);
+        const uint64_t pk = static_cast<uint64_t>(k) * p.xor_dims;
+        const uint32_t sc = s.cell * p.xor_dims;
+        x0 = __ldg(p.xor_points + pk) ^ __ldg(p.xor_scramble + sc);
+        x1 = __ldg(p.xor_points + pk + 1) ^ __ldg(p.xor_scramble + sc + 1);
     }
 }
 

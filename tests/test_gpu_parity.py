@@ -550,3 +550,48 @@ def test_stratification_vs_reference(ref, kind, dims):
             assert hist.sum() == 1 << m
     with pytest.raises(ValueError):
         q.check_1d_stratification("sobol", 0, 21, 2)
+
+
+# ------------------------------------------------------------ XOR tables
+def test_xor_tables_file_roundtrip_and_sampling(ref):
+    """XQT1 tables: the reference writes a white-noise file; the product loads
+    it with the CLI's stored point set and samples bit-identically; our
+    writer reproduces the same bytes (imageplane.cpp:154-248)."""
+    import ctypes as C
+    dims, pc, seed = 3, 256, 9
+    n = C.c_uint64(0)
+    assert ref.ref_white_noise_xor_file(dims, pc, seed, None, C.byref(n)) == 0
+    buf = np.zeros(n.value, np.uint8)
+    assert ref.ref_white_noise_xor_file(dims, pc, seed, ptr(buf), C.byref(n)) == 0
+    data = buf.tobytes()
+    assert data[:4] == b"XQT1"
+    # the product's white-noise tables write the same file
+    assert q.XorTables.white_noise(dims, pc, seed).to_bytes() == data
+    # CLI point set: Sobol' fixed points, XOR-scrambled with pixel_hash(j, seed, 0x5eed)
+    words = [q.pixel_hash(j, seed, 0x5EED) for j in range(dims)]
+    pts = u32(q.sobol_fill(pc, dims, scramble="xor", words=words, fixed=True)).reshape(pc, dims)
+    t = q.XorTables.load(data, dims, pts, pc)
+    assert (t.dims, t.point_count) == (dims, pc)
+    for px, py in [(0, 0), (5, 77), (127, 127), (300, 129)]:
+        got = u32(q.stream_fill("sobol-xor-table", pc, dims, xor_tables=t,
+                                pixel=(px, py))).reshape(pc, dims)
+        exp = np.zeros((pc, dims), np.uint32)
+        assert ref.ref_xor_stream_fill(data, len(data), dims, seed, pc, px, py, 0, pc,
+                                       ptr(exp)) == 0, ref.ref_last_error()
+        np.testing.assert_array_equal(got, exp)
+    with pytest.raises(q.ConfigError):
+        q.XorTables.load(b"XQT0" + data[4:], dims, pts, pc)
+    with pytest.raises(q.ConfigError):
+        q.XorTables.load(data[:100], dims, pts, pc)
+    with pytest.raises(IndexError):
+        q.stream_fill("sobol-xor-table", pc + 1, dims, xor_tables=t)
+
+
+def test_render_with_loaded_tables(ref):
+    """render() with caller tables equals render() with the white-noise
+    tables the job would build (render.cpp:102-104)."""
+    spp, seed = 8, 4
+    t = q.XorTables.white_noise(2, 8, seed)
+    a = q.render(40, 30, spp, kind="sobol-xor-table", seed=seed).cpu().numpy()
+    b = q.render(40, 30, spp, kind="sobol-xor-table", seed=seed, tables=t).cpu().numpy()
+    np.testing.assert_array_equal(a, b)
