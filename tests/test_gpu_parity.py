@@ -595,3 +595,19 @@ def test_render_with_loaded_tables(ref):
     a = q.render(40, 30, spp, kind="sobol-xor-table", seed=seed).cpu().numpy()
     b = q.render(40, 30, spp, kind="sobol-xor-table", seed=seed, tables=t).cpu().numpy()
     np.testing.assert_array_equal(a, b)
+
+
+def test_fills_capture_in_cuda_graph():
+    """Fills are stream-ordered single launches with no host sync, so they
+    can be captured in a CUDA graph and replayed (launch-bound configs)."""
+    n = 1 << 16
+    out = torch.zeros(n * 32, dtype=torch.float32, device="cuda")
+    ref_out = q.sobol_fill(n, 32, first=7, scramble="xor", words=list(range(32)))
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        q.sobol_fill(n, 32, first=7, scramble="xor", words=list(range(32)), out=out,
+                     stream=s.cuda_stream)
+    g.replay()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(u32(out), u32(ref_out).reshape(-1))
