@@ -172,6 +172,12 @@ __global__ void __launch_bounds__(kBlock)
         else
             load_small<DPL>(words + dq * DPL, xr);
     }
+    uint32_t omul[DPL], oadd[DPL]; // Owen seed terms, folded (owen_lk_folded)
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) {
+        omul[e] = (seed[e] >> 16) | 1u;
+        oadd[e] = seed[e] * omul[e];
+    }
 #pragma unroll
     for (int k = 0; k < LOG_PPS; ++k)
         if ((r >> k) & 1u) {
@@ -209,7 +215,7 @@ __global__ void __launch_bounds__(kBlock)
                 for (int e = 0; e < DPL; ++e) {
                     uint32_t val = x[e];
                     if (MODE == 2)
-                        val = brev32(owen_lk(val, seed[e]));
+                        val = brev32(owen_lk_folded(val, omul[e], oadd[e]));
                     y[e] = U32OUT ? val : map_bits(val);
                 }
                 if (!decltype(check)::value || (p0 + u * PPS) - first < n)
