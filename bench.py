@@ -438,7 +438,9 @@ def run_extra(q, stream, peak, args):
     img = torch.empty((2160, 3840), dtype=torch.float32, device="cuda")
     c5 = {}
     for spp in (1, 16, 64, 256):
-        for kind in ("pixel-shifted-lattice",):
+        kinds = ("pixel-shifted-lattice",) if spp != 64 else (
+            "pixel-shifted-lattice", "image-plane-halton", "pixel-random-lattice", "sobol")
+        for kind in kinds:
             fn = lambda: q.render(3840, 2160, spp, kind=kind, out=img)  # noqa: E731
             for _ in range(2):
                 fn()
@@ -448,6 +450,11 @@ def run_extra(q, stream, peak, args):
             c5["%s/spp%d" % (kind, spp)] = {
                 "value": 3840 * 2160 * spp / (avg * 1e-3) / 1e9, "unit": "G pixel-samples/s",
                 "ms_per_step": avg}
+    # the paper's comparison: pixel-shifted
+    # lattice vs the image-plane Halton enumeration, same render
+    c5["ratio_psl_over_image_plane_halton_spp64"] = {
+        "value": c5["pixel-shifted-lattice/spp64"]["value"] /
+        c5["image-plane-halton/spp64"]["value"], "unit": "x"}
     res["c5_render_4k"] = c5
     # next row: fused QMC integration (quality.cpp:214-282), Sobol' 8 dims
     ni = 1 << 26
