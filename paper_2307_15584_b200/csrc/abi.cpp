@@ -396,31 +396,33 @@ private:
 };
 
 // Fills SmallArgs array `which` (0 = a, 1 = b) by value when it fits the
-// parameter space, else stages a device copy through `args` (patched in
-// finish_small after the upload).
-void set_small(SmallArgs& sa, int which, const uint32_t* host, uint32_t n, CallArgs& args)
+// parameter space, else stages a device copy through `args`; the device
+// address is patched in by finish_small after the upload.
+struct SmallStage {
+    size_t off[2] = {SIZE_MAX, SIZE_MAX};
+};
+
+void set_small(SmallArgs& sa, SmallStage& st, int which, const uint32_t* host, uint32_t n,
+               CallArgs& args)
 {
-    uint32_t* dst = which ? sa.b : sa.a;
     if (n <= kSmall) {
-        std::memcpy(dst, host, n * 4);
+        std::memcpy(which ? sa.b : sa.a, host, n * 4);
         (which ? sa.has_b : sa.has_a) = 1;
         return;
     }
-    std::vector<uint32_t> pad(std::max<uint32_t>(n, 8) + 8, 0u);
+    std::vector<uint32_t> pad(std::max<uint32_t>(n, 8) + 8, 0u); // room for 32-B loads
     std::memcpy(pad.data(), host, n * 4);
-    const size_t off = args.add(pad.data(), pad.size() * 4);
-    (which ? sa.has_b : sa.has_a) = static_cast<uint32_t>(off + 1); // patched below
-    (which ? sa.dev_b : sa.dev_a) = reinterpret_cast<const uint32_t*>(uintptr_t(1));
+    st.off[which] = args.add(pad.data(), pad.size() * 4);
 }
 
-void finish_small(SmallArgs& sa, const CallArgs& args)
+void finish_small(SmallArgs& sa, const SmallStage& st, const CallArgs& args)
 {
-    if (sa.dev_a) {
-        sa.dev_a = args.at<uint32_t>(sa.has_a - 1);
+    if (st.off[0] != SIZE_MAX) {
+        sa.dev_a = args.at<uint32_t>(st.off[0]);
         sa.has_a = 1;
     }
-    if (sa.dev_b) {
-        sa.dev_b = args.at<uint32_t>(sa.has_b - 1);
+    if (st.off[1] != SIZE_MAX) {
+        sa.dev_b = args.at<uint32_t>(st.off[1]);
         sa.has_b = 1;
     }
 }
@@ -862,10 +864,11 @@ static void sobol_fill_impl(qmc_matrices* m, uint64_t first, uint64_t n, uint32_
     const uint32_t* colsT_rev = static_cast<const uint32_t*>(dev.colsT_rev.get());
     CallArgs args(s);
     SmallArgs small{};
+    SmallStage stage;
     if (words && sc != QMC_SOBOL_NONE)
-        set_small(small, 0, words, dims, args);
+        set_small(small, stage, 0, words, dims, args);
     args.upload();
-    finish_small(small, args);
+    finish_small(small, stage, args);
     const int mode = sc == QMC_SOBOL_OWEN ? 2 : 0;
     const bool u32 = kind == QMC_OUT_U32;
     place_fill(out, first, n, dims, s, [&](const FillRange& r, cudaStream_t st) {
@@ -953,11 +956,12 @@ static void lattice_fill_impl(const uint32_t* g, const uint32_t* shifts, uint32_
         fail(QMC_INVALID_ARGUMENT, "generator vector is null");
     CallArgs args(s);
     SmallArgs small{};
-    set_small(small, 0, g, dims, args);
+    SmallStage stage;
+    set_small(small, stage, 0, g, dims, args);
     if (shifts)
-        set_small(small, 1, shifts, dims, args);
+        set_small(small, stage, 1, shifts, dims, args);
     args.upload();
-    finish_small(small, args);
+    finish_small(small, stage, args);
     const bool u32 = kind == QMC_OUT_U32;
     place_fill(out, first, n, dims, s, [&](const FillRange& r, cudaStream_t st) {
         return launch_lattice(small, dims, u32, r, st);
