@@ -409,6 +409,16 @@ def run_extra(q, stream, peak, args):
     r1["l2"] = "4 rotating 64 MiB outputs (256 MiB > L2)"
     res["c1_vdc_2^24"] = r1
     del o1, g1
+    # the paper's "previous approach": linearly scrambled Halton, 32 dims
+    # (prime-base digit loops with tensor tables; ALU-bound, not HBM-bound)
+    nh = 1 << 24
+    oh = torch.empty((nh, 32), dtype=torch.float32, device="cuda")
+    rh = measure_fill("halton linear 2^24 x 32", lambda: q.halton_fill(nh, 32, scramble="linear",
+                                                                      out=oh),
+                      nh * 32, 5, 2, peak, stream)
+    rh["roofline"]["bound"] = "alu (digit loops)"
+    res["halton_linear_2^24x32"] = rh
+    del oh
     # C3: Owen / XOR scrambled Sobol' 2^28 x 64
     n3, d3 = 1 << 28, 64
     seeds = [q.pixel_hash(j, 1, 0x5EED) for j in range(d3)]

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <array>
 #include <map>
+#include <tuple>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -538,6 +539,55 @@ void place_fill(void* out, uint64_t first, uint64_t n, uint32_t dims, cudaStream
 
 cudaStream_t as_stream(qmc_stream s) { return static_cast<cudaStream_t>(s); }
 
+// Multi-digit tables (tensor_digit_table, radical.cpp:76-110) on the device:
+// d = the most base-b digits with b^d <= 4096 (so a table stays 16 KB and
+// L1-resident), entry v = the d digits of v permuted by sigma and mirrored.
+// Built once per (device, base, scramble) and kept for the process.
+struct DigitTable {
+    const uint32_t* ptr = nullptr;
+    uint32_t group = 0;
+};
+
+constexpr uint32_t kDigitTableMax = 4096;
+
+DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor)
+{
+    static std::mutex mu;
+    static std::map<std::tuple<int, uint32_t, uint32_t, uint32_t>, std::pair<DevPtr, uint32_t>>
+        cache;
+    uint32_t d = 0, group = 1;
+    while (static_cast<uint64_t>(group) * b <= kDigitTableMax) {
+        group *= b;
+        ++d;
+    }
+    if (d < 2)
+        return {};
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(mu);
+    auto& slot = cache[{dev, b, mode, factor}];
+    if (!slot.first) {
+        std::vector<uint32_t> sigma(b);
+        if (mode == 2) {
+            sigma = faure(b);
+        } else {
+            for (uint32_t a = 0; a < b; ++a)
+                sigma[a] = mode == 1 ? static_cast<uint32_t>((uint64_t(factor) * a) % b) : a;
+        }
+        std::vector<uint32_t> t(group + 8, 0u);
+        for (uint32_t v = 0; v < group; ++v) {
+            uint32_t rem = v, out = 0;
+            for (uint32_t k = 0; k < d; ++k) {
+                out = out * b + sigma[rem % b];
+                rem /= b;
+            }
+            t[v] = out;
+        }
+        slot.first = dev_upload(t.data(), t.size() * 4);
+        slot.second = group;
+    }
+    return {static_cast<const uint32_t*>(slot.first.get()), slot.second};
+}
+
 // RadicalDim table for `dims` prime bases (radical.cpp:130-181).
 std::vector<RadicalDim> radical_dims(uint32_t dims, uint32_t first_prime, qmc_radical_scramble sc,
                                      const uint32_t* factors, std::vector<uint32_t>& sigma_pool,
@@ -556,6 +606,9 @@ std::vector<RadicalDim> radical_dims(uint32_t dims, uint32_t first_prime, qmc_ra
         r.mode = 0;
         r.factor = 0;
         r.sigma = nullptr;
+        r.table = nullptr;
+        r.group = 0;
+        r.divg = Div32{0, 0};
         if (sc == QMC_RADICAL_LINEAR) {
             const uint32_t f = factors ? factors[j] : b - 1;
             if (f == 0 || f >= b)
@@ -568,6 +621,14 @@ std::vector<RadicalDim> radical_dims(uint32_t dims, uint32_t first_prime, qmc_ra
             sigma_off[j] = sigma_pool.size();
             sigma_pool.insert(sigma_pool.end(), s.begin(), s.end());
             r.mode = 2;
+        }
+        if (b > 2) {
+            const DigitTable t = digit_table(b, r.mode, r.factor);
+            if (t.ptr) {
+                r.table = t.ptr;
+                r.group = t.group;
+                r.divg = make_div32(t.group);
+            }
         }
     }
     return rd;
@@ -1171,6 +1232,7 @@ void resolve_stream(qmc_sampler_kind kind, const qmc_stream_params* p, cudaStrea
                 "make_stream: pixel outside the 2^order grid");
     };
     PixelStreamParams& q = r.q;
+    q.tab3 = digit_table(3, 0, 0).ptr;
     q.kind = kind;
     q.dims = dims;
     q.px = p->px;
@@ -1676,6 +1738,7 @@ qmc_status qmc_render(const qmc_render_job* job, uint32_t row_begin, uint32_t ro
             p.scr0 = pixel_hash_host(0, job->seed, 0);
             p.scr1 = pixel_hash_host(1, job->seed, 0);
         }
+        p.tab3 = digit_table(3, 0, 0).ptr; // phi_3, seven ternary digits per step
         std::vector<uint32_t> cols2(104, 0u);
         if (job->matrices) {
             require(job->matrices->dims >= 2, "make_stream: dims beyond the generator matrices");

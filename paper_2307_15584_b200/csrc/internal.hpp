@@ -44,6 +44,7 @@ struct RenderParams {
     const uint32_t* xor_scramble; // device, 128*128*2
     const uint32_t* xor_points;   // device, point_count*xor_dims
     uint32_t xor_point_count, xor_dims;
+    const uint32_t* tab3;         // device phi_3 7-digit table (or null)
 };
 
 // Per-stream (one pixel context) parameters for qmc_stream_fill kinds that
@@ -60,6 +61,7 @@ struct PixelStreamParams {
     const uint32_t* xor_scramble;
     const uint32_t* xor_points;
     uint32_t xor_point_count, xor_dims;
+    const uint32_t* tab3;        // device phi_3 7-digit table (or null)
 };
 
 // Small per-call arrays (XOR words / Owen seeds, generator vector, CP

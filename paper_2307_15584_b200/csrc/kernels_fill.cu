@@ -397,18 +397,38 @@ __global__ void __launch_bounds__(kBlock)
     }
 }
 
+// Prime-base Halton (radical.cpp:240-269), shared-memory tiled: a CTA owns
+// tiles of tp consecutive points; warp w computes dimensions w, w+8, ... for
+// the tile's points (one base per warp -> uniform digit loops, the
+// RadicalDim record is a warp-uniform load) into a padded [tp][dims+1]
+// shared tile, then the whole tile — tp*dims consecutive output words — is
+// written out coalesced.
 template <bool U32OUT>
 __global__ void __launch_bounds__(kBlock)
-    k_halton_generic(const RadicalDim* __restrict__ rd, uint32_t dims, Div32 div_dims,
-                     uint64_t first, uint32_t elems, uint32_t* __restrict__ out)
+    k_halton_tiled(const RadicalDim* __restrict__ rd, uint32_t dims, Div32 div_dims, uint32_t tp,
+                   uint64_t first, uint64_t n, uint64_t ntiles, uint32_t* __restrict__ out)
 {
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < elems; e += stride) {
-        const uint32_t p = point_of(e, dims, div_dims);
-        const uint32_t j = e - p * dims;
-        const RadicalDim r = rd[j];
-        const uint32_t x = radical_fixed(static_cast<uint32_t>(first + p), r);
-        out[e] = U32OUT ? x : map_bits(x);
+    extern __shared__ uint32_t tile[];
+    const uint32_t ld = dims + 1;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, nwarps = blockDim.x >> 5;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint64_t p0 = t * tp;
+        const uint32_t cnt = static_cast<uint32_t>(n - p0 < tp ? n - p0 : tp);
+        for (uint32_t j = warp; j < dims; j += nwarps) {
+            const RadicalDim r = rd[j];
+            for (uint32_t p = lane; p < cnt; p += 32) {
+                const uint32_t x = radical_fixed(static_cast<uint32_t>(first + p0 + p), r);
+                tile[p * ld + j] = U32OUT ? x : map_bits(x);
+            }
+        }
+        __syncthreads();
+        uint32_t* o = out + p0 * dims;
+        const uint32_t words = cnt * dims;
+        for (uint32_t e = threadIdx.x; e < words; e += blockDim.x) {
+            const uint32_t p = point_of(e, dims, div_dims);
+            o[e] = tile[p * ld + (e - p * dims)];
+        }
+        __syncthreads();
     }
 }
 
@@ -658,14 +678,29 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
 {
     if (r.n == 0)
         return cudaSuccess;
-    // rd[0].base == 2 is known to the caller; dims == 1 with base 2 is C1.
-    const Div32 d = dims >= 2 ? make_div32(dims) : Div32{0, 0};
-    return launch_chunked(dims, r, [&](unsigned grid, uint64_t first, uint32_t elems, uint32_t* o) {
-        u32 ? k_halton_generic<true><<<grid, kBlock, 0, s>>>(
-                  static_cast<const RadicalDim*>(rd), dims, d, first, elems, o)
-            : k_halton_generic<false><<<grid, kBlock, 0, s>>>(
-                  static_cast<const RadicalDim*>(rd), dims, d, first, elems, o);
-    });
+    // tile of tp points x (dims + 1) padded words: <= 32 KB, >= 32 points
+    uint32_t tp = (8192u / (dims + 1)) & ~31u;
+    if (tp < 32)
+        tp = 32;
+    const size_t smem = static_cast<size_t>(tp) * (dims + 1) * 4;
+    auto kern = u32 ? k_halton_tiled<true> : k_halton_tiled<false>;
+    if (smem > 48 * 1024) {
+        const cudaError_t e =
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess)
+            return e;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem) != cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    const uint64_t ntiles = (r.n + tp - 1) / tp;
+    const uint64_t cap = static_cast<uint64_t>(sm_count()) * per_sm;
+    const unsigned grid = static_cast<unsigned>(ntiles < cap ? ntiles : cap);
+    const Div32 dd = dims >= 2 ? make_div32(dims) : Div32{0, 0};
+    kern<<<grid, kBlock, smem, s>>>(static_cast<const RadicalDim*>(rd), dims, dd, tp, r.first,
+                                    r.n, ntiles, static_cast<uint32_t*>(r.out));
+    return cudaGetLastError();
 }
 
 cudaError_t launch_vdc(bool u32, const FillRange& r, cudaStream_t s)

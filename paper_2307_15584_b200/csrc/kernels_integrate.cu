@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kBlock)
     uint32_t shift = 0, ipx0 = 0, ipy0 = 0, cell = 0;
     uint64_t block = 0, off = 0;
     if (KIND == 4)
-        shift = phi3_fixed(static_cast<uint32_t>(hilbert_index(q.px, q.py, q.order)));
+        shift = phi3_fixed(static_cast<uint32_t>(hilbert_index(q.px, q.py, q.order)), q.tab3);
     if (KIND == 3)
         block = hilbert_index(q.px, q.py, q.order) * q.spp;
     if (KIND == 6) {
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kBlock)
                     x = brev32(~i) * (pixel_hash(j, q.px, q.py) | 1u);
                 else if (KIND == 6)
                     x = j == 0   ? rad2(ipx0 + i * q.scale_y)
-                        : j == 1 ? phi3_fixed(ipy0 + i * q.scale_x)
+                        : j == 1 ? phi3_fixed(ipy0 + i * q.scale_x, q.tab3)
                                  : radical_fixed(static_cast<uint32_t>(off + idx * q.stride), rd[j]);
                 else {
                     const uint32_t k = i ^ __ldg(q.xor_reorder + cell);

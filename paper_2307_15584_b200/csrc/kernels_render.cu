@@ -55,7 +55,7 @@ __device__ __forceinline__ PixelState pixel_state(uint32_t px, uint32_t py, cons
 {
     PixelState s{};
     if (KIND == 4) // pixel_shifted_lattice: phi_3(hilbert_index), imageplane.cpp:16-21
-        s.shift = phi3_fixed(static_cast<uint32_t>(hilbert_index(px, py, p.order)));
+        s.shift = phi3_fixed(static_cast<uint32_t>(hilbert_index(px, py, p.order)), p.tab3);
     if (KIND == 5) { // pixel_random_lattice, lattice.hpp:51-56
         s.g0 = pixel_hash(0, px, py) | 1u;
         s.g1 = pixel_hash(1, px, py) | 1u;
@@ -87,7 +87,7 @@ __device__ __forceinline__ void sample2(uint32_t i, const PixelState& s, const R
         x1 = sob1;
     } else if (KIND == 1) { // halton (plain)
         x0 = rad2(i);
-        x1 = phi3_fixed(i);
+        x1 = phi3_fixed(i, p.tab3);
     } else if (KIND == 2) { // lattice
         const uint32_t b = brev32(i);
         x0 = b * p.g0;
@@ -95,7 +95,7 @@ __device__ __forceinline__ void sample2(uint32_t i, const PixelState& s, const R
     } else if (KIND == 3) { // halton_hilbert
         const uint32_t gi = static_cast<uint32_t>(s.block + i);
         x0 = rad2(gi);
-        x1 = phi3_fixed(gi);
+        x1 = phi3_fixed(gi, p.tab3);
     } else if (KIND == 4) { // pixel_shifted_lattice (Eq. 3)
         const uint32_t b = brev32(i) + s.shift;
         x0 = b * p.g0;
@@ -106,7 +106,7 @@ __device__ __forceinline__ void sample2(uint32_t i, const PixelState& s, const R
         x1 = b * s.g1;
     } else if (KIND == 6) { // image_plane_halton: (offset + i*stride)>>a, / 3^b
         x0 = rad2(s.ipx0 + i * p.scale_y);
-        x1 = phi3_fixed(s.ipy0 + i * p.scale_x);
+        x1 = phi3_fixed(s.ipy0 + i * p.scale_x, p.tab3);
     } else { // sobol_xor_table, imageplane.cpp:231-243
         const uint32_t k = i ^ __ldg(p.xor_reorder + s.cell);
         const uint64_t pk = static_cast<uint64_t>(k) * p.xor_dims;
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(256)
     uint32_t shift = 0, ipx0 = 0, ipy0 = 0, cell = 0;
     uint64_t block = 0, off = 0;
     if (KIND == 4)
-        shift = phi3_fixed(static_cast<uint32_t>(hilbert_index(p.px, p.py, p.order)));
+        shift = phi3_fixed(static_cast<uint32_t>(hilbert_index(p.px, p.py, p.order)), p.tab3);
     if (KIND == 3)
         block = hilbert_index(p.px, p.py, p.order) * p.spp;
     if (KIND == 6) {
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(256)
             if (j == 0)
                 x = rad2(ipx0 + i * p.scale_y);
             else if (j == 1)
-                x = phi3_fixed(ipy0 + i * p.scale_x);
+                x = phi3_fixed(ipy0 + i * p.scale_x, p.tab3);
             else
                 x = radical_fixed(static_cast<uint32_t>(off + idx * p.stride), rd[j]);
         } else { // KIND == 7
