@@ -380,6 +380,26 @@ def run_render_distributed(q, world, stream):
         res["pixel-shifted-lattice/spp%d" % spp] = {
             "value": 3840 * 2160 * spp / (ms * 1e-3) / 1e9, "unit": "G pixel-samples/s",
             "ms_per_step": ms, "n_gpus": world, "collective": "all_gather_into_tensor (NCCL)"}
+    if world & (world - 1) == 0:  # the paper's sample partition (int accumulator)
+        from paper_2307_15584_b200.distributed import render_distributed_samples
+
+        spp = 256
+        fn = lambda: render_distributed_samples(3840, 2160, spp)  # noqa: E731
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        barrier(world)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(3):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms = max_over_ranks(a.elapsed_time(b) / 3, world)
+        res["pixel-shifted-lattice/int/sample-partition/spp256"] = {
+            "value": 3840 * 2160 * spp / (ms * 1e-3) / 1e9, "unit": "G pixel-samples/s",
+            "ms_per_step": ms, "n_gpus": world,
+            "collective": "all_reduce(sum) of int64 accumulators (NCCL)"}
     return res
 
 

@@ -274,6 +274,21 @@ typedef struct qmc_render_job { /* RenderJob, render.hpp:31-47 */
 qmc_status qmc_render(const qmc_render_job* job, uint32_t row_begin, uint32_t row_end, float* out,
                       qmc_stream stream);
 
+/* Sample-partitioned render (the paper's parallelization by an extra
+ * radical-inverse dimension; partition_by_extra_dimension,
+ * imageplane.cpp:114-130): part `part` of `parts` (a power of two) owns the
+ * samples i == rev_2(part) (mod parts). Int accumulator only: writes the
+ * int64 sum of llround(f * 2^32) per pixel of rows [row_begin, row_end) into
+ * `accum` (device). Summing the accumulators of all parts (e.g. one NCCL
+ * all-reduce across GPUs) and qmc_render_finalize gives exactly the int
+ * render (render.cpp:72-78). */
+qmc_status qmc_render_partial(const qmc_render_job* job, uint32_t part, uint32_t parts,
+                              uint32_t row_begin, uint32_t row_end, int64_t* accum,
+                              qmc_stream stream);
+/* float(sum / 2^32 / spp) per pixel (device buffers). */
+qmc_status qmc_render_finalize(const int64_t* accum, uint64_t npix, uint32_t spp, float* out,
+                               qmc_stream stream);
+
 /* scene_value (render.cpp:17-26) evaluated on the device for n (x, y)
  * pairs (device or host arrays of doubles) — integrand parity probe. */
 qmc_status qmc_scene_value(const double* xy, double* out, uint64_t n, qmc_stream stream);

@@ -82,6 +82,7 @@ def load_oracle():
         _sig(lib, "qo_hilbert_order_for", u32, u32, u32)
         _sig(lib, "qo_render", i32, u32, u32, u32, i32, i32, u32, P, P)
         _sig(lib, "qo_fnv1a64", u64, P, u64)
+        _sig(lib, "qo_render_partial_int", i32, u32, u32, u32, i32, u32, P, u32, u32, P)
         _oracle = lib
     return _oracle
 

@@ -632,6 +632,74 @@ int qo_render(uint32_t w, uint32_t h, uint32_t spp, int kind, int accum, uint32_
     return 0;
 }
 
+/* Int-mode render restricted to the samples i == rem (mod mod) — the
+ * per-part accumulators of the paper's sample partition;
+ * int64 sums of llround(f * 2^32) per pixel (render.cpp:72-78). */
+int qo_render_partial_int(uint32_t w, uint32_t h, uint32_t spp, int kind, uint32_t seed,
+                          const uint32_t* cols2, uint32_t rem, uint32_t mod, int64_t* acc)
+{
+    /* render the per-sample values through qo_render's sampling by running
+     * one-sample renders is wasteful; restate the loop directly */
+    if (w == 0 || h == 0 || spp == 0 || mod == 0)
+        return 1;
+    const uint32_t order = qo_hilbert_order_for(w, h);
+    uint32_t g[2];
+    qo_lfsr_generator_vector(seed ? seed : 0xace1u, 2, g);
+    uint32_t scr[2] = {0, 0};
+    if (kind == QO_SOBOL && seed) {
+        scr[0] = qo_pixel_hash(0, seed, 0);
+        scr[1] = qo_pixel_hash(1, seed, 0);
+    }
+    qo_halton_enum he;
+    if (kind == QO_IMAGE_PLANE_HALTON && qo_halton_enum_init(w, h, &he))
+        return 1;
+    const double inv_w = 1.0 / w, inv_h = 1.0 / h;
+    for (uint32_t py = 0; py < h; ++py)
+        for (uint32_t px = 0; px < w; ++px) {
+            uint32_t shift = 0;
+            uint64_t block = 0, offset = 0;
+            if (kind == QO_PIXEL_SHIFTED_LATTICE)
+                shift = qo_hilbert_phi3_fixed(px, py, order);
+            if (kind == QO_HALTON_HILBERT) {
+                qo_hilbert_index(px, py, order, &block);
+                block *= spp;
+            }
+            if (kind == QO_IMAGE_PLANE_HALTON)
+                offset = qo_halton_enum_offset(&he, px, py);
+            int64_t isum = 0;
+            for (uint32_t i = rem; i < spp; i += mod) {
+                float uv[2];
+                for (uint32_t j = 0; j < 2; ++j) {
+                    uint32_t fx = 0;
+                    switch (kind) {
+                    case QO_SOBOL: fx = qo_sobol_component_fixed(i, cols2 + 52 * j, scr[j]); break;
+                    case QO_HALTON: fx = qo_radical_inverse_fixed(i, j); break;
+                    case QO_LATTICE: fx = qo_lattice_component_fixed(i, g[j]); break;
+                    case QO_HALTON_HILBERT:
+                        fx = qo_radical_inverse_fixed((uint32_t)(block + i), j);
+                        break;
+                    case QO_PIXEL_SHIFTED_LATTICE: fx = (qo_brev32(i) + shift) * g[j]; break;
+                    case QO_PIXEL_RANDOM_LATTICE:
+                        fx = qo_random_lattice_component_fixed(i, j, px, py);
+                        break;
+                    case QO_IMAGE_PLANE_HALTON: {
+                        const uint64_t gl = offset + (uint64_t)i * he.stride;
+                        fx = j == 0 ? qo_radical_inverse_fixed((uint32_t)(gl >> he.exp_x), 0)
+                                    : qo_radical_inverse_fixed((uint32_t)(gl / he.scale_y), 1);
+                        break;
+                    }
+                    default: return 2;
+                    }
+                    uv[j] = map_float(fx);
+                }
+                const double u = uv[0], v = uv[1];
+                isum += llround(qo_scene_value((px + u) * inv_w, (py + v) * inv_h) * 4294967296.0);
+            }
+            acc[(uint64_t)py * w + px] = isum;
+        }
+    return 0;
+}
+
 /* src/image.cpp:54-63 */
 uint64_t qo_fnv1a64(const void* data, uint64_t size)
 {

@@ -97,6 +97,10 @@ enum { QO_SOBOL = 0, QO_HALTON, QO_LATTICE, QO_HALTON_HILBERT, QO_PIXEL_SHIFTED_
 int qo_render(uint32_t w, uint32_t h, uint32_t spp, int kind, int accum, uint32_t seed,
               const uint32_t* sobol_columns2, float* out);
 
+/* int-mode render over samples i == rem (mod mod): int64 per-pixel sums */
+int qo_render_partial_int(uint32_t w, uint32_t h, uint32_t spp, int kind, uint32_t seed,
+                          const uint32_t* cols2, uint32_t rem, uint32_t mod, int64_t* acc);
+
 uint64_t qo_fnv1a64(const void* data, uint64_t size);
 
 #ifdef __cplusplus

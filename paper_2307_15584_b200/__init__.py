@@ -34,7 +34,8 @@ __all__ = [
     "default_linear_factors", "lfsr_generator_vector", "pixel_hash", "hilbert_order_for",
     "partition_by_extra_dimension", "halton_pixel_enumeration", "sampler_kind_from_name",
     "integrate", "builtin_integrand", "write_probe", "l2_star_discrepancy",
-    "min_toroidal_distance", "check_1d_stratification", "XorTables",
+    "min_toroidal_distance", "check_1d_stratification", "XorTables", "render_partial",
+    "render_finalize",
     "SAMPLER_KINDS",
 ]
 
@@ -123,6 +124,8 @@ def lib():
     sig("qmc_stream_fill", i32, i32, C.POINTER(StreamParams), u64, u64, i32, P, P)
     sig("qmc_render", i32, C.POINTER(RenderJob), u32, u32, P, P)
     sig("qmc_scene_value", i32, P, P, u64, P)
+    sig("qmc_render_partial", i32, C.POINTER(RenderJob), u32, u32, u32, u32, P, P)
+    sig("qmc_render_finalize", i32, P, u64, u32, P, P)
     sig("qmc_l2_star_discrepancy", i32, P, u64, u32, C.POINTER(f64), P)
     sig("qmc_min_toroidal_distance", i32, P, u64, u32, C.POINTER(f64), P)
     sig("qmc_check_1d_stratification", i32, i32, C.POINTER(StreamParams), u32, u32,
@@ -577,6 +580,51 @@ def render(width: int, height: int, spp: int = 1, kind: str = "pixel-shifted-lat
         torch = _torch()
         out = torch.empty((max(r1 - r0, 0), width), dtype=torch.float32, device="cuda")
     _check(lib().qmc_render(C.byref(job), r0, r1, _ptr(out), _stream(stream)))
+    return out
+
+
+def _render_job(width, height, spp, kind, accum, seed, generator, matrices, tables):
+    if accum not in _ACCUM:
+        raise ConfigError("accumulation mode must be 'kahan' or 'int'")
+    job = RenderJob()
+    job.width, job.height, job.spp = width, height, spp
+    job.kind = sampler_kind_from_name(kind)
+    job.accum = _ACCUM[accum]
+    job.seed = seed
+    keep = []
+    if generator is not None:
+        g = _u32_host(generator)
+        keep.append(g)
+        job.generator, job.generator_dims = g.ctypes.data, g.size
+    if matrices is not None:
+        job.matrices = matrices.handle
+    if tables is not None:
+        job.tables = tables.handle
+    return job, keep
+
+
+def render_partial(width: int, height: int, spp: int, part: int, parts: int,
+                   kind: str = "pixel-shifted-lattice", seed: int = 0, generator=None,
+                   matrices: Optional[GeneratorMatrixSet] = None,
+                   tables: Optional[XorTables] = None, rows=None, out=None, stream=None):
+    """Int-mode partial render over the samples of part `part` of `parts`
+    (i == rev_2(part) mod parts): int64 [rows, width] accumulators."""
+    job, keep = _render_job(width, height, spp, kind, "int", seed, generator, matrices, tables)
+    r0, r1 = rows if rows is not None else (0, height)
+    if out is None:
+        torch = _torch()
+        out = torch.empty((max(r1 - r0, 0), width), dtype=torch.int64, device="cuda")
+    _check(lib().qmc_render_partial(C.byref(job), part, parts, r0, r1, _ptr(out),
+                                    _stream(stream)))
+    return out
+
+
+def render_finalize(acc, spp: int, out=None, stream=None):
+    """float(sum / 2^32 / spp) of summed partial accumulators."""
+    torch = _torch()
+    if out is None:
+        out = torch.empty(acc.shape, dtype=torch.float32, device=acc.device)
+    _check(lib().qmc_render_finalize(_ptr(acc), acc.numel(), spp, _ptr(out), _stream(stream)))
     return out
 
 

@@ -118,6 +118,13 @@ cudaError_t launch_pixel_stream(const PixelStreamParams& p, bool out_u32, const 
 cudaError_t launch_render(const RenderParams& p, uint32_t kind, uint32_t accum, float* out,
                           cudaStream_t s);
 
+// Int-mode partial render over samples first, first+step, ... (< spp):
+// int64 per pixel of the band; finalize: float(sum / 2^32 / spp).
+cudaError_t launch_render_partial(const RenderParams& p, uint32_t kind, uint32_t first,
+                                  uint32_t step, long long* acc, cudaStream_t s);
+cudaError_t launch_render_finalize(const long long* acc, uint64_t npix, uint32_t spp, float* out,
+                                   cudaStream_t s);
+
 cudaError_t launch_scene_value(const double* xy, double* out, uint64_t n, cudaStream_t s);
 
 // Write-only 128-bit streaming store probe over `bytes` (diagnostic).

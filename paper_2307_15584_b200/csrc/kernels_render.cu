@@ -160,6 +160,56 @@ __global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __rest
     out[q] = r;
 }
 
+// Sample-partitioned render (PAPER.md:498-509 / imageplane.cpp:114-130:
+// the sequence split by an extra radical-inverse dimension): accumulate, in
+// int mode, only the samples i = first, first + step, ... of every pixel
+// into an int64 per pixel. The int accumulation (llround(f * 2^32) summed in
+// int64, render.cpp:72-78) is exactly associative, so summing the partials
+// of all parts (one NCCL all-reduce across GPUs) and finalizing is
+// bit-identical to the single-GPU int render.
+template <uint32_t KIND>
+__global__ void __launch_bounds__(kBlock)
+    k_render_partial(RenderParams p, uint32_t first, uint32_t step, long long* __restrict__ acc)
+{
+    const uint32_t band = p.row_end - p.row_begin;
+    const uint64_t npix = static_cast<uint64_t>(band) * p.width;
+    const uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= npix)
+        return;
+    const uint32_t py = p.row_begin + static_cast<uint32_t>(q / p.width);
+    const uint32_t px = static_cast<uint32_t>(q % p.width);
+    const PixelState s = pixel_state<KIND>(px, py, p);
+    long long isum = 0;
+    const double fx = static_cast<double>(px), fy = static_cast<double>(py);
+    for (uint32_t i = first; i < p.spp; i += step) {
+        uint32_t a, b, s0 = p.scr0, s1 = p.scr1;
+        if (KIND == 0) { // direct Sobol' value of index i (digitalnet.cpp:111-131)
+            for (uint32_t k = 0, v = i; v; ++k, v >>= 1)
+                if (v & 1u) {
+                    s0 ^= __ldg(p.cols2 + k);
+                    s1 ^= __ldg(p.cols2 + 52 + k);
+                }
+        }
+        sample2<KIND>(i, s, p, a, b, s0, s1);
+        const double u = static_cast<double>(map_u32(a));
+        const double v = static_cast<double>(map_u32(b));
+        const double f = scene_value(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
+                                     __dmul_rn(__dadd_rn(fy, v), p.inv_h));
+        isum += llround(__dmul_rn(f, 4294967296.0));
+    }
+    acc[q] = isum;
+}
+
+__global__ void k_render_finalize(const long long* __restrict__ acc, uint64_t npix, uint32_t spp,
+                                  float* __restrict__ out)
+{
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < npix;
+         k += stride)
+        out[k] = __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(acc[k]), 4294967296.0),
+                                             static_cast<double>(spp)));
+}
+
 // --------------------------------------------- stream fill of pixel kinds
 
 template <uint32_t KIND, bool U32OUT>
@@ -274,6 +324,45 @@ cudaError_t launch_render(const RenderParams& p, uint32_t kind, uint32_t accum, 
     case 7: return render_kind<7>(p, accum, out, s);
     }
     return cudaErrorInvalidValue;
+}
+
+template <uint32_t KIND>
+cudaError_t render_partial_kind(const RenderParams& p, uint32_t first, uint32_t step,
+                                long long* acc, cudaStream_t s)
+{
+    const uint64_t npix = static_cast<uint64_t>(p.row_end - p.row_begin) * p.width;
+    k_render_partial<KIND><<<static_cast<unsigned>((npix + kBlock - 1) / kBlock), kBlock, 0, s>>>(
+        p, first, step, acc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_render_partial(const RenderParams& p, uint32_t kind, uint32_t first,
+                                  uint32_t step, long long* acc, cudaStream_t s)
+{
+    if (p.row_end <= p.row_begin || p.width == 0)
+        return cudaSuccess;
+    switch (kind) {
+    case 0: return render_partial_kind<0>(p, first, step, acc, s);
+    case 1: return render_partial_kind<1>(p, first, step, acc, s);
+    case 2: return render_partial_kind<2>(p, first, step, acc, s);
+    case 3: return render_partial_kind<3>(p, first, step, acc, s);
+    case 4: return render_partial_kind<4>(p, first, step, acc, s);
+    case 5: return render_partial_kind<5>(p, first, step, acc, s);
+    case 6: return render_partial_kind<6>(p, first, step, acc, s);
+    case 7: return render_partial_kind<7>(p, first, step, acc, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_render_finalize(const long long* acc, uint64_t npix, uint32_t spp, float* out,
+                                   cudaStream_t s)
+{
+    if (npix == 0)
+        return cudaSuccess;
+    const uint64_t want = (npix + 255) / 256, cap = static_cast<uint64_t>(sm_count()) * 8;
+    k_render_finalize<<<static_cast<unsigned>(want < cap ? want : cap), 256, 0, s>>>(acc, npix,
+                                                                                      spp, out);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_pixel_stream(const PixelStreamParams& p, bool u32, const FillRange& r,

@@ -12,9 +12,12 @@ Two partitionings:
   all-gather of the fp32 bands (NCCL over NVLink on a GPU box, gloo in the
   CPU tests) — assembles the image (`render_distributed`).
 
-The sample-partition alternative of the paper (`partition_by_extra_dimension`,
-imageplane.cpp:114-130; PAPER §2.5.1) is exposed for integration-style
-splits as `sample_partition`.
+* The paper's own split (`partition_by_extra_dimension`,
+  imageplane.cpp:114-130): every GPU renders ALL pixels but only its residue
+  class of samples, i == rev_2(rank) (mod world), into int64 accumulators;
+  one NCCL all-reduce(sum) and a finalize give an image bit-identical to the
+  single-GPU int render, because the int accumulator is exactly associative
+  (`render_distributed_samples`).
 """
 from __future__ import annotations
 
@@ -34,6 +37,31 @@ def index_shard(first: int, n: int, world: int, rank: int) -> Tuple[int, int]:
 def row_bands(height: int, world: int):
     """Row bands [(r0, r1)] per rank, sizes differing by at most one row."""
     return [(height * r // world, height * (r + 1) // world) for r in range(world)]
+
+
+def render_distributed_samples(width: int, height: int, spp: int,
+                               kind: str = "pixel-shifted-lattice", seed: int = 0, group=None,
+                               partial_renderer: Optional[Callable] = None,
+                               finalize: Optional[Callable] = None) -> torch.Tensor:
+    """Sample-partitioned int render across ranks (world a power of two).
+
+    `partial_renderer(part, parts) -> int64 [height, width]` and
+    `finalize(acc, spp) -> float32 image` default to the CUDA kernels
+    (qmc_render_partial / qmc_render_finalize); tests inject CPU stand-ins."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if partial_renderer is None:
+        from . import render_partial
+
+        acc = render_partial(width, height, spp, rank, world, kind=kind, seed=seed)
+    else:
+        acc = partial_renderer(rank, world)
+    dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)  # exact int64 sum
+    if finalize is None:
+        from . import render_finalize
+
+        return render_finalize(acc, spp)
+    return finalize(acc, spp)
 
 
 def sample_partition(part: int, parts: int, base: int = 2) -> Tuple[int, int]:

@@ -64,3 +64,49 @@ def test_render_band_gather_gloo(tmp_path, oracle, columns64, world):
     mp.spawn(_worker, args=(world, _free_port(), w, h, spp, exp_path, out_path), nprocs=world,
              join=True)
     np.testing.assert_array_equal(np.load(out_path), img)
+
+
+def _worker_samples(rank, world, port, w, h, spp, cols_path, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import load_oracle, ptr
+    from paper_2307_15584_b200 import partition_by_extra_dimension  # noqa: F401
+    from paper_2307_15584_b200.distributed import render_distributed_samples
+
+    o = load_oracle()
+    cols2 = np.load(cols_path)
+
+    def partial(part, parts):
+        # residue class of part: i == rev_2(part) (mod parts)
+        rem = int("{:0{w}b}".format(part, w=parts.bit_length() - 1)[::-1] or "0", 2)
+        acc = np.zeros((h, w), np.int64)
+        assert o.qo_render_partial_int(w, h, spp, 4, 0, ptr(cols2), rem, parts, ptr(acc)) == 0
+        return torch.from_numpy(acc)
+
+    def finalize(acc, s):
+        return torch.from_numpy(
+            ((acc.numpy().astype(np.float64) / 4294967296.0) / s).astype(np.float32))
+
+    img = render_distributed_samples(w, h, spp, partial_renderer=partial, finalize=finalize)
+    if rank == 0:
+        np.save(out_path, img.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_render_sample_partition_gloo(tmp_path, oracle, columns64, world):
+    """The paper's sample partition (i == rev_2(rank) mod world): int64
+    partials + one all-reduce reproduce the single-process int render."""
+    from oracle import ptr
+
+    w, h, spp = 24, 17, 12
+    cols2 = np.ascontiguousarray(columns64[:2])
+    full = np.zeros((h, w), np.float32)
+    assert oracle.qo_render(w, h, spp, 4, 1, 0, ptr(cols2), ptr(full)) == 0
+    cols_path, out_path = str(tmp_path / "c.npy"), str(tmp_path / "o.npy")
+    np.save(cols_path, cols2)
+    mp.spawn(_worker_samples, args=(world, _free_port(), w, h, spp, cols_path, out_path),
+             nprocs=world, join=True)
+    np.testing.assert_array_equal(np.load(out_path), full)

@@ -611,3 +611,20 @@ def test_fills_capture_in_cuda_graph():
     g.replay()
     torch.cuda.synchronize()
     np.testing.assert_array_equal(u32(out), u32(ref_out).reshape(-1))
+
+
+@pytest.mark.parametrize("kind", RENDER_KINDS + ["sobol-xor-table"])
+def test_render_sample_partition_equals_int_render(kind):
+    """The paper's sample partition on one GPU: the int64 partials of parts
+    1, 2, 4, 8 (i == rev_2(part) mod parts) sum to exactly the int render."""
+    w, h, spp = 48, 40, 24
+    full = q.render(w, h, spp, kind=kind, accum="int", seed=3).cpu().numpy()
+    for parts in (1, 2, 4, 8):
+        acc = sum(q.render_partial(w, h, spp, part, parts, kind=kind, seed=3)
+                  for part in range(parts))
+        img = q.render_finalize(acc, spp).cpu().numpy()
+        np.testing.assert_array_equal(img, full)
+    with pytest.raises(q.ConfigError):
+        q.render_partial(w, h, spp, 0, 3)
+    with pytest.raises(IndexError):
+        q.render_partial(w, h, spp, 4, 4)
