@@ -582,6 +582,37 @@ __global__ void __launch_bounds__(kBlock) k_write_probe(uint4* __restrict__ out,
     }
 }
 
+// mode 5: TMA bulk stores — each warp fills a 2 KB shared-memory buffer
+// (double-buffered) and one lane issues cp.async.bulk shared->global.
+__global__ void __launch_bounds__(kBlock) k_write_probe_tma(uint4* __restrict__ out, uint64_t n16)
+{
+    __shared__ __align__(128) uint4 buf[kBlock / 32][2][128]; // 2 x 2 KB per warp
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    const uint64_t chunks = n16 / 128; // 2 KB chunks
+    uint32_t k = 0;
+    for (uint64_t c = gw; c < chunks; c += nw, k ^= 1u) {
+        if (lane == 0)
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        uint4* b = buf[warp][k];
+        for (int e = lane; e < 128; e += 32)
+            b[e] = make_uint4(static_cast<uint32_t>(c), e, 0x3f000000u, lane);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+            const uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(b));
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 2048;" ::"l"(out + c * 128),
+                         "r"(src)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+    }
+    if (lane == 0)
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 } // namespace
 
 cudaError_t launch_write_probe(void* out, uint64_t bytes, int mode, cudaStream_t s)
@@ -593,6 +624,9 @@ cudaError_t launch_write_probe(void* out, uint64_t bytes, int mode, cudaStream_t
     case 2: k_write_probe<2><<<grid, kBlock, 0, s>>>(o, bytes / 16); break;
     case 3: k_write_probe<3><<<grid, kBlock, 0, s>>>(o, bytes / 16); break;
     case 4: return cudaMemsetAsync(out, 0, bytes, s);
+    case 5:
+        k_write_probe_tma<<<static_cast<unsigned>(sm_count() * 4), kBlock, 0, s>>>(o, bytes / 16);
+        break;
     default: k_write_probe<0><<<grid, kBlock, 0, s>>>(o, bytes / 16); break;
     }
     return cudaGetLastError();

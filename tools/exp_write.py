@@ -18,7 +18,7 @@ def t(fn, k=10):
     ms = sorted(a.elapsed_time(b) for a, b in ev)
     return B / (ms[len(ms)//2] * 1e-3) / 1e9, B / (ms[0] * 1e-3) / 1e9
 for rep in range(2):
-    for mode in range(5):
+    for mode in range(6):
         print("probe mode %d: median %.0f GB/s best %.0f" % ((mode,) + t(lambda: q.write_probe(out, mode))))
     print("C2 fill      : median %.0f GB/s best %.0f" % t(lambda: q.sobol_fill(n, d, matrices=m, out=out)))
     print("torch zero_  : median %.0f GB/s best %.0f" % t(lambda: out.zero_()))
