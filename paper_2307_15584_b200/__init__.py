@@ -25,7 +25,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("QMCGPU_LIB") or os.path.join(HERE, "libqmcgpu.so")
+LIB_PATH = os.path.join(HERE, "libqmcgpu.so")
 
 __all__ = [
     "ConfigError", "CudaError", "lib", "GeneratorMatrixSet", "map_u32_to_unifloat",

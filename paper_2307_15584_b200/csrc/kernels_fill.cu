@@ -13,7 +13,6 @@
 //     lattice update is one IMAD with a compile-time brev constant;
 //   * the float map is 9 full-rate ops (device.cuh map_u32).
 #include <algorithm>
-#include <cstdlib>
 #include <cstdint>
 #include <type_traits>
 
@@ -491,12 +490,8 @@ cudaError_t launch_chunked(uint32_t dims, const FillRange& r, F&& f)
 // TB/s), while the HBM-bound kernels gain ~1.5 % from 256-bit stores.
 int fast_dpl(uint32_t dims, const FillRange& r, bool issue_bound = false)
 {
-    static const int forced = [] {
-        const char* e = std::getenv("QMCGPU_FAST_DPL"); // experiment knob: 4 or 8
-        return e ? std::atoi(e) : 0;
-    }();
     const uintptr_t a = reinterpret_cast<uintptr_t>(r.out);
-    if (forced != 4 && !issue_bound && dims >= 8 && dims <= 256 && (256 % dims) == 0 && (a & 31u) == 0)
+    if (!issue_bound && dims >= 8 && dims <= 256 && (256 % dims) == 0 && (a & 31u) == 0)
         return 8;
     if (dims >= 4 && dims <= 128 && (128 % dims) == 0 && (a & 15u) == 0)
         return 4;
