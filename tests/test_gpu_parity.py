@@ -628,3 +628,60 @@ def test_render_sample_partition_equals_int_render(kind):
         q.render_partial(w, h, spp, 0, 3)
     with pytest.raises(IndexError):
         q.render_partial(w, h, spp, 4, 4)
+
+
+# ---------------------------------------------- out-of-bounds write canaries
+GUARD = 4096  # words of canary on each side (compute-sanitizer is closed on this pool)
+
+
+def _guarded(n_words, dtype=torch.int32):
+    buf = torch.full((n_words + 2 * GUARD,), 0x5A5A5A5A, dtype=dtype, device="cuda")
+    return buf, buf[GUARD:GUARD + n_words]
+
+
+def _canaries_intact(buf):
+    head, tail = buf[:GUARD], buf[-GUARD:]
+    return bool((head == 0x5A5A5A5A).all()) and bool((tail == 0x5A5A5A5A).all())
+
+
+@pytest.mark.parametrize("dims", [1, 3, 4, 8, 16, 32, 48, 64, 128, 256])
+def test_fills_write_exactly_their_range(dims):
+    for first, n in [(0, 1), (5, 777), (4096 * 7 + 3, 5000), ((1 << 40) + 11, 3001)]:
+        for call in (
+            lambda o: q.sobol_fill(n, dims, first=first, matrices=q.GeneratorMatrixSet.from_columns(
+                np.arange(dims * 52, dtype=np.uint32).reshape(dims, 52) | 1), out=o),
+            lambda o: q.sobol_fill(n, dims, first=first, scramble="owen", out=o,
+                                   words=list(range(dims)),
+                                   matrices=q.GeneratorMatrixSet.from_columns(
+                                       np.arange(dims * 52, dtype=np.uint32).reshape(dims, 52))),
+            lambda o: q.lattice_fill(n, [2 * k + 1 for k in range(dims)], first=first, out=o),
+            lambda o: q.halton_fill(n, min(dims, 100), first=first,
+                                    out=o[: n * min(dims, 100)]),
+        ):
+            buf, mid = _guarded(n * dims)
+            call(mid)
+            torch.cuda.synchronize()
+            assert _canaries_intact(buf), (dims, first, n)
+
+
+def test_render_and_streams_write_exactly_their_range():
+    for kind in q.SAMPLER_KINDS:
+        buf, mid = _guarded(23 * 37)
+        q.render(37, 30, 3, kind=kind, rows=(4, 27), out=mid.view(torch.float32))
+        torch.cuda.synchronize()
+        assert _canaries_intact(buf), kind
+        kw = {}
+        if kind in ("lattice", "pixel-shifted-lattice"):
+            kw["generator"] = q.lfsr_generator_vector(0xACE1, 3)
+        if kind in ("halton-hilbert", "pixel-shifted-lattice"):
+            kw.update(order=6, pixel=(5, 7))
+        if kind == "halton-hilbert":
+            kw["spp"] = 50
+        if kind == "image-plane-halton":
+            kw.update(width=30, height=20, pixel=(5, 7))
+        if kind == "sobol-xor-table":
+            kw.update(xor_point_count=64, xor_seed=3)
+        buf, mid = _guarded(50 * 3)
+        q.stream_fill(kind, 50, 3, out=mid, **kw)
+        torch.cuda.synchronize()
+        assert _canaries_intact(buf), kind

@@ -1,0 +1,49 @@
+"""Small calls of every kernel family, for compute-sanitizer (memcheck /
+racecheck / initcheck) runs: ragged sizes, tails, both lane widths."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import paper_2307_15584_b200 as q
+
+torch.cuda.set_device(0)
+for dims in (1, 3, 4, 8, 16, 32, 48, 64):
+    for first, n in ((0, 777), (12345, 1000), ((1 << 52) - 500, 500)):
+        q.sobol_fill(n, dims, first=first)
+        q.sobol_fill(n, dims, first=first, scramble="xor", words=list(range(dims)))
+        q.sobol_fill(n, dims, first=first, scramble="owen", words=list(range(dims)), fixed=True)
+    g = [2 * k + 1 for k in range(dims)]
+    q.lattice_fill(999, g, first=(1 << 32) - 100, shifts=list(range(dims)))
+    q.halton_fill(333, dims, first=77, scramble="faure")
+q.radical_inverse_fill(1001, 0)
+q.radical_inverse_fill(1001, 5, scramble="linear", factor=3)
+q.map_u32_to_unifloat(torch.arange(1000, dtype=torch.int32, device="cuda"))
+for kind in q.SAMPLER_KINDS:
+    kw = {}
+    if kind in ("lattice", "pixel-shifted-lattice"):
+        kw["generator"] = q.lfsr_generator_vector(0xACE1, 3)
+    if kind in ("halton-hilbert", "pixel-shifted-lattice"):
+        kw.update(order=6, pixel=(5, 7))
+    if kind == "halton-hilbert":
+        kw["spp"] = 50
+    if kind == "image-plane-halton":
+        kw.update(width=30, height=20, pixel=(5, 7))
+    if kind == "sobol-xor-table":
+        kw.update(xor_point_count=64, xor_seed=3)
+    q.stream_fill(kind, 50, 3, **kw)
+    q.render(37, 23, 5, kind=kind, seed=2)
+    q.render(37, 23, 5, kind=kind, accum="int", rows=(3, 11))
+    if kind != "sobol-xor-table":
+        q.integrate(kind, "product-sine", 5000, 3, stream_dims=3, **kw) if kind != "halton-hilbert" else None
+    acc = q.render_partial(37, 23, 5, 1, 2, kind=kind)
+    q.render_finalize(acc, 5)
+pts = q.sobol_fill(300, 5).contiguous()
+q.l2_star_discrepancy(pts)
+q.min_toroidal_distance(pts)
+q.check_1d_stratification("sobol", 1, 10, 4)
+t = q.XorTables.white_noise(3, 128, 1)
+q.stream_fill("sobol-xor-table", 100, 3, xor_tables=t, pixel=(3, 4))
+out = np.empty((5000, 16), np.float32)
+q.sobol_fill(5000, 16, out=out)
+torch.cuda.synchronize()
+print("sanitize smoke done")
