@@ -251,31 +251,83 @@ __global__ void __launch_bounds__(kBlock)
     }
 }
 
-// Any dims: one thread per (point, dim) element of a chunk whose element
-// count fits 32 bits; direct per-set-bit evaluation (digitalnet.cpp:111-131).
+// Any dims, shared-memory tiled: a CTA owns tiles of tp = 2^k consecutive
+// points; warp w computes dimensions w, w+8, ...: lane l holds points
+// p0 + l + 32 m, whose value is X(p0) ^ X(l) ^ X(32 m) (disjoint index bits).
+// X(32 m) for m < tp/32 is a per-CTA shared table T[j][m] built once, so the
+// m loop has no dependency chain (one LDS + XOR per sample). The padded
+// [tp][dims+1] tile is then written out as consecutive words.
 template <int MODE, bool U32OUT>
 __global__ void __launch_bounds__(kBlock)
-    k_sobol_generic(const uint32_t* __restrict__ colsT, const __grid_constant__ SmallArgs args,
-                    uint32_t dims, Div32 div_dims, uint64_t first, uint32_t elems,
-                    uint32_t* __restrict__ out)
+    k_sobol_tiled(const uint32_t* __restrict__ colsT, const __grid_constant__ SmallArgs args,
+                  uint32_t dims, Div32 div_dims, uint32_t tp, uint64_t first, uint64_t n,
+                  uint64_t tile0, uint64_t ntiles, uint32_t* __restrict__ out)
 {
+    extern __shared__ uint32_t smem[];
+    const uint32_t ld = dims + 1;
+    const uint32_t mt = tp / 32; // m steps per tile
+    uint32_t* tile = smem;
+    uint32_t* T = smem + static_cast<size_t>(tp) * ld; // [dims][mt]: X(32 m)
+    uint32_t* L = T + static_cast<size_t>(dims) * mt;  // [dims][32]: X(lane)
+    uint32_t* XP = L + static_cast<size_t>(dims) * 32; // [dims]: words ^ X(p0)
     const uint32_t* words = small_a(args);
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < elems; e += stride) {
-        const uint32_t p = point_of(e, dims, div_dims);
-        const uint32_t j = e - p * dims;
-        uint64_t i = first + p;
-        uint32_t x = (MODE == 0 && words) ? words[j] : 0u;
-        for (uint32_t k = 0; i; ++k, i >>= 1)
-            if (i & 1u)
-                x ^= __ldg(colsT + k * dims + j);
-        if (MODE == 2)
-            x = brev32(owen_lk(brev32(x), words ? words[j] : 0u));
-        out[e] = U32OUT ? x : map_bits(x);
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, nwarps = blockDim.x >> 5;
+    auto col = [&](uint32_t k, uint32_t j) {
+        return __ldg(colsT + static_cast<size_t>(k) * dims + j);
+    };
+    for (uint32_t e = threadIdx.x; e < dims * mt; e += blockDim.x) {
+        const uint32_t j = e / mt, m = e - j * mt;
+        uint32_t x = 0;
+        for (uint32_t k = 0; (m >> k) != 0; ++k)
+            if ((m >> k) & 1u)
+                x ^= col(5 + k, j);
+        T[e] = x;
+    }
+    for (uint32_t e = threadIdx.x; e < dims * 32; e += blockDim.x) {
+        const uint32_t j = e >> 5, l = e & 31u;
+        uint32_t x = 0;
+        for (uint32_t k = 0; k < 5; ++k)
+            if ((l >> k) & 1u)
+                x ^= col(k, j);
+        L[e] = x;
+    }
+    for (uint64_t t = tile0 + blockIdx.x; t < tile0 + ntiles; t += gridDim.x) {
+        const uint64_t p0 = t * tp; // absolute index of the tile's first point
+        __syncthreads(); // T/L ready (first tile), XP free (later tiles)
+        for (uint32_t j = threadIdx.x; j < dims; j += blockDim.x) {
+            uint32_t x = (MODE == 0 && words) ? words[j] : 0u;
+            for (uint64_t b = p0; b; b &= b - 1)
+                x ^= col(__ffsll(static_cast<long long>(b)) - 1, j);
+            XP[j] = x;
+        }
+        __syncthreads();
+        for (uint32_t j = warp; j < dims; j += nwarps) {
+            const uint32_t x = XP[j] ^ L[j * 32 + lane];
+            const uint32_t seed = (MODE == 2 && words) ? words[j] : 0u;
+            const uint32_t* Tj = T + j * mt;
+            for (uint32_t m = 0; m < mt; ++m) {
+                const uint64_t i = p0 + lane + 32ull * m;
+                uint32_t v = x ^ Tj[m];
+                if (MODE == 2)
+                    v = brev32(owen_lk(v, seed));
+                if (i - first < n)
+                    tile[(lane + 32 * m) * ld + j] = U32OUT ? v : map_bits(v);
+            }
+        }
+        __syncthreads();
+        // rows [lo, hi) of the tile that belong to [first, first + n)
+        const uint64_t lo = p0 > first ? p0 : first;
+        const uint64_t hi = (p0 + tp < first + n) ? p0 + tp : first + n;
+        const uint32_t r0 = static_cast<uint32_t>(lo - p0);
+        const uint32_t words_out = static_cast<uint32_t>(hi - lo) * dims;
+        uint32_t* o = out + (lo - first) * dims;
+        for (uint32_t e = threadIdx.x; e < words_out; e += blockDim.x) {
+            const uint32_t pr = point_of(e, dims, div_dims);
+            o[e] = tile[(r0 + pr) * ld + (e - pr * dims)];
+        }
+        __syncthreads();
     }
 }
-
-// ---------------------------------------------------------------- lattice
 
 // x_j(i) = brev((uint32_t)i) * g_j + s_j (mod 2^32). Inside a tile the index
 // is P | (u << LOG_PPS) | r with disjoint bits, so brev(i) = brev(P | r) +
@@ -670,16 +722,32 @@ cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const
         return by_log_pps<4>(dims, [&](auto lp) {
             return sobol_fast_dispatch<4, decltype(lp)::value>(cols, words, mode, u32, r, s);
         });
-    // the generic kernel reads columns in the normal domain for both modes
+    // shared-memory tiled path: tp = 2^k points with tp*(dims+1) <= 8192 words
+    uint32_t tp = 32;
+    while (tp * 2 * (dims + 1) <= 8192u)
+        tp *= 2;
+    const size_t smem = (static_cast<size_t>(tp) * (dims + 1) +
+                         static_cast<size_t>(dims) * (tp / 32 + 33)) * 4;
+    auto kern = mode == 2 ? (u32 ? k_sobol_tiled<2, true> : k_sobol_tiled<2, false>)
+                          : (u32 ? k_sobol_tiled<0, true> : k_sobol_tiled<0, false>);
+    if (smem > 48 * 1024) {
+        const cudaError_t e =
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess)
+            return e;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem) != cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    const uint64_t tile0 = r.first / tp;
+    const uint64_t ntiles = (r.first + r.n + tp - 1) / tp - tile0;
+    const uint64_t cap = static_cast<uint64_t>(sm_count()) * per_sm;
+    const unsigned grid = static_cast<unsigned>(ntiles < cap ? ntiles : cap);
     const Div32 d = dims >= 2 ? make_div32(dims) : Div32{0, 0};
-    return launch_chunked(dims, r, [&](unsigned grid, uint64_t first, uint32_t elems, uint32_t* o) {
-        if (mode == 2)
-            u32 ? k_sobol_generic<2, true><<<grid, kBlock, 0, s>>>(colsT, words, dims, d, first, elems, o)
-                : k_sobol_generic<2, false><<<grid, kBlock, 0, s>>>(colsT, words, dims, d, first, elems, o);
-        else
-            u32 ? k_sobol_generic<0, true><<<grid, kBlock, 0, s>>>(colsT, words, dims, d, first, elems, o)
-                : k_sobol_generic<0, false><<<grid, kBlock, 0, s>>>(colsT, words, dims, d, first, elems, o);
-    });
+    kern<<<grid, kBlock, smem, s>>>(cols, words, dims, d, tp, r.first, r.n, tile0, ntiles,
+                                    static_cast<uint32_t*>(r.out));
+    return cudaGetLastError();
 }
 
 cudaError_t launch_lattice(const SmallArgs& args, uint32_t dims, bool u32, const FillRange& r,
