@@ -160,6 +160,62 @@ __global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __rest
     out[q] = r;
 }
 
+// Few pixels, many samples (npix < kWarpPixels, spp >= 64): one warp per
+// pixel, lane l takes samples l, l + 32, ... and the warp reduces with
+// shuffles. int: exact int64 butterfly sum -> bit-identical to the
+// sequential sum. kahan: per-lane Neumaier, lanes combined by a fixed
+// compensated butterfly -> deterministic, within ~1e-16 relative of the
+// reference's sequential order (north_star tolerance 1e-6).
+template <uint32_t KIND, uint32_t ACCUM>
+__global__ void __launch_bounds__(kBlock) k_render_warp(RenderParams p, float* __restrict__ out)
+{
+    const uint32_t band = p.row_end - p.row_begin;
+    const uint64_t npix = static_cast<uint64_t>(band) * p.width;
+    const uint64_t q = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31u;
+    if (q >= npix)
+        return; // whole warp
+    const uint32_t py = p.row_begin + static_cast<uint32_t>(q / p.width);
+    const uint32_t px = static_cast<uint32_t>(q % p.width);
+    const PixelState s = pixel_state<KIND>(px, py, p);
+    double sum = 0.0, comp = 0.0;
+    long long isum = 0;
+    const double fx = static_cast<double>(px), fy = static_cast<double>(py);
+    for (uint32_t i = lane; i < p.spp; i += 32) {
+        uint32_t a, b, s0 = p.scr0, s1 = p.scr1;
+        if (KIND == 0) // direct Sobol' value of index i (digitalnet.cpp:111-131)
+            for (uint32_t k = 0, v = i; v; ++k, v >>= 1)
+                if (v & 1u) {
+                    s0 ^= __ldg(p.cols2 + k);
+                    s1 ^= __ldg(p.cols2 + 52 + k);
+                }
+        sample2<KIND>(i, s, p, a, b, s0, s1);
+        const double u = static_cast<double>(map_u32(a));
+        const double v = static_cast<double>(map_u32(b));
+        const double f = scene_value(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
+                                     __dmul_rn(__dadd_rn(fy, v), p.inv_h));
+        if (ACCUM == 0)
+            neumaier_add(sum, comp, f);
+        else
+            isum += llround(__dmul_rn(f, 4294967296.0));
+    }
+    for (int o = 16; o; o >>= 1) {
+        if (ACCUM == 0) {
+            const double os = __shfl_xor_sync(0xffffffffu, sum, o);
+            const double oc = __shfl_xor_sync(0xffffffffu, comp, o);
+            neumaier_add(sum, comp, os);
+            comp = __dadd_rn(comp, oc);
+        } else {
+            isum += __shfl_xor_sync(0xffffffffu, isum, o);
+        }
+    }
+    if (lane == 0)
+        out[q] = ACCUM == 0
+                     ? __double2float_rn(__ddiv_rn(__dadd_rn(sum, comp), static_cast<double>(p.spp)))
+                     : __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(isum), 4294967296.0),
+                                                   static_cast<double>(p.spp)));
+}
+
 // Sample-partitioned render (PAPER.md:498-509 / imageplane.cpp:114-130:
 // the sequence split by an extra radical-inverse dimension): accumulate, in
 // int mode, only the samples i = first, first + step, ... of every pixel
@@ -270,10 +326,20 @@ __global__ void k_scene_value(const double* __restrict__ xy, double* __restrict_
         out[k] = scene_value(xy[2 * k], xy[2 * k + 1]);
 }
 
+constexpr uint64_t kWarpPixels = 32768; // below this (and spp >= 64): warp per pixel
+
 template <uint32_t KIND>
 cudaError_t render_kind(const RenderParams& p, uint32_t accum, float* out, cudaStream_t s)
 {
     const uint64_t npix = static_cast<uint64_t>(p.row_end - p.row_begin) * p.width;
+    if (npix < kWarpPixels && p.spp >= 64) {
+        const unsigned wgrid = static_cast<unsigned>((npix * 32 + kBlock - 1) / kBlock);
+        if (accum == 0)
+            k_render_warp<KIND, 0><<<wgrid, kBlock, 0, s>>>(p, out);
+        else
+            k_render_warp<KIND, 1><<<wgrid, kBlock, 0, s>>>(p, out);
+        return cudaGetLastError();
+    }
     const unsigned grid = static_cast<unsigned>((npix + kBlock - 1) / kBlock);
     if (accum == 0)
         k_render<KIND, 0><<<grid, kBlock, 0, s>>>(p, out);

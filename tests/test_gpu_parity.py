@@ -685,3 +685,21 @@ def test_render_and_streams_write_exactly_their_range():
         q.stream_fill(kind, 50, 3, out=mid, **kw)
         torch.cuda.synchronize()
         assert _canaries_intact(buf), kind
+
+
+@pytest.mark.parametrize("kind", ["pixel-shifted-lattice", "sobol", "image-plane-halton",
+                                  "pixel-random-lattice"])
+def test_render_small_image_high_spp_warp_path(ref, kind):
+    """Few pixels x many samples takes the warp-per-pixel kernel (shuffle
+    reductions): int mode stays bit-identical to the reference's sequential
+    int sum; Kahan mode within 1e-12 relative."""
+    w, h, spp = 24, 16, 1000
+    for accum in ("int", "kahan"):
+        exp = np.zeros((h, w), np.float32)
+        assert ref.ref_render(w, h, spp, kind.encode(), accum.encode(), 0, 8, ptr(exp)) == 0
+        got = q.render(w, h, spp, kind=kind, accum=accum).cpu().numpy()
+        if accum == "int":
+            np.testing.assert_array_equal(got, exp)
+        else:
+            rel = np.abs(got.astype(np.float64) - exp) / np.maximum(np.abs(exp), 1e-30)
+            assert rel.max() <= 1e-6, rel.max()
