@@ -329,6 +329,186 @@ __global__ void __launch_bounds__(kBlock)
     }
 }
 
+// dims 1 and 2: a lane owns Q = 8 / D consecutive points (8 words, one
+// 256-bit store); a warp step covers PPS = 32 Q points. Point base + o of a
+// lane has value X(P) ^ X(u PPS) ^ X(lane Q) ^ X(o) (disjoint index bits):
+// X(o) are 7 register constants, the step update is the usual compile-time
+// ctz mask. One XOR + the map per sample.
+template <int D, int MODE, bool U32OUT>
+__global__ void __launch_bounds__(kBlock)
+    k_sobol_narrow(const uint32_t* __restrict__ colsT, const __grid_constant__ SmallArgs args,
+                   uint64_t first, uint64_t n, uint64_t tile0, uint64_t ntiles, uint64_t per_warp,
+                   uint32_t* __restrict__ out)
+{
+    constexpr int Q = 8 / D, LOG_Q = D == 1 ? 3 : 2;
+    constexpr int LOG_PPS = LOG_Q + 5, PPS = 1 << LOG_PPS;
+    constexpr int LOG_TP = LOG_PPS + 5;
+    uint64_t t, tend;
+    if (!warp_tiles(tile0, ntiles, per_warp, t, tend))
+        return;
+    const uint32_t lane = threadIdx.x & 31u;
+    auto col = [&](uint32_t k, int d) { return __ldg(colsT + k * D + d); };
+    uint32_t xo[Q][D], Dm[5][D], xl[D], xp[D], seed[D], omul[D], oadd[D];
+    const uint32_t* words = small_a(args);
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        seed[d] = (MODE == 2 && words) ? words[d] : 0u;
+        omul[d] = (seed[d] >> 16) | 1u;
+        oadd[d] = seed[d] * omul[d];
+        uint32_t acc = 0;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            acc ^= col(LOG_PPS + k, d);
+            Dm[k][d] = acc;
+        }
+#pragma unroll
+        for (int o = 0; o < Q; ++o) {
+            uint32_t v = 0;
+#pragma unroll
+            for (int k = 0; k < LOG_Q; ++k)
+                if ((o >> k) & 1)
+                    v ^= col(k, d);
+            xo[o][d] = v;
+        }
+        uint32_t v = (MODE == 0 && words) ? words[d] : 0u;
+#pragma unroll
+        for (int k = 0; k < 5; ++k)
+            if ((lane >> k) & 1u)
+                v ^= col(LOG_Q + k, d);
+        xl[d] = v;
+        xp[d] = 0;
+        for (uint64_t b = t; b; b &= b - 1)
+            xp[d] ^= col(LOG_TP + __ffsll(static_cast<long long>(b)) - 1, d);
+    }
+    for (;;) {
+        const uint64_t p0 = (t << LOG_TP) + lane * Q; // lane's first point at step 0
+        uint32_t x[D], y[8];
+#pragma unroll
+        for (int d = 0; d < D; ++d)
+            x[d] = xp[d] ^ xl[d];
+        const uint64_t lo = t << LOG_TP, hi = (t + 1) << LOG_TP;
+        const bool full = lo >= first && hi <= first + n;
+        uint32_t* o = out + (p0 - first) * D;
+        auto group = [&](uint32_t v, auto check) {
+#pragma unroll
+            for (uint32_t w = 0; w < 8; ++w) {
+                const uint32_t u = 8 * v + w;
+#pragma unroll
+                for (int q = 0; q < Q; ++q)
+#pragma unroll
+                    for (int d = 0; d < D; ++d) {
+                        uint32_t val = x[d] ^ xo[q][d];
+                        if (MODE == 2)
+                            val = brev32(owen_lk_folded(val, omul[d], oadd[d]));
+                        y[q * D + d] = U32OUT ? val : map_bits(val);
+                    }
+                if (!decltype(check)::value) {
+                    store_vec<8>(o + u * 256, y);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < Q; ++q)
+                        if ((p0 + u * PPS + q) - first < n)
+#pragma unroll
+                            for (int d = 0; d < D; ++d)
+                                o[u * 256 + q * D + d] = y[q * D + d];
+                }
+                if (w < 7) {
+#pragma unroll
+                    for (int d = 0; d < D; ++d)
+                        x[d] ^= Dm[ctz_const(w + 1)][d];
+                }
+            }
+#pragma unroll
+            for (int d = 0; d < D; ++d)
+                x[d] ^= (v == 1) ? Dm[4][d] : Dm[3][d];
+        };
+        if (full) {
+#pragma unroll 1
+            for (uint32_t v = 0; v < 4; ++v)
+                group(v, std::false_type{});
+        } else {
+#pragma unroll 1
+            for (uint32_t v = 0; v < 4; ++v)
+                group(v, std::true_type{});
+        }
+        if (++t >= tend)
+            break;
+        const int cz = __ffsll(static_cast<long long>(t)) - 1;
+        for (int k = 0; k <= cz; ++k)
+#pragma unroll
+            for (int d = 0; d < D; ++d)
+                xp[d] ^= col(LOG_TP + k, d);
+    }
+}
+
+// Lattice, dims 1 and 2 (same lane layout as k_sobol_narrow):
+// brev(i) = brev(P + lane Q) + brev(u PPS) + brev(o), disjoint bits.
+template <int D, bool U32OUT>
+__global__ void __launch_bounds__(kBlock)
+    k_lattice_narrow(const uint32_t* __restrict__ unused, const __grid_constant__ SmallArgs args,
+                     uint64_t first, uint64_t n, uint64_t tile0, uint64_t ntiles,
+                     uint64_t per_warp, uint32_t* __restrict__ out)
+{
+    constexpr int Q = 8 / D, LOG_Q = D == 1 ? 3 : 2;
+    constexpr int LOG_PPS = LOG_Q + 5, PPS = 1 << LOG_PPS;
+    constexpr int LOG_TP = LOG_PPS + 5;
+    uint64_t t, tend;
+    if (!warp_tiles(tile0, ntiles, per_warp, t, tend))
+        return;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t* g = small_a(args);
+    const uint32_t* sh = small_b(args);
+    uint32_t gv[D], sv[D], G[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        gv[d] = g[d];
+        sv[d] = sh ? sh[d] : 0u;
+        G[d] = gv[d] << (27 - LOG_PPS);
+    }
+    for (; t < tend; ++t) {
+        const uint64_t p0 = (t << LOG_TP) + lane * Q;
+        const uint32_t b = brev32(static_cast<uint32_t>(p0));
+        uint32_t x0[D], y[8];
+#pragma unroll
+        for (int d = 0; d < D; ++d)
+            x0[d] = b * gv[d] + sv[d];
+        const uint64_t lo = t << LOG_TP, hi = (t + 1) << LOG_TP;
+        const bool full = lo >= first && hi <= first + n;
+        uint32_t* o = out + (p0 - first) * D;
+#pragma unroll 1
+        for (uint32_t v = 0; v < 4; ++v) {
+            const uint32_t cv = ((v & 1u) << 1) | (v >> 1);
+#pragma unroll
+            for (uint32_t w = 0; w < 8; ++w) {
+                const uint32_t u = 8 * v + w;
+                const uint32_t cw = (((w & 1u) << 2) | (w & 2u) | (w >> 2)) << 2;
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    // brev of the in-lane offset q (LOG_Q bits) at the top
+                    const uint32_t cq = (D == 1 ? (((q & 1) << 2) | (q & 2) | (q >> 2))
+                                                : (((q & 1) << 1) | (q >> 1)))
+                                        << (32 - LOG_Q);
+#pragma unroll
+                    for (int d = 0; d < D; ++d) {
+                        const uint32_t xx = x0[d] + (cw | cv) * G[d] + cq * gv[d];
+                        y[q * D + d] = U32OUT ? xx : map_bits(xx);
+                    }
+                }
+                if (full) {
+                    store_vec<8>(o + u * 256, y);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < Q; ++q)
+                        if ((p0 + u * PPS + q) - first < n)
+#pragma unroll
+                            for (int d = 0; d < D; ++d)
+                                o[u * 256 + q * D + d] = y[q * D + d];
+                }
+            }
+        }
+    }
+}
+
 // x_j(i) = brev((uint32_t)i) * g_j + s_j (mod 2^32). Inside a tile the index
 // is P | (u << LOG_PPS) | r with disjoint bits, so brev(i) = brev(P | r) +
 // brev5(u) << (27 - LOG_PPS): one IMAD per sample with a compile-time
@@ -722,6 +902,18 @@ cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const
         return by_log_pps<4>(dims, [&](auto lp) {
             return sobol_fast_dispatch<4, decltype(lp)::value>(cols, words, mode, u32, r, s);
         });
+    if ((dims == 1 || dims == 2) && (reinterpret_cast<uintptr_t>(r.out) & 31u) == 0) {
+        constexpr int kLogTp1 = 13, kLogTp2 = 12; // 8192 / D points per tile
+        if (dims == 1)
+            return mode == 2 ? (u32 ? launch_tiled(k_sobol_narrow<1, 2, true>, kLogTp1, r, s, cols, words)
+                                    : launch_tiled(k_sobol_narrow<1, 2, false>, kLogTp1, r, s, cols, words))
+                             : (u32 ? launch_tiled(k_sobol_narrow<1, 0, true>, kLogTp1, r, s, cols, words)
+                                    : launch_tiled(k_sobol_narrow<1, 0, false>, kLogTp1, r, s, cols, words));
+        return mode == 2 ? (u32 ? launch_tiled(k_sobol_narrow<2, 2, true>, kLogTp2, r, s, cols, words)
+                                : launch_tiled(k_sobol_narrow<2, 2, false>, kLogTp2, r, s, cols, words))
+                         : (u32 ? launch_tiled(k_sobol_narrow<2, 0, true>, kLogTp2, r, s, cols, words)
+                                : launch_tiled(k_sobol_narrow<2, 0, false>, kLogTp2, r, s, cols, words));
+    }
     // shared-memory tiled path: tp = 2^k points with tp*(dims+1) <= 8192 words
     uint32_t tp = 32;
     while (tp * 2 * (dims + 1) <= 8192u)
@@ -764,6 +956,13 @@ cudaError_t launch_lattice(const SmallArgs& args, uint32_t dims, bool u32, const
         return by_log_pps<4>(dims, [&](auto lp) {
             return lattice_fast_dispatch<4, decltype(lp)::value>(args, u32, r, s);
         });
+    if ((dims == 1 || dims == 2) && (reinterpret_cast<uintptr_t>(r.out) & 31u) == 0) {
+        if (dims == 1)
+            return u32 ? launch_tiled(k_lattice_narrow<1, true>, 13, r, s, nullptr, args)
+                       : launch_tiled(k_lattice_narrow<1, false>, 13, r, s, nullptr, args);
+        return u32 ? launch_tiled(k_lattice_narrow<2, true>, 12, r, s, nullptr, args)
+                   : launch_tiled(k_lattice_narrow<2, false>, 12, r, s, nullptr, args);
+    }
     const Div32 d = dims >= 2 ? make_div32(dims) : Div32{0, 0};
     return launch_chunked(dims, r, [&](unsigned grid, uint64_t first, uint32_t elems, uint32_t* o) {
         k_lattice_generic<<<grid, kBlock, 0, s>>>(args, dims, d, first, elems, u32, o);
