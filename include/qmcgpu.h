@@ -253,6 +253,22 @@ qmc_status qmc_check_1d_stratification(qmc_sampler_kind kind, const qmc_stream_p
                                        uint32_t j, uint32_t m, int* ok, uint32_t* histogram,
                                        qmc_stream stream);
 
+/* ------------------------------------------- file formats (host + device) */
+/* load_generator_vector (lattice.cpp:21-46): decimal components, '#'
+ * comments. *dims = count; out (capacity words) may be NULL to query. */
+qmc_status qmc_load_generator_vector(const char* text, uint32_t* out, uint32_t capacity,
+                                     uint32_t* dims);
+/* load_linear_factors (radical.cpp:281-306): out[dims] = defaults (b-1)
+ * overridden by the file's "base factor" lines. */
+qmc_status qmc_load_linear_factors(const char* text, uint32_t dims, uint32_t* out);
+/* fnv1a64 (image.cpp:54-63). */
+uint64_t qmc_fnv1a64(const void* data, uint64_t size);
+/* write_pgm (channels 1, P5) / write_ppm (channels 3, P6) (image.cpp:34-52)
+ * of a row-major float image (device or host) into `bytes`; bytes = NULL
+ * queries the size in *len. The quantization runs on the device. */
+qmc_status qmc_write_pnm(const float* image, uint32_t width, uint32_t height, uint32_t channels,
+                         void* bytes, size_t* len, qmc_stream stream);
+
 /* --------------------------------------------------- render (render.cpp:83-143) */
 typedef struct qmc_render_job { /* RenderJob, render.hpp:31-47 */
     uint32_t width, height, spp;

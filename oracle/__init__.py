@@ -137,6 +137,9 @@ def load_ref():
         _sig(lib, "ref_min_toroidal", i32, P, u64, u32, C.POINTER(f64))
         _sig(lib, "ref_stratification", i32, cstr, u32, u32, u32, u32, C.POINTER(i32))
         _sig(lib, "ref_white_noise_xor_file", i32, u32, u32, u32, P, pu64)
+        _sig(lib, "ref_load_generator_vector", i32, cstr, P, u32, pu32)
+        _sig(lib, "ref_load_linear_factors", i32, cstr, u32, P)
+        _sig(lib, "ref_write_pnm", i32, P, u32, u32, i32, P, pu64)
         _sig(lib, "ref_xor_stream_fill", i32, P, u64, u32, u32, u32, u32, u32, u64, u64, P)
         _ref = lib
     return _ref

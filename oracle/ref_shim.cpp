@@ -496,6 +496,43 @@ int ref_xor_stream_fill(const unsigned char* bytes, std::uint64_t len, std::uint
                 out[i * dims + j] = std::bit_cast<std::uint32_t>(s.sample(first + i, j));
     });
 }
+int ref_load_generator_vector(const char* text, std::uint32_t* out, std::uint32_t cap,
+                              std::uint32_t* dims)
+{
+    return guard([&] {
+        std::istringstream in(text);
+        const auto g = qmc::load_generator_vector(in);
+        *dims = g.dims();
+        if (out && cap >= g.dims())
+            std::memcpy(out, g.g.data(), g.g.size() * 4);
+    });
+}
+int ref_load_linear_factors(const char* text, std::uint32_t dims, std::uint32_t* out)
+{
+    return guard([&] {
+        std::istringstream in(text);
+        const auto f = qmc::load_linear_factors(in, dims);
+        std::memcpy(out, f.data(), f.size() * 4);
+    });
+}
+// write_pgm (p6 = 0) / write_ppm (p6 = 1) of a float image into `out`.
+int ref_write_pnm(const float* values, std::uint32_t w, std::uint32_t h, int p6,
+                  unsigned char* out, std::uint64_t* len)
+{
+    return guard([&] {
+        qmc::ImageBuffer img = qmc::make_image(w, h);
+        std::memcpy(img.values.data(), values, img.values.size() * 4);
+        std::ostringstream os;
+        if (p6)
+            qmc::write_ppm(img, os);
+        else
+            qmc::write_pgm(img, os);
+        const std::string b = os.str();
+        if (out && *len >= b.size())
+            std::memcpy(out, b.data(), b.size());
+        *len = b.size();
+    });
+}
 double ref_neumaier(const double* v, std::uint64_t n)
 {
     qmc::CompensatedSum s;

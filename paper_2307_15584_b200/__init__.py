@@ -35,7 +35,7 @@ __all__ = [
     "partition_by_extra_dimension", "halton_pixel_enumeration", "sampler_kind_from_name",
     "integrate", "builtin_integrand", "write_probe", "l2_star_discrepancy",
     "min_toroidal_distance", "check_1d_stratification", "XorTables", "render_partial",
-    "render_finalize",
+    "render_finalize", "load_generator_vector", "load_linear_factors", "fnv1a64", "write_pnm",
     "SAMPLER_KINDS",
 ]
 
@@ -124,6 +124,10 @@ def lib():
     sig("qmc_stream_fill", i32, i32, C.POINTER(StreamParams), u64, u64, i32, P, P)
     sig("qmc_render", i32, C.POINTER(RenderJob), u32, u32, P, P)
     sig("qmc_scene_value", i32, P, P, u64, P)
+    sig("qmc_load_generator_vector", i32, C.c_char_p, P, u32, C.POINTER(u32))
+    sig("qmc_load_linear_factors", i32, C.c_char_p, u32, P)
+    sig("qmc_fnv1a64", u64, P, u64)
+    sig("qmc_write_pnm", i32, P, u32, u32, u32, P, C.POINTER(C.c_size_t), P)
     sig("qmc_render_partial", i32, C.POINTER(RenderJob), u32, u32, u32, u32, P, P)
     sig("qmc_render_finalize", i32, P, u64, u32, P, P)
     sig("qmc_l2_star_discrepancy", i32, P, u64, u32, C.POINTER(f64), P)
@@ -626,6 +630,41 @@ def render_finalize(acc, spp: int, out=None, stream=None):
         out = torch.empty(acc.shape, dtype=torch.float32, device=acc.device)
     _check(lib().qmc_render_finalize(_ptr(acc), acc.numel(), spp, _ptr(out), _stream(stream)))
     return out
+
+
+def load_generator_vector(text: str) -> list:
+    """load_generator_vector (lattice.cpp:21-46)."""
+    n = u32()
+    _check(lib().qmc_load_generator_vector(text.encode(), None, 0, C.byref(n)))
+    out = np.zeros(n.value, np.uint32)
+    _check(lib().qmc_load_generator_vector(text.encode(), out.ctypes.data, n.value, C.byref(n)))
+    return out.tolist()
+
+
+def load_linear_factors(text: str, dims: int) -> list:
+    """load_linear_factors (radical.cpp:281-306)."""
+    out = np.zeros(max(dims, 1), np.uint32)
+    _check(lib().qmc_load_linear_factors(text.encode(), dims, out.ctypes.data))
+    return out[:dims].tolist()
+
+
+def fnv1a64(data) -> int:
+    """fnv1a64 (image.cpp:54-63) of bytes or an array's bytes."""
+    buf = np.ascontiguousarray(np.frombuffer(data, np.uint8) if isinstance(data, (bytes, bytearray))
+                               else data)
+    return lib().qmc_fnv1a64(buf.ctypes.data, buf.nbytes)
+
+
+def write_pnm(image, channels: int = 1, stream=None) -> bytes:
+    """write_pgm (channels=1) / write_ppm (channels=3) of an [h, w] float image."""
+    if isinstance(image, np.ndarray):
+        image = np.ascontiguousarray(image, dtype=np.float32)
+    h, w = image.shape
+    n = C.c_size_t(0)
+    _check(lib().qmc_write_pnm(_ptr(image), w, h, channels, None, C.byref(n), _stream(stream)))
+    buf = C.create_string_buffer(n.value)
+    _check(lib().qmc_write_pnm(_ptr(image), w, h, channels, buf, C.byref(n), _stream(stream)))
+    return buf.raw[: n.value]
 
 
 def scene_value(xy, out=None, stream=None):

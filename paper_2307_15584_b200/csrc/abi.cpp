@@ -1689,6 +1689,140 @@ qmc_status qmc_check_1d_stratification(qmc_sampler_kind kind, const qmc_stream_p
     });
 }
 
+// ------------------------------------------------------------------ formats
+
+// load_generator_vector (lattice.cpp:21-46): one decimal component per line,
+// '#' comments; ConfigError for components beyond 32 bits, even components,
+// or an empty file.
+qmc_status qmc_load_generator_vector(const char* text, uint32_t* out, uint32_t capacity,
+                                     uint32_t* dims)
+{
+    return guard([&] {
+        if (!text || !dims)
+            fail(QMC_INVALID_ARGUMENT, "load_generator_vector: null argument");
+        std::istringstream in(text);
+        std::string line;
+        size_t no = 0;
+        std::vector<uint32_t> g;
+        while (std::getline(in, line)) {
+            ++no;
+            const auto hash = line.find('#');
+            if (hash != std::string::npos)
+                line.erase(hash);
+            std::istringstream ls(line);
+            uint64_t v = 0;
+            if (!(ls >> v))
+                continue;
+            if (v > 0xffffffffull)
+                fail(QMC_CONFIG, "generator vector, line " + std::to_string(no) +
+                                     ": component beyond 32 bits");
+            if (v % 2 == 0)
+                fail(QMC_CONFIG,
+                     "generator vector, line " + std::to_string(no) + ": component is even");
+            g.push_back(static_cast<uint32_t>(v));
+        }
+        if (g.empty())
+            fail(QMC_CONFIG, "generator vector file holds no components");
+        *dims = static_cast<uint32_t>(g.size());
+        if (out) {
+            if (capacity < g.size())
+                fail(QMC_INVALID_ARGUMENT, "load_generator_vector: output capacity too small");
+            std::memcpy(out, g.data(), g.size() * 4);
+        }
+    });
+}
+
+// load_linear_factors (radical.cpp:281-306): "base factor" lines override the
+// default factor (base - 1) of the matching prime among the first dims.
+qmc_status qmc_load_linear_factors(const char* text, uint32_t dims, uint32_t* out)
+{
+    return guard([&] {
+        if (!text || !out)
+            fail(QMC_INVALID_ARGUMENT, "load_linear_factors: null argument");
+        if (dims > kPrimes)
+            fail(QMC_INVALID_ARGUMENT, "default_linear_factors: dims beyond the prime table");
+        std::vector<uint32_t> f(dims);
+        for (uint32_t j = 0; j < dims; ++j)
+            f[j] = primes().p[j] - 1;
+        std::istringstream in(text);
+        std::string line;
+        size_t no = 0;
+        while (std::getline(in, line)) {
+            ++no;
+            const auto hash = line.find('#');
+            if (hash != std::string::npos)
+                line.erase(hash);
+            std::istringstream ls(line);
+            uint64_t base = 0, factor = 0;
+            if (!(ls >> base))
+                continue;
+            if (!(ls >> factor))
+                fail(QMC_CONFIG, "scramble factor file, line " + std::to_string(no) +
+                                     ": expected 'base factor'");
+            if (base < 2 || factor == 0 || factor >= base)
+                fail(QMC_CONFIG, "scramble factor file, line " + std::to_string(no) +
+                                     ": factor must be in [1, base)");
+            for (uint32_t j = 0; j < dims; ++j)
+                if (primes().p[j] == base)
+                    f[j] = static_cast<uint32_t>(factor);
+        }
+        std::memcpy(out, f.data(), f.size() * 4);
+    });
+}
+
+// fnv1a64 (image.cpp:54-63) — checksum of serialized output.
+uint64_t qmc_fnv1a64(const void* data, uint64_t size)
+{
+    const unsigned char* p = static_cast<const unsigned char*>(data);
+    uint64_t h = 0xcbf29ce484222325ull;
+    for (uint64_t k = 0; k < size; ++k) {
+        h ^= p[k];
+        h *= 0x100000001b3ull;
+    }
+    return h;
+}
+
+// write_pgm / write_ppm (image.cpp:34-52): header on the host, the per-pixel
+// quantization (image.cpp:25-30) on the device.
+qmc_status qmc_write_pnm(const float* image, uint32_t width, uint32_t height, uint32_t channels,
+                         void* bytes, size_t* len, qmc_stream stream)
+{
+    return guard([&] {
+        if (!len)
+            fail(QMC_INVALID_ARGUMENT, "write_pnm: null length");
+        if (channels != 1 && channels != 3)
+            fail(QMC_INVALID_ARGUMENT, "write_pnm: channels must be 1 (P5) or 3 (P6)");
+        if (width == 0 || height == 0)
+            fail(QMC_INVALID_ARGUMENT, "make_image: image must be at least 1x1");
+        const std::string header = std::string(channels == 1 ? "P5\n" : "P6\n") +
+                                   std::to_string(width) + " " + std::to_string(height) +
+                                   "\n255\n";
+        const uint64_t npix = static_cast<uint64_t>(width) * height;
+        const size_t need = header.size() + npix * channels;
+        if (!bytes || *len < need) {
+            *len = need;
+            if (bytes)
+                fail(QMC_INVALID_ARGUMENT, "write_pnm: output buffer too small");
+            return;
+        }
+        if (!image)
+            fail(QMC_INVALID_ARGUMENT, "write_pnm: null image");
+        const cudaStream_t s = as_stream(stream);
+        pool_keep_memory();
+        DevPoints dv(image, npix, s);
+        unsigned char* d = nullptr;
+        cuda_ok(cudaMallocAsync(&d, npix * channels + 1, s), "cudaMallocAsync");
+        cuda_ok(launch_quantize(dv.ptr, npix, channels, d, s), "launch_quantize");
+        unsigned char* o = static_cast<unsigned char*>(bytes);
+        std::memcpy(o, header.data(), header.size());
+        cuda_ok(cudaMemcpyAsync(o + header.size(), d, npix * channels, cudaMemcpyDeviceToHost, s),
+                "D2H");
+        cudaFreeAsync(d, s);
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        *len = need;
+    });
+}
+
 // ------------------------------------------------------------------ render
 
 namespace {

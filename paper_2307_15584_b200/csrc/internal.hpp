@@ -125,6 +125,10 @@ cudaError_t launch_render_partial(const RenderParams& p, uint32_t kind, uint32_t
 cudaError_t launch_render_finalize(const long long* acc, uint64_t npix, uint32_t spp, float* out,
                                    cudaStream_t s);
 
+// image.cpp:25-30 quantization to bytes, `channels` copies per pixel.
+cudaError_t launch_quantize(const float* v, uint64_t npix, uint32_t channels, unsigned char* out,
+                            cudaStream_t s);
+
 cudaError_t launch_scene_value(const double* xy, double* out, uint64_t n, cudaStream_t s);
 
 // Write-only 128-bit streaming store probe over `bytes` (diagnostic).

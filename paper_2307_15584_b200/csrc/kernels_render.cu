@@ -318,6 +318,24 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// image.cpp:25-30: clamp to [0,1], round half up in fp32 (mul then add, no
+// FMA, as the x86 reference), min 255; `channels` copies per pixel (P5: 1,
+// P6: 3).
+__global__ void k_quantize(const float* __restrict__ v, uint64_t npix, uint32_t channels,
+                           unsigned char* __restrict__ out)
+{
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < npix;
+         k += stride) {
+        float c = v[k];
+        c = c < 0.0f ? 0.0f : (1.0f < c ? 1.0f : c);
+        const int q = __float2int_rz(__fadd_rn(__fmul_rn(c, 255.0f), 0.5f));
+        const unsigned char b = static_cast<unsigned char>(q < 255 ? q : 255);
+        for (uint32_t ch = 0; ch < channels; ++ch)
+            out[k * channels + ch] = b;
+    }
+}
+
 __global__ void k_scene_value(const double* __restrict__ xy, double* __restrict__ out, uint64_t n)
 {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -444,6 +462,17 @@ cudaError_t launch_pixel_stream(const PixelStreamParams& p, bool u32, const Fill
     case 7: return pixel_stream_kind<7>(p, u32, r, s);
     }
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_quantize(const float* v, uint64_t npix, uint32_t channels, unsigned char* out,
+                            cudaStream_t s)
+{
+    if (npix == 0)
+        return cudaSuccess;
+    const uint64_t want = (npix + 255) / 256, cap = static_cast<uint64_t>(sm_count()) * 8;
+    k_quantize<<<static_cast<unsigned>(want < cap ? want : cap), 256, 0, s>>>(v, npix, channels,
+                                                                              out);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_scene_value(const double* xy, double* out, uint64_t n, cudaStream_t s)

@@ -113,3 +113,40 @@ def test_div32_magic_host_emulation():
         t = (n * np.uint64(m)) >> np.uint64(32)
         qq = (t + ((n - t) >> np.uint64(1))) >> np.uint64(s)
         np.testing.assert_array_equal(qq, n // np.uint64(d))
+
+
+GV_CASES = ["1\n3\n5\n", "# header\n1 # first\n\n1276675999\n", "7", "1\n4\n", "1\n4294967297\n",
+            "# only comments\n\n", "1\n  3  \n"]
+FACTOR_CASES = ["3 2\n5 3\n", "# c\n7 6\n\n", "2 1\n", "3\n", "3 0\n", "3 3\n", "1 0\n",
+                "997 5\n"]
+
+
+@pytest.mark.parametrize("text", GV_CASES)
+def test_load_generator_vector_matches_reference(ref, text):
+    import ctypes as C
+    n = C.c_uint32()
+    out = np.zeros(16, np.uint32)
+    rc = ref.ref_load_generator_vector(text.encode(), ptr(out), 16, C.byref(n))
+    if rc != 0:
+        with pytest.raises(q.ConfigError) as ei:
+            q.load_generator_vector(text)
+        assert str(ei.value) == ref.ref_last_error().decode()
+    else:
+        assert q.load_generator_vector(text) == out[: n.value].tolist()
+
+
+@pytest.mark.parametrize("text", FACTOR_CASES)
+def test_load_linear_factors_matches_reference(ref, text):
+    out = np.zeros(200, np.uint32)
+    rc = ref.ref_load_linear_factors(text.encode(), 200, ptr(out))
+    if rc != 0:
+        with pytest.raises(q.ConfigError) as ei:
+            q.load_linear_factors(text, 200)
+        assert str(ei.value) == ref.ref_last_error().decode()
+    else:
+        assert q.load_linear_factors(text, 200) == out.tolist()
+
+
+def test_fnv1a64(golden):
+    assert q.fnv1a64(b"") == 0xCBF29CE484222325
+    assert q.fnv1a64(b"a") == 0xAF63DC4C8601EC8C

@@ -703,3 +703,18 @@ def test_render_small_image_high_spp_warp_path(ref, kind):
         else:
             rel = np.abs(got.astype(np.float64) - exp) / np.maximum(np.abs(exp), 1e-30)
             assert rel.max() <= 1e-6, rel.max()
+
+
+def test_write_pnm_matches_reference(ref):
+    """write_pgm / write_ppm (image.cpp:25-52) of a render: byte-identical."""
+    import ctypes as C
+    img = q.render(57, 31, 8, kind="image-plane-halton")
+    host = img.cpu().numpy()
+    host[0, :4] = [-0.5, 1.5, 0.5, 0.998]  # clamp and rounding edges
+    for ch, p6 in ((1, 0), (3, 1)):
+        n = C.c_uint64(0)
+        assert ref.ref_write_pnm(ptr(host), 57, 31, p6, None, C.byref(n)) == 0
+        buf = np.zeros(n.value, np.uint8)
+        assert ref.ref_write_pnm(ptr(host), 57, 31, p6, ptr(buf), C.byref(n)) == 0
+        assert q.write_pnm(host, ch) == buf.tobytes()
+        assert q.write_pnm(torch.from_numpy(host).cuda(), ch) == buf.tobytes()
