@@ -261,6 +261,11 @@ qmc_status qmc_load_generator_vector(const char* text, uint32_t* out, uint32_t c
 /* load_linear_factors (radical.cpp:281-306): out[dims] = defaults (b-1)
  * overridden by the file's "base factor" lines. */
 qmc_status qmc_load_linear_factors(const char* text, uint32_t dims, uint32_t* out);
+/* `qmckit points --format csv` text (qmckit.cpp:225-235): "%.9f" values,
+ * comma-separated rows; points device or host; bytes = NULL queries *len.
+ * (--format bin is the fills' row-major little-endian fp32 output itself.) */
+qmc_status qmc_write_points_csv(const float* points, uint64_t n, uint32_t dims, void* bytes,
+                                size_t* len, qmc_stream stream);
 /* fnv1a64 (image.cpp:54-63). */
 uint64_t qmc_fnv1a64(const void* data, uint64_t size);
 /* write_pgm (channels 1, P5) / write_ppm (channels 3, P6) (image.cpp:34-52)

@@ -36,6 +36,7 @@ __all__ = [
     "integrate", "builtin_integrand", "write_probe", "l2_star_discrepancy",
     "min_toroidal_distance", "check_1d_stratification", "XorTables", "render_partial",
     "render_finalize", "load_generator_vector", "load_linear_factors", "fnv1a64", "write_pnm",
+    "write_points_csv",
     "SAMPLER_KINDS",
 ]
 
@@ -127,6 +128,7 @@ def lib():
     sig("qmc_load_generator_vector", i32, C.c_char_p, P, u32, C.POINTER(u32))
     sig("qmc_load_linear_factors", i32, C.c_char_p, u32, P)
     sig("qmc_fnv1a64", u64, P, u64)
+    sig("qmc_write_points_csv", i32, P, u64, u32, P, C.POINTER(C.c_size_t), P)
     sig("qmc_write_pnm", i32, P, u32, u32, u32, P, C.POINTER(C.c_size_t), P)
     sig("qmc_render_partial", i32, C.POINTER(RenderJob), u32, u32, u32, u32, P, P)
     sig("qmc_render_finalize", i32, P, u64, u32, P, P)
@@ -653,6 +655,18 @@ def fnv1a64(data) -> int:
     buf = np.ascontiguousarray(np.frombuffer(data, np.uint8) if isinstance(data, (bytes, bytearray))
                                else data)
     return lib().qmc_fnv1a64(buf.ctypes.data, buf.nbytes)
+
+
+def write_points_csv(points, stream=None) -> bytes:
+    """`qmckit points --format csv` text of an [n, dims] float array."""
+    if isinstance(points, np.ndarray):
+        points = np.ascontiguousarray(points, dtype=np.float32)
+    n, dims = points.shape
+    ln = C.c_size_t(0)
+    _check(lib().qmc_write_points_csv(_ptr(points), n, dims, None, C.byref(ln), _stream(stream)))
+    buf = C.create_string_buffer(max(ln.value, 1))
+    _check(lib().qmc_write_points_csv(_ptr(points), n, dims, buf, C.byref(ln), _stream(stream)))
+    return buf.raw[: ln.value]
 
 
 def write_pnm(image, channels: int = 1, stream=None) -> bytes:

@@ -1782,6 +1782,47 @@ uint64_t qmc_fnv1a64(const void* data, uint64_t size)
     return h;
 }
 
+// `qmckit points --format csv` rows (qmckit.cpp:225-235): "%.9f" per
+// component, comma-separated, one line per point. Host formatting of a
+// device or host float array; bytes = NULL queries the size.
+qmc_status qmc_write_points_csv(const float* points, uint64_t n, uint32_t dims, void* bytes,
+                                size_t* len, qmc_stream stream)
+{
+    return guard([&] {
+        if (!len || (!points && n))
+            fail(QMC_INVALID_ARGUMENT, "write_points_csv: null argument");
+        std::vector<float> host;
+        const float* p = points;
+        if (n && is_device_pointer(points)) {
+            host.resize(n * dims);
+            const cudaStream_t s = as_stream(stream);
+            cuda_ok(cudaMemcpyAsync(host.data(), points, host.size() * 4, cudaMemcpyDeviceToHost,
+                                    s),
+                    "D2H");
+            cuda_ok(cudaStreamSynchronize(s), "sync");
+            p = host.data();
+        }
+        std::string text;
+        text.reserve(n * dims * 12);
+        char buf[32];
+        for (uint64_t i = 0; i < n; ++i) {
+            for (uint32_t j = 0; j < dims; ++j) {
+                std::snprintf(buf, sizeof buf, "%.9f", static_cast<double>(p[i * dims + j]));
+                if (j)
+                    text += ',';
+                text += buf;
+            }
+            text += '\n';
+        }
+        if (bytes) {
+            if (*len < text.size())
+                fail(QMC_INVALID_ARGUMENT, "write_points_csv: output buffer too small");
+            std::memcpy(bytes, text.data(), text.size());
+        }
+        *len = text.size();
+    });
+}
+
 // write_pgm / write_ppm (image.cpp:34-52): header on the host, the per-pixel
 // quantization (image.cpp:25-30) on the device.
 qmc_status qmc_write_pnm(const float* image, uint32_t width, uint32_t height, uint32_t channels,

@@ -150,3 +150,16 @@ def test_load_linear_factors_matches_reference(ref, text):
 def test_fnv1a64(golden):
     assert q.fnv1a64(b"") == 0xCBF29CE484222325
     assert q.fnv1a64(b"a") == 0xAF63DC4C8601EC8C
+
+
+def test_points_csv_format_host():
+    """sobol N=4 dims=2 CSV -> 4 lines, first "0.000000000,0.000000000"."""
+    pts = np.array([[0.0, 0.0], [0.5, 0.5], [0.75, 0.25], [0.25, 0.75]], np.float32)
+    text = q.write_points_csv(pts).decode()
+    lines = text.splitlines()
+    assert len(lines) == 4 and lines[0] == "0.000000000,0.000000000"
+    assert lines[2] == "0.750000000,0.250000000"
+    rng = np.random.default_rng(0)
+    x = rng.random((50, 3)).astype(np.float32)
+    assert q.write_points_csv(x).decode() == "".join(
+        ",".join("%.9f" % v for v in row) + "\n" for row in x.astype(np.float64))
