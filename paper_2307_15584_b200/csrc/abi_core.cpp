@@ -1,681 +1,26 @@
-// abi.cpp — the extern "C" boundary (include/qmcgpu.h) of libqmcgpu.
+// abi_core.cpp — the extern "C" boundary (include/qmcgpu.h) of libqmcgpu:
+// status strings, L0 map, host setup, generator matrices, the fills, the
+// SampleStream façade, integration, XOR tables, quality metrics and formats.
+// (The fused render lives in abi_render.cpp.)
 //
 // Host responsibilities only: validate arguments with the reference's
-// conditions (so callers see the same error classes), build the immutable
-// tables the reference builds on the host (primes, direction-number
-// matrices, Faure permutations, generator vectors, XOR tables), upload
-// per-call parameters, place the output (device pointer: one asynchronous
-// launch; host pointer: chunked device fill + D2H pipeline), and launch the
-// kernels. No per-sample arithmetic happens here.
-#include "qmcgpu.h"
+// conditions (so callers see the same error classes), upload per-call
+// parameters, place the output (device pointer: one asynchronous launch;
+// host pointer: chunked device fill + D2H pipeline), and launch the kernels.
+// No per-sample arithmetic happens here.
+#include "objects.hpp"
 
-#include <algorithm>
-#include <array>
-#include <map>
-#include <tuple>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
-#include <cstring>
-#include <memory>
-#include <mutex>
 #include <random>
 #include <sstream>
-#include <string>
-#include <vector>
-
-#include <cuda_runtime.h>
-
-#include "device.cuh" // RadicalDim layout (host-visible struct)
-#include "internal.hpp"
 
 using namespace qmcgpu;
+using namespace qmcgpu::host;
 
-namespace {
-
-// ------------------------------------------------------------- errors
-
-thread_local std::string g_error;
-
-struct Fail {
-    qmc_status status;
-    std::string msg;
-};
-
-[[noreturn]] void fail(qmc_status s, std::string msg) { throw Fail{s, std::move(msg)}; }
-
-void cuda_ok(cudaError_t e, const char* what)
-{
-    if (e != cudaSuccess)
-        fail(QMC_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-template <typename F>
-qmc_status guard(F&& f)
-{
-    try {
-        f();
-        return QMC_OK;
-    } catch (const Fail& e) {
-        g_error = e.msg;
-        return e.status;
-    } catch (const std::bad_alloc&) {
-        g_error = "out of host memory";
-        return QMC_INTERNAL;
-    } catch (const std::exception& e) {
-        g_error = e.what();
-        return QMC_INTERNAL;
-    }
-}
-
-// ---------------------------------------------------------- prime table
-
-constexpr uint32_t kPrimes = 1000;
-
-struct PrimeTable {
-    std::array<uint32_t, kPrimes> p{}, maxpow{};
-    PrimeTable()
-    {
-        uint32_t found = 0;
-        for (uint32_t c = 2; found < kPrimes; ++c) {
-            bool prime = true;
-            for (uint32_t k = 0; k < found && p[k] * p[k] <= c; ++k)
-                if (c % p[k] == 0) {
-                    prime = false;
-                    break;
-                }
-            if (prime)
-                p[found++] = c;
-        }
-        for (uint32_t k = 0; k < kPrimes; ++k) {
-            uint64_t x = p[k];
-            while (x * p[k] <= 0xffffffffull)
-                x *= p[k];
-            maxpow[k] = static_cast<uint32_t>(x);
-        }
-    }
-};
-
-const PrimeTable& primes()
-{
-    static const PrimeTable t;
-    return t;
-}
-
-uint32_t prime_at(uint32_t index)
-{
-    if (index >= kPrimes)
-        fail(QMC_OUT_OF_RANGE, "prime: index beyond the bundled prime table");
-    return primes().p[index];
-}
-
-// radical.cpp:50-74
-std::vector<uint32_t> faure(uint32_t b)
-{
-    if (b < 2)
-        fail(QMC_INVALID_ARGUMENT, "faure_permutation: base must be >= 2");
-    if (b == 2)
-        return {0u, 1u};
-    std::vector<uint32_t> s;
-    s.reserve(b);
-    if (b % 2 == 0) {
-        const auto h = faure(b / 2);
-        for (uint32_t v : h)
-            s.push_back(2 * v);
-        for (uint32_t v : h)
-            s.push_back(2 * v + 1);
-    } else {
-        const auto prev = faure(b - 1);
-        const uint32_t mid = (b - 1) / 2;
-        for (uint32_t k = 0; k < prev.size(); ++k) {
-            if (k == mid)
-                s.push_back(mid);
-            s.push_back(prev[k] >= mid ? prev[k] + 1 : prev[k]);
-        }
-    }
-    return s;
-}
-
-// ------------------------------------------------- direction numbers
-
-struct DirRow {
-    uint32_t s, a;
-    std::vector<uint32_t> m;
-};
-
-struct BuiltinRow {
-    uint32_t s, a;
-    uint32_t m[32];
-};
-const BuiltinRow kJoeKuo[] = {
-#include "joe_kuo_64.inc"
-};
-
-std::vector<DirRow> builtin_rows()
-{
-    std::vector<DirRow> rows;
-    for (const BuiltinRow& r : kJoeKuo)
-        rows.push_back(DirRow{r.s, r.a, std::vector<uint32_t>(r.m, r.m + r.s)});
-    return rows;
-}
-
-// digitalnet.cpp:23-65 — same grammar, checks and ConfigError messages.
-std::vector<DirRow> parse_rows(const std::string& text)
-{
-    std::vector<DirRow> rows;
-    std::istringstream in(text);
-    std::string line;
-    size_t no = 0;
-    bool header = false;
-    auto bad = [&](const std::string& w) {
-        fail(QMC_CONFIG, "direction numbers, line " + std::to_string(no) + ": " + w);
-    };
-    while (std::getline(in, line)) {
-        ++no;
-        if (!header) {
-            header = true;
-            continue;
-        }
-        std::istringstream ls(line);
-        uint32_t d = 0, s = 0, a = 0;
-        if (!(ls >> d))
-            continue;
-        if (!(ls >> s >> a))
-            bad("expected 'd s a m_1 ... m_s'");
-        if (d != rows.size() + 2)
-            bad("dimensions must be consecutive starting at 2");
-        if (s == 0 || s > 32)
-            bad("degree s out of range");
-        if (s > 1 && a >= (1u << (s - 1)))
-            bad("coefficient a has more than s-1 bits");
-        DirRow row{s, a, {}};
-        for (uint32_t k = 1; k <= s; ++k) {
-            uint64_t mk = 0;
-            if (!(ls >> mk))
-                bad("expected " + std::to_string(s) + " direction numbers");
-            if (mk % 2 == 0)
-                bad("direction number m_" + std::to_string(k) + " is even");
-            if (mk >= (1ull << k))
-                bad("direction number m_" + std::to_string(k) + " must be < 2^" +
-                    std::to_string(k));
-            row.m.push_back(static_cast<uint32_t>(mk));
-        }
-        std::string rest;
-        if (ls >> rest)
-            bad("trailing tokens after the m values");
-        rows.push_back(std::move(row));
-    }
-    return rows;
-}
-
-// digitalnet.cpp:79-109 — MSB-aligned columns, 52 per dimension.
-std::vector<uint32_t> build_columns(const std::vector<DirRow>& rows, uint32_t dims)
-{
-    if (dims > rows.size() + 1)
-        fail(QMC_CONFIG, "build_matrices: requested " + std::to_string(dims) +
-                             " dimensions, direction numbers provide " +
-                             std::to_string(rows.size() + 1));
-    std::vector<uint32_t> c(static_cast<size_t>(dims) * 52, 0u);
-    if (dims == 0)
-        return c;
-    for (uint32_t k = 0; k < 32; ++k)
-        c[k] = 0x80000000u >> k;
-    for (uint32_t j = 1; j < dims; ++j) {
-        const DirRow& r = rows[j - 1];
-        uint32_t* v = c.data() + static_cast<size_t>(j) * 52;
-        for (uint32_t k = 0; k < r.s && k < 52; ++k)
-            v[k] = r.m[k] << (31 - k);
-        for (uint32_t k = r.s; k < 52; ++k) {
-            uint32_t x = v[k - r.s] ^ (v[k - r.s] >> r.s);
-            for (uint32_t l = 1; l < r.s; ++l)
-                if ((r.a >> (r.s - 1 - l)) & 1u)
-                    x ^= v[k - l];
-            v[k] = x;
-        }
-    }
-    return c;
-}
-
-uint32_t brev_host(uint32_t v)
-{
-    uint32_t r = 0;
-    for (int k = 0; k < 32; ++k)
-        r |= ((v >> k) & 1u) << (31 - k);
-    return r;
-}
-
-// lattice.cpp:59-77
-uint32_t fmix_host(uint32_t h)
-{
-    h = (h ^ (h >> 16)) * 0x85ebca6bu;
-    h = (h ^ (h >> 13)) * 0xc2b2ae35u;
-    return h ^ (h >> 16);
-}
-uint32_t pixel_hash_host(uint32_t j, uint32_t px, uint32_t py)
-{
-    return fmix_host(fmix_host(fmix_host(0x9e3779b9u ^ j) ^ px) ^ py);
-}
-
-std::vector<uint32_t> lfsr(uint32_t seed, uint32_t dims)
-{
-    if (seed == 0)
-        fail(QMC_INVALID_ARGUMENT, "lfsr_generator_vector: zero seed is the absorbing state");
-    if (dims < 1)
-        fail(QMC_INVALID_ARGUMENT, "lfsr_generator_vector: dims must be >= 1");
-    std::vector<uint32_t> g{1u};
-    uint32_t x = seed;
-    for (uint32_t j = 1; j < dims; ++j) {
-        x ^= x << 13;
-        x ^= x >> 17;
-        x ^= x << 5;
-        g.push_back(2u * x + 1u);
-    }
-    return g;
-}
-
-uint32_t hilbert_order(uint32_t w, uint32_t h)
-{
-    uint32_t o = 1;
-    while (o < 32 && ((1ull << o) < w || (1ull << o) < h))
-        ++o;
-    return o;
-}
-
-// ------------------------------------------ Halton pixel enumeration
-
-uint64_t inverse_mod(uint64_t a, uint64_t n)
-{
-    if (n == 1)
-        return 0;
-    int64_t r0 = static_cast<int64_t>(n), r1 = static_cast<int64_t>(a % n), t0 = 0, t1 = 1;
-    while (r1) {
-        const int64_t q = r0 / r1;
-        const int64_t r2 = r0 - q * r1, t2 = t0 - q * t1;
-        r0 = r1;
-        r1 = r2;
-        t0 = t1;
-        t1 = t2;
-    }
-    const int64_t m = static_cast<int64_t>(n);
-    return static_cast<uint64_t>(((t0 % m) + m) % m);
-}
-
-struct HaltonEnum {
-    uint32_t sx = 1, sy = 1, ex = 0, ey = 0;
-    uint64_t stride = 1, crt_x = 0, crt_y = 0;
-};
-
-// imageplane.cpp:80-98
-HaltonEnum halton_enum(uint32_t w, uint32_t h)
-{
-    if (w == 0 || h == 0)
-        fail(QMC_CONFIG, "HaltonPixelEnumeration: image must be at least 1x1");
-    if (w > (1u << 20) || h > 1594323u)
-        fail(QMC_CONFIG, "HaltonPixelEnumeration: image too large for the index range");
-    HaltonEnum e;
-    while (e.sx < w) {
-        e.sx *= 2;
-        ++e.ex;
-    }
-    while (e.sy < h) {
-        e.sy *= 3;
-        ++e.ey;
-    }
-    e.stride = static_cast<uint64_t>(e.sx) * e.sy;
-    e.crt_x = e.sy * inverse_mod(e.sy % e.sx, e.sx);
-    e.crt_y = e.sx * inverse_mod(e.sx % e.sy, e.sy);
-    return e;
-}
-
-uint64_t digit_reverse_host(uint64_t v, uint32_t base, uint32_t digits)
-{
-    uint64_t r = 0;
-    for (uint32_t k = 0; k < digits; ++k) {
-        r = r * base + v % base;
-        v /= base;
-    }
-    return r;
-}
-
-// ------------------------------------------------------ device buffers
-
-struct DevFree {
-    void operator()(void* p) const { cudaFree(p); }
-};
-using DevPtr = std::unique_ptr<void, DevFree>;
-
-DevPtr dev_upload(const void* host, size_t bytes)
-{
-    void* d = nullptr;
-    cuda_ok(cudaMalloc(&d, bytes ? bytes : 16), "cudaMalloc");
-    DevPtr p(d);
-    if (bytes)
-        cuda_ok(cudaMemcpy(d, host, bytes, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
-    return p;
-}
-
-// Small per-call parameter arrays, uploaded with one stream-ordered copy
-// and released stream-ordered after the launches.
-void pool_keep_memory();
-
-class CallArgs {
-public:
-    explicit CallArgs(cudaStream_t s) : s_(s) {}
-    ~CallArgs()
-    {
-        if (dev_)
-            cudaFreeAsync(dev_, s_);
-    }
-    // returns the byte offset of the array inside the blob (16-B aligned)
-    size_t add(const void* p, size_t bytes)
-    {
-        const size_t off = (blob_.size() + 15) & ~size_t(15);
-        blob_.resize(off + bytes);
-        if (bytes)
-            std::memcpy(blob_.data() + off, p, bytes);
-        return off;
-    }
-    void upload()
-    {
-        if (blob_.empty())
-            return;
-        pool_keep_memory();
-        cuda_ok(cudaMallocAsync(&dev_, blob_.size(), s_), "cudaMallocAsync");
-        cuda_ok(cudaMemcpyAsync(dev_, blob_.data(), blob_.size(), cudaMemcpyHostToDevice, s_),
-                "cudaMemcpyAsync args");
-    }
-    template <typename T>
-    const T* at(size_t off) const
-    {
-        return reinterpret_cast<const T*>(static_cast<const char*>(dev_) + off);
-    }
-
-private:
-    cudaStream_t s_;
-    std::vector<char> blob_;
-    void* dev_ = nullptr;
-};
-
-// Fills SmallArgs array `which` (0 = a, 1 = b) by value when it fits the
-// parameter space, else stages a device copy through `args`; the device
-// address is patched in by finish_small after the upload.
-struct SmallStage {
-    size_t off[2] = {SIZE_MAX, SIZE_MAX};
-};
-
-void set_small(SmallArgs& sa, SmallStage& st, int which, const uint32_t* host, uint32_t n,
-               CallArgs& args)
-{
-    if (n <= kSmall) {
-        std::memcpy(which ? sa.b : sa.a, host, n * 4);
-        (which ? sa.has_b : sa.has_a) = 1;
-        return;
-    }
-    std::vector<uint32_t> pad(std::max<uint32_t>(n, 8) + 8, 0u); // room for 32-B loads
-    std::memcpy(pad.data(), host, n * 4);
-    st.off[which] = args.add(pad.data(), pad.size() * 4);
-}
-
-void finish_small(SmallArgs& sa, const SmallStage& st, const CallArgs& args)
-{
-    if (st.off[0] != SIZE_MAX) {
-        sa.dev_a = args.at<uint32_t>(st.off[0]);
-        sa.has_a = 1;
-    }
-    if (st.off[1] != SIZE_MAX) {
-        sa.dev_b = args.at<uint32_t>(st.off[1]);
-        sa.has_b = 1;
-    }
-}
-
-// Per-device resources for the host-output pipeline.
-struct DeviceCtx {
-    std::mutex mu;
-    cudaStream_t streams[2] = {nullptr, nullptr};
-    void* staging[2] = {nullptr, nullptr};
-    size_t staging_bytes = 0;
-};
-
-DeviceCtx& device_ctx(int dev)
-{
-    static std::mutex mu;
-    static std::vector<std::unique_ptr<DeviceCtx>> ctxs;
-    std::lock_guard<std::mutex> lk(mu);
-    if (ctxs.size() <= static_cast<size_t>(dev))
-        ctxs.resize(dev + 1);
-    if (!ctxs[dev])
-        ctxs[dev] = std::make_unique<DeviceCtx>();
-    return *ctxs[dev];
-}
-
-int current_device()
-{
-    int dev = 0;
-    cuda_ok(cudaGetDevice(&dev), "cudaGetDevice");
-    return dev;
-}
-
-// Keep the stream-ordered pool's memory cached across synchronizations, so
-// the per-call argument blobs (cudaMallocAsync) never remap physical memory
-// in a timed loop (the default release threshold of 0 returns it at every
-// sync, which cost milliseconds per call).
-void pool_keep_memory()
-{
-    static std::mutex mu;
-    static std::vector<char> done;
-    const int dev = current_device();
-    std::lock_guard<std::mutex> lk(mu);
-    if (done.size() <= static_cast<size_t>(dev))
-        done.resize(dev + 1, 0);
-    if (done[dev])
-        return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t keep = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    done[dev] = 1;
-}
-
-bool is_device_pointer(const void* p)
-{
-    cudaPointerAttributes a{};
-    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
-}
-
-constexpr size_t kStagingBytes = size_t(64) << 20;
-
-// Places a fill of n points x dims 32-bit words at `out`. launch(range, s)
-// enqueues the kernels writing device memory.
-template <typename Launch>
-void place_fill(void* out, uint64_t first, uint64_t n, uint32_t dims, cudaStream_t s,
-                Launch&& launch)
-{
-    if (n == 0 || dims == 0)
-        return;
-    if (!out)
-        fail(QMC_INVALID_ARGUMENT, "output pointer is null");
-    if (is_device_pointer(out)) {
-        cuda_ok(launch(FillRange{first, n, out}, s), "kernel launch");
-        return;
-    }
-    // host output: ordered after prior work on the caller's stream
-    cuda_ok(cudaStreamSynchronize(s), "cudaStreamSynchronize");
-    DeviceCtx& ctx = device_ctx(current_device());
-    std::lock_guard<std::mutex> lk(ctx.mu);
-    if (!ctx.streams[0]) {
-        for (auto& st : ctx.streams)
-            cuda_ok(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
-    }
-    if (ctx.staging_bytes < kStagingBytes) {
-        for (auto& b : ctx.staging) {
-            if (b)
-                cudaFree(b);
-            cuda_ok(cudaMalloc(&b, kStagingBytes), "cudaMalloc staging");
-        }
-        ctx.staging_bytes = kStagingBytes;
-    }
-    const uint64_t row = static_cast<uint64_t>(dims) * 4;
-    uint64_t chunk = std::max<uint64_t>(1, kStagingBytes / row);
-    if (chunk > 4096)
-        chunk &= ~uint64_t(4095); // keep chunk starts tile-aligned relative to `first`
-    char* host = static_cast<char*>(out);
-    uint64_t k = 0;
-    for (uint64_t done = 0; done < n; done += chunk, ++k) {
-        const uint64_t cnt = std::min(chunk, n - done);
-        cudaStream_t st = ctx.streams[k & 1];
-        cuda_ok(launch(FillRange{first + done, cnt, ctx.staging[k & 1]}, st), "kernel launch");
-        cuda_ok(cudaMemcpyAsync(host + done * row, ctx.staging[k & 1], cnt * row,
-                                cudaMemcpyDeviceToHost, st),
-                "cudaMemcpyAsync D2H");
-    }
-    for (auto& st : ctx.streams)
-        cuda_ok(cudaStreamSynchronize(st), "cudaStreamSynchronize");
-}
-
-cudaStream_t as_stream(qmc_stream s) { return static_cast<cudaStream_t>(s); }
-
-// Multi-digit tables (tensor_digit_table, radical.cpp:76-110) on the device:
-// d = the most base-b digits with b^d <= 4096 (so a table stays 16 KB and
-// L1-resident), entry v = the d digits of v permuted by sigma and mirrored.
-// Built once per (device, base, scramble) and kept for the process.
-struct DigitTable {
-    const uint32_t* ptr = nullptr;
-    uint32_t group = 0;
-};
-
-constexpr uint32_t kDigitTableMax = 4096;
-
-DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor)
-{
-    static std::mutex mu;
-    static std::map<std::tuple<int, uint32_t, uint32_t, uint32_t>, std::pair<DevPtr, uint32_t>>
-        cache;
-    uint32_t d = 0, group = 1;
-    while (static_cast<uint64_t>(group) * b <= kDigitTableMax) {
-        group *= b;
-        ++d;
-    }
-    if (d < 2)
-        return {};
-    const int dev = current_device();
-    std::lock_guard<std::mutex> lk(mu);
-    auto& slot = cache[{dev, b, mode, factor}];
-    if (!slot.first) {
-        std::vector<uint32_t> sigma(b);
-        if (mode == 2) {
-            sigma = faure(b);
-        } else {
-            for (uint32_t a = 0; a < b; ++a)
-                sigma[a] = mode == 1 ? static_cast<uint32_t>((uint64_t(factor) * a) % b) : a;
-        }
-        std::vector<uint32_t> t(group + 8, 0u);
-        for (uint32_t v = 0; v < group; ++v) {
-            uint32_t rem = v, out = 0;
-            for (uint32_t k = 0; k < d; ++k) {
-                out = out * b + sigma[rem % b];
-                rem /= b;
-            }
-            t[v] = out;
-        }
-        slot.first = dev_upload(t.data(), t.size() * 4);
-        slot.second = group;
-    }
-    return {static_cast<const uint32_t*>(slot.first.get()), slot.second};
-}
-
-// RadicalDim table for `dims` prime bases (radical.cpp:130-181).
-std::vector<RadicalDim> radical_dims(uint32_t dims, uint32_t first_prime, qmc_radical_scramble sc,
-                                     const uint32_t* factors, std::vector<uint32_t>& sigma_pool,
-                                     std::vector<size_t>& sigma_off)
-{
-    std::vector<RadicalDim> rd(dims);
-    sigma_off.assign(dims, SIZE_MAX);
-    for (uint32_t j = 0; j < dims; ++j) {
-        const uint32_t pi = first_prime + j;
-        const uint32_t b = prime_at(pi);
-        RadicalDim& r = rd[j];
-        r.base = b;
-        r.maxpow = primes().maxpow[pi];
-        r.divb = make_div32(b);
-        r.divmp = make_div32(r.maxpow);
-        r.mode = 0;
-        r.factor = 0;
-        r.sigma = nullptr;
-        r.table = nullptr;
-        r.group = 0;
-        r.divg = Div32{0, 0};
-        if (sc == QMC_RADICAL_LINEAR) {
-            const uint32_t f = factors ? factors[j] : b - 1;
-            if (f == 0 || f >= b)
-                fail(QMC_INVALID_ARGUMENT,
-                     "radical_inverse_linscramble: factor must be in [1, base)");
-            r.mode = 1;
-            r.factor = f;
-        } else if (sc == QMC_RADICAL_FAURE) {
-            const auto s = faure(b);
-            sigma_off[j] = sigma_pool.size();
-            sigma_pool.insert(sigma_pool.end(), s.begin(), s.end());
-            r.mode = 2;
-        }
-        if (b > 2) {
-            const DigitTable t = digit_table(b, r.mode, r.factor);
-            if (t.ptr) {
-                r.table = t.ptr;
-                r.group = t.group;
-                r.divg = make_div32(t.group);
-            }
-        }
-    }
-    return rd;
-}
-
-} // namespace
-
-// =====================================================================
-//                               C ABI
-// =====================================================================
-
-struct qmc_matrices {
-    uint32_t dims;
-    std::vector<uint32_t> columns; // [dims][52]
-    std::mutex mu;
-    struct Dev {
-        DevPtr colsT, colsT_rev;
-    };
-    // per (device, dims prefix): the k-major column tables the kernels read
-    std::map<std::pair<int, uint32_t>, std::unique_ptr<Dev>> dev;
-
-    // [52][prefix] (and bit-reversed) columns of the first `prefix`
-    // dimensions on the current device; built once, then cached.
-    const Dev& on_device(uint32_t prefix)
-    {
-        const int d = current_device();
-        std::lock_guard<std::mutex> lk(mu);
-        auto& slot = dev[{d, prefix}];
-        if (!slot) {
-            const uint32_t pd = std::max<uint32_t>(prefix, 8); // room for 32-B loads
-            std::vector<uint32_t> t(52 * static_cast<size_t>(pd), 0u), tr(t.size(), 0u);
-            for (uint32_t j = 0; j < prefix; ++j)
-                for (uint32_t k = 0; k < 52; ++k) {
-                    t[k * static_cast<size_t>(prefix) + j] = columns[j * 52 + k];
-                    tr[k * static_cast<size_t>(prefix) + j] = brev_host(columns[j * 52 + k]);
-                }
-            auto e = std::make_unique<Dev>();
-            e->colsT = dev_upload(t.data(), t.size() * 4);
-            e->colsT_rev = dev_upload(tr.data(), tr.size() * 4);
-            slot = std::move(e);
-        }
-        return *slot;
-    }
-    const Dev& on_device() { return on_device(dims); }
-};
-
-namespace {
+namespace qmcgpu {
+namespace host {
 
 // build_matrices(builtin_direction_numbers(), dims), built once per dims
 // and kept for the process (the reference's builtin_direction_numbers() is
@@ -695,11 +40,120 @@ qmc_matrices* builtin_matrices(uint32_t dims)
     return m.get();
 }
 
-} // namespace
+void sobol_fill_impl(qmc_matrices* m, uint64_t first, uint64_t n, uint32_t dims,
+                     qmc_sobol_scramble sc, const uint32_t* words, qmc_output kind, void* out,
+                     cudaStream_t s)
+{
+    if (!m)
+        fail(QMC_INVALID_ARGUMENT, "matrices handle is null");
+    if (n == 0 || dims == 0)
+        return;
+    if (first >= (1ull << 52) || n > (1ull << 52) - first)
+        fail(QMC_INVALID_ARGUMENT, "sobol_component: index must be below 2^52");
+    if (dims > m->dims)
+        fail(QMC_OUT_OF_RANGE, "sobol_component: dimension beyond the matrix set");
+    if (sc != QMC_SOBOL_NONE && sc != QMC_SOBOL_XOR && sc != QMC_SOBOL_OWEN)
+        fail(QMC_INVALID_ARGUMENT, "sobol_fill: unknown scramble kind");
+    // the kernels read dims-strided columns: tables for this dims prefix
+    const auto& dev = m->on_device(dims);
+    const uint32_t* colsT = static_cast<const uint32_t*>(dev.colsT.get());
+    const uint32_t* colsT_rev = static_cast<const uint32_t*>(dev.colsT_rev.get());
+    CallArgs args(s);
+    SmallArgs small{};
+    SmallStage stage;
+    if (words && sc != QMC_SOBOL_NONE)
+        set_small(small, stage, 0, words, dims, args);
+    args.upload();
+    finish_small(small, stage, args);
+    const int mode = sc == QMC_SOBOL_OWEN ? 2 : 0;
+    const bool u32 = kind == QMC_OUT_U32;
+    place_fill(out, first, n, dims, s, [&](const FillRange& r, cudaStream_t st) {
+        return launch_sobol(colsT, colsT_rev, small, dims, mode, u32, r, st);
+    });
+}
+
+// white_noise_xor_tables (imageplane.cpp:197-229): std::mt19937 words on the
+// host, in the reference's draw order.
+std::unique_ptr<qmc_xor_tables> make_white_noise(uint32_t dims, uint32_t point_count,
+                                                 uint32_t seed)
+{
+    if (dims == 0)
+        fail(QMC_CONFIG, "white_noise_xor_tables: dims must be >= 1");
+    if (point_count == 0 || (point_count & (point_count - 1)) != 0)
+        fail(QMC_CONFIG, "white_noise_xor_tables: point count must be a power of two");
+    auto t = std::make_unique<qmc_xor_tables>();
+    t->dims = dims;
+    t->point_count = point_count;
+    t->white_noise = true;
+    std::mt19937 rng(seed);
+    t->dim_scramble.assign(dims, 0u);
+    if (seed != 0)
+        for (auto& w : t->dim_scramble)
+            w = rng();
+    t->reorder.resize(kXorTile);
+    t->scramble.resize(kXorTile * dims);
+    for (auto& v : t->reorder)
+        v = rng() & (point_count - 1);
+    for (auto& v : t->scramble)
+        v = rng();
+    return t;
+}
+
+XorTablesDev xor_view(const qmc_xor_tables* given, uint32_t dims, uint32_t point_count,
+                      uint32_t seed, cudaStream_t s)
+{
+    XorTablesDev v;
+    qmc_xor_tables* t = const_cast<qmc_xor_tables*>(given);
+    if (!t) {
+        v.own = make_white_noise(dims, point_count, seed);
+        t = v.own.get();
+    }
+    const auto& d = t->on_device(s);
+    v.dims = t->dims;
+    v.point_count = t->point_count;
+    v.reorder = static_cast<const uint32_t*>(d.reorder.get());
+    v.scramble = static_cast<const uint32_t*>(d.scramble.get());
+    v.points = static_cast<const uint32_t*>(d.points.get());
+    return v;
+}
+
+} // namespace host
+} // namespace qmcgpu
+
+const qmc_xor_tables::Dev& qmc_xor_tables::on_device(cudaStream_t s)
+{
+    const int d = current_device();
+    std::lock_guard<std::mutex> lk(mu);
+    auto& slot = dev[d];
+    if (!slot) {
+        auto e = std::make_unique<Dev>();
+        e->reorder = dev_upload(reorder.data(), reorder.size() * 4);
+        e->scramble = dev_upload(scramble.data(), scramble.size() * 4);
+        if (white_noise) {
+            // the first point_count Sobol' points at the integer stage,
+            // XOR-scrambled per dimension when seeded (imageplane.cpp:224-227),
+            // generated by the device fill
+            void* pts = nullptr;
+            cuda_ok(cudaMalloc(&pts, static_cast<size_t>(point_count) * dims * 4 + 32),
+                    "cudaMalloc");
+            e->points.reset(pts);
+            const bool scr = std::any_of(dim_scramble.begin(), dim_scramble.end(),
+                                         [](uint32_t w) { return w != 0; });
+            sobol_fill_impl(builtin_matrices(dims), 0, point_count, dims,
+                            scr ? QMC_SOBOL_XOR : QMC_SOBOL_NONE, dim_scramble.data(),
+                            QMC_OUT_U32, pts, s);
+            cuda_ok(cudaStreamSynchronize(s), "sync");
+        } else {
+            e->points = dev_upload(points.data(), points.size() * 4);
+        }
+        slot = std::move(e);
+    }
+    return *slot;
+}
 
 extern "C" {
 
-const char* qmc_last_error(void) { return g_error.c_str(); }
+const char* qmc_last_error(void) { return last_error().c_str(); }
 
 const char* qmc_status_string(qmc_status s)
 {
@@ -905,38 +359,6 @@ void qmc_matrices_destroy(qmc_matrices* m) { delete m; }
 
 // ----------------------------------------------------------------- fills
 
-static void sobol_fill_impl(qmc_matrices* m, uint64_t first, uint64_t n, uint32_t dims,
-                            qmc_sobol_scramble sc, const uint32_t* words, qmc_output kind,
-                            void* out, cudaStream_t s)
-{
-    if (!m)
-        fail(QMC_INVALID_ARGUMENT, "matrices handle is null");
-    if (n == 0 || dims == 0)
-        return;
-    if (first >= (1ull << 52) || n > (1ull << 52) - first)
-        fail(QMC_INVALID_ARGUMENT, "sobol_component: index must be below 2^52");
-    if (dims > m->dims)
-        fail(QMC_OUT_OF_RANGE, "sobol_component: dimension beyond the matrix set");
-    if (sc != QMC_SOBOL_NONE && sc != QMC_SOBOL_XOR && sc != QMC_SOBOL_OWEN)
-        fail(QMC_INVALID_ARGUMENT, "sobol_fill: unknown scramble kind");
-    // the kernels read dims-strided columns: tables for this dims prefix
-    const auto& dev = m->on_device(dims);
-    const uint32_t* colsT = static_cast<const uint32_t*>(dev.colsT.get());
-    const uint32_t* colsT_rev = static_cast<const uint32_t*>(dev.colsT_rev.get());
-    CallArgs args(s);
-    SmallArgs small{};
-    SmallStage stage;
-    if (words && sc != QMC_SOBOL_NONE)
-        set_small(small, stage, 0, words, dims, args);
-    args.upload();
-    finish_small(small, stage, args);
-    const int mode = sc == QMC_SOBOL_OWEN ? 2 : 0;
-    const bool u32 = kind == QMC_OUT_U32;
-    place_fill(out, first, n, dims, s, [&](const FillRange& r, cudaStream_t st) {
-        return launch_sobol(colsT, colsT_rev, small, dims, mode, u32, r, st);
-    });
-}
-
 qmc_status qmc_sobol_fill(const qmc_matrices* m, uint64_t first_index, uint64_t n, uint32_t dims,
                           qmc_sobol_scramble scramble, const uint32_t* words, qmc_output kind,
                           void* out, qmc_stream stream)
@@ -1066,122 +488,6 @@ const char* qmc_sampler_kind_name(qmc_sampler_kind kind)
 {
     return (kind >= 0 && kind < 8) ? kKindNames[kind] : "";
 }
-
-namespace {
-
-void require(bool ok, const char* what)
-{
-    if (!ok)
-        fail(QMC_CONFIG, what);
-}
-
-} // namespace
-
-// XOR-table sampler data (imageplane.hpp:92-120): 128x128 reorder words,
-// 128x128xdims scramble words and the stored integer-stage point set.
-// Immutable; the device copy is built once per GPU.
-struct qmc_xor_tables {
-    uint32_t dims = 0, point_count = 0;
-    std::vector<uint32_t> reorder, scramble; // host
-    std::vector<uint32_t> points;            // host (loaded) — empty for white noise
-    std::vector<uint32_t> dim_scramble;      // white noise: per-dim XOR of the points
-    bool white_noise = false;
-    std::mutex mu;
-    struct Dev {
-        DevPtr reorder, scramble, points;
-    };
-    std::map<int, std::unique_ptr<Dev>> dev;
-
-    const Dev& on_device(cudaStream_t s)
-    {
-        const int d = current_device();
-        std::lock_guard<std::mutex> lk(mu);
-        auto& slot = dev[d];
-        if (!slot) {
-            auto e = std::make_unique<Dev>();
-            e->reorder = dev_upload(reorder.data(), reorder.size() * 4);
-            e->scramble = dev_upload(scramble.data(), scramble.size() * 4);
-            if (white_noise) {
-                // the first point_count Sobol' points at the integer stage,
-                // XOR-scrambled per dimension when seeded (imageplane.cpp:224-227),
-                // generated by the device fill
-                void* pts = nullptr;
-                cuda_ok(cudaMalloc(&pts, static_cast<size_t>(point_count) * dims * 4 + 32),
-                        "cudaMalloc");
-                e->points.reset(pts);
-                const bool scr = std::any_of(dim_scramble.begin(), dim_scramble.end(),
-                                             [](uint32_t w) { return w != 0; });
-                sobol_fill_impl(builtin_matrices(dims), 0, point_count, dims,
-                                scr ? QMC_SOBOL_XOR : QMC_SOBOL_NONE, dim_scramble.data(),
-                                QMC_OUT_U32, pts, s);
-                cuda_ok(cudaStreamSynchronize(s), "sync");
-            } else {
-                e->points = dev_upload(points.data(), points.size() * 4);
-            }
-            slot = std::move(e);
-        }
-        return *slot;
-    }
-};
-
-namespace {
-
-constexpr size_t kXorTile = 128 * 128;
-
-// white_noise_xor_tables (imageplane.cpp:197-229): std::mt19937 words on the
-// host, in the reference's draw order.
-std::unique_ptr<qmc_xor_tables> make_white_noise(uint32_t dims, uint32_t point_count,
-                                                 uint32_t seed)
-{
-    if (dims == 0)
-        fail(QMC_CONFIG, "white_noise_xor_tables: dims must be >= 1");
-    if (point_count == 0 || (point_count & (point_count - 1)) != 0)
-        fail(QMC_CONFIG, "white_noise_xor_tables: point count must be a power of two");
-    auto t = std::make_unique<qmc_xor_tables>();
-    t->dims = dims;
-    t->point_count = point_count;
-    t->white_noise = true;
-    std::mt19937 rng(seed);
-    t->dim_scramble.assign(dims, 0u);
-    if (seed != 0)
-        for (auto& w : t->dim_scramble)
-            w = rng();
-    t->reorder.resize(kXorTile);
-    t->scramble.resize(kXorTile * dims);
-    for (auto& v : t->reorder)
-        v = rng() & (point_count - 1);
-    for (auto& v : t->scramble)
-        v = rng();
-    return t;
-}
-
-// Device view of the tables a stream / render uses: the caller's handle, or
-// white-noise tables made for this call.
-struct XorTablesDev {
-    uint32_t dims = 0, point_count = 0;
-    const uint32_t *reorder = nullptr, *scramble = nullptr, *points = nullptr;
-    std::unique_ptr<qmc_xor_tables> own;
-};
-
-XorTablesDev xor_view(const qmc_xor_tables* given, uint32_t dims, uint32_t point_count,
-                      uint32_t seed, cudaStream_t s)
-{
-    XorTablesDev v;
-    qmc_xor_tables* t = const_cast<qmc_xor_tables*>(given);
-    if (!t) {
-        v.own = make_white_noise(dims, point_count, seed);
-        t = v.own.get();
-    }
-    const auto& d = t->on_device(s);
-    v.dims = t->dims;
-    v.point_count = t->point_count;
-    v.reorder = static_cast<const uint32_t*>(d.reorder.get());
-    v.scramble = static_cast<const uint32_t*>(d.scramble.get());
-    v.points = static_cast<const uint32_t*>(d.points.get());
-    return v;
-}
-
-} // namespace
 
 namespace {
 
@@ -1579,28 +885,6 @@ void qmc_xor_tables_destroy(qmc_xor_tables* t) { delete t; }
 
 namespace {
 
-// Device copy of a row-major float point set (host arrays are staged).
-struct DevPoints {
-    const float* ptr = nullptr;
-    float* own = nullptr;
-    cudaStream_t s;
-    DevPoints(const float* p, uint64_t count, cudaStream_t st) : s(st)
-    {
-        if (is_device_pointer(p)) {
-            ptr = p;
-            return;
-        }
-        cuda_ok(cudaMallocAsync(&own, count * 4 + 4, s), "cudaMallocAsync");
-        cuda_ok(cudaMemcpyAsync(own, p, count * 4, cudaMemcpyHostToDevice, s), "H2D");
-        ptr = own;
-    }
-    ~DevPoints()
-    {
-        if (own)
-            cudaFreeAsync(own, s);
-    }
-};
-
 double pairwise_metric(const float* points, uint64_t n, uint32_t dims, cudaStream_t s, bool l2)
 {
     if (dims > quality_max_dims())
@@ -1672,7 +956,7 @@ qmc_status qmc_check_1d_stratification(qmc_sampler_kind kind, const qmc_stream_p
         if (st != QMC_OK) {
             cudaFreeAsync(pts, s);
             cudaFreeAsync(hist, s);
-            fail(st, g_error);
+            fail(st, last_error());
         }
         bad = reinterpret_cast<unsigned int*>(hist + count);
         cuda_ok(launch_stratification(pts, m, params->dims, j, hist, bad, s), "launch");
@@ -1861,194 +1145,6 @@ qmc_status qmc_write_pnm(const float* image, uint32_t width, uint32_t height, ui
         cudaFreeAsync(d, s);
         cuda_ok(cudaStreamSynchronize(s), "sync");
         *len = need;
-    });
-}
-
-// ------------------------------------------------------------------ render
-
-namespace {
-
-// render() validation and defaults (render.cpp:83-106) resolved into the
-// kernel parameters; owns the XOR tables view for the call.
-struct ResolvedRender {
-    RenderParams p{};
-    XorTablesDev xt;
-    uint64_t npix = 0;
-};
-
-void resolve_render(const qmc_render_job* job, uint32_t row_begin, uint32_t row_end,
-                    cudaStream_t s, CallArgs& args, ResolvedRender& rr)
-{
-    if (!job)
-        fail(QMC_INVALID_ARGUMENT, "render job is null");
-    if (job->width == 0 || job->height == 0)
-        fail(QMC_CONFIG, "render: image must be at least 1x1");
-    if (job->spp == 0)
-        fail(QMC_CONFIG, "render: spp must be >= 1");
-    if (job->kind < 0 || job->kind > 7)
-        fail(QMC_CONFIG, "unknown sampler kind");
-    if (job->accum != QMC_ACCUM_KAHAN && job->accum != QMC_ACCUM_INT)
-        fail(QMC_CONFIG, "accumulation mode must be 'kahan' or 'int'");
-    if (row_begin > row_end || row_end > job->height)
-        fail(QMC_OUT_OF_RANGE, "render: row band outside the image");
-    RenderParams& p = rr.p;
-    p.width = job->width;
-    p.height = job->height;
-    p.spp = job->spp;
-    p.order = hilbert_order(job->width, job->height);
-    p.row_begin = row_begin;
-    p.row_end = row_end;
-    p.inv_w = 1.0 / job->width;
-    p.inv_h = 1.0 / job->height;
-    std::vector<uint32_t> g = job->generator && job->generator_dims
-                                  ? std::vector<uint32_t>(job->generator,
-                                                          job->generator + job->generator_dims)
-                                  : lfsr(job->seed ? job->seed : 0xace1u, 2);
-    const uint32_t kind = job->kind;
-    if (kind == QMC_KIND_HALTON_HILBERT || kind == QMC_KIND_PIXEL_SHIFTED_LATTICE)
-        require(p.order >= 1 && p.order <= 31, "make_stream: pixel order must be in [1, 31]");
-    if (kind == QMC_KIND_LATTICE || kind == QMC_KIND_PIXEL_SHIFTED_LATTICE) {
-        for (uint32_t v : g)
-            require(v & 1u, "make_stream: generator components must be odd");
-        require(g.size() >= 2, "make_stream: dims beyond the generator vector");
-    }
-    if (g.size() < 2)
-        g.resize(2, 1u);
-    p.g0 = g[0];
-    p.g1 = g[1];
-    if (kind == QMC_KIND_SOBOL && job->seed != 0) {
-        p.scr0 = pixel_hash_host(0, job->seed, 0);
-        p.scr1 = pixel_hash_host(1, job->seed, 0);
-    }
-    p.tab3 = digit_table(3, 0, 0).ptr; // phi_3, seven ternary digits per step
-    std::vector<uint32_t> cols2(104, 0u);
-    if (job->matrices) {
-        require(job->matrices->dims >= 2, "make_stream: dims beyond the generator matrices");
-        std::memcpy(cols2.data(), job->matrices->columns.data(), 104 * 4);
-    } else {
-        cols2 = build_columns(builtin_rows(), 2);
-    }
-    if (kind == QMC_KIND_IMAGE_PLANE_HALTON) {
-        const HaltonEnum he = halton_enum(job->width, job->height);
-        p.scale_x = he.sx;
-        p.scale_y = he.sy;
-        p.exp_x = he.ex;
-        p.exp_y = he.ey;
-        p.stride = he.stride;
-        p.crt_x = he.crt_x;
-        p.crt_y = he.crt_y;
-    }
-    if (kind == QMC_KIND_SOBOL_XOR_TABLE) {
-        uint32_t pc = 1;
-        while (pc < job->spp)
-            pc <<= 1;
-        rr.xt = xor_view(job->tables, 2, pc, job->seed, s);
-        require(rr.xt.dims >= 2, "make_stream: dims beyond the stored point set");
-        p.xor_reorder = rr.xt.reorder;
-        p.xor_scramble = rr.xt.scramble;
-        p.xor_points = rr.xt.points;
-        p.xor_point_count = rr.xt.point_count;
-        p.xor_dims = rr.xt.dims;
-    }
-    const size_t coff = args.add(cols2.data(), cols2.size() * 4);
-    args.upload();
-    p.cols2 = args.at<uint32_t>(coff);
-    rr.npix = static_cast<uint64_t>(row_end - row_begin) * job->width;
-}
-
-} // namespace
-
-qmc_status qmc_render(const qmc_render_job* job, uint32_t row_begin, uint32_t row_end, float* out,
-                      qmc_stream stream)
-{
-    return guard([&] {
-        const cudaStream_t s = as_stream(stream);
-        CallArgs args(s);
-        ResolvedRender rr;
-        resolve_render(job, row_begin, row_end, s, args, rr);
-        if (rr.npix == 0)
-            return;
-        if (!out)
-            fail(QMC_INVALID_ARGUMENT, "output pointer is null");
-        if (is_device_pointer(out)) {
-            cuda_ok(launch_render(rr.p, job->kind, job->accum, out, s), "launch_render");
-            if (job->kind == QMC_KIND_SOBOL_XOR_TABLE && !job->tables)
-                cuda_ok(cudaStreamSynchronize(s), "sync"); // temporary tables die with the call
-            return;
-        }
-        float* d = nullptr;
-        cuda_ok(cudaMallocAsync(&d, rr.npix * 4, s), "cudaMallocAsync");
-        cuda_ok(launch_render(rr.p, job->kind, job->accum, d, s), "launch_render");
-        cuda_ok(cudaMemcpyAsync(out, d, rr.npix * 4, cudaMemcpyDeviceToHost, s), "D2H");
-        cudaFreeAsync(d, s);
-        cuda_ok(cudaStreamSynchronize(s), "sync");
-    });
-}
-
-qmc_status qmc_render_partial(const qmc_render_job* job, uint32_t part, uint32_t parts,
-                              uint32_t row_begin, uint32_t row_end, int64_t* accum,
-                              qmc_stream stream)
-{
-    return guard([&] {
-        const cudaStream_t s = as_stream(stream);
-        if (job && job->accum != QMC_ACCUM_INT)
-            fail(QMC_INVALID_ARGUMENT,
-                 "render_partial: sample partitions need the int accumulator (exactly associative)");
-        uint64_t rem = 0, mod = 1;
-        const qmc_status st = qmc_partition_by_extra_dimension(part, parts, 2, &rem, &mod);
-        if (st != QMC_OK)
-            fail(st, g_error);
-        CallArgs args(s);
-        ResolvedRender rr;
-        resolve_render(job, row_begin, row_end, s, args, rr);
-        if (rr.npix == 0)
-            return;
-        if (!accum || !is_device_pointer(accum))
-            fail(QMC_INVALID_ARGUMENT, "render_partial: accum must be a device buffer");
-        cuda_ok(launch_render_partial(rr.p, job->kind, static_cast<uint32_t>(rem),
-                                      static_cast<uint32_t>(mod),
-                                      reinterpret_cast<long long*>(accum), s),
-                "launch_render_partial");
-        if (job->kind == QMC_KIND_SOBOL_XOR_TABLE && !job->tables)
-            cuda_ok(cudaStreamSynchronize(s), "sync");
-    });
-}
-
-qmc_status qmc_render_finalize(const int64_t* accum, uint64_t npix, uint32_t spp, float* out,
-                               qmc_stream stream)
-{
-    return guard([&] {
-        if (spp == 0)
-            fail(QMC_CONFIG, "render: spp must be >= 1");
-        if (npix == 0)
-            return;
-        if (!accum || !out || !is_device_pointer(accum) || !is_device_pointer(out))
-            fail(QMC_INVALID_ARGUMENT, "render_finalize: device buffers required");
-        cuda_ok(launch_render_finalize(reinterpret_cast<const long long*>(accum), npix, spp, out,
-                                       as_stream(stream)),
-                "launch_render_finalize");
-    });
-}
-
-qmc_status qmc_scene_value(const double* xy, double* out, uint64_t n, qmc_stream stream)
-{
-    return guard([&] {
-        if (n == 0)
-            return;
-        const cudaStream_t s = as_stream(stream);
-        if (is_device_pointer(xy) && is_device_pointer(out)) {
-            cuda_ok(launch_scene_value(xy, out, n, s), "launch_scene_value");
-            return;
-        }
-        double *dxy = nullptr, *dout = nullptr;
-        cuda_ok(cudaMallocAsync(&dxy, n * 16, s), "cudaMallocAsync");
-        cuda_ok(cudaMallocAsync(&dout, n * 8, s), "cudaMallocAsync");
-        cuda_ok(cudaMemcpyAsync(dxy, xy, n * 16, cudaMemcpyDefault, s), "H2D");
-        cuda_ok(launch_scene_value(dxy, dout, n, s), "launch_scene_value");
-        cuda_ok(cudaMemcpyAsync(out, dout, n * 8, cudaMemcpyDefault, s), "D2H");
-        cudaFreeAsync(dxy, s);
-        cudaFreeAsync(dout, s);
-        cuda_ok(cudaStreamSynchronize(s), "sync");
     });
 }
 

@@ -1,0 +1,200 @@
+// abi_render.cpp — the fused per-pixel render of the C ABI (render.cpp:58-143
+// on the device): qmc_render, the sample-partitioned qmc_render_partial /
+// qmc_render_finalize, and qmc_scene_value.
+#include "objects.hpp"
+
+using namespace qmcgpu;
+using namespace qmcgpu::host;
+
+extern "C" {
+
+// ------------------------------------------------------------------ render
+
+namespace {
+
+// render() validation and defaults (render.cpp:83-106) resolved into the
+// kernel parameters; owns the XOR tables view for the call.
+struct ResolvedRender {
+    RenderParams p{};
+    XorTablesDev xt;
+    uint64_t npix = 0;
+};
+
+void resolve_render(const qmc_render_job* job, uint32_t row_begin, uint32_t row_end,
+                    cudaStream_t s, CallArgs& args, ResolvedRender& rr)
+{
+    if (!job)
+        fail(QMC_INVALID_ARGUMENT, "render job is null");
+    if (job->width == 0 || job->height == 0)
+        fail(QMC_CONFIG, "render: image must be at least 1x1");
+    if (job->spp == 0)
+        fail(QMC_CONFIG, "render: spp must be >= 1");
+    if (job->kind < 0 || job->kind > 7)
+        fail(QMC_CONFIG, "unknown sampler kind");
+    if (job->accum != QMC_ACCUM_KAHAN && job->accum != QMC_ACCUM_INT)
+        fail(QMC_CONFIG, "accumulation mode must be 'kahan' or 'int'");
+    if (row_begin > row_end || row_end > job->height)
+        fail(QMC_OUT_OF_RANGE, "render: row band outside the image");
+    RenderParams& p = rr.p;
+    p.width = job->width;
+    p.height = job->height;
+    p.spp = job->spp;
+    p.order = hilbert_order(job->width, job->height);
+    p.row_begin = row_begin;
+    p.row_end = row_end;
+    p.inv_w = 1.0 / job->width;
+    p.inv_h = 1.0 / job->height;
+    std::vector<uint32_t> g = job->generator && job->generator_dims
+                                  ? std::vector<uint32_t>(job->generator,
+                                                          job->generator + job->generator_dims)
+                                  : lfsr(job->seed ? job->seed : 0xace1u, 2);
+    const uint32_t kind = job->kind;
+    if (kind == QMC_KIND_HALTON_HILBERT || kind == QMC_KIND_PIXEL_SHIFTED_LATTICE)
+        require(p.order >= 1 && p.order <= 31, "make_stream: pixel order must be in [1, 31]");
+    if (kind == QMC_KIND_LATTICE || kind == QMC_KIND_PIXEL_SHIFTED_LATTICE) {
+        for (uint32_t v : g)
+            require(v & 1u, "make_stream: generator components must be odd");
+        require(g.size() >= 2, "make_stream: dims beyond the generator vector");
+    }
+    if (g.size() < 2)
+        g.resize(2, 1u);
+    p.g0 = g[0];
+    p.g1 = g[1];
+    if (kind == QMC_KIND_SOBOL && job->seed != 0) {
+        p.scr0 = pixel_hash_host(0, job->seed, 0);
+        p.scr1 = pixel_hash_host(1, job->seed, 0);
+    }
+    p.tab3 = digit_table(3, 0, 0).ptr; // phi_3, seven ternary digits per step
+    std::vector<uint32_t> cols2(104, 0u);
+    if (job->matrices) {
+        require(job->matrices->dims >= 2, "make_stream: dims beyond the generator matrices");
+        std::memcpy(cols2.data(), job->matrices->columns.data(), 104 * 4);
+    } else {
+        cols2 = build_columns(builtin_rows(), 2);
+    }
+    if (kind == QMC_KIND_IMAGE_PLANE_HALTON) {
+        const HaltonEnum he = halton_enum(job->width, job->height);
+        p.scale_x = he.sx;
+        p.scale_y = he.sy;
+        p.exp_x = he.ex;
+        p.exp_y = he.ey;
+        p.stride = he.stride;
+        p.crt_x = he.crt_x;
+        p.crt_y = he.crt_y;
+    }
+    if (kind == QMC_KIND_SOBOL_XOR_TABLE) {
+        uint32_t pc = 1;
+        while (pc < job->spp)
+            pc <<= 1;
+        rr.xt = xor_view(job->tables, 2, pc, job->seed, s);
+        require(rr.xt.dims >= 2, "make_stream: dims beyond the stored point set");
+        p.xor_reorder = rr.xt.reorder;
+        p.xor_scramble = rr.xt.scramble;
+        p.xor_points = rr.xt.points;
+        p.xor_point_count = rr.xt.point_count;
+        p.xor_dims = rr.xt.dims;
+    }
+    const size_t coff = args.add(cols2.data(), cols2.size() * 4);
+    args.upload();
+    p.cols2 = args.at<uint32_t>(coff);
+    rr.npix = static_cast<uint64_t>(row_end - row_begin) * job->width;
+}
+
+} // namespace
+
+qmc_status qmc_render(const qmc_render_job* job, uint32_t row_begin, uint32_t row_end, float* out,
+                      qmc_stream stream)
+{
+    return guard([&] {
+        const cudaStream_t s = as_stream(stream);
+        CallArgs args(s);
+        ResolvedRender rr;
+        resolve_render(job, row_begin, row_end, s, args, rr);
+        if (rr.npix == 0)
+            return;
+        if (!out)
+            fail(QMC_INVALID_ARGUMENT, "output pointer is null");
+        if (is_device_pointer(out)) {
+            cuda_ok(launch_render(rr.p, job->kind, job->accum, out, s), "launch_render");
+            if (job->kind == QMC_KIND_SOBOL_XOR_TABLE && !job->tables)
+                cuda_ok(cudaStreamSynchronize(s), "sync"); // temporary tables die with the call
+            return;
+        }
+        float* d = nullptr;
+        cuda_ok(cudaMallocAsync(&d, rr.npix * 4, s), "cudaMallocAsync");
+        cuda_ok(launch_render(rr.p, job->kind, job->accum, d, s), "launch_render");
+        cuda_ok(cudaMemcpyAsync(out, d, rr.npix * 4, cudaMemcpyDeviceToHost, s), "D2H");
+        cudaFreeAsync(d, s);
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+    });
+}
+
+qmc_status qmc_render_partial(const qmc_render_job* job, uint32_t part, uint32_t parts,
+                              uint32_t row_begin, uint32_t row_end, int64_t* accum,
+                              qmc_stream stream)
+{
+    return guard([&] {
+        const cudaStream_t s = as_stream(stream);
+        if (job && job->accum != QMC_ACCUM_INT)
+            fail(QMC_INVALID_ARGUMENT,
+                 "render_partial: sample partitions need the int accumulator (exactly associative)");
+        uint64_t rem = 0, mod = 1;
+        const qmc_status st = qmc_partition_by_extra_dimension(part, parts, 2, &rem, &mod);
+        if (st != QMC_OK)
+            fail(st, last_error());
+        CallArgs args(s);
+        ResolvedRender rr;
+        resolve_render(job, row_begin, row_end, s, args, rr);
+        if (rr.npix == 0)
+            return;
+        if (!accum || !is_device_pointer(accum))
+            fail(QMC_INVALID_ARGUMENT, "render_partial: accum must be a device buffer");
+        cuda_ok(launch_render_partial(rr.p, job->kind, static_cast<uint32_t>(rem),
+                                      static_cast<uint32_t>(mod),
+                                      reinterpret_cast<long long*>(accum), s),
+                "launch_render_partial");
+        if (job->kind == QMC_KIND_SOBOL_XOR_TABLE && !job->tables)
+            cuda_ok(cudaStreamSynchronize(s), "sync");
+    });
+}
+
+qmc_status qmc_render_finalize(const int64_t* accum, uint64_t npix, uint32_t spp, float* out,
+                               qmc_stream stream)
+{
+    return guard([&] {
+        if (spp == 0)
+            fail(QMC_CONFIG, "render: spp must be >= 1");
+        if (npix == 0)
+            return;
+        if (!accum || !out || !is_device_pointer(accum) || !is_device_pointer(out))
+            fail(QMC_INVALID_ARGUMENT, "render_finalize: device buffers required");
+        cuda_ok(launch_render_finalize(reinterpret_cast<const long long*>(accum), npix, spp, out,
+                                       as_stream(stream)),
+                "launch_render_finalize");
+    });
+}
+
+qmc_status qmc_scene_value(const double* xy, double* out, uint64_t n, qmc_stream stream)
+{
+    return guard([&] {
+        if (n == 0)
+            return;
+        const cudaStream_t s = as_stream(stream);
+        if (is_device_pointer(xy) && is_device_pointer(out)) {
+            cuda_ok(launch_scene_value(xy, out, n, s), "launch_scene_value");
+            return;
+        }
+        double *dxy = nullptr, *dout = nullptr;
+        cuda_ok(cudaMallocAsync(&dxy, n * 16, s), "cudaMallocAsync");
+        cuda_ok(cudaMallocAsync(&dout, n * 8, s), "cudaMallocAsync");
+        cuda_ok(cudaMemcpyAsync(dxy, xy, n * 16, cudaMemcpyDefault, s), "H2D");
+        cuda_ok(launch_scene_value(dxy, dout, n, s), "launch_scene_value");
+        cuda_ok(cudaMemcpyAsync(out, dout, n * 8, cudaMemcpyDefault, s), "D2H");
+        cudaFreeAsync(dxy, s);
+        cudaFreeAsync(dout, s);
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+    });
+}
+
+} // extern "C"
+

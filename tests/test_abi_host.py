@@ -24,6 +24,22 @@ def test_library_exports_header_symbols():
     assert L.qmc_abi_version() == 1
 
 
+def test_library_exports_only_the_c_abi():
+    """exports.map: the dynamic symbol table is exactly the header's qmc_*
+    functions (no C++ internals, no static cudart)."""
+    import shutil
+    import subprocess
+
+    if shutil.which("nm") is None:
+        pytest.skip("nm not available")
+    out = subprocess.run(["nm", "-D", "--defined-only", q.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    syms = [ln.split()[-1] for ln in out.splitlines() if ln.strip()]
+    hdr = open(os.path.join(ROOT, "include", "qmcgpu.h")).read()
+    names = set(re.findall(r"^[A-Za-z_][\w \*]*?\b(qmc_[a-z0-9_]+)\(", hdr, re.M))
+    assert sorted(s for s in syms if s not in names) == []
+
+
 def test_primes_and_max_powers(golden_arrays):
     for k in [0, 1, 2, 10, 500, 999]:
         assert q.prime(k) == golden_arrays["primes"][k]
