@@ -127,7 +127,10 @@ struct DigitTable {
     uint32_t group = 0;
 };
 
-DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor);
+// min_digits: the table must invert at least that many digits per step
+DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor, uint32_t min_digits = 2);
+// floor(2^64 / b^D) for D = 0..32 (0 where b^D >= 2^32), on the current device
+const uint64_t* pow_magic(uint32_t b);
 std::vector<RadicalDim> radical_dims(uint32_t dims, uint32_t first_prime, qmc_radical_scramble sc,
                                      const uint32_t* factors, std::vector<uint32_t>& sigma_pool,
                                      std::vector<size_t>& sigma_off);

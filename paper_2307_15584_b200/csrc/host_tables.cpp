@@ -250,7 +250,7 @@ uint64_t digit_reverse_host(uint64_t v, uint32_t base, uint32_t digits)
 // Built once per (device, base, scramble) and kept for the process.
 constexpr uint32_t kDigitTableMax = 4096;
 
-DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor)
+DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor, uint32_t min_digits)
 {
     static std::mutex mu;
     static std::map<std::tuple<int, uint32_t, uint32_t, uint32_t>, std::pair<DevPtr, uint32_t>>
@@ -260,7 +260,7 @@ DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor)
         group *= b;
         ++d;
     }
-    if (d < 2)
+    if (d < min_digits || d == 0)
         return {};
     const int dev = current_device();
     std::lock_guard<std::mutex> lk(mu);
@@ -286,6 +286,23 @@ DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor)
         slot.second = group;
     }
     return {static_cast<const uint32_t*>(slot.first.get()), slot.second};
+}
+
+const uint64_t* pow_magic(uint32_t b)
+{
+    static std::mutex mu;
+    static std::map<std::pair<int, uint32_t>, DevPtr> cache;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(mu);
+    auto& slot = cache[{dev, b}];
+    if (!slot) {
+        std::vector<uint64_t> m(33, 0);
+        uint64_t p = 1;
+        for (uint32_t d = 0; d < 33 && p < (1ull << 32); ++d, p *= b)
+            m[d] = p == 1 ? ~0ull : ~0ull / p; // b odd: floor((2^64-1)/p) = floor(2^64/p)
+        slot = dev_upload(m.data(), m.size() * 8);
+    }
+    return static_cast<const uint64_t*>(slot.get());
 }
 
 // RadicalDim table for `dims` prime bases (radical.cpp:130-181).
@@ -322,12 +339,26 @@ std::vector<RadicalDim> radical_dims(uint32_t dims, uint32_t first_prime, qmc_ra
             sigma_pool.insert(sigma_pool.end(), s.begin(), s.end());
             r.mode = 2;
         }
+        r.ftable = nullptr;
+        r.magic = nullptr;
+        r.fgroup = r.fdigits = r.himod = 0;
+        r.fdivg = Div32{0, 0};
         if (b > 2) {
             const DigitTable t = digit_table(b, r.mode, r.factor);
             if (t.ptr) {
                 r.table = t.ptr;
                 r.group = t.group;
                 r.divg = make_div32(t.group);
+            }
+            const DigitTable f = digit_table(b, r.mode, r.factor, 1);
+            if (f.ptr) {
+                r.ftable = f.ptr;
+                r.fgroup = f.group;
+                r.fdivg = make_div32(f.group);
+                for (uint32_t g = f.group; g > 1; g /= b)
+                    ++r.fdigits;
+                r.himod = r.maxpow / f.group;
+                r.magic = pow_magic(b);
             }
         }
     }

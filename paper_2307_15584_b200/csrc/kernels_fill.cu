@@ -628,29 +628,124 @@ __global__ void __launch_bounds__(kBlock)
     }
 }
 
+// Continuation state of one dimension's incremental walk (shared memory,
+// 16 words): valid when `live` and the next run starts at index `next`.
+struct HaltonState {
+    uint32_t next, lob, h1, live;
+    HiRecord r0, r1;
+    uint32_t pad[2];
+};
+static_assert(sizeof(HaltonState) == 64, "HaltonState is 16 words");
+
+// One warp, one dimension, `cnt` consecutive indices from i0 into the
+// padded tile column starting at tile[off] (row stride ld). `st` (or null)
+// carries the incremental state from the previous contiguous run.
+template <bool U32OUT>
+__device__ __forceinline__ void halton_run(const RadicalDim& r, uint32_t i0, uint32_t cnt,
+                                           uint32_t lane, uint32_t* tile, uint32_t off,
+                                           uint32_t ld, HaltonState* st)
+{
+    if (r.base == 2) {
+        for (uint32_t p = lane; p < cnt; p += 32) {
+            const uint32_t x = brev32((i0 + p) & 0x7fffffffu);
+            tile[off + p * ld] = U32OUT ? x : map_bits(x);
+        }
+    } else if (r.ftable && i0 <= 0xffffffffu - cnt) {
+        // incremental split i = h * G + lo (G = fgroup > 32): per 32-point
+        // step the warp's indices span at most h and h+1, whose reversals
+        // are warp-uniform records; a lane adds one table lookup, one IMAD
+        // and an integer division by magic.
+        const uint32_t G = r.fgroup;
+        uint32_t lob, h1;
+        HiRecord r0, r1;
+        if (st && st->live && st->next == i0) {
+            lob = st->lob;
+            h1 = st->h1;
+            r0 = st->r0;
+            r1 = st->r1;
+        } else {
+            const uint32_t ir = i0 - div32(i0, r.divmp) * r.maxpow; // i %= maxpow
+            const uint32_t h = div32(ir, r.fdivg);
+            lob = ir - h * G;
+            h1 = h + 1 == r.himod ? 0u : h + 1;
+            r0 = hi_record(h, r);
+            r1 = hi_record(h1, r);
+        }
+        const uint32_t steps = (cnt + 31) >> 5;
+        for (uint32_t s = 0; s < steps; ++s) {
+            const uint32_t p = (s << 5) + lane;
+            uint32_t lo = lob + lane;
+            const bool up = lo >= G;
+            lo = up ? lo - G : lo;
+            const uint32_t acc =
+                __ldg(r.ftable + lo) * (up ? r1.mul : r0.mul) + (up ? r1.acc : r0.acc);
+            const uint32_t x = frac_div_magic(acc, up ? r1.scale : r0.scale, up ? r1.mlo : r0.mlo,
+                                              up ? r1.mhi : r0.mhi);
+            if (p < cnt)
+                tile[off + p * ld] = U32OUT ? x : map_bits(x);
+            lob += 32;
+            if (lob >= G) { // warp-uniform
+                lob -= G;
+                h1 = h1 + 1 == r.himod ? 0u : h1 + 1;
+                r0 = r1;
+                r1 = hi_record(h1, r);
+            }
+        }
+        if (st && lane == 0) {
+            st->next = i0 + (steps << 5);
+            st->lob = lob;
+            st->h1 = h1;
+            st->r0 = r0;
+            st->r1 = r1;
+            st->live = 1;
+        }
+    } else {
+        for (uint32_t p = lane; p < cnt; p += 32) {
+            const uint32_t x = radical_fixed(i0 + p, r);
+            tile[off + p * ld] = U32OUT ? x : map_bits(x);
+        }
+    }
+}
+
 // Prime-base Halton (radical.cpp:240-269), shared-memory tiled: a CTA owns
-// tiles of tp consecutive points; warp w computes dimensions w, w+8, ... for
-// the tile's points (one base per warp -> uniform digit loops, the
-// RadicalDim record is a warp-uniform load) into a padded [tp][dims+1]
-// shared tile, then the whole tile — tp*dims consecutive output words — is
-// written out coalesced.
+// a contiguous range of tiles of tp consecutive points; a warp computes one
+// (dimension, run of consecutive points) item at a time into a padded
+// [tp][dims+1] shared tile (one base per warp -> uniform digit loops and
+// records, halton_run), then the whole tile — tp*dims consecutive output
+// words — is written out coalesced. With one run per dimension the same warp
+// owns a dimension in every tile, so its incremental state carries over from
+// tile to tile (HaltonState, after the tile in shared memory).
 template <bool U32OUT>
 __global__ void __launch_bounds__(kBlock)
     k_halton_tiled(const RadicalDim* __restrict__ rd, uint32_t dims, Div32 div_dims, uint32_t tp,
                    uint64_t first, uint64_t n, uint64_t ntiles, uint32_t* __restrict__ out)
 {
-    extern __shared__ uint32_t tile[];
+    extern __shared__ __align__(16) uint32_t tile[];
     const uint32_t ld = dims + 1;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, nwarps = blockDim.x >> 5;
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    // (dim, point run) work items: several warps share a dimension when
+    // dims < warps per CTA (no carried state then)
+    const bool carry = dims >= nwarps; // launch_halton sizes the state slots alike
+    const uint32_t runs = carry ? 1u : nwarps / dims;
+    HaltonState* states =
+        carry ? reinterpret_cast<HaltonState*>(tile + ((tp * ld + 15u) & ~15u)) : nullptr;
+    if (states)
+        for (uint32_t j = threadIdx.x; j < dims; j += blockDim.x)
+            states[j].live = 0;
+    __syncthreads();
+    const uint64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+    const uint64_t t1 = min(ntiles, (blockIdx.x + 1) * per);
+    for (uint64_t t = blockIdx.x * per; t < t1; ++t) {
         const uint64_t p0 = t * tp;
         const uint32_t cnt = static_cast<uint32_t>(n - p0 < tp ? n - p0 : tp);
-        for (uint32_t j = warp; j < dims; j += nwarps) {
-            const RadicalDim r = rd[j];
-            for (uint32_t p = lane; p < cnt; p += 32) {
-                const uint32_t x = radical_fixed(static_cast<uint32_t>(first + p0 + p), r);
-                tile[p * ld + j] = U32OUT ? x : map_bits(x);
-            }
+        const uint32_t chunk = ((cnt + runs - 1) / runs + 31u) & ~31u;
+        for (uint32_t item = warp; item < dims * runs; item += nwarps) {
+            const uint32_t j = runs == 1 ? item : item % dims;
+            const uint32_t pb = (runs == 1 ? 0u : item / dims) * chunk;
+            const uint32_t pe = min(cnt, pb + chunk);
+            if (pb < pe)
+                halton_run<U32OUT>(rd[j], static_cast<uint32_t>(first + p0 + pb), pe - pb, lane,
+                                   tile, pb * ld + j, ld, states ? states + j : nullptr);
         }
         __syncthreads();
         uint32_t* o = out + p0 * dims;
@@ -974,11 +1069,13 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
 {
     if (r.n == 0)
         return cudaSuccess;
-    // tile of tp points x (dims + 1) padded words: <= 32 KB, >= 32 points
+    // tile of tp points x (dims + 1) padded words: <= 32 KB, >= 32 points;
+    // then 64 B of carried state per dimension when dims >= warps per CTA
     uint32_t tp = (8192u / (dims + 1)) & ~31u;
     if (tp < 32)
         tp = 32;
-    const size_t smem = static_cast<size_t>(tp) * (dims + 1) * 4;
+    const size_t tile_words = (static_cast<size_t>(tp) * (dims + 1) + 15) & ~size_t(15);
+    const size_t smem = tile_words * 4 + (dims >= kBlock / 32 ? size_t(dims) * 64 : 0);
     auto kern = u32 ? k_halton_tiled<true> : k_halton_tiled<false>;
     if (smem > 48 * 1024) {
         const cudaError_t e =

@@ -107,6 +107,55 @@ def test_halton_many_dims_vs_oracle(oracle):
             assert got[k, j] == oracle.qo_radical_inverse_fixed(i, j)
 
 
+_MODE = {"plain": 0, "linear": 1, "faure": 2}
+
+
+@pytest.mark.parametrize("pi", [1, 2, 3, 6, 17, 18, 40, 100, 563, 564, 999])
+@pytest.mark.parametrize("mode", ["plain", "linear", "faure"])
+def test_radical_fill_windows_vs_reference(ref, pi, mode):
+    """Contiguous fills (incremental hi/lo split, table bases up to 4096, the
+    per-sample loop beyond) against the reference per index: windows across
+    prime_max_power (i %= maxpow), across 2^31 and across the u32 wrap."""
+    b, mp = q.prime(pi), q.prime_max_power(pi)
+    factor = max(1, (b * 5) // 7) if mode == "linear" else 1
+    for first, n in [(0, 5000), (mp - 2100, 4200), (2**31 - 1000, 3000), (2**32 - 2000, 3000),
+                     (987654321, 3000), (3 * mp + 17, 777)]:
+        if first + n > 2**32 + 2000:
+            continue
+        exp = np.zeros(n, np.uint32)
+        assert ref.ref_radical_fixed_fill(first & 0xFFFFFFFF, n, pi, _MODE[mode], factor,
+                                          ptr(exp)) == 0
+        got = u32(q.radical_inverse_fill(n, pi, first=first, scramble=mode, factor=factor,
+                                         fixed=True))
+        np.testing.assert_array_equal(got, exp, err_msg=f"first={first}")
+
+
+@pytest.mark.parametrize("mode", ["plain", "linear", "faure"])
+def test_halton_fill_windows_vs_reference(ref, mode):
+    dims = 40
+    for first, n in [(0, 700), (3486784401 - 300, 700), (2**32 - 500, 700), (12345678, 333)]:
+        got = u32(q.halton_fill(n, dims, first=first, scramble=mode, fixed=True)).reshape(n, dims)
+        for j in range(dims):
+            b = q.prime(j)
+            exp = np.zeros(n, np.uint32)
+            assert ref.ref_radical_fixed_fill(first, n, j, _MODE[mode], b - 1 if b > 2 else 1,
+                                              ptr(exp)) == 0
+            np.testing.assert_array_equal(got[:, j], exp, err_msg=f"first={first} dim={j}")
+
+
+@pytest.mark.parametrize("mode", ["plain", "faure"])
+@pytest.mark.parametrize("first", [0, 3486784401 - (1 << 18), 2**32 - (1 << 18), 2**33 + 5])
+def test_halton_fill_long_runs_vs_reference(ref, mode, first):
+    """Long contiguous fills: the per-dimension state carried from tile to
+    tile across the base-3 prime_max_power boundary and the u32 index wrap."""
+    n, dims = 1 << 19, 12
+    got = u32(q.halton_fill(n, dims, first=first, scramble=mode, fixed=True)).reshape(n, dims)
+    for j in range(dims):
+        exp = np.zeros(n, np.uint32)
+        assert ref.ref_radical_fixed_fill(first & 0xFFFFFFFF, n, j, _MODE[mode], 1, ptr(exp)) == 0
+        np.testing.assert_array_equal(got[:, j], exp, err_msg=f"dim={j}")
+
+
 # ---------------------------------------------------------------- Sobol'
 def test_sobol_vs_golden(golden_arrays, golden, oracle):
     got = u32(q.sobol_fill(1024, 64, fixed=True))

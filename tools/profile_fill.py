@@ -39,6 +39,10 @@ elif a.config == "c1":
     n = 1 << 24
     out = torch.empty(n, dtype=torch.float32, device="cuda")
     fn = lambda: q.radical_inverse_fill(n, 0, out=out)  # noqa: E731
+elif a.config == "halton":
+    n, d = 1 << 24, 32
+    out = torch.empty((n, d), dtype=torch.float32, device="cuda")
+    fn = lambda: q.halton_fill(n, d, scramble="linear", out=out)  # noqa: E731
 elif a.config.startswith("c5"):
     spp = int(a.config[2:] or 64)
     out = torch.empty((2160, 3840), dtype=torch.float32, device="cuda")
