@@ -127,8 +127,14 @@ struct DigitTable {
     uint32_t group = 0;
 };
 
-// min_digits: the table must invert at least that many digits per step
-DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor, uint32_t min_digits = 2);
+// Widest b^d-entry table (b^d <= max_entries) inverting d >= min_digits
+// digits per step with the digit permutation of `mode`; cached per device.
+// Random-access users (radical_fixed) keep tables L1-sized; the contiguous
+// fills read theirs sequentially and take wider ones (fewer block crossings).
+constexpr uint32_t kDigitTableMax = 4096;
+constexpr uint32_t kFillTableMax = 16384;
+DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor, uint32_t min_digits = 2,
+                       uint32_t max_entries = kDigitTableMax);
 // floor(2^64 / b^D) for D = 0..32 (0 where b^D >= 2^32), on the current device
 const uint64_t* pow_magic(uint32_t b);
 std::vector<RadicalDim> radical_dims(uint32_t dims, uint32_t first_prime, qmc_radical_scramble sc,

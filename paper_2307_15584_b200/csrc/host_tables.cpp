@@ -248,15 +248,15 @@ uint64_t digit_reverse_host(uint64_t v, uint32_t base, uint32_t digits)
 // d = the most base-b digits with b^d <= 4096 (so a table stays 16 KB and
 // L1-resident), entry v = the d digits of v permuted by sigma and mirrored.
 // Built once per (device, base, scramble) and kept for the process.
-constexpr uint32_t kDigitTableMax = 4096;
-
-DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor, uint32_t min_digits)
+DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor, uint32_t min_digits,
+                       uint32_t max_entries)
 {
     static std::mutex mu;
-    static std::map<std::tuple<int, uint32_t, uint32_t, uint32_t>, std::pair<DevPtr, uint32_t>>
+    static std::map<std::tuple<int, uint32_t, uint32_t, uint32_t, uint32_t>,
+                    std::pair<DevPtr, uint32_t>>
         cache;
     uint32_t d = 0, group = 1;
-    while (static_cast<uint64_t>(group) * b <= kDigitTableMax) {
+    while (static_cast<uint64_t>(group) * b <= max_entries) {
         group *= b;
         ++d;
     }
@@ -264,7 +264,7 @@ DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor, uint32_t min_
         return {};
     const int dev = current_device();
     std::lock_guard<std::mutex> lk(mu);
-    auto& slot = cache[{dev, b, mode, factor}];
+    auto& slot = cache[{dev, b, mode, factor, max_entries}];
     if (!slot.first) {
         std::vector<uint32_t> sigma(b);
         if (mode == 2) {
@@ -350,7 +350,7 @@ std::vector<RadicalDim> radical_dims(uint32_t dims, uint32_t first_prime, qmc_ra
                 r.group = t.group;
                 r.divg = make_div32(t.group);
             }
-            const DigitTable f = digit_table(b, r.mode, r.factor, 1);
+            const DigitTable f = digit_table(b, r.mode, r.factor, 1, kFillTableMax);
             if (f.ptr) {
                 r.ftable = f.ptr;
                 r.fgroup = f.group;

@@ -633,62 +633,90 @@ __global__ void __launch_bounds__(kBlock)
 struct HaltonState {
     uint32_t next, lob, h1, live;
     HiRecord r0, r1;
-    uint32_t pad[2];
+    uint32_t g0, mulg; // hi_advance state of r1
 };
 static_assert(sizeof(HaltonState) == 64, "HaltonState is 16 words");
 
+// No memory clobber: the tile is only read back after __syncthreads(), and
+// leaving it out lets the table loads of later steps move ahead of the stores.
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v)
+{
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v));
+}
+
 // One warp, one dimension, `cnt` consecutive indices from i0 into the
-// padded tile column starting at tile[off] (row stride ld). `st` (or null)
-// carries the incremental state from the previous contiguous run.
+// padded tile column at shared address col (row stride ld words). `st` (or
+// null) carries the incremental state from the previous contiguous run.
 template <bool U32OUT>
 __device__ __forceinline__ void halton_run(const RadicalDim& r, uint32_t i0, uint32_t cnt,
-                                           uint32_t lane, uint32_t* tile, uint32_t off,
-                                           uint32_t ld, HaltonState* st)
+                                           uint32_t lane, uint32_t col, uint32_t ld,
+                                           HaltonState* st)
 {
+    const uint32_t row = ld * 4;
     if (r.base == 2) {
         for (uint32_t p = lane; p < cnt; p += 32) {
             const uint32_t x = brev32((i0 + p) & 0x7fffffffu);
-            tile[off + p * ld] = U32OUT ? x : map_bits(x);
+            sts32(col + p * row, U32OUT ? x : map_bits(x));
         }
     } else if (r.ftable && i0 <= 0xffffffffu - cnt) {
-        // incremental split i = h * G + lo (G = fgroup > 32): per 32-point
-        // step the warp's indices span at most h and h+1, whose reversals
-        // are warp-uniform records; a lane adds one table lookup, one IMAD
-        // and an integer division by magic.
+        // incremental split i = h * G + lo (G = fgroup > 32): the warp's 32
+        // indices of a step span h, or h and h+1 on the step that crosses a
+        // multiple of G; the records of h and h+1 are warp-uniform, so a lane
+        // adds one table lookup, one IMAD and an integer division by magic.
         const uint32_t G = r.fgroup;
-        uint32_t lob, h1;
+        uint32_t lob, h1, g0, mulg;
         HiRecord r0, r1;
         if (st && st->live && st->next == i0) {
             lob = st->lob;
             h1 = st->h1;
             r0 = st->r0;
             r1 = st->r1;
+            g0 = st->g0;
+            mulg = st->mulg;
         } else {
             const uint32_t ir = i0 - div32(i0, r.divmp) * r.maxpow; // i %= maxpow
-            const uint32_t h = div32(ir, r.fdivg);
+            uint32_t h = div32(ir, r.fdivg);
             lob = ir - h * G;
-            h1 = h + 1 == r.himod ? 0u : h + 1;
-            r0 = hi_record(h, r);
-            r1 = hi_record(h1, r);
+            r0 = hi_record(h, r, g0, mulg);
+            h1 = h;
+            r1 = r0;
+            hi_advance(h1, r1, g0, mulg, r);
         }
+        // Rows up to the next multiple of 32 past cnt stay inside the tile
+        // (tp is a multiple of 32), so every step stores unconditionally.
+        const uint32_t stride = 32 * row;
+        uint32_t addr = col + lane * row;
         const uint32_t steps = (cnt + 31) >> 5;
-        for (uint32_t s = 0; s < steps; ++s) {
-            const uint32_t p = (s << 5) + lane;
-            uint32_t lo = lob + lane;
-            const bool up = lo >= G;
-            lo = up ? lo - G : lo;
-            const uint32_t acc =
-                __ldg(r.ftable + lo) * (up ? r1.mul : r0.mul) + (up ? r1.acc : r0.acc);
-            const uint32_t x = frac_div_magic(acc, up ? r1.scale : r0.scale, up ? r1.mlo : r0.mlo,
-                                              up ? r1.mhi : r0.mhi);
-            if (p < cnt)
-                tile[off + p * ld] = U32OUT ? x : map_bits(x);
-            lob += 32;
-            if (lob >= G) { // warp-uniform
+        for (uint32_t s = 0; s < steps;) {
+            // steps whose 32 indices all lie in h's block: one record
+            const uint32_t nf = min(steps - s, (G - lob) >> 5);
+            const uint32_t* tab = r.ftable + lob + lane;
+            for (uint32_t e = 0; e < nf; ++e) {
+                const uint32_t acc = __ldg(tab) * r0.mul + r0.acc;
+                const uint32_t x = frac_div_magic(acc, r0.scale, r0.mlo, r0.mhi);
+                sts32(addr, U32OUT ? x : map_bits(x));
+                addr += stride;
+                tab += 32;
+            }
+            lob += nf << 5;
+            s += nf;
+            if (lob < G && s < steps) { // the step crossing into h+1's block
+                uint32_t lo = lob + lane;
+                const bool up = lo >= G;
+                lo = up ? lo - G : lo;
+                const uint32_t acc =
+                    __ldg(r.ftable + lo) * (up ? r1.mul : r0.mul) + (up ? r1.acc : r0.acc);
+                const uint32_t x = frac_div_magic(acc, up ? r1.scale : r0.scale,
+                                                  up ? r1.mlo : r0.mlo, up ? r1.mhi : r0.mhi);
+                sts32(addr, U32OUT ? x : map_bits(x));
+                addr += stride;
+                lob += 32;
+                ++s;
+            }
+            if (lob >= G) {
                 lob -= G;
-                h1 = h1 + 1 == r.himod ? 0u : h1 + 1;
                 r0 = r1;
-                r1 = hi_record(h1, r);
+                hi_advance(h1, r1, g0, mulg, r);
             }
         }
         if (st && lane == 0) {
@@ -697,12 +725,14 @@ __device__ __forceinline__ void halton_run(const RadicalDim& r, uint32_t i0, uin
             st->h1 = h1;
             st->r0 = r0;
             st->r1 = r1;
+            st->g0 = g0;
+            st->mulg = mulg;
             st->live = 1;
         }
     } else {
         for (uint32_t p = lane; p < cnt; p += 32) {
             const uint32_t x = radical_fixed(i0 + p, r);
-            tile[off + p * ld] = U32OUT ? x : map_bits(x);
+            sts32(col + p * row, U32OUT ? x : map_bits(x));
         }
     }
 }
@@ -712,17 +742,20 @@ __device__ __forceinline__ void halton_run(const RadicalDim& r, uint32_t i0, uin
 // (dimension, run of consecutive points) item at a time into a padded
 // [tp][dims+1] shared tile (one base per warp -> uniform digit loops and
 // records, halton_run), then the whole tile — tp*dims consecutive output
-// words — is written out coalesced. With one run per dimension the same warp
-// owns a dimension in every tile, so its incremental state carries over from
-// tile to tile (HaltonState, after the tile in shared memory).
+// words — is written out coalesced (16-B stores when `vec4`). With one run
+// per dimension the same warp owns a dimension in every tile, so its
+// incremental state carries over from tile to tile (HaltonState, after the
+// tile in shared memory).
 template <bool U32OUT>
 __global__ void __launch_bounds__(kBlock)
     k_halton_tiled(const RadicalDim* __restrict__ rd, uint32_t dims, Div32 div_dims, uint32_t tp,
-                   uint64_t first, uint64_t n, uint64_t ntiles, uint32_t* __restrict__ out)
+                   uint64_t first, uint64_t n, uint64_t ntiles, bool vec4,
+                   uint32_t* __restrict__ out)
 {
     extern __shared__ __align__(16) uint32_t tile[];
     const uint32_t ld = dims + 1;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, nwarps = blockDim.x >> 5;
+    const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(tile));
     // (dim, point run) work items: several warps share a dimension when
     // dims < warps per CTA (no carried state then)
     const bool carry = dims >= nwarps; // launch_halton sizes the state slots alike
@@ -745,12 +778,47 @@ __global__ void __launch_bounds__(kBlock)
             const uint32_t pe = min(cnt, pb + chunk);
             if (pb < pe)
                 halton_run<U32OUT>(rd[j], static_cast<uint32_t>(first + p0 + pb), pe - pb, lane,
-                                   tile, pb * ld + j, ld, states ? states + j : nullptr);
+                                   sbase + (pb * ld + j) * 4, ld, states ? states + j : nullptr);
         }
         __syncthreads();
         uint32_t* o = out + p0 * dims;
         const uint32_t words = cnt * dims;
-        for (uint32_t e = threadIdx.x; e < words; e += blockDim.x) {
+        uint32_t e0 = 0;
+        if (vec4 && (dims & 3) == 0) {
+            // 16-B stores of row-aligned quads: (row, col) advance by a fixed
+            // step per iteration, no division
+            e0 = words;
+            const uint32_t stride = blockDim.x * 4;
+            const uint32_t pstep = stride / dims, cstep = stride - pstep * dims;
+            uint32_t e = threadIdx.x * 4;
+            uint32_t p = e / dims, c = e - p * dims;
+            for (; e < words; e += stride) {
+                const uint32_t* src = tile + p * ld + c;
+                __stcs(reinterpret_cast<uint4*>(o + e), make_uint4(src[0], src[1], src[2], src[3]));
+                p += pstep;
+                c += cstep;
+                if (c >= dims) {
+                    c -= dims;
+                    ++p;
+                }
+            }
+        } else if (vec4) { // o is 16-B aligned (p0 * dims * 4 is a multiple of 128)
+            e0 = words & ~3u;
+            for (uint32_t e = threadIdx.x * 4; e < e0; e += blockDim.x * 4) {
+                uint32_t p = point_of(e, dims, div_dims), c = e - p * dims;
+                uint32_t v[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    v[k] = tile[p * ld + c];
+                    if (++c == dims) {
+                        c = 0;
+                        ++p;
+                    }
+                }
+                __stcs(reinterpret_cast<uint4*>(o + e), make_uint4(v[0], v[1], v[2], v[3]));
+            }
+        }
+        for (uint32_t e = e0 + threadIdx.x; e < words; e += blockDim.x) {
             const uint32_t p = point_of(e, dims, div_dims);
             o[e] = tile[p * ld + (e - p * dims)];
         }
@@ -1069,9 +1137,9 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
 {
     if (r.n == 0)
         return cudaSuccess;
-    // tile of tp points x (dims + 1) padded words: <= 32 KB, >= 32 points;
+    // tile of tp points x (dims + 1) padded words: <= 64 KB, >= 32 points;
     // then 64 B of carried state per dimension when dims >= warps per CTA
-    uint32_t tp = (8192u / (dims + 1)) & ~31u;
+    uint32_t tp = (16384u / (dims + 1)) & ~31u;
     if (tp < 32)
         tp = 32;
     const size_t tile_words = (static_cast<size_t>(tp) * (dims + 1) + 15) & ~size_t(15);
@@ -1091,8 +1159,9 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
     const uint64_t cap = static_cast<uint64_t>(sm_count()) * per_sm;
     const unsigned grid = static_cast<unsigned>(ntiles < cap ? ntiles : cap);
     const Div32 dd = dims >= 2 ? make_div32(dims) : Div32{0, 0};
+    const bool vec4 = (reinterpret_cast<uintptr_t>(r.out) & 15) == 0;
     kern<<<grid, kBlock, smem, s>>>(static_cast<const RadicalDim*>(rd), dims, dd, tp, r.first,
-                                    r.n, ntiles, static_cast<uint32_t*>(r.out));
+                                    r.n, ntiles, vec4, static_cast<uint32_t*>(r.out));
     return cudaGetLastError();
 }
 
