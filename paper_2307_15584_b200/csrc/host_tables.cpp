@@ -341,14 +341,17 @@ std::vector<RadicalDim> radical_dims(uint32_t dims, uint32_t first_prime, qmc_ra
         }
         r.ftable = nullptr;
         r.magic = nullptr;
-        r.fgroup = r.fdigits = r.himod = 0;
+        r.gdigits = r.fgroup = r.fdigits = r.himod = 0;
         r.fdivg = Div32{0, 0};
         if (b > 2) {
+            r.magic = pow_magic(b);
             const DigitTable t = digit_table(b, r.mode, r.factor);
             if (t.ptr) {
                 r.table = t.ptr;
                 r.group = t.group;
                 r.divg = make_div32(t.group);
+                for (uint32_t g = t.group; g > 1; g /= b)
+                    ++r.gdigits;
             }
             const DigitTable f = digit_table(b, r.mode, r.factor, 1, kFillTableMax);
             if (f.ptr) {
@@ -358,7 +361,6 @@ std::vector<RadicalDim> radical_dims(uint32_t dims, uint32_t first_prime, qmc_ra
                 for (uint32_t g = f.group; g > 1; g /= b)
                     ++r.fdigits;
                 r.himod = r.maxpow / f.group;
-                r.magic = pow_magic(b);
             }
         }
     }

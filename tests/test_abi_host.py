@@ -131,6 +131,34 @@ def test_div32_magic_host_emulation():
         np.testing.assert_array_equal(qq, n // np.uint64(d))
 
 
+def test_frac_div_magic_host_emulation():
+    """device.cuh frac_div_magic: floor(acc * 2^32 / scale) from
+    m = floor(2^64 / scale) (pow_magic) with one 64-bit check, emulated with
+    Python integers for every divisor family the kernels use: b^D for the
+    first 1000 primes (all D with b^D < 2^32), acc at the edges and random."""
+    rng = np.random.default_rng(1)
+    scales = set()
+    for k in range(0, 1000, 3):
+        b, p = q.prime(k), q.prime(k)
+        while p < (1 << 32):
+            scales.add(p)
+            p *= b
+    scales.discard(2)
+    scales = sorted(s for s in scales if s & 1)  # base 2 never divides (brev path)
+    checked = 0
+    for s in scales:
+        m = ((1 << 64) - 1) // s
+        mlo, mhi = m & 0xFFFFFFFF, m >> 32
+        accs = {0, 1, s - 1, s // 2, (s - 1) // 3} | {int(a) for a in rng.integers(0, s, 12)}
+        for acc in accs:
+            qe = (acc * mhi + ((acc * mlo) >> 32)) & 0xFFFFFFFF
+            if (qe + 1) * s <= acc << 32:
+                qe += 1
+            assert qe == (acc << 32) // s, (acc, s)
+            checked += 1
+    assert checked > 5000
+
+
 GV_CASES = ["1\n3\n5\n", "# header\n1 # first\n\n1276675999\n", "7", "1\n4\n", "1\n4294967297\n",
             "# only comments\n\n", "1\n  3  \n"]
 FACTOR_CASES = ["3 2\n5 3\n", "# c\n7 6\n\n", "2 1\n", "3\n", "3 0\n", "3 3\n", "1 0\n",
