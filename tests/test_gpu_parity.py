@@ -713,6 +713,33 @@ def test_fills_write_exactly_their_range(dims):
             assert _canaries_intact(buf), (dims, first, n)
 
 
+@pytest.mark.parametrize("shift", [1, 2, 3])
+def test_fills_misaligned_outputs(shift):
+    """Outputs 4, 8 or 12 bytes off a 16-B boundary take the scalar store paths
+    (no v4/v8 stores): same values as the aligned fill, canaries intact."""
+    cases = [
+        (8, lambda n, d, o: q.sobol_fill(n, d, first=77, fixed=True, out=o)),
+        (32, lambda n, d, o: q.sobol_fill(n, d, scramble="owen", words=list(range(d)), fixed=True,
+                                          out=o)),
+        (16, lambda n, d, o: q.lattice_fill(n, q.lfsr_generator_vector(0xACE1, d), first=5,
+                                            shifts=list(range(d)), fixed=True, out=o)),
+        (32, lambda n, d, o: q.halton_fill(n, d, first=1000, scramble="linear", fixed=True, out=o)),
+        (12, lambda n, d, o: q.halton_fill(n, d, first=3486784401 - 999, fixed=True, out=o)),
+        (1, lambda n, d, o: q.radical_inverse_fill(n, 5, first=12345, fixed=True, out=o)),
+    ]
+    n = 6001
+    for dims, call in cases:
+        ref_out = torch.empty(n * dims, dtype=torch.int32, device="cuda")
+        call(n, dims, ref_out)
+        buf = torch.full((n * dims + 2 * GUARD,), 0x5A5A5A5A, dtype=torch.int32, device="cuda")
+        mid = buf[GUARD + shift: GUARD + shift + n * dims]
+        call(n, dims, mid)
+        torch.cuda.synchronize()
+        assert torch.equal(mid, ref_out), dims
+        head, tail = buf[:GUARD + shift], buf[GUARD + shift + n * dims:]
+        assert bool((head == 0x5A5A5A5A).all()) and bool((tail == 0x5A5A5A5A).all()), dims
+
+
 def test_render_and_streams_write_exactly_their_range():
     for kind in q.SAMPLER_KINDS:
         buf, mid = _guarded(23 * 37)
