@@ -1137,9 +1137,12 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
 {
     if (r.n == 0)
         return cudaSuccess;
-    // tile of tp points x (dims + 1) padded words: <= 64 KB, >= 32 points;
+    // tile of tp points x (dims + 1) padded words: <= 48 KB, >= 32 points;
     // then 64 B of carried state per dimension when dims >= warps per CTA
-    uint32_t tp = (16384u / (dims + 1)) & ~31u;
+    // 48 KB tiles: 4 CTAs (32 warps) per SM; larger tiles amortise the
+    // per-(tile, dimension) bookkeeping better but lose more to latency
+    // (measured 8-32K words at 8-64 dims, tools/exp_halton.py)
+    uint32_t tp = (12288u / (dims + 1)) & ~31u;
     if (tp < 32)
         tp = 32;
     const size_t tile_words = (static_cast<size_t>(tp) * (dims + 1) + 15) & ~size_t(15);
