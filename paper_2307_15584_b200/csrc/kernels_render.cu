@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __rest
         sample2<KIND>(i, s, p, a, b, sob0, sob1);
         const double u = static_cast<double>(map_u32(a));
         const double v = static_cast<double>(map_u32(b));
-        const double f = scene_value(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
+        const double f = scene_value<true>(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
                                      __dmul_rn(__dadd_rn(fy, v), p.inv_h));
         if (ACCUM == 0)
             neumaier_add(sum, comp, f);
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kBlock) k_render_warp(RenderParams p, float* _
         sample2<KIND>(i, s, p, a, b, s0, s1);
         const double u = static_cast<double>(map_u32(a));
         const double v = static_cast<double>(map_u32(b));
-        const double f = scene_value(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
+        const double f = scene_value<true>(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
                                      __dmul_rn(__dadd_rn(fy, v), p.inv_h));
         if (ACCUM == 0)
             neumaier_add(sum, comp, f);
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(kBlock)
         sample2<KIND>(i, s, p, a, b, s0, s1);
         const double u = static_cast<double>(map_u32(a));
         const double v = static_cast<double>(map_u32(b));
-        const double f = scene_value(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
+        const double f = scene_value<true>(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
                                      __dmul_rn(__dadd_rn(fy, v), p.inv_h));
         isum += llround(__dmul_rn(f, 4294967296.0));
     }

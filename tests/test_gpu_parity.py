@@ -352,6 +352,33 @@ def test_scene_value_vs_reference(ref):
     assert err.max() <= 4e-15  # a few ulp of values in [0, 1.25]
 
 
+def test_sin_cw_matches_cuda_sin_bit_for_bit():
+    """device.cuh sin_cw (the render's sine: CUDA's reduction and polynomials
+    without the infinity / Payne-Hanek checks) equals CUDA's double sin on
+    every argument: scene_value through qmc_scene_value against the same
+    expression in torch float64 on the GPU (torch.sin is libdevice __nv_sin),
+    one rounded op per torch call like the kernel's explicit _rn intrinsics."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(7)
+    n = 1 << 22
+    xy = torch.rand((n, 2), dtype=torch.float64, device="cuda", generator=g)
+    xy[: n // 4] *= 2.0                                   # the render's range [0, 2)
+    xy[n // 4: n // 2] = (xy[n // 4: n // 2] - 0.5) * 2e6  # large |arg|, below 2^31
+    xy[-8:] = torch.tensor([[0.0, 0.25], [0.5, 1.0], [1.0 / 16, 3.0 / 16], [1e-300, -0.0],
+                            [-1.5, 2.0], [7.0, -7.0], [85.0, 85.4], [0.125, 0.375]],
+                           dtype=torch.float64)
+    got = q.scene_value(xy)
+    k = 25.132741228718345
+    x, y = xy[:, 0], xy[:, 1]
+    s = torch.sin(x * k) * torch.sin(y * k)
+    v = (s + 1.0) * 0.5
+    dx, dy = x - 0.5, y - 0.5
+    inside = (dx * dx + dy * dy) < (0.3 * 0.3)
+    exp = torch.where(inside, v + 0.25, v)
+    bad = (got != exp).sum().item()
+    assert bad == 0, bad
+
+
 # ------------------------------------------------ full-size properties
 @pytest.mark.slow
 def test_c2_full_size_properties(oracle, columns64):
