@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstring>
 
 #include <cuda_runtime.h>
 
@@ -30,7 +31,31 @@ struct FillRange {
 };
 
 // Render parameters resolved on the host (render.cpp:83-106 defaults).
+// Constants of the render's sine (device.cuh sin_cw) and integrand, carried
+// in the kernel parameters so the per-sample loop reads them from the
+// constant bank instead of rematerialising 64-bit immediates every sample.
+struct SinConsts {
+    double k8pi;                        // 8 * pi (render.hpp:24-27)
+    double two_over_pi;                 // 0x3fe45f306dc9c883
+    double pio2_hi, pio2_mid, pio2_lo;  // pi/2 in three parts, negated
+};
+
+__host__ __device__ inline double bits_to_double(uint64_t b)
+{
+    double d;
+    memcpy(&d, &b, 8);
+    return d;
+}
+
+__host__ __device__ inline SinConsts make_sin_consts()
+{
+    return {25.132741228718345, bits_to_double(0x3fe45f306dc9c883ull),
+            -bits_to_double(0x3ff921fb54442d18ull), -bits_to_double(0x3c91a62633145c00ull),
+            -bits_to_double(0x397b839a252049c0ull)};
+}
+
 struct RenderParams {
+    SinConsts sc;
     uint32_t width, height, spp, order;
     uint32_t row_begin, row_end;
     double inv_w, inv_h;

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __rest
         const double u = static_cast<double>(map_u32(a));
         const double v = static_cast<double>(map_u32(b));
         const double f = scene_value<true>(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
-                                     __dmul_rn(__dadd_rn(fy, v), p.inv_h));
+                                           __dmul_rn(__dadd_rn(fy, v), p.inv_h), p.sc);
         if (ACCUM == 0)
             neumaier_add(sum, comp, f);
         else
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kBlock) k_render_warp(RenderParams p, float* _
         const double u = static_cast<double>(map_u32(a));
         const double v = static_cast<double>(map_u32(b));
         const double f = scene_value<true>(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
-                                     __dmul_rn(__dadd_rn(fy, v), p.inv_h));
+                                           __dmul_rn(__dadd_rn(fy, v), p.inv_h), p.sc);
         if (ACCUM == 0)
             neumaier_add(sum, comp, f);
         else
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kBlock)
         const double u = static_cast<double>(map_u32(a));
         const double v = static_cast<double>(map_u32(b));
         const double f = scene_value<true>(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
-                                     __dmul_rn(__dadd_rn(fy, v), p.inv_h));
+                                           __dmul_rn(__dadd_rn(fy, v), p.inv_h), p.sc);
         isum += llround(__dmul_rn(f, 4294967296.0));
     }
     acc[q] = isum;
