@@ -112,6 +112,7 @@ struct IntegrateParams {
     const uint32_t* colsT; // sobol: device [52][mdims]
     uint32_t mdims;
     const uint32_t* words; // sobol: device XOR scrambles or null
+    SinConsts sc;          // product-sine's sine (sin_cw)
 };
 
 // ------------------------------------------------------------ launchers

@@ -35,12 +35,12 @@ __device__ __forceinline__ uint64_t digit_reverse3(uint64_t v, uint32_t digits)
 // One integrand factor (quality.cpp:35-63). Returns false for the
 // indicator's early exit.
 template <uint32_t FN>
-__device__ __forceinline__ bool factor(float xs, double& v)
+__device__ __forceinline__ bool factor(float xs, double& v, const SinConsts& sc)
 {
     const double x = static_cast<double>(xs);
-    if (FN == 0) { // product-sine: v *= (0.5*pi) * sin(pi * x)
+    if (FN == 0) { // product-sine: v *= (0.5*pi) * sin(pi * x); pi*x in [0, pi)
         const double pi = 3.141592653589793;
-        v = __dmul_rn(v, __dmul_rn(1.5707963267948966, sin(__dmul_rn(pi, x))));
+        v = __dmul_rn(v, __dmul_rn(1.5707963267948966, sin_cw(__dmul_rn(pi, x), sc)));
     } else if (FN == 1) { // product-poly: v *= (3.0 * x) * x
         v = __dmul_rn(v, __dmul_rn(__dmul_rn(3.0, x), x));
     } else { // indicator: [x < 0.7]
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kBlock)
                     x = __ldg(q.xor_points + static_cast<uint64_t>(k) * q.xor_dims + j) ^
                         __ldg(q.xor_scramble + cell * q.xor_dims + j);
                 }
-                alive = factor<FN>(map_u32(x), v);
+                alive = factor<FN>(map_u32(x), v, p.sc);
             }
             if (FN == 2)
                 v = alive ? 1.0 : 0.0;
