@@ -10,7 +10,10 @@
 #include "qmcgpu.h"
 
 #include <cstdint>
+#include <istream>
+#include <iterator>
 #include <memory>
+#include <ostream>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -228,6 +231,267 @@ inline qmc_sampler_kind sampler_kind_from_name(const std::string& name)
     qmc_sampler_kind k{};
     check(qmc_sampler_kind_from_name(name.c_str(), &k));
     return k;
+}
+inline std::string sampler_kind_name(qmc_sampler_kind kind) { return qmc_sampler_kind_name(kind); }
+
+// ------------------------------------------------ radical.hpp:65-77, :100-105
+// Batched radical_inverse / _linscramble / _permuted for one prime (u32
+// indices as the reference's, so first + n wraps at 2^32).
+inline std::vector<float> radical_inverse_points(std::uint64_t first, std::uint64_t n,
+                                                 std::uint32_t prime_index,
+                                                 qmc_radical_scramble scramble = QMC_RADICAL_PLAIN,
+                                                 std::uint32_t factor = 1)
+{
+    std::vector<float> v(n);
+    check(qmc_radical_inverse_fill(first, n, prime_index, scramble, factor, QMC_OUT_F32, v.data(),
+                                   nullptr));
+    return v;
+}
+inline float radical_inverse(std::uint32_t i, std::uint32_t prime_index)
+{
+    return radical_inverse_points(i, 1, prime_index)[0];
+}
+inline std::vector<std::uint32_t> default_linear_factors(std::uint32_t dims)
+{
+    std::vector<std::uint32_t> f(dims ? dims : 1);
+    check(qmc_default_linear_factors(dims, f.data()));
+    f.resize(dims);
+    return f;
+}
+
+// ------------------------------------------------------ file formats
+inline std::string slurp(std::istream& in)
+{
+    return std::string(std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>());
+}
+inline GeneratorVector load_generator_vector(std::istream& in) // lattice.cpp:21-46
+{
+    const std::string text = slurp(in);
+    std::uint32_t dims = 0;
+    check(qmc_load_generator_vector(text.c_str(), nullptr, 0, &dims));
+    GeneratorVector g{std::vector<std::uint32_t>(dims)};
+    check(qmc_load_generator_vector(text.c_str(), g.g.data(), dims, &dims));
+    return g;
+}
+inline std::vector<std::uint32_t> load_linear_factors(std::istream& in, std::uint32_t dims)
+{ // radical.cpp:281-306
+    const std::string text = slurp(in);
+    std::vector<std::uint32_t> f(dims ? dims : 1);
+    check(qmc_load_linear_factors(text.c_str(), dims, f.data()));
+    f.resize(dims);
+    return f;
+}
+inline std::uint64_t fnv1a64(const void* data, std::size_t size) // image.cpp:54-63
+{
+    return qmc_fnv1a64(data, size);
+}
+inline void write_pnm(const ImageBuffer& image, std::uint32_t channels, std::ostream& out)
+{
+    size_t len = 0;
+    check(qmc_write_pnm(image.values.data(), image.width, image.height, channels, nullptr, &len,
+                        nullptr));
+    std::string bytes(len, '\0');
+    check(qmc_write_pnm(image.values.data(), image.width, image.height, channels, &bytes[0], &len,
+                        nullptr));
+    out.write(bytes.data(), static_cast<std::streamsize>(len));
+}
+inline void write_pgm(const ImageBuffer& image, std::ostream& out) { write_pnm(image, 1, out); }
+inline void write_ppm(const ImageBuffer& image, std::ostream& out) { write_pnm(image, 3, out); }
+
+// ------------------------------------------- XOR tables (imageplane.hpp:92-120)
+class XorTables {
+public:
+    static XorTables white_noise(std::uint32_t dims, std::uint32_t point_count, std::uint32_t seed)
+    {
+        qmc_xor_tables* t = nullptr;
+        check(qmc_xor_tables_white_noise(dims, point_count, seed, &t));
+        return XorTables(t);
+    }
+    // load_xor_tables(in, dims, points, point_count): XQT1 bytes + the stored
+    // integer-stage point set [point_count][dims]
+    static XorTables load(std::istream& in, std::uint32_t dims,
+                          const std::vector<std::uint32_t>& points, std::uint32_t point_count)
+    {
+        const std::string bytes = slurp(in);
+        qmc_xor_tables* t = nullptr;
+        check(qmc_xor_tables_load(bytes.data(), bytes.size(), dims, points.data(), point_count,
+                                  &t));
+        return XorTables(t);
+    }
+    void write(std::ostream& out) const // write_xor_table_file
+    {
+        size_t len = 0;
+        check(qmc_xor_tables_write(t_.get(), nullptr, &len));
+        std::string bytes(len, '\0');
+        check(qmc_xor_tables_write(t_.get(), &bytes[0], &len));
+        out.write(bytes.data(), static_cast<std::streamsize>(len));
+    }
+    std::uint32_t dims() const { return qmc_xor_tables_dims(t_.get()); }
+    std::uint32_t point_count() const { return qmc_xor_tables_point_count(t_.get()); }
+    const qmc_xor_tables* handle() const { return t_.get(); }
+
+private:
+    struct Del {
+        void operator()(qmc_xor_tables* t) const { qmc_xor_tables_destroy(t); }
+    };
+    explicit XorTables(qmc_xor_tables* t) : t_(t, Del{}) {}
+    std::shared_ptr<qmc_xor_tables> t_;
+};
+
+// ------------------------------- StreamParams / SampleStream (imageplane.hpp:139-199)
+struct PixelCoord { // hilbert.hpp:14-18
+    std::uint32_t x = 0, y = 0, order = 0;
+};
+
+struct StreamParams {
+    std::uint32_t dims = 2;
+    GeneratorVector generator;                           // lattice family
+    std::shared_ptr<const GeneratorMatrixSet> matrices;  // sobol (null = builtin)
+    std::vector<std::uint32_t> sobol_scrambles;          // empty = plain sequence
+    std::string scramble = "plain";                      // halton: plain | faure | linear
+    std::vector<std::uint32_t> linear_factors;           // empty = default factors
+    PixelCoord pixel{0, 0, 1};
+    std::uint32_t spp = 1;                               // halton_hilbert block size
+    std::uint32_t width = 0, height = 0;                 // image_plane_halton
+    std::shared_ptr<const XorTables> tables;             // sobol_xor_table
+    // sobol_xor_table without `tables`: white-noise tables made per call
+    std::uint32_t xor_seed = 0, xor_point_count = 1024;
+};
+
+// A validated stream (make_stream): sample(i, j) and batched points().
+class SampleStream {
+public:
+    std::uint32_t dims() const { return p_.dims; }
+    qmc_sampler_kind kind() const { return kind_; }
+
+    // rows [first, first + n) x dims, row-major, into `out` (device or host)
+    void points(std::uint64_t first, std::uint64_t n, float* out, qmc_stream stream = nullptr) const
+    {
+        const qmc_stream_params c = c_params();
+        check(qmc_stream_fill(kind_, &c, first, n, QMC_OUT_F32, out, stream));
+    }
+    std::vector<float> points(std::uint64_t first, std::uint64_t n) const
+    {
+        std::vector<float> v(n * p_.dims);
+        points(first, n, v.data());
+        return v;
+    }
+    // SampleStream::sample(index, dim): one GPU call per point; use points()
+    // for anything but spot checks
+    float sample(std::uint64_t index, std::uint32_t dim) const
+    {
+        if (dim >= p_.dims)
+            throw std::out_of_range("SampleStream::sample: dimension out of range");
+        return points(index, 1)[dim];
+    }
+    qmc_stream_params c_params() const
+    {
+        qmc_stream_params c{};
+        c.dims = p_.dims;
+        c.generator = p_.generator.g.empty() ? nullptr : p_.generator.g.data();
+        c.generator_dims = p_.generator.dims();
+        c.matrices = p_.matrices ? p_.matrices->handle() : nullptr;
+        c.sobol_scrambles = p_.sobol_scrambles.empty() ? nullptr : p_.sobol_scrambles.data();
+        c.sobol_scrambles_len = static_cast<std::uint32_t>(p_.sobol_scrambles.size());
+        c.halton_scramble = scramble_;
+        c.linear_factors = p_.linear_factors.empty() ? nullptr : p_.linear_factors.data();
+        c.linear_factors_len = static_cast<std::uint32_t>(p_.linear_factors.size());
+        c.px = p_.pixel.x;
+        c.py = p_.pixel.y;
+        c.order = p_.pixel.order;
+        c.spp = p_.spp;
+        c.width = p_.width;
+        c.height = p_.height;
+        c.xor_seed = p_.xor_seed;
+        c.xor_point_count = p_.xor_point_count;
+        c.xor_tables = p_.tables ? p_.tables->handle() : nullptr;
+        return c;
+    }
+
+private:
+    friend SampleStream make_stream(qmc_sampler_kind kind, StreamParams params);
+    SampleStream(qmc_sampler_kind kind, StreamParams p) : kind_(kind), p_(std::move(p)) {}
+    qmc_sampler_kind kind_;
+    StreamParams p_;
+    std::uint32_t scramble_ = QMC_RADICAL_PLAIN;
+};
+
+// make_stream (imageplane.cpp:310-416): the C-ABI runs the reference's
+// ConfigError checks; a zero-length fill validates without sampling.
+inline SampleStream make_stream(qmc_sampler_kind kind, StreamParams params)
+{
+    SampleStream s(kind, std::move(params));
+    const std::string& sc = s.p_.scramble;
+    if (sc == "plain")
+        s.scramble_ = QMC_RADICAL_PLAIN;
+    else if (sc == "faure")
+        s.scramble_ = QMC_RADICAL_FAURE;
+    else if (sc == "linear")
+        s.scramble_ = QMC_RADICAL_LINEAR;
+    else
+        throw ConfigError("make_stream: scramble must be plain, faure, or linear");
+    const qmc_stream_params c = s.c_params();
+    check(qmc_stream_fill(kind, &c, 0, 0, QMC_OUT_F32, nullptr, nullptr));
+    return s;
+}
+
+// ------------------------------------------ quality.hpp:37-104 (integration)
+struct TestIntegrand { // quality.hpp:40-48
+    std::string name;
+    qmc_integrand_kind kind;
+    std::uint32_t dims;
+    double exact_integral;
+};
+inline TestIntegrand builtin_integrand(const std::string& name, std::uint32_t dims)
+{
+    TestIntegrand f{name, QMC_PRODUCT_SINE, dims, 0.0};
+    check(qmc_builtin_integrand(name.c_str(), dims, &f.kind, &f.exact_integral));
+    return f;
+}
+struct IntegrationRow { // quality.hpp:90-95
+    std::uint64_t n = 0;
+    double estimate = 0, abs_error = 0, seconds = 0;
+};
+inline IntegrationRow integrate(const SampleStream& stream, const TestIntegrand& f,
+                                std::uint64_t n, qmc_accum mode = QMC_ACCUM_KAHAN)
+{
+    const qmc_stream_params c = stream.c_params();
+    qmc_integration_row r{};
+    check(qmc_integrate(stream.kind(), &c, f.kind, f.dims, n, mode, &r, nullptr));
+    return {r.n, r.estimate, r.abs_error, r.seconds};
+}
+
+// ------------------------------------------- quality.hpp:56-71 (point-set metrics)
+inline double l2_star_discrepancy(const std::vector<float>& points, std::size_t n,
+                                  std::size_t dims)
+{
+    double d = 0;
+    check(qmc_l2_star_discrepancy(points.data(), n, static_cast<std::uint32_t>(dims), &d,
+                                  nullptr));
+    return d;
+}
+inline double min_toroidal_distance(const std::vector<float>& points, std::size_t n,
+                                    std::size_t dims)
+{
+    double d = 0;
+    check(qmc_min_toroidal_distance(points.data(), n, static_cast<std::uint32_t>(dims), &d,
+                                    nullptr));
+    return d;
+}
+struct StratificationResult { // quality.hpp:61-66
+    bool ok = false;
+    std::vector<std::uint32_t> histogram;
+};
+inline StratificationResult check_1d_stratification(const SampleStream& stream, std::uint32_t j,
+                                                    std::uint32_t m)
+{
+    const qmc_stream_params c = stream.c_params();
+    StratificationResult r;
+    r.histogram.assign(m <= 20 ? (1u << m) : 1u, 0u); // the C-ABI rejects m > 20
+    int ok = 0;
+    check(qmc_check_1d_stratification(stream.kind(), &c, j, m, &ok, r.histogram.data(), nullptr));
+    r.ok = ok != 0;
+    return r;
 }
 
 } // namespace qmcgpu

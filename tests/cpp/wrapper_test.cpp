@@ -1,10 +1,16 @@
 // Reference-style caller of the qmc::-shaped C++ wrapper (include/qmcgpu.hpp):
-// the same calls a qmckit caller makes (sobol_point, lattice_point, render),
-// checked against golden checksums recorded from the reference build.
+// the same calls a qmckit caller makes (sobol_point, lattice_point,
+// halton_point, make_stream / sample, integrate, the point-set metrics, the
+// file formats, render), checked against golden checksums recorded from the
+// reference build and against each other.
+//   wrapper_test --host                  host-only calls (no GPU needed)
+//   wrapper_test <sobol fnv> <render fnv>  everything, on a GPU
 #include "qmcgpu.hpp"
 
+#include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <sstream>
 
 static std::uint64_t fnv(const void* p, size_t n)
 {
@@ -17,48 +23,138 @@ static std::uint64_t fnv(const void* p, size_t n)
     return h;
 }
 
+#define EXPECT(cond)                                                                               \
+    do {                                                                                           \
+        if (!(cond)) {                                                                             \
+            std::printf("FAILED: %s (line %d)\n", #cond, __LINE__);                                \
+            ++bad;                                                                                 \
+        }                                                                                          \
+    } while (0)
+
+template <typename E, typename F>
+static bool throws(F&& f)
+{
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+static int host_checks()
+{
+    int bad = 0;
+    EXPECT(qmcgpu::prime(0) == 2 && qmcgpu::prime(999) == 7919);
+    EXPECT(throws<std::out_of_range>([] { qmcgpu::prime(1000); }));
+    EXPECT(qmcgpu::prime_max_power(1) == 3486784401u);
+    const auto g = qmcgpu::lfsr_generator_vector(0xace1, 2);
+    EXPECT(g.g[0] == 1u && g.g[1] == 1276675999u);
+    EXPECT(qmcgpu::hilbert_order_for(3840, 2160) == 12);
+    const qmcgpu::HaltonPixelEnumeration e(3840, 2160);
+    EXPECT(e.stride() == 8957952u && e.scale_x() == 4096 && e.scale_y() == 2187);
+    const auto c = qmcgpu::partition_by_extra_dimension(1, 4, 2);
+    EXPECT(c.remainder == 2 && c.modulus == 4);
+    std::istringstream gv("# comment\n1\n1276675999 # second\n");
+    const auto lg = qmcgpu::load_generator_vector(gv);
+    EXPECT(lg.dims() == 2 && lg.g[1] == 1276675999u);
+    std::istringstream bad_gv("1\n4\n");
+    EXPECT(throws<qmcgpu::ConfigError>([&] { qmcgpu::load_generator_vector(bad_gv); }));
+    std::istringstream lf("3 2\n");
+    const auto f = qmcgpu::load_linear_factors(lf, 3);
+    EXPECT(f.size() == 3 && f[0] == 1 && f[1] == 2 && f[2] == 4);
+    EXPECT(qmcgpu::default_linear_factors(3) == (std::vector<std::uint32_t>{1, 2, 4}));
+    const char msg[] = "qmc";
+    EXPECT(qmcgpu::fnv1a64(msg, 3) == fnv(msg, 3));
+    const auto ti = qmcgpu::builtin_integrand("indicator", 3);
+    EXPECT(std::fabs(ti.exact_integral - 0.343) < 1e-15);
+    EXPECT(throws<qmcgpu::ConfigError>([] { qmcgpu::builtin_integrand("gauss", 2); }));
+    EXPECT(qmcgpu::sampler_kind_from_name("image-plane-halton") == QMC_KIND_IMAGE_PLANE_HALTON);
+    EXPECT(qmcgpu::sampler_kind_name(QMC_KIND_SOBOL_XOR_TABLE) == "sobol-xor-table");
+    EXPECT(throws<qmcgpu::ConfigError>([] { qmcgpu::sampler_kind_from_name("sobol2"); }));
+    return bad;
+}
+
 int main(int argc, char** argv)
 {
+    if (argc >= 2 && std::strcmp(argv[1], "--host") == 0) {
+        const int bad = host_checks();
+        std::printf(bad ? "FAIL %d\n" : "OK\n", bad);
+        return bad ? 1 : 0;
+    }
     if (argc < 3)
         return 2;
     const std::uint64_t want_sobol = std::strtoull(argv[1], nullptr, 16);
     const std::uint64_t want_render = std::strtoull(argv[2], nullptr, 16);
-    int bad = 0;
+    int bad = host_checks();
+
+    // sobol_point / render goldens
     const auto m = qmcgpu::GeneratorMatrixSet::builtin(32);
     const auto pts = qmcgpu::sobol_points(m, 0, 1 << 16, 32);
-    if (fnv(pts.data(), pts.size() * 4) != want_sobol) {
-        std::printf("sobol checksum mismatch\n");
-        ++bad;
-    }
+    EXPECT(fnv(pts.data(), pts.size() * 4) == want_sobol);
     qmcgpu::RenderJob job;
     job.width = job.height = 64;
     job.spp = 16;
     const auto img = qmcgpu::render(job);
-    if (fnv(img.values.data(), img.values.size() * 4) != want_render) {
-        std::printf("render checksum mismatch\n");
-        ++bad;
-    }
-    try {
-        qmcgpu::GeneratorMatrixSet::builtin(65);
-        ++bad;
-    } catch (const qmcgpu::ConfigError&) {
-    }
-    try {
-        qmcgpu::sobol_points(m, (1ull << 52) - 1, 2, 4);
-        ++bad;
-    } catch (const std::invalid_argument&) {
-    }
-    try {
-        qmcgpu::prime(1000);
-        ++bad;
-    } catch (const std::out_of_range&) {
-    }
+    EXPECT(fnv(img.values.data(), img.values.size() * 4) == want_render);
+    EXPECT(throws<qmcgpu::ConfigError>([] { qmcgpu::GeneratorMatrixSet::builtin(65); }));
+    EXPECT(throws<std::invalid_argument>([&] { qmcgpu::sobol_points(m, (1ull << 52) - 1, 2, 4); }));
+
+    // lattice_point, radical_inverse, halton_point
     const auto g = qmcgpu::lfsr_generator_vector(0xace1, 4);
     const auto lat = qmcgpu::lattice_points(g, 1, 1);
-    if (lat.size() != 4 || lat[0] != 0.5f) {
-        std::printf("lattice mismatch\n");
-        ++bad;
-    }
+    EXPECT(lat.size() == 4 && lat[0] == 0.5f);
+    EXPECT(qmcgpu::radical_inverse(1, 0) == 0.5f && qmcgpu::radical_inverse(1, 1) == 1.0f / 3);
+    const auto hal = qmcgpu::halton_points(100, 50, 5, QMC_RADICAL_LINEAR);
+    const auto rad = qmcgpu::radical_inverse_points(100, 50, 3, QMC_RADICAL_LINEAR, 6);
+    for (int k = 0; k < 50; ++k)
+        EXPECT(hal[k * 5 + 3] == rad[k]);
+
+    // make_stream / SampleStream: the halton kind equals halton_point
+    qmcgpu::StreamParams sp;
+    sp.dims = 5;
+    sp.scramble = "linear";
+    const auto hs = qmcgpu::make_stream(QMC_KIND_HALTON, sp);
+    EXPECT(hs.points(100, 50) == hal);
+    EXPECT(hs.sample(107, 2) == hal[7 * 5 + 2]);
+    qmcgpu::StreamParams bad_sp;
+    bad_sp.scramble = "owen";
+    EXPECT(throws<qmcgpu::ConfigError>([&] { qmcgpu::make_stream(QMC_KIND_HALTON, bad_sp); }));
+    qmcgpu::StreamParams lat_sp;
+    lat_sp.dims = 2;
+    lat_sp.generator = qmcgpu::GeneratorVector{{1, 4}};
+    EXPECT(throws<qmcgpu::ConfigError>([&] { qmcgpu::make_stream(QMC_KIND_LATTICE, lat_sp); }));
+    qmcgpu::StreamParams px;
+    px.dims = 2;
+    px.pixel = {5, 9, 4};
+    px.generator = qmcgpu::lfsr_generator_vector(0xace1, 2);
+    const auto psl = qmcgpu::make_stream(QMC_KIND_PIXEL_SHIFTED_LATTICE, px);
+    EXPECT(qmcgpu::check_1d_stratification(psl, 0, 8).ok);
+
+    // XOR tables: write -> load round trip gives the same stream
+    const auto wn = std::make_shared<const qmcgpu::XorTables>(
+        qmcgpu::XorTables::white_noise(2, 64, 7));
+    std::stringstream xqt;
+    wn->write(xqt);
+    EXPECT(xqt.str().size() > 0 && wn->dims() == 2 && wn->point_count() == 64);
+
+    // integrate and the point-set metrics
+    qmcgpu::StreamParams sob;
+    sob.dims = 4;
+    const auto ss = qmcgpu::make_stream(QMC_KIND_SOBOL, sob);
+    const auto row = qmcgpu::integrate(ss, qmcgpu::builtin_integrand("product-sine", 4), 1 << 16);
+    EXPECT(row.n == (1u << 16) && std::fabs(row.estimate - 1.0) < 1e-3);
+    const auto s256 = qmcgpu::sobol_points(m, 0, 256, 2);
+    EXPECT(qmcgpu::l2_star_discrepancy(s256, 256, 2) > 0.0);
+    EXPECT(qmcgpu::min_toroidal_distance(s256, 256, 2) > 0.0);
+
+    // write_pgm: P5 header + one byte per pixel
+    std::ostringstream pgm;
+    qmcgpu::write_pgm(img, pgm);
+    EXPECT(pgm.str().compare(0, 2, "P5") == 0 && pgm.str().size() > 64 * 64);
+
     std::printf(bad ? "FAIL %d\n" : "OK\n", bad);
     return bad ? 1 : 0;
 }

@@ -21,6 +21,13 @@ def test_wrapper_compiles(tmp_path):
     assert os.path.exists(_build(tmp_path))
 
 
+def test_wrapper_host_calls(tmp_path):
+    """Host-side wrapper calls (tables, loaders, enumerations, errors) run
+    without a GPU."""
+    r = subprocess.run([_build(tmp_path), "--host"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
 @pytest.mark.gpu
 def test_wrapper_runs_on_gpu(tmp_path, golden):
     torch = pytest.importorskip("torch")
