@@ -43,6 +43,75 @@ __device__ __forceinline__ uint32_t point_of(uint32_t e, uint32_t dims, const Di
     return dims == 1 ? e : div32(e, d);
 }
 
+// Block-wide copy of rows [r0, r0 + rows) of a padded shared tile (row
+// stride ld >= dims words) to the consecutive global words o[0, rows*dims).
+// Each thread walks its (row, col) position by a fixed stride (no division
+// per word) and writes one 16-B streaming store per step. With dims % 4 == 0
+// and o 16-B aligned, quads never straddle a row; otherwise scalar stores run
+// up to the first 16-B boundary of o, the quads check the row wrap per word,
+// and the tail is scalar.
+__device__ __noinline__ void tile_store_rows_any(const uint32_t* src, uint32_t ld, uint32_t dims,
+                                                 Div32 div_dims, uint32_t words, uint32_t* o)
+{
+    const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(o) & 15u);
+    const uint32_t head = min(words, (mis & 3u) ? words : ((16u - mis) & 15u) >> 2);
+    const uint32_t quads = (words - head) >> 2;
+    const uint32_t adv = blockDim.x * 4 - 4; // end of one quad -> start of the thread's next
+    const uint32_t padv = adv / dims, cadv = adv - padv * dims;
+    const uint32_t e = head + threadIdx.x * 4;
+    uint32_t p = point_of(e, dims, div_dims), c = e - p * dims;
+    for (uint32_t qd = threadIdx.x; qd < quads; qd += blockDim.x) {
+        uint32_t v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            v[k] = src[p * ld + c];
+            if (++c == dims) {
+                c = 0;
+                ++p;
+            }
+        }
+        __stcs(reinterpret_cast<uint4*>(o + head + qd * 4), make_uint4(v[0], v[1], v[2], v[3]));
+        p += padv;
+        c += cadv;
+        if (c >= dims) {
+            c -= dims;
+            ++p;
+        }
+    }
+    const uint32_t tail0 = head + quads * 4; // head and tail: < 4 + 4 words
+    for (uint32_t w = threadIdx.x; w < head + (words - tail0); w += blockDim.x) {
+        const uint32_t ew = w < head ? w : tail0 + (w - head);
+        const uint32_t pw = point_of(ew, dims, div_dims);
+        o[ew] = src[pw * ld + (ew - pw * dims)];
+    }
+}
+
+__device__ __forceinline__ void tile_store_rows(const uint32_t* tile, uint32_t ld, uint32_t dims,
+                                                const Div32& div_dims, uint32_t r0, uint32_t rows,
+                                                uint32_t* o)
+{
+    const uint32_t words = rows * dims;
+    const uint32_t* src = tile + r0 * ld;
+    if ((dims & 3u) != 0 || (reinterpret_cast<uintptr_t>(o) & 15u) != 0) {
+        tile_store_rows_any(src, ld, dims, div_dims, words, o);
+        return;
+    }
+    const uint32_t stride = blockDim.x * 4;
+    const uint32_t pstep = stride / dims, cstep = stride - pstep * dims;
+    uint32_t e = threadIdx.x * 4;
+    uint32_t p = point_of(e, dims, div_dims), c = e - p * dims;
+    for (; e < words; e += stride) {
+        const uint32_t* s4 = src + p * ld + c;
+        __stcs(reinterpret_cast<uint4*>(o + e), make_uint4(s4[0], s4[1], s4[2], s4[3]));
+        p += pstep;
+        c += cstep;
+        if (c >= dims) {
+            c -= dims;
+            ++p;
+        }
+    }
+}
+
 // Warp tiles [t, tend) owned by the calling warp: contiguous runs, so the
 // tile-to-tile update is incremental.
 __device__ __forceinline__ bool warp_tiles(uint64_t tile0, uint64_t ntiles, uint64_t per_warp,
@@ -318,13 +387,8 @@ __global__ void __launch_bounds__(kBlock)
         // rows [lo, hi) of the tile that belong to [first, first + n)
         const uint64_t lo = p0 > first ? p0 : first;
         const uint64_t hi = (p0 + tp < first + n) ? p0 + tp : first + n;
-        const uint32_t r0 = static_cast<uint32_t>(lo - p0);
-        const uint32_t words_out = static_cast<uint32_t>(hi - lo) * dims;
-        uint32_t* o = out + (lo - first) * dims;
-        for (uint32_t e = threadIdx.x; e < words_out; e += blockDim.x) {
-            const uint32_t pr = point_of(e, dims, div_dims);
-            o[e] = tile[(r0 + pr) * ld + (e - pr * dims)];
-        }
+        tile_store_rows(tile, ld, dims, div_dims, static_cast<uint32_t>(lo - p0),
+                        static_cast<uint32_t>(hi - lo), out + (lo - first) * dims);
         __syncthreads();
     }
 }
@@ -742,15 +806,14 @@ __device__ __forceinline__ void halton_run(const RadicalDim& r, uint32_t i0, uin
 // (dimension, run of consecutive points) item at a time into a padded
 // [tp][dims+1] shared tile (one base per warp -> uniform digit loops and
 // records, halton_run), then the whole tile — tp*dims consecutive output
-// words — is written out coalesced (16-B stores when `vec4`). With one run
+// words — is written out coalesced (tile_store_rows). With one run
 // per dimension the same warp owns a dimension in every tile, so its
 // incremental state carries over from tile to tile (HaltonState, after the
 // tile in shared memory).
 template <bool U32OUT>
 __global__ void __launch_bounds__(kBlock)
     k_halton_tiled(const RadicalDim* __restrict__ rd, uint32_t dims, Div32 div_dims, uint32_t tp,
-                   uint64_t first, uint64_t n, uint64_t ntiles, bool vec4,
-                   uint32_t* __restrict__ out)
+                   uint64_t first, uint64_t n, uint64_t ntiles, uint32_t* __restrict__ out)
 {
     extern __shared__ __align__(16) uint32_t tile[];
     const uint32_t ld = dims + 1;
@@ -781,47 +844,7 @@ __global__ void __launch_bounds__(kBlock)
                                    sbase + (pb * ld + j) * 4, ld, states ? states + j : nullptr);
         }
         __syncthreads();
-        uint32_t* o = out + p0 * dims;
-        const uint32_t words = cnt * dims;
-        uint32_t e0 = 0;
-        if (vec4 && (dims & 3) == 0) {
-            // 16-B stores of row-aligned quads: (row, col) advance by a fixed
-            // step per iteration, no division
-            e0 = words;
-            const uint32_t stride = blockDim.x * 4;
-            const uint32_t pstep = stride / dims, cstep = stride - pstep * dims;
-            uint32_t e = threadIdx.x * 4;
-            uint32_t p = e / dims, c = e - p * dims;
-            for (; e < words; e += stride) {
-                const uint32_t* src = tile + p * ld + c;
-                __stcs(reinterpret_cast<uint4*>(o + e), make_uint4(src[0], src[1], src[2], src[3]));
-                p += pstep;
-                c += cstep;
-                if (c >= dims) {
-                    c -= dims;
-                    ++p;
-                }
-            }
-        } else if (vec4) { // o is 16-B aligned (p0 * dims * 4 is a multiple of 128)
-            e0 = words & ~3u;
-            for (uint32_t e = threadIdx.x * 4; e < e0; e += blockDim.x * 4) {
-                uint32_t p = point_of(e, dims, div_dims), c = e - p * dims;
-                uint32_t v[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    v[k] = tile[p * ld + c];
-                    if (++c == dims) {
-                        c = 0;
-                        ++p;
-                    }
-                }
-                __stcs(reinterpret_cast<uint4*>(o + e), make_uint4(v[0], v[1], v[2], v[3]));
-            }
-        }
-        for (uint32_t e = e0 + threadIdx.x; e < words; e += blockDim.x) {
-            const uint32_t p = point_of(e, dims, div_dims);
-            o[e] = tile[p * ld + (e - p * dims)];
-        }
+        tile_store_rows(tile, ld, dims, div_dims, 0, cnt, out + p0 * dims);
         __syncthreads();
     }
 }
@@ -1162,9 +1185,8 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
     const uint64_t cap = static_cast<uint64_t>(sm_count()) * per_sm;
     const unsigned grid = static_cast<unsigned>(ntiles < cap ? ntiles : cap);
     const Div32 dd = dims >= 2 ? make_div32(dims) : Div32{0, 0};
-    const bool vec4 = (reinterpret_cast<uintptr_t>(r.out) & 15) == 0;
     kern<<<grid, kBlock, smem, s>>>(static_cast<const RadicalDim*>(rd), dims, dd, tp, r.first,
-                                    r.n, ntiles, vec4, static_cast<uint32_t*>(r.out));
+                                    r.n, ntiles, static_cast<uint32_t*>(r.out));
     return cudaGetLastError();
 }
 
