@@ -320,12 +320,14 @@ __global__ void __launch_bounds__(kBlock)
     }
 }
 
-// Any dims, shared-memory tiled: a CTA owns tiles of tp = 2^k consecutive
-// points; warp w computes dimensions w, w+8, ...: lane l holds points
-// p0 + l + 32 m, whose value is X(p0) ^ X(l) ^ X(32 m) (disjoint index bits).
-// X(32 m) for m < tp/32 is a per-CTA shared table T[j][m] built once, so the
-// m loop has no dependency chain (one LDS + XOR per sample). The padded
-// [tp][dims+1] tile is then written out as consecutive words.
+// Any dims, shared-memory tiled: a CTA owns a contiguous range of tiles of
+// tp = 2^k consecutive points; a warp computes one (dimension, run of m)
+// item at a time: lane l holds points p0 + l + 32 m, whose value is
+// X(p0) ^ X(l) ^ X(32 m) (disjoint index bits). X(32 m) for m < tp/32 is a
+// per-CTA shared table T[j][m] built once, so the m loop has no dependency
+// chain (one LDS + XOR per sample); X(p0) advances from tile to tile through
+// the index bits that change. The padded [tp][dims+1] tile is then written
+// out with tile_store_rows.
 template <int MODE, bool U32OUT>
 __global__ void __launch_bounds__(kBlock)
     k_sobol_tiled(const uint32_t* __restrict__ colsT, const __grid_constant__ SmallArgs args,
@@ -360,21 +362,42 @@ __global__ void __launch_bounds__(kBlock)
                 x ^= col(k, j);
         L[e] = x;
     }
-    for (uint64_t t = tile0 + blockIdx.x; t < tile0 + ntiles; t += gridDim.x) {
+    // a contiguous range of tiles per CTA: X(p0) advances incrementally
+    // (only the index bits that change between consecutive tiles), and
+    // several warps share a dimension when dims < warps per CTA
+    const uint64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+    const uint64_t tb = tile0 + blockIdx.x * per;
+    const uint64_t te = min(tile0 + ntiles, tb + per);
+    const uint32_t runs = dims >= nwarps ? 1u : nwarps / dims;
+    const uint32_t mchunk = (mt + runs - 1) / runs;
+    uint64_t prev = 0;
+    for (uint64_t t = tb; t < te; ++t) {
         const uint64_t p0 = t * tp; // absolute index of the tile's first point
-        __syncthreads(); // T/L ready (first tile), XP free (later tiles)
+        __syncthreads(); // T/L ready (first tile), XP and the tile free (later tiles)
         for (uint32_t j = threadIdx.x; j < dims; j += blockDim.x) {
-            uint32_t x = (MODE == 0 && words) ? words[j] : 0u;
-            for (uint64_t b = p0; b; b &= b - 1)
+            uint32_t x;
+            uint64_t b;
+            if (t == tb) {
+                x = (MODE == 0 && words) ? words[j] : 0u;
+                b = p0;
+            } else {
+                x = XP[j];
+                b = p0 ^ prev;
+            }
+            for (; b; b &= b - 1)
                 x ^= col(__ffsll(static_cast<long long>(b)) - 1, j);
             XP[j] = x;
         }
+        prev = p0;
         __syncthreads();
-        for (uint32_t j = warp; j < dims; j += nwarps) {
+        for (uint32_t item = warp; item < dims * runs; item += nwarps) {
+            const uint32_t j = runs == 1 ? item : item % dims;
+            const uint32_t mb = (runs == 1 ? 0u : item / dims) * mchunk;
+            const uint32_t me = min(mt, mb + mchunk);
             const uint32_t x = XP[j] ^ L[j * 32 + lane];
             const uint32_t seed = (MODE == 2 && words) ? words[j] : 0u;
             const uint32_t* Tj = T + j * mt;
-            for (uint32_t m = 0; m < mt; ++m) {
+            for (uint32_t m = mb; m < me; ++m) {
                 const uint64_t i = p0 + lane + 32ull * m;
                 uint32_t v = x ^ Tj[m];
                 if (MODE == 2)
