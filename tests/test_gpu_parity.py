@@ -379,6 +379,42 @@ def test_sin_cw_matches_cuda_sin_bit_for_bit():
     assert bad == 0, bad
 
 
+def test_concurrent_host_threads():
+    """The C-ABI is reentrant: 8 host threads on their own streams run fills,
+    streams and renders at once (first use of per-base tables included) and
+    get exactly the single-threaded results."""
+    import threading
+    import torch
+
+    def work(k):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            a = q.radical_inverse_fill(5000, 900 + k, first=123, fixed=True, stream=s.cuda_stream)
+            b = q.halton_fill(3000, 24 + k, first=77 * k, scramble="faure", fixed=True,
+                              stream=s.cuda_stream)
+            c = q.sobol_fill(4000, 5 + k, first=1 << 33, scramble="owen", words=list(range(5 + k)),
+                             fixed=True, stream=s.cuda_stream)
+            d = q.render(48, 40, 8, kind=q.SAMPLER_KINDS[k % len(q.SAMPLER_KINDS)],
+                         stream=s.cuda_stream)
+        s.synchronize()
+        return [x.cpu() for x in (a, b, c, d)]
+
+    results = [None] * 8
+
+    def run(k):
+        results[k] = work(k)
+
+    threads = [threading.Thread(target=run, args=(k,)) for k in range(8)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for k in range(8):
+        again = work(k)
+        for x, y in zip(results[k], again):
+            assert torch.equal(x, y), k
+
+
 # ------------------------------------------------ full-size properties
 @pytest.mark.slow
 def test_c2_full_size_properties(oracle, columns64):
