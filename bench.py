@@ -404,99 +404,135 @@ def run_render_distributed(q, world, stream):
 
 
 def run_extra(q, stream, peak, args):
-    """Other BASELINE configs, one line each (not the headline)."""
+    """Other BASELINE configs and the §8f rows, one entry each (not the
+    headline). Each section is guarded: a failing config records its error
+    instead of costing the headline line."""
     import torch
 
     res = {}
     steps, warm = 5, 3
-    # C1: van der Corput 2^24 x 1 (launch-bound parity config): the fill is
-    # captured once in a CUDA graph and replayed, so the device time is not
-    # hidden behind per-call host latency
-    n1 = 1 << 24
-    # 4 rotating 64 MiB outputs (256 MiB > 126 MB L2), so consecutive launches
-    # write different buffers and the stores reach HBM
-    o1 = [torch.empty(n1, dtype=torch.float32, device="cuda") for _ in range(4)]
-    q.radical_inverse_fill(n1, 0, out=o1[0])
-    torch.cuda.synchronize()
-    g1 = torch.cuda.CUDAGraph()
-    cap = torch.cuda.Stream()
-    with torch.cuda.graph(g1, stream=cap):
-        for k in range(12):
-            q.radical_inverse_fill(n1, 0, out=o1[k % 4], stream=cap.cuda_stream)
-    r1 = measure_fill("vdc 2^24 x 1 (CUDA graph of 12 launches over 4 rotating buffers)",
-                      g1.replay, n1 * 12, 20, 5, peak, stream)
-    r1["ms_per_step"] /= 12
-    r1["l2"] = "4 rotating 64 MiB outputs (256 MiB > L2)"
-    res["c1_vdc_2^24"] = r1
-    del o1, g1
-    # the paper's "previous approach": linearly scrambled Halton, 32 dims
-    # (incremental hi/lo split: a table load, an integer magic division and
-    # the map per sample; issue-bound, not HBM-bound)
-    nh = 1 << 24
-    oh = torch.empty((nh, 32), dtype=torch.float32, device="cuda")
-    rh = measure_fill("halton linear 2^24 x 32", lambda: q.halton_fill(nh, 32, scramble="linear",
-                                                                      out=oh),
-                      nh * 32, 5, 3, peak, stream)
-    rh["roofline"]["bound"] = "issue (table load + magic division + map per sample)"
-    res["halton_linear_2^24x32"] = rh
-    del oh
-    # C3: Owen / XOR scrambled Sobol' 2^28 x 64
-    n3, d3 = 1 << 28, 64
-    seeds = [q.pixel_hash(j, 1, 0x5EED) for j in range(d3)]
-    m64 = q.GeneratorMatrixSet.builtin(d3)
-    o3 = torch.empty((n3, d3), dtype=torch.float32, device="cuda")
-    res["c3_owen_2^28x64"] = measure_fill(
-        "owen sobol 2^28 x 64", lambda: q.sobol_fill(n3, d3, matrices=m64, scramble="owen",
-                                                     words=seeds, out=o3), n3 * d3, steps, warm,
-        peak, stream)
-    res["c3_xor_2^28x64"] = measure_fill(
-        "xor sobol 2^28 x 64", lambda: q.sobol_fill(n3, d3, matrices=m64, scramble="xor",
-                                                    words=seeds, out=o3), n3 * d3, steps, warm,
-        peak, stream)
-    del o3
-    torch.cuda.empty_cache()
-    # C4: lattice 2^30 x 16 + integer CP rotation
-    n4, d4 = 1 << 30, 16
-    g = q.lfsr_generator_vector(0xACE1, d4)
-    s = [q.pixel_hash(j, 1, 0x5EED) for j in range(d4)]
-    o4 = torch.empty((n4, d4), dtype=torch.float32, device="cuda")
-    res["c4_lattice_cp_2^30x16"] = measure_fill(
-        "lattice+cp 2^30 x 16", lambda: q.lattice_fill(n4, g, shifts=s, out=o4), n4 * d4, steps,
-        warm, peak, stream)
-    del o4
-    torch.cuda.empty_cache()
-    # C5: fused per-pixel render 3840x2160, pixel-shifted lattice, Kahan
-    img = torch.empty((2160, 3840), dtype=torch.float32, device="cuda")
-    c5 = {}
-    for spp in (1, 16, 64, 256):
-        kinds = ("pixel-shifted-lattice",) if spp != 64 else (
-            "pixel-shifted-lattice", "image-plane-halton", "pixel-random-lattice", "sobol")
-        for kind in kinds:
-            fn = lambda: q.render(3840, 2160, spp, kind=kind, out=img)  # noqa: E731
-            for _ in range(2):
-                fn()
-            torch.cuda.synchronize()
-            ms = time_steps(fn, 3, stream)
-            avg = sum(ms) / len(ms)
-            c5["%s/spp%d" % (kind, spp)] = {
-                "value": 3840 * 2160 * spp / (avg * 1e-3) / 1e9, "unit": "G pixel-samples/s",
-                "ms_per_step": avg}
-    # the paper's comparison (PAPER.md:771-774, SPEC.md:626): pixel-shifted
-    # lattice vs the image-plane Halton enumeration, same render
-    c5["ratio_psl_over_image_plane_halton_spp64"] = {
-        "value": c5["pixel-shifted-lattice/spp64"]["value"] /
-        c5["image-plane-halton/spp64"]["value"], "unit": "x"}
-    res["c5_render_4k"] = c5
-    # next row: fused QMC integration (quality.cpp:214-282), Sobol' 8 dims
-    ni = 1 << 26
-    fn = lambda: q.integrate("sobol", "product-sine", ni, 8, "kahan")  # noqa: E731
-    fn()
-    t0 = time.perf_counter()
-    row = fn()
-    sec = time.perf_counter() - t0
-    res["integrate_sobol_product_sine_2^26x8"] = {
-        "value": ni * 8 / sec / 1e9, "unit": "Gsamples/s (host-timed call incl. D2H combine)",
-        "estimate": row["estimate"], "abs_error": row["abs_error"]}
+
+    def section(fn):
+        try:
+            fn()
+        except Exception as e:  # noqa: BLE001 - reported in the JSON line
+            res.setdefault("errors", {})[fn.__name__] = "%s: %s" % (type(e).__name__, e)
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+
+    def c1():
+        # van der Corput 2^24 x 1 (launch-bound parity config): captured once
+        # in a CUDA graph and replayed, so the device time is not hidden
+        # behind per-call host latency; 4 rotating 64 MiB outputs (256 MiB >
+        # 126 MB L2), so consecutive launches write different buffers
+        n1 = 1 << 24
+        o1 = [torch.empty(n1, dtype=torch.float32, device="cuda") for _ in range(4)]
+        q.radical_inverse_fill(n1, 0, out=o1[0])
+        torch.cuda.synchronize()
+        g1 = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        with torch.cuda.graph(g1, stream=cap):
+            for k in range(12):
+                q.radical_inverse_fill(n1, 0, out=o1[k % 4], stream=cap.cuda_stream)
+        r1 = measure_fill("vdc 2^24 x 1 (CUDA graph of 12 launches over 4 rotating buffers)",
+                          g1.replay, n1 * 12, 20, 5, peak, stream)
+        r1["ms_per_step"] /= 12
+        r1["l2"] = "4 rotating 64 MiB outputs (256 MiB > L2)"
+        res["c1_vdc_2^24"] = r1
+
+    def halton():
+        # the paper's "previous approach": linearly scrambled Halton, 32 dims
+        # (incremental hi/lo split: a table load, an integer magic division
+        # and the map per sample; issue-bound, not HBM-bound)
+        nh = 1 << 24
+        oh = torch.empty((nh, 32), dtype=torch.float32, device="cuda")
+        rh = measure_fill("halton linear 2^24 x 32",
+                          lambda: q.halton_fill(nh, 32, scramble="linear", out=oh), nh * 32, steps,
+                          warm, peak, stream)
+        rh["roofline"]["bound"] = "issue (table load + magic division + map per sample)"
+        res["halton_linear_2^24x32"] = rh
+
+    def c3():
+        # Owen / XOR scrambled Sobol' 2^28 x 64
+        n3, d3 = 1 << 28, 64
+        seeds = [q.pixel_hash(j, 1, 0x5EED) for j in range(d3)]
+        m64 = q.GeneratorMatrixSet.builtin(d3)
+        o3 = torch.empty((n3, d3), dtype=torch.float32, device="cuda")
+        res["c3_owen_2^28x64"] = measure_fill(
+            "owen sobol 2^28 x 64", lambda: q.sobol_fill(n3, d3, matrices=m64, scramble="owen",
+                                                         words=seeds, out=o3), n3 * d3, steps,
+            warm, peak, stream)
+        res["c3_xor_2^28x64"] = measure_fill(
+            "xor sobol 2^28 x 64", lambda: q.sobol_fill(n3, d3, matrices=m64, scramble="xor",
+                                                        words=seeds, out=o3), n3 * d3, steps,
+            warm, peak, stream)
+
+    def c4():
+        # lattice 2^30 x 16 + integer CP rotation
+        n4, d4 = 1 << 30, 16
+        g = q.lfsr_generator_vector(0xACE1, d4)
+        s = [q.pixel_hash(j, 1, 0x5EED) for j in range(d4)]
+        o4 = torch.empty((n4, d4), dtype=torch.float32, device="cuda")
+        res["c4_lattice_cp_2^30x16"] = measure_fill(
+            "lattice+cp 2^30 x 16", lambda: q.lattice_fill(n4, g, shifts=s, out=o4), n4 * d4,
+            steps, warm, peak, stream)
+
+    def c5():
+        # fused per-pixel render 3840x2160, Kahan; pixel-shifted lattice at
+        # every spp, the other kinds (incl. the XOR-table sampler, §8f rank 2)
+        # at 64 spp
+        img = torch.empty((2160, 3840), dtype=torch.float32, device="cuda")
+        c5r = {}
+        xt = q.XorTables.white_noise(2, 1 << 12, 7)
+        for spp in (1, 16, 64, 256):
+            kinds = ("pixel-shifted-lattice",) if spp != 64 else (
+                "pixel-shifted-lattice", "image-plane-halton", "pixel-random-lattice", "sobol",
+                "sobol-xor-table")
+            for kind in kinds:
+                kw = {"tables": xt} if kind == "sobol-xor-table" else {}
+                fn = lambda: q.render(3840, 2160, spp, kind=kind, out=img, **kw)  # noqa: E731
+                for _ in range(2):
+                    fn()
+                torch.cuda.synchronize()
+                ms = time_steps(fn, 3, stream)
+                avg = sum(ms) / len(ms)
+                c5r["%s/spp%d" % (kind, spp)] = {
+                    "value": 3840 * 2160 * spp / (avg * 1e-3) / 1e9,
+                    "unit": "G pixel-samples/s", "ms_per_step": avg}
+        # the paper's comparison (PAPER.md:771-774, SPEC.md:626): pixel-shifted
+        # lattice vs the image-plane Halton enumeration, same render
+        c5r["ratio_psl_over_image_plane_halton_spp64"] = {
+            "value": c5r["pixel-shifted-lattice/spp64"]["value"] /
+            c5r["image-plane-halton/spp64"]["value"], "unit": "x"}
+        res["c5_render_4k"] = c5r
+
+    def integrate():
+        # §8f rank 1: fused QMC integration (quality.cpp:214-282), Sobol' 8 dims
+        ni = 1 << 26
+        fn = lambda: q.integrate("sobol", "product-sine", ni, 8, "kahan")  # noqa: E731
+        fn()
+        t0 = time.perf_counter()
+        row = fn()
+        sec = time.perf_counter() - t0
+        res["integrate_sobol_product_sine_2^26x8"] = {
+            "value": ni * 8 / sec / 1e9, "unit": "Gsamples/s (host-timed call incl. D2H combine)",
+            "estimate": row["estimate"], "abs_error": row["abs_error"]}
+
+    def l2_star():
+        # §8f rank 4: Warnock L2-star discrepancy, O(N^2 s) pair terms
+        # (quality.cpp:76-114)
+        nl, dl = 1 << 14, 4
+        pts = q.sobol_fill(nl, dl)
+        q.l2_star_discrepancy(pts)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        q.l2_star_discrepancy(pts)
+        sec = time.perf_counter() - t0
+        res["l2_star_2^14x4"] = {"value": nl * (nl - 1) / 2 / sec / 1e9,
+                                 "unit": "G pair terms/s (host-timed call)", "ms": sec * 1e3}
+
+    for fn in (c1, halton, c3, c4, c5, integrate, l2_star):
+        section(fn)
     return res
 
 
