@@ -669,6 +669,16 @@ qmc_status qmc_stream_fill(qmc_sampler_kind kind, const qmc_stream_params* p,
             fail(QMC_OUT_OF_RANGE, "xor_table_sample: index beyond the stored point set");
         if (n == 0)
             return;
+        if (kind == QMC_KIND_HALTON_HILBERT) {
+            // sample(i, j) = halton_component(u32(block_start + i), j)
+            // (imageplane.cpp:378, :439-442): the contiguous Halton fill
+            const uint64_t block = hilbert_index(p->px, p->py, p->order) * p->spp;
+            halton_fill_impl(block + first_index, n, dims, 0,
+                             static_cast<qmc_radical_scramble>(p->halton_scramble),
+                             p->linear_factors, out_kind, out, s);
+            cuda_ok(cudaStreamSynchronize(s), "sync");
+            return;
+        }
         const bool u32 = out_kind == QMC_OUT_U32;
         place_fill(out, first_index, n, dims, s, [&](const FillRange& fr, cudaStream_t st) {
             return launch_pixel_stream(r.q, u32, fr, st);
