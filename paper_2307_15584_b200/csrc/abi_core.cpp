@@ -754,7 +754,7 @@ qmc_status qmc_integrate(qmc_sampler_kind kind, const qmc_stream_params* p,
         ip.fn = f;
         ip.fdims = f_dims;
         ip.n = n;
-        ip.sc = make_sin_consts();
+        ip.sc = make_scene_consts();
         if (kind == QMC_KIND_SOBOL) {
             const auto& dev = r.matrices->on_device(dims_of_integrand);
             ip.colsT = static_cast<const uint32_t*>(dev.colsT.get());

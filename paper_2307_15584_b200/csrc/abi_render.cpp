@@ -65,7 +65,7 @@ void resolve_render(const qmc_render_job* job, uint32_t row_begin, uint32_t row_
         p.scr1 = pixel_hash_host(1, job->seed, 0);
     }
     p.tab3 = digit_table(3, 0, 0).ptr; // phi_3, seven ternary digits per step
-    p.sc = make_sin_consts();
+    p.sc = make_scene_consts();
     std::vector<uint32_t> cols2(104, 0u);
     if (job->matrices) {
         require(job->matrices->dims >= 2, "make_stream: dims beyond the generator matrices");

@@ -34,10 +34,11 @@ struct FillRange {
 // Constants of the render's sine (device.cuh sin_cw) and integrand, carried
 // in the kernel parameters so the per-sample loop reads them from the
 // constant bank instead of rematerialising 64-bit immediates every sample.
-struct SinConsts {
+struct SceneConsts {
     double k8pi;                        // 8 * pi (render.hpp:24-27)
     double two_over_pi;                 // 0x3fe45f306dc9c883
     double pio2_hi, pio2_mid, pio2_lo;  // pi/2 in three parts, negated
+    double disc_r2;                     // 0.3 * 0.3 rounded (render.cpp:23-24)
 };
 
 __host__ __device__ inline double bits_to_double(uint64_t b)
@@ -47,15 +48,15 @@ __host__ __device__ inline double bits_to_double(uint64_t b)
     return d;
 }
 
-__host__ __device__ inline SinConsts make_sin_consts()
+__host__ __device__ inline SceneConsts make_scene_consts()
 {
     return {25.132741228718345, bits_to_double(0x3fe45f306dc9c883ull),
             -bits_to_double(0x3ff921fb54442d18ull), -bits_to_double(0x3c91a62633145c00ull),
-            -bits_to_double(0x397b839a252049c0ull)};
+            -bits_to_double(0x397b839a252049c0ull), bits_to_double(0x3fb70a3d70a3d70aull)};
 }
 
 struct RenderParams {
-    SinConsts sc;
+    SceneConsts sc;
     uint32_t width, height, spp, order;
     uint32_t row_begin, row_end;
     double inv_w, inv_h;
@@ -112,7 +113,7 @@ struct IntegrateParams {
     const uint32_t* colsT; // sobol: device [52][mdims]
     uint32_t mdims;
     const uint32_t* words; // sobol: device XOR scrambles or null
-    SinConsts sc;          // product-sine's sine (sin_cw)
+    SceneConsts sc;          // product-sine's sine (sin_cw)
 };
 
 // ------------------------------------------------------------ launchers

@@ -35,7 +35,7 @@ __device__ __forceinline__ uint64_t digit_reverse3(uint64_t v, uint32_t digits)
 // One integrand factor (quality.cpp:35-63). Returns false for the
 // indicator's early exit.
 template <uint32_t FN>
-__device__ __forceinline__ bool factor(float xs, double& v, const SinConsts& sc)
+__device__ __forceinline__ bool factor(float xs, double& v, const SceneConsts& sc)
 {
     const double x = static_cast<double>(xs);
     if (FN == 0) { // product-sine: v *= (0.5*pi) * sin(pi * x); pi*x in [0, pi)
