@@ -119,6 +119,8 @@ __device__ __forceinline__ void sample2(uint32_t i, const PixelState& s, const R
 template <uint32_t KIND, uint32_t ACCUM>
 __global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __restrict__ out)
 {
+    __shared__ double2 s_poly[8];
+    load_sin_poly(s_poly);
     const uint32_t band = p.row_end - p.row_begin;
     const uint64_t npix = static_cast<uint64_t>(band) * p.width;
     const uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -138,7 +140,7 @@ __global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __rest
         const double u = static_cast<double>(map_u32(a));
         const double v = static_cast<double>(map_u32(b));
         const double f = scene_value<true>(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
-                                           __dmul_rn(__dadd_rn(fy, v), p.inv_h), p.sc);
+                                           __dmul_rn(__dadd_rn(fy, v), p.inv_h), p.sc, s_poly);
         if (ACCUM == 0)
             neumaier_add(sum, comp, f);
         else
@@ -169,6 +171,8 @@ __global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __rest
 template <uint32_t KIND, uint32_t ACCUM>
 __global__ void __launch_bounds__(kBlock) k_render_warp(RenderParams p, float* __restrict__ out)
 {
+    __shared__ double2 s_poly[8];
+    load_sin_poly(s_poly);
     const uint32_t band = p.row_end - p.row_begin;
     const uint64_t npix = static_cast<uint64_t>(band) * p.width;
     const uint64_t q = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -193,7 +197,7 @@ __global__ void __launch_bounds__(kBlock) k_render_warp(RenderParams p, float* _
         const double u = static_cast<double>(map_u32(a));
         const double v = static_cast<double>(map_u32(b));
         const double f = scene_value<true>(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
-                                           __dmul_rn(__dadd_rn(fy, v), p.inv_h), p.sc);
+                                           __dmul_rn(__dadd_rn(fy, v), p.inv_h), p.sc, s_poly);
         if (ACCUM == 0)
             neumaier_add(sum, comp, f);
         else
@@ -227,6 +231,8 @@ template <uint32_t KIND>
 __global__ void __launch_bounds__(kBlock)
     k_render_partial(RenderParams p, uint32_t first, uint32_t step, long long* __restrict__ acc)
 {
+    __shared__ double2 s_poly[8];
+    load_sin_poly(s_poly);
     const uint32_t band = p.row_end - p.row_begin;
     const uint64_t npix = static_cast<uint64_t>(band) * p.width;
     const uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -250,7 +256,7 @@ __global__ void __launch_bounds__(kBlock)
         const double u = static_cast<double>(map_u32(a));
         const double v = static_cast<double>(map_u32(b));
         const double f = scene_value<true>(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
-                                           __dmul_rn(__dadd_rn(fy, v), p.inv_h), p.sc);
+                                           __dmul_rn(__dadd_rn(fy, v), p.inv_h), p.sc, s_poly);
         isum += llround(__dmul_rn(f, 4294967296.0));
     }
     acc[q] = isum;
