@@ -415,6 +415,23 @@ def test_concurrent_host_threads():
             assert torch.equal(x, y), k
 
 
+@pytest.mark.parametrize("wh", [(2, 3), (5, 2), (64, 27)])
+def test_image_plane_halton_long_streams_vs_reference(ref, wh):
+    """The phi_3 fast path (two 7-digit table steps below 3^14) and the digit
+    loop above it: image-plane Halton streams whose y dimension
+    phi_3(ipy0 + i * 2^a) runs through [0, 2^23) and past 3^14 = 4782969,
+    against the reference stream bit for bit (fp32 bits)."""
+    w, h = wh
+    n, dims = 1 << 21, 3
+    for px, py in [(0, 0), (w - 1, h - 1)]:
+        got = u32(q.stream_fill("image-plane-halton", n, dims, width=w, height=h,
+                                pixel=(px, py))).reshape(n, dims)
+        exp = np.zeros((n, dims), np.uint32)
+        assert ref.ref_stream_fill(b"image-plane-halton", dims, 0, b"plain", px, py, 1, 1, w, h,
+                                   0, n, ptr(exp)) == 0, ref.ref_last_error()
+        np.testing.assert_array_equal(got, exp)
+
+
 # ------------------------------------------------ full-size properties
 @pytest.mark.slow
 def test_c2_full_size_properties(oracle, columns64):
