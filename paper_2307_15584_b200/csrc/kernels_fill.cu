@@ -675,13 +675,36 @@ __global__ void __launch_bounds__(kBlock)
     const uint32_t* g = small_a(args);
     const uint32_t* shifts = small_b(args);
     const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < elems; e += stride) {
-        const uint32_t p = point_of(e, dims, div_dims);
-        const uint32_t j = e - p * dims;
+    auto value = [&](uint32_t p, uint32_t j) {
         uint32_t x = brev32(static_cast<uint32_t>(first + p)) * g[j];
         if (shifts)
             x += shifts[j];
-        out[e] = u32out ? x : map_bits(x);
+        return u32out ? x : map_bits(x);
+    };
+    const uint32_t t0 = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t e0 = 0;
+    if ((reinterpret_cast<uintptr_t>(out) & 15u) == 0) {
+        // four consecutive elements per thread, one 16-B streaming store;
+        // (point, dim) walk with the row wrap checked per element
+        const uint32_t quads = elems >> 2;
+        e0 = quads << 2;
+        for (uint32_t qd = t0; qd < quads; qd += stride) {
+            uint32_t p = point_of(qd * 4, dims, div_dims), j = qd * 4 - p * dims;
+            uint32_t v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                v[k] = value(p, j);
+                if (++j == dims) {
+                    j = 0;
+                    ++p;
+                }
+            }
+            __stcs(reinterpret_cast<uint4*>(out) + qd, make_uint4(v[0], v[1], v[2], v[3]));
+        }
+    }
+    for (uint32_t e = e0 + t0; e < elems; e += stride) {
+        const uint32_t p = point_of(e, dims, div_dims);
+        out[e] = value(p, e - p * dims);
     }
 }
 

@@ -20,3 +20,12 @@ for dims in (3, 5, 12, 48, 100):
     print(dims, "plain", t(lambda: q.sobol_fill(n, dims, matrices=m, out=out), B),
           "owen", t(lambda: q.sobol_fill(n, dims, matrices=m, scramble="owen", words=list(range(dims)), out=out), B))
     del out
+
+for dims in (3, 5, 12, 48, 100):
+    n = (1 << 30) // dims // 4 * 4
+    g = q.lfsr_generator_vector(0xACE1, dims)
+    out = torch.empty((n, dims), dtype=torch.float32, device="cuda")
+    B = out.numel() * 4
+    print(dims, "lattice", t(lambda: q.lattice_fill(n, g, out=out), B),
+          "cp", t(lambda: q.lattice_fill(n, g, shifts=list(range(dims)), out=out), B))
+    del out
