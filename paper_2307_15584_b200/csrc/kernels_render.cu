@@ -295,10 +295,7 @@ __global__ void __launch_bounds__(256)
         cell = (p.px % 128u) + (p.py % 128u) * 128u;
     const RadicalDim* rd = static_cast<const RadicalDim*>(p.radical_dims);
 
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < elems; e += stride) {
-        const uint32_t pt = p.dims == 1 ? e : div32(e, div_dims);
-        const uint32_t j = e - pt * p.dims;
+    auto value = [&](uint32_t pt, uint32_t j) {
         const uint64_t idx = first + pt;
         const uint32_t i = static_cast<uint32_t>(idx);
         uint32_t x;
@@ -320,7 +317,33 @@ __global__ void __launch_bounds__(256)
             x = __ldg(p.xor_points + static_cast<uint64_t>(k) * p.xor_dims + j) ^
                 __ldg(p.xor_scramble + cell * p.xor_dims + j);
         }
-        out[e] = U32OUT ? x : map_bits(x);
+        return U32OUT ? x : map_bits(x);
+    };
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t t0 = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t e0 = 0;
+    if ((reinterpret_cast<uintptr_t>(out) & 15u) == 0) {
+        // four consecutive elements per thread, one 16-B streaming store
+        const uint32_t quads = elems >> 2;
+        e0 = quads << 2;
+        for (uint32_t qd = t0; qd < quads; qd += stride) {
+            uint32_t pt = p.dims == 1 ? qd * 4 : div32(qd * 4, div_dims);
+            uint32_t j = qd * 4 - pt * p.dims;
+            uint32_t v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                v[k] = value(pt, j);
+                if (++j == p.dims) {
+                    j = 0;
+                    ++pt;
+                }
+            }
+            __stcs(reinterpret_cast<uint4*>(out) + qd, make_uint4(v[0], v[1], v[2], v[3]));
+        }
+    }
+    for (uint32_t e = e0 + t0; e < elems; e += stride) {
+        const uint32_t pt = p.dims == 1 ? e : div32(e, div_dims);
+        out[e] = value(pt, e - pt * p.dims);
     }
 }
 
