@@ -294,6 +294,15 @@ __global__ void __launch_bounds__(256)
     if (KIND == 7)
         cell = (p.px % 128u) + (p.py % 128u) * 128u;
     const RadicalDim* rd = static_cast<const RadicalDim*>(p.radical_dims);
+    // pixel_random_lattice: the per-dimension hashed generator depends on the
+    // pixel only (lattice.hpp:51-56), so it is hashed once per block
+    __shared__ uint32_t s_gen[KIND == 5 ? 256 : 1];
+    const bool gen_cached = KIND == 5 && p.dims <= 256;
+    if (gen_cached) {
+        for (uint32_t j = threadIdx.x; j < p.dims; j += blockDim.x)
+            s_gen[j] = pixel_hash(j, p.px, p.py) | 1u;
+        __syncthreads();
+    }
 
     auto value = [&](uint32_t pt, uint32_t j) {
         const uint64_t idx = first + pt;
@@ -304,7 +313,7 @@ __global__ void __launch_bounds__(256)
         } else if (KIND == 4) {
             x = (brev32(i) + shift) * __ldg(p.generator + j);
         } else if (KIND == 5) {
-            x = brev32(~i) * (pixel_hash(j, p.px, p.py) | 1u);
+            x = brev32(~i) * (gen_cached ? s_gen[j] : (pixel_hash(j, p.px, p.py) | 1u));
         } else if (KIND == 6) { // imageplane.cpp:448-456
             if (j == 0)
                 x = rad2(ipx0 + i * p.scale_y);
