@@ -132,7 +132,7 @@ struct DigitTable {
 // Random-access users (radical_fixed) keep tables L1-sized; the contiguous
 // fills read theirs sequentially and take wider ones (fewer block crossings).
 constexpr uint32_t kDigitTableMax = 4096;
-constexpr uint32_t kFillTableMax = 16384;
+constexpr uint32_t kFillTableMax = 65536;
 DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor, uint32_t min_digits = 2,
                        uint32_t max_entries = kDigitTableMax);
 // floor(2^64 / b^D) for D = 0..32 (0 where b^D >= 2^32), on the current device
