@@ -320,6 +320,146 @@ __global__ void __launch_bounds__(kBlock)
     }
 }
 
+// Any dims whose tables fit shared memory (dims <= kElemMaxDims), element-
+// wise with no transpose: a CTA owns a contiguous range of output words,
+// walked in chunks of at most 1024 points. Word (p, j) is
+// XP[tile][j] ^ T[j][(p >> 5) & 31] ^ L[j][p & 31] with 1024-point tiles
+// (disjoint index bits): three shared loads and two XORs, then the map, and
+// four consecutive words leave as one 16-B store. XP (X of the tile base,
+// scramble included) advances by the index bits that change from one tile to
+// the next; the chunk's points span the current tile and the next.
+constexpr uint32_t kElemMaxDims = 128;
+
+template <int MODE, bool U32OUT>
+__global__ void __launch_bounds__(kBlock)
+    k_sobol_elem(const uint32_t* __restrict__ colsT, const __grid_constant__ SmallArgs args,
+                 uint32_t dims, Div32 div_dims, uint64_t first, uint64_t words_total,
+                 uint64_t words_per_cta, uint32_t chunk_words, uint32_t* __restrict__ out)
+{
+    extern __shared__ uint32_t sm[];
+    // [32][dims+1] rows: the lanes of a warp read consecutive dimensions of
+    // one or a few points, so a padded row per index value keeps them on
+    // distinct banks
+    const uint32_t ld = dims + 1;
+    uint32_t* L = sm;              // [32][ld]: X(l)
+    uint32_t* T = L + 32 * ld;     // [32][ld]: X(32 m)
+    uint32_t* XP = T + 32 * ld;    // [2][dims]: tiles tc, tc+1
+    const uint32_t* words = small_a(args);
+    auto col = [&](uint32_t k, uint32_t j) {
+        return __ldg(colsT + static_cast<size_t>(k) * dims + j);
+    };
+    for (uint32_t e = threadIdx.x; e < dims * 32; e += blockDim.x) {
+        const uint32_t j = e >> 5, l = e & 31u;
+        uint32_t xl = 0, xt = 0;
+        for (uint32_t k = 0; k < 5; ++k)
+            if ((l >> k) & 1u) {
+                xl ^= col(k, j);
+                xt ^= col(5 + k, j);
+            }
+        L[l * ld + j] = xl;
+        T[l * ld + j] = xt;
+    }
+    const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * words_per_cta;
+    const uint64_t w1 = min(words_total, w0 + words_per_cta);
+    if (w0 >= w1)
+        return;
+    // tile of the CTA's first point: XP = X(tile base) (^ XOR words)
+    uint64_t tc = (first + w0 / dims) >> 10;
+    for (uint32_t j = threadIdx.x; j < dims; j += blockDim.x) {
+        uint32_t x0 = (MODE == 0 && words) ? words[j] : 0u;
+        for (uint64_t b = tc << 10; b; b &= b - 1)
+            x0 ^= col(__ffsll(static_cast<long long>(b)) - 1, j);
+        uint32_t x1 = x0;
+        for (uint64_t b = (tc << 10) ^ ((tc + 1) << 10); b; b &= b - 1)
+            x1 ^= col(__ffsll(static_cast<long long>(b)) - 1, j);
+        XP[j] = x0;
+        XP[dims + j] = x1;
+    }
+    const bool vec = (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+    const uint32_t adv = blockDim.x * 4 - 4; // end of a thread's quad -> its next quad
+    const uint32_t padv = adv / dims, cadv = adv - padv * dims;
+    for (uint64_t c0 = w0; c0 < w1; c0 += chunk_words) {
+        const uint32_t cw = static_cast<uint32_t>(w1 - c0 < chunk_words ? w1 - c0 : chunk_words);
+        __syncthreads(); // tables / XP ready
+        const uint64_t pa = c0 / dims; // chunk's first point (relative)
+        const uint64_t ta = (first + pa) >> 10;
+        if (ta != tc) { // the chunk starts in tile tc + 1: shift the pair
+            for (uint32_t j = threadIdx.x; j < dims; j += blockDim.x) {
+                const uint32_t x1 = XP[dims + j];
+                uint32_t x2 = x1;
+                for (uint64_t b = ((ta) << 10) ^ ((ta + 1) << 10); b; b &= b - 1)
+                    x2 ^= col(__ffsll(static_cast<long long>(b)) - 1, j);
+                XP[j] = x1;
+                XP[dims + j] = x2;
+            }
+            tc = ta;
+            __syncthreads();
+        }
+        const uint32_t rem = static_cast<uint32_t>(c0 - pa * dims); // column of word c0
+        // shared-memory rows of point pr (relative to pa): its XP, T and L rows
+        auto rows = [&](uint32_t pr, const uint32_t*& xr, const uint32_t*& tr,
+                        const uint32_t*& lr) {
+            const uint64_t i = first + pa + pr;
+            xr = XP + (static_cast<uint32_t>(i >> 10) != static_cast<uint32_t>(tc)) * dims;
+            tr = T + (static_cast<uint32_t>(i >> 5) & 31u) * ld;
+            lr = L + (static_cast<uint32_t>(i) & 31u) * ld;
+        };
+        auto finish = [&](uint32_t v, uint32_t j) {
+            if (MODE == 2)
+                v = brev32(owen_lk(v, words ? words[j] : 0u));
+            return U32OUT ? v : map_bits(v);
+        };
+        uint32_t* o = out + c0;
+        uint32_t e0 = 0;
+        if (vec) {
+            const uint32_t quads = cw >> 2;
+            e0 = quads << 2;
+            const uint32_t e = threadIdx.x * 4 + rem;
+            uint32_t p = point_of(e, dims, div_dims), c = e - p * dims;
+            for (uint32_t qd = threadIdx.x; qd < quads; qd += blockDim.x) {
+                uint32_t v[4];
+                if (dims >= 8) { // a quad spans at most two points: rows per point
+                    const uint32_t *xr, *tr, *lr;
+                    rows(p, xr, tr, lr);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        v[k] = finish(xr[c] ^ tr[c] ^ lr[c], c);
+                        if (++c == dims) {
+                            c = 0;
+                            ++p;
+                            rows(p, xr, tr, lr);
+                        }
+                    }
+                } else { // few dims: rows per word, no divergent re-fetch
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t *xr, *tr, *lr;
+                        rows(p, xr, tr, lr);
+                        v[k] = finish(xr[c] ^ tr[c] ^ lr[c], c);
+                        if (++c == dims) {
+                            c = 0;
+                            ++p;
+                        }
+                    }
+                }
+                __stcs(reinterpret_cast<uint4*>(o) + qd, make_uint4(v[0], v[1], v[2], v[3]));
+                p += padv;
+                c += cadv;
+                if (c >= dims) {
+                    c -= dims;
+                    ++p;
+                }
+            }
+        }
+        for (uint32_t e = e0 + threadIdx.x; e < cw; e += blockDim.x) {
+            const uint32_t p = point_of(e + rem, dims, div_dims), c = e + rem - p * dims;
+            const uint32_t *xr, *tr, *lr;
+            rows(p, xr, tr, lr);
+            o[e] = finish(xr[c] ^ tr[c] ^ lr[c], c);
+        }
+    }
+}
+
 // Any dims, shared-memory tiled: a CTA owns a contiguous range of tiles of
 // tp = 2^k consecutive points; a warp computes one (dimension, run of m)
 // item at a time: lane l holds points p0 + l + 32 m, whose value is
@@ -1145,6 +1285,27 @@ cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const
                                 : launch_tiled(k_sobol_narrow<2, 2, false>, kLogTp2, r, s, cols, words))
                          : (u32 ? launch_tiled(k_sobol_narrow<2, 0, true>, kLogTp2, r, s, cols, words)
                                 : launch_tiled(k_sobol_narrow<2, 0, false>, kLogTp2, r, s, cols, words));
+    }
+    if (dims <= kElemMaxDims) {
+        // element-wise path: chunks of <= 1022 points (two 1024-point tiles)
+        auto kern = mode == 2 ? (u32 ? k_sobol_elem<2, true> : k_sobol_elem<2, false>)
+                              : (u32 ? k_sobol_elem<0, true> : k_sobol_elem<0, false>);
+        const size_t smem = (static_cast<size_t>(dims + 1) * 64 + 2 * dims) * 4;
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem) !=
+                cudaSuccess ||
+            per_sm < 1)
+            per_sm = 1;
+        const uint32_t chunk = std::min<uint32_t>(4096u, (1022u * dims) & ~3u);
+        const uint64_t total = r.n * dims;
+        const uint64_t want = (total + chunk - 1) / chunk;
+        const uint64_t cap = static_cast<uint64_t>(sm_count()) * per_sm;
+        const unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
+        const uint64_t per = (((total + grid - 1) / grid) + 3) & ~3ull;
+        const Div32 d = make_div32(dims);
+        kern<<<grid, kBlock, smem, s>>>(cols, words, dims, d, r.first, total, per, chunk,
+                                        static_cast<uint32_t*>(r.out));
+        return cudaGetLastError();
     }
     // shared-memory tiled path: tp = 2^k points with tp*(dims+1) <= 8192 words
     uint32_t tp = 32;
