@@ -459,19 +459,24 @@ def test_c2_full_size_properties(oracle, columns64):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("dims", [8, 256, 300])
+@pytest.mark.parametrize("dims", [8, 100, 128, 129, 200, 256, 300])
 def test_large_dims_args_paths(oracle, dims):
     """Per-dim word arrays beyond the by-value parameter block (dims > 256)
-    take the device-copy path; both must match the oracle."""
+    take the device-copy path; dims <= 128 not dividing 256 the element-wise
+    kernel, larger ones the tiled kernel. XOR and Owen match the oracle."""
     rng = np.random.default_rng(dims)
     cols = rng.integers(0, 1 << 32, (dims, 52), dtype=np.uint64).astype(np.uint32)
     m = q.GeneratorMatrixSet.from_columns(cols)
     words = rng.integers(0, 1 << 32, dims, dtype=np.uint64).astype(np.uint32)
-    n, first = 600, 12345
+    n, first = 3000, (1 << 33) + 12345
     got = u32(q.sobol_fill(n, dims, first=first, scramble="xor", words=words, matrices=m,
                            fixed=True)).reshape(n, dims)
     exp = np.zeros((n, dims), np.uint32)
     oracle.qo_sobol_fill_fixed(first, n, dims, ptr(cols), ptr(words), ptr(exp))
+    np.testing.assert_array_equal(got, exp)
+    got = u32(q.sobol_fill(n, dims, first=first, scramble="owen", words=words, matrices=m,
+                           fixed=True)).reshape(n, dims)
+    oracle.qo_sobol_owen_fill_fixed(first, n, dims, ptr(cols), ptr(words), ptr(exp))
     np.testing.assert_array_equal(got, exp)
     g = (rng.integers(0, 1 << 31, dims) * 2 + 1).astype(np.uint32)
     s = rng.integers(0, 1 << 32, dims, dtype=np.uint64).astype(np.uint32)
