@@ -90,6 +90,20 @@ uint32_t qmc_hilbert_order_for(uint32_t width, uint32_t height);
 /* imageplane.cpp:114-130 */
 qmc_status qmc_partition_by_extra_dimension(uint32_t part, uint32_t parts, uint32_t base,
                                             uint64_t* remainder, uint64_t* modulus);
+/* hilbert.hpp:39-56: invalid_argument unless order in [1, 31], out_of_range
+ * for a pixel outside the 2^order grid */
+qmc_status qmc_hilbert_index(uint32_t x, uint32_t y, uint32_t order, uint64_t* out);
+/* hilbert.hpp:59-78: the inverse (same orientation) */
+qmc_status qmc_hilbert_xy(uint64_t d, uint32_t order, uint32_t* x, uint32_t* y);
+/* imageplane.cpp:43-51: the `digits` least significant base-b digits of v,
+ * reversed */
+uint64_t qmc_digit_reverse(uint64_t v, uint32_t base, uint32_t digits);
+/* lattice_shift_fixed (lattice.cpp:157-170): delta_j = brev(k * 2^m) * g_j,
+ * the integer shift that maps block 0 of 2^m lattice points onto block k
+ * (pass it as qmc_lattice_fill's `shifts`); invalid_argument for m > 32,
+ * overflow when k * 2^m does not fit 32 bits. out has `dims` entries. */
+qmc_status qmc_lattice_shift_fixed(uint32_t k, uint32_t m, const uint32_t* g, uint32_t dims,
+                                   uint32_t* out);
 /* imageplane.cpp:80-106: scales, exponents, stride; offset of (px, py) */
 typedef struct qmc_halton_enumeration {
     uint32_t scale_x, scale_y, exponent_x, exponent_y;

@@ -82,6 +82,20 @@ inline std::uint32_t hilbert_order_for(std::uint32_t w, std::uint32_t h)
     return qmc_hilbert_order_for(w, h);
 }
 
+inline std::uint64_t digit_reverse(std::uint64_t v, std::uint32_t base, std::uint32_t digits)
+{ // imageplane.cpp:43-51
+    return qmc_digit_reverse(v, base, digits);
+}
+// lattice_shift_fixed (lattice.cpp:157-170): pass as lattice_points' shifts
+inline std::vector<std::uint32_t> lattice_shift_fixed(std::uint32_t k, std::uint32_t m,
+                                                      const GeneratorVector& g)
+{
+    std::vector<std::uint32_t> d(g.dims() ? g.dims() : 1);
+    check(qmc_lattice_shift_fixed(k, m, g.g.data(), g.dims(), d.data()));
+    d.resize(g.dims());
+    return d;
+}
+
 struct IndexCongruence { // imageplane.hpp:77-84
     std::uint64_t remainder = 0, modulus = 1;
     bool contains(std::uint64_t i) const { return i % modulus == remainder; }
@@ -342,6 +356,18 @@ private:
 struct PixelCoord { // hilbert.hpp:14-18
     std::uint32_t x = 0, y = 0, order = 0;
 };
+inline std::uint64_t hilbert_index(const PixelCoord& p) // hilbert.hpp:39-56
+{
+    std::uint64_t d = 0;
+    check(qmc_hilbert_index(p.x, p.y, p.order, &d));
+    return d;
+}
+inline PixelCoord hilbert_xy(std::uint64_t d, std::uint32_t order) // hilbert.hpp:59-78
+{
+    PixelCoord p{0, 0, order};
+    check(qmc_hilbert_xy(d, order, &p.x, &p.y));
+    return p;
+}
 
 struct StreamParams {
     std::uint32_t dims = 2;

@@ -36,7 +36,7 @@ __all__ = [
     "integrate", "builtin_integrand", "write_probe", "l2_star_discrepancy",
     "min_toroidal_distance", "check_1d_stratification", "XorTables", "render_partial",
     "render_finalize", "load_generator_vector", "load_linear_factors", "fnv1a64", "write_pnm",
-    "write_points_csv",
+    "write_points_csv", "hilbert_index", "hilbert_xy", "digit_reverse", "lattice_shift_fixed",
     "SAMPLER_KINDS",
 ]
 
@@ -109,6 +109,10 @@ def lib():
     sig("qmc_pixel_hash", u32, u32, u32, u32)
     sig("qmc_hilbert_order_for", u32, u32, u32)
     sig("qmc_partition_by_extra_dimension", i32, u32, u32, u32, C.POINTER(u64), C.POINTER(u64))
+    sig("qmc_hilbert_index", i32, u32, u32, u32, C.POINTER(u64))
+    sig("qmc_hilbert_xy", i32, u64, u32, C.POINTER(u32), C.POINTER(u32))
+    sig("qmc_digit_reverse", u64, u64, u32, u32)
+    sig("qmc_lattice_shift_fixed", i32, u32, u32, P, u32, P)
     sig("qmc_halton_pixel_enumeration", i32, u32, u32, u32, u32, C.POINTER(HaltonEnumeration),
         C.POINTER(u64))
     sig("qmc_matrices_builtin", i32, u32, C.POINTER(P))
@@ -253,6 +257,34 @@ def partition_by_extra_dimension(part: int, parts: int, base: int):
     r, m = u64(), u64()
     _check(lib().qmc_partition_by_extra_dimension(part, parts, base, C.byref(r), C.byref(m)))
     return r.value, m.value
+
+
+def hilbert_index(x: int, y: int, order: int) -> int:
+    """hilbert_index(PixelCoord{x, y, order}) (hilbert.hpp:39-56)."""
+    d = u64()
+    _check(lib().qmc_hilbert_index(x, y, order, C.byref(d)))
+    return d.value
+
+
+def hilbert_xy(d: int, order: int):
+    """hilbert_xy(d, order) -> (x, y) (hilbert.hpp:59-78)."""
+    x, y = u32(), u32()
+    _check(lib().qmc_hilbert_xy(d, order, C.byref(x), C.byref(y)))
+    return x.value, y.value
+
+
+def digit_reverse(v: int, base: int, digits: int) -> int:
+    """digit_reverse (imageplane.cpp:43-51)."""
+    return lib().qmc_digit_reverse(v, base, digits)
+
+
+def lattice_shift_fixed(k: int, m: int, g) -> list:
+    """lattice_shift_fixed(k, m, g) (lattice.cpp:157-170): the integer shift
+    mapping block 0 of 2^m points onto block k (qmc_lattice_fill `shifts`)."""
+    gv = _u32_host(g)
+    out = np.zeros(max(gv.size, 1), np.uint32)
+    _check(lib().qmc_lattice_shift_fixed(k, m, gv.ctypes.data, gv.size, out.ctypes.data))
+    return out[:gv.size].tolist()
 
 
 def halton_pixel_enumeration(width: int, height: int, px: int = 0, py: int = 0):

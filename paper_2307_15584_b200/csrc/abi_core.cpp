@@ -267,6 +267,54 @@ qmc_status qmc_lfsr_generator_vector(uint32_t seed, uint32_t dims, uint32_t* out
 
 uint32_t qmc_pixel_hash(uint32_t j, uint32_t px, uint32_t py) { return pixel_hash_host(j, px, py); }
 
+qmc_status qmc_hilbert_index(uint32_t x, uint32_t y, uint32_t order, uint64_t* out)
+{
+    return guard([&] {
+        if (!out)
+            fail(QMC_INVALID_ARGUMENT, "output pointer is null");
+        if (order == 0 || order > 31)
+            fail(QMC_INVALID_ARGUMENT, "hilbert_index: order must be in [1, 31]");
+        if (x >= (1u << order) || y >= (1u << order))
+            fail(QMC_OUT_OF_RANGE, "hilbert_index: pixel outside the 2^order grid");
+        *out = hilbert_index(x, y, order);
+    });
+}
+
+qmc_status qmc_hilbert_xy(uint64_t d, uint32_t order, uint32_t* x, uint32_t* y)
+{
+    return guard([&] {
+        if (!x || !y)
+            fail(QMC_INVALID_ARGUMENT, "output pointer is null");
+        if (order == 0 || order > 31)
+            fail(QMC_INVALID_ARGUMENT, "hilbert_xy: order must be in [1, 31]");
+        if (d >= (1ull << (2 * order)))
+            fail(QMC_OUT_OF_RANGE, "hilbert_xy: index beyond 4^order");
+        hilbert_xy_host(d, order, *x, *y);
+    });
+}
+
+uint64_t qmc_digit_reverse(uint64_t v, uint32_t base, uint32_t digits)
+{
+    return base < 2 ? 0 : digit_reverse_host(v, base, digits);
+}
+
+qmc_status qmc_lattice_shift_fixed(uint32_t k, uint32_t m, const uint32_t* g, uint32_t dims,
+                                   uint32_t* out)
+{
+    return guard([&] {
+        if ((!g || !out) && dims)
+            fail(QMC_INVALID_ARGUMENT, "generator or output pointer is null");
+        if (m > 32)
+            fail(QMC_INVALID_ARGUMENT, "lattice_shift: m must be <= 32");
+        const uint64_t scaled = static_cast<uint64_t>(k) << m;
+        if (scaled > 0xffffffffull)
+            fail(QMC_OVERFLOW, "lattice_shift: k * 2^m does not fit 32 bits");
+        const uint32_t rev = brev_host(static_cast<uint32_t>(scaled));
+        for (uint32_t j = 0; j < dims; ++j)
+            out[j] = rev * g[j];
+    });
+}
+
 uint32_t qmc_hilbert_order_for(uint32_t width, uint32_t height)
 {
     return hilbert_order(width, height);

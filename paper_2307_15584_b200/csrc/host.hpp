@@ -121,6 +121,7 @@ struct HaltonEnum {
 
 HaltonEnum halton_enum(uint32_t w, uint32_t h);                      // imageplane.cpp:80-98
 uint64_t digit_reverse_host(uint64_t v, uint32_t base, uint32_t digits);
+void hilbert_xy_host(uint64_t d, uint32_t order, uint32_t& x, uint32_t& y); // hilbert.hpp:59-78
 
 struct DigitTable {
     const uint32_t* ptr = nullptr;

@@ -234,6 +234,29 @@ HaltonEnum halton_enum(uint32_t w, uint32_t h)
     return e;
 }
 
+// hilbert.hpp:59-78, the inverse of hilbert_index for its orientation
+// (order validated by the caller).
+void hilbert_xy_host(uint64_t d, uint32_t order, uint32_t& x, uint32_t& y)
+{
+    x = y = 0;
+    const uint32_t n = 1u << order;
+    for (uint32_t s = 1; s < n; s <<= 1, d >>= 2) {
+        const uint32_t rx = 1u & static_cast<uint32_t>(d >> 1);
+        const uint32_t ry = 1u & static_cast<uint32_t>(d ^ rx);
+        if (ry == 0) { // rotate the s x s quadrant
+            if (rx == 1) {
+                x = s - 1 - x;
+                y = s - 1 - y;
+            }
+            const uint32_t tmp = x;
+            x = y;
+            y = tmp;
+        }
+        x += s * rx;
+        y += s * ry;
+    }
+}
+
 uint64_t digit_reverse_host(uint64_t v, uint32_t base, uint32_t digits)
 {
     uint64_t r = 0;

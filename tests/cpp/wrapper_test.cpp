@@ -55,6 +55,14 @@ static int host_checks()
     EXPECT(qmcgpu::hilbert_order_for(3840, 2160) == 12);
     const qmcgpu::HaltonPixelEnumeration e(3840, 2160);
     EXPECT(e.stride() == 8957952u && e.scale_x() == 4096 && e.scale_y() == 2187);
+    EXPECT(qmcgpu::hilbert_index({0, 1, 1}) == 1 && qmcgpu::hilbert_index({1, 0, 1}) == 3);
+    const auto hp = qmcgpu::hilbert_xy(qmcgpu::hilbert_index({5, 9, 4}), 4);
+    EXPECT(hp.x == 5 && hp.y == 9);
+    EXPECT(throws<std::invalid_argument>([] { qmcgpu::hilbert_index({0, 0, 0}); }));
+    EXPECT(throws<std::out_of_range>([] { qmcgpu::hilbert_index({16, 0, 4}); }));
+    EXPECT(qmcgpu::digit_reverse(5, 2, 3) == 5 && qmcgpu::digit_reverse(1, 3, 2) == 3);
+    EXPECT(throws<std::overflow_error>([&] { qmcgpu::lattice_shift_fixed(2, 32, g); }));
+    EXPECT(qmcgpu::lattice_shift_fixed(1, 31, g)[0] == 1u);
     const auto c = qmcgpu::partition_by_extra_dimension(1, 4, 2);
     EXPECT(c.remainder == 2 && c.modulus == 4);
     std::istringstream gv("# comment\n1\n1276675999 # second\n");

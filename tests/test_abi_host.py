@@ -207,3 +207,43 @@ def test_points_csv_format_host():
     x = rng.random((50, 3)).astype(np.float32)
     assert q.write_points_csv(x).decode() == "".join(
         ",".join("%.9f" % v for v in row) + "\n" for row in x.astype(np.float64))
+
+
+def test_hilbert_digit_reverse_lattice_shift_vs_reference(ref):
+    """Host helpers of the lattice / image-plane family against the
+    reference: values and exception classes (status codes match the shim's)."""
+    import ctypes as C
+
+    rng = np.random.default_rng(11)
+    L = q.lib()
+    for order in (1, 2, 5, 12, 16, 31):
+        n = 1 << order
+        for x, y in [(0, 0), (n - 1, n - 1)] + [tuple(int(v) for v in rng.integers(0, n, 2))
+                                                for _ in range(50)]:
+            d, e = C.c_uint64(), C.c_uint64()
+            assert ref.ref_hilbert_index(x, y, order, C.byref(e)) == 0
+            assert q.hilbert_index(x, y, order) == e.value
+            assert q.hilbert_xy(e.value, order) == (x, y)
+        for dd in [0, (1 << (2 * order)) - 1] + [int(v) for v in rng.integers(0, 1 << (2 * order),
+                                                                               20, dtype=np.uint64)]:
+            rx, ry = C.c_uint32(), C.c_uint32()
+            assert ref.ref_hilbert_xy(dd, order, C.byref(rx), C.byref(ry)) == 0
+            assert q.hilbert_xy(dd, order) == (rx.value, ry.value)
+    for args in [(0, 0, 0), (0, 0, 32), (2, 0, 1), (0, 4, 2)]:
+        d, e = C.c_uint64(), C.c_uint64()
+        assert L.qmc_hilbert_index(*args, C.byref(d)) == ref.ref_hilbert_index(*args, C.byref(e))
+    for args in [(0, 0), (4, 1), (16, 2)]:
+        a, b = C.c_uint32(), C.c_uint32()
+        assert L.qmc_hilbert_xy(*args, C.byref(a), C.byref(b)) == \
+            ref.ref_hilbert_xy(*args, C.byref(a), C.byref(b))
+    for v, b, k in [(0, 2, 0), (5, 2, 3), (12345678901, 3, 22), (2**64 - 1, 7, 20), (99, 10, 2)]:
+        assert q.digit_reverse(v, b, k) == ref.ref_digit_reverse(v, b, k)
+    g = np.array(q.lfsr_generator_vector(0xACE1, 8), np.uint32)
+    for k, m in [(0, 0), (1, 1), (3, 10), (5, 29), (1, 31), (0, 32)]:
+        exp = np.zeros(8, np.uint32)
+        assert ref.ref_lattice_shift_fixed(k, m, g.ctypes.data, 8, exp.ctypes.data) == 0
+        assert q.lattice_shift_fixed(k, m, g) == exp.tolist()
+    out = np.zeros(8, np.uint32)
+    for k, m in [(1, 33), (1, 32), (2, 32), (1 << 20, 20)]:
+        assert L.qmc_lattice_shift_fixed(k, m, g.ctypes.data, 8, out.ctypes.data) == \
+            ref.ref_lattice_shift_fixed(k, m, g.ctypes.data, 8, out.ctypes.data) != 0

@@ -432,6 +432,17 @@ def test_image_plane_halton_long_streams_vs_reference(ref, wh):
         np.testing.assert_array_equal(got, exp)
 
 
+def test_lattice_shifted_block_identity():
+    """SPEC.md:354-362 / lattice.cpp:157-170: block k of 2^m lattice points is
+    block 0 under the integer shift lattice_shift_fixed(k, m, g) — the CP-shift
+    input of the fill reproduces the index-offset fill bit for bit."""
+    g = q.lfsr_generator_vector(0xACE1, 16)
+    for k, m in [(1, 10), (5, 12), (77, 16), (3, 20)]:
+        direct = q.lattice_fill(1 << m, g, first=k << m, fixed=True)
+        shifted = q.lattice_fill(1 << m, g, shifts=q.lattice_shift_fixed(k, m, g), fixed=True)
+        assert torch.equal(direct, shifted), (k, m)
+
+
 # ------------------------------------------------ full-size properties
 @pytest.mark.slow
 def test_c2_full_size_properties(oracle, columns64):
