@@ -400,6 +400,22 @@ def run_render_distributed(q, world, stream):
             "value": 3840 * 2160 * spp / (ms * 1e-3) / 1e9, "unit": "G pixel-samples/s",
             "ms_per_step": ms, "n_gpus": world,
             "collective": "all_reduce(sum) of int64 accumulators (NCCL)"}
+    # §8f rank 1 across ranks: chunk ranges + one all-gather of the Kahan
+    # partials, combined by reduce_deterministic (bit-identical to 1 GPU)
+    from paper_2307_15584_b200.distributed import integrate_distributed
+
+    ni = 1 << 28
+    fn = lambda: integrate_distributed("sobol", "product-sine", ni, 8)  # noqa: E731
+    fn()
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = time.perf_counter()
+    est = fn()
+    sec = max_over_ranks(time.perf_counter() - t0, world)
+    res["integrate_sobol_product_sine_2^28x8"] = {
+        "value": ni * 8 / sec / 1e9, "unit": "Gsamples/s (host-timed, max over ranks)",
+        "n_gpus": world, "estimate": est,
+        "collective": "all_gather_into_tensor of chunk partials (NCCL) + reduce_deterministic"}
     return res
 
 

@@ -250,6 +250,23 @@ qmc_status qmc_integrate(qmc_sampler_kind kind, const qmc_stream_params* params,
                          qmc_integrand_kind f, uint32_t f_dims, uint64_t n, qmc_accum mode,
                          qmc_integration_row* row, qmc_stream stream);
 
+/* The same integration over only the 4096-index chunks [chunk_begin,
+ * chunk_end) of [0, n) — the per-rank share of a multi-GPU integration.
+ * Kahan mode: partials[chunk - chunk_begin] = the chunk's compensated sum
+ * (chunk_sum_kahan, quality.cpp:180-194). Int mode: *int_sum = the exact sum
+ * of llround(f * 2^32) over the range (quality.cpp:196-210). Combining all
+ * chunks' partials with qmc_reduce_deterministic (ranks = chunk indices), or
+ * adding the int sums, gives exactly qmc_integrate's estimate * n. */
+qmc_status qmc_integrate_partials(qmc_sampler_kind kind, const qmc_stream_params* params,
+                                  qmc_integrand_kind f, uint32_t f_dims, uint64_t n,
+                                  uint64_t chunk_begin, uint64_t chunk_end, qmc_accum mode,
+                                  double* partials, int64_t* int_sum, qmc_stream stream);
+
+/* reduce_deterministic (quality.cpp:158-166): the values sorted by rank
+ * (stable), then one CompensatedSum in rank order. */
+qmc_status qmc_reduce_deterministic(const uint64_t* ranks, const double* values, uint64_t count,
+                                    double* out);
+
 /* ------------------------------- quality metrics (quality.cpp:76-156) */
 /* Warnock's L2-star discrepancy of a row-major [n][dims] float point set
  * (device or host). Per-term products follow the reference's operation order;

@@ -133,6 +133,7 @@ def load_ref():
         _sig(lib, "ref_run_bench_kernel", i32, cstr, u64, u32, C.POINTER(f64), pu64)
         _sig(lib, "ref_integrate", i32, cstr, u32, u32, cstr, u64, cstr, u32, C.POINTER(f64))
         _sig(lib, "ref_neumaier", f64, P, u64)
+        _sig(lib, "ref_reduce_deterministic", f64, P, P, u64)
         _sig(lib, "ref_l2_star", i32, P, u64, u32, C.POINTER(f64))
         _sig(lib, "ref_min_toroidal", i32, P, u64, u32, C.POINTER(f64))
         _sig(lib, "ref_stratification", i32, cstr, u32, u32, u32, u32, C.POINTER(i32))

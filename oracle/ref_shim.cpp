@@ -541,4 +541,13 @@ double ref_neumaier(const double* v, std::uint64_t n)
     return s.value();
 }
 
+// reduce_deterministic (quality.cpp:158-166) over (rank, value) pairs
+double ref_reduce_deterministic(const std::uint32_t* ranks, const double* values, std::uint64_t n)
+{
+    std::vector<qmc::RankedPartial> p(n);
+    for (std::uint64_t k = 0; k < n; ++k)
+        p[k] = qmc::RankedPartial{ranks[k], values[k]};
+    return qmc::reduce_deterministic(std::move(p));
+}
+
 } // extern "C"

@@ -37,6 +37,7 @@ __all__ = [
     "min_toroidal_distance", "check_1d_stratification", "XorTables", "render_partial",
     "render_finalize", "load_generator_vector", "load_linear_factors", "fnv1a64", "write_pnm",
     "write_points_csv", "hilbert_index", "hilbert_xy", "digit_reverse", "lattice_shift_fixed",
+    "integrate_partials", "reduce_deterministic",
     "SAMPLER_KINDS",
 ]
 
@@ -110,6 +111,9 @@ def lib():
     sig("qmc_hilbert_order_for", u32, u32, u32)
     sig("qmc_partition_by_extra_dimension", i32, u32, u32, u32, C.POINTER(u64), C.POINTER(u64))
     sig("qmc_hilbert_index", i32, u32, u32, u32, C.POINTER(u64))
+    sig("qmc_integrate_partials", i32, i32, C.POINTER(StreamParams), i32, u32, u64, u64, u64, i32,
+        P, C.POINTER(C.c_int64), P)
+    sig("qmc_reduce_deterministic", i32, P, P, u64, C.POINTER(f64))
     sig("qmc_hilbert_xy", i32, u64, u32, C.POINTER(u32), C.POINTER(u32))
     sig("qmc_digit_reverse", u64, u64, u32, u32)
     sig("qmc_lattice_shift_fixed", i32, u32, u32, P, u32, P)
@@ -589,6 +593,43 @@ def integrate(kind: str, integrand: str, n: int, dims: int, accum: str = "kahan"
                                C.byref(row), _stream(stream)))
     return {"n": row.n, "estimate": row.estimate, "abs_error": row.abs_error,
             "seconds": row.seconds}
+
+
+def integrate_partials(kind: str, integrand: str, n: int, dims: int, chunk_begin: int,
+                       chunk_end: int, accum: str = "kahan", *, stream_dims: Optional[int] = None,
+                       generator=None, matrices: Optional[GeneratorMatrixSet] = None,
+                       sobol_scrambles=None, scramble: str = "plain", linear_factors=None,
+                       pixel=(0, 0), order: int = 1, spp: int = 1, width: int = 0,
+                       height: int = 0, xor_seed: int = 0, xor_point_count: int = 1, stream=None):
+    """The integration restricted to 4096-index chunks [chunk_begin, chunk_end)
+    of [0, n): a float64 array of the chunks' Kahan partials (kahan) or the
+    exact int64 sum of llround(f * 2^32) (int). Rank shares of a multi-GPU
+    integrate (paper_2307_15584_b200.distributed.integrate_distributed)."""
+    k = sampler_kind_from_name(kind)
+    if accum not in _ACCUM:
+        raise ConfigError("accumulation mode must be 'kahan' or 'int'")
+    if integrand not in _INTEGRANDS:
+        raise ConfigError("unknown integrand: " + integrand)
+    sd = dims if stream_dims is None else stream_dims
+    p, keep = _stream_params(sd, generator, matrices, sobol_scrambles, scramble, linear_factors,
+                             pixel, order, spp, width, height, xor_seed, xor_point_count)
+    parts = np.zeros(max(chunk_end - chunk_begin, 1), np.float64)
+    isum = C.c_int64(0)
+    _check(lib().qmc_integrate_partials(k, C.byref(p), _INTEGRANDS[integrand], dims, n,
+                                        chunk_begin, chunk_end, _ACCUM[accum], parts.ctypes.data,
+                                        C.byref(isum), _stream(stream)))
+    return parts[:chunk_end - chunk_begin] if accum == "kahan" else isum.value
+
+
+def reduce_deterministic(ranks, values) -> float:
+    """reduce_deterministic (quality.cpp:158-166): CompensatedSum in rank order."""
+    r = np.ascontiguousarray(ranks, dtype=np.uint64)
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    if r.size != v.size:
+        raise ValueError("ranks and values differ in length")
+    out = f64()
+    _check(lib().qmc_reduce_deterministic(r.ctypes.data, v.ctypes.data, r.size, C.byref(out)))
+    return out.value
 
 
 def render(width: int, height: int, spp: int = 1, kind: str = "pixel-shifted-lattice",

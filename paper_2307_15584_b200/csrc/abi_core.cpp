@@ -758,93 +758,124 @@ qmc_status qmc_builtin_integrand(const char* name, uint32_t dims, qmc_integrand_
     });
 }
 
+} // extern "C"
+
+namespace {
+
+// integrate() (quality.cpp:214-282) over the 4096-index chunks [c0, c1) of
+// [0, n): validation with the reference's conditions, one launch, and the
+// per-chunk Kahan partials (kahan mode) or the exact int64 sum (int mode).
+void integrate_chunks(qmc_sampler_kind kind, const qmc_stream_params* p, qmc_integrand_kind f,
+                      uint32_t f_dims, uint64_t n, uint64_t c0, uint64_t c1, qmc_accum mode,
+                      cudaStream_t s, std::vector<double>& partials, long long& isum)
+{
+    if (f < 0 || f > 2)
+        fail(QMC_CONFIG, "unknown integrand");
+    if (f_dims == 0)
+        fail(QMC_INVALID_ARGUMENT, "builtin_integrands: dims must be >= 1");
+    if (mode != QMC_ACCUM_KAHAN && mode != QMC_ACCUM_INT)
+        fail(QMC_CONFIG, "accumulation mode must be 'kahan' or 'int'");
+    if (n == 0)
+        fail(QMC_INVALID_ARGUMENT, "integrate: n must be >= 1");
+    if (!p)
+        fail(QMC_INVALID_ARGUMENT, "stream params are null");
+    if (p->dims < f_dims)
+        fail(QMC_INVALID_ARGUMENT, "integrate: stream has fewer dimensions than the integrand");
+    if (f_dims > integrate_max_dims())
+        fail(QMC_INVALID_ARGUMENT, "integrate: at most 64 integrand dimensions on the device");
+    const uint64_t chunks = (n + 4095) / 4096;
+    if (c0 > c1 || c1 > chunks)
+        fail(QMC_OUT_OF_RANGE, "integrate: chunk range outside [0, ceil(n / 4096))");
+    CallArgs args(s), pargs(s);
+    ResolvedStream r;
+    resolve_stream(kind, p, s, r, args, pargs);
+    // sample-time preconditions of SampleStream::sample over [0, n)
+    if (kind == QMC_KIND_SOBOL && n > (1ull << 52))
+        fail(QMC_INVALID_ARGUMENT, "sobol_component: index must be below 2^52");
+    if (kind == QMC_KIND_HALTON_HILBERT && n > p->spp)
+        fail(QMC_OUT_OF_RANGE, "SampleStream: sample index beyond the pixel block");
+    if (kind == QMC_KIND_SOBOL_XOR_TABLE && n > r.q.xor_point_count)
+        fail(QMC_OUT_OF_RANGE, "xor_table_sample: index beyond the stored point set");
+    if (kind == QMC_KIND_HALTON || kind == QMC_KIND_HALTON_HILBERT ||
+        kind == QMC_KIND_IMAGE_PLANE_HALTON)
+        for (const RadicalDim& d : r.rd)
+            if (d.mode == 1 && (d.factor == 0 || d.factor >= d.base))
+                fail(QMC_INVALID_ARGUMENT,
+                     "radical_inverse_linscramble: factor must be in [1, base)");
+
+    const uint32_t dims_of_integrand = p->dims; // stream dims (>= f_dims)
+    IntegrateParams ip{};
+    ip.pix = r.q;
+    ip.fn = f;
+    ip.fdims = f_dims;
+    ip.n = n;
+    ip.sc = make_scene_consts();
+    ip.chunk0 = c0;
+    ip.nchunks = c1 - c0;
+    if (kind == QMC_KIND_SOBOL) {
+        const auto& dev = r.matrices->on_device(dims_of_integrand);
+        ip.colsT = static_cast<const uint32_t*>(dev.colsT.get());
+        ip.mdims = dims_of_integrand;
+        ip.words = r.woff == SIZE_MAX ? nullptr : args.at<uint32_t>(r.woff);
+    }
+    const uint64_t nc = c1 - c0;
+    double* partial = nullptr;
+    unsigned long long* scal = nullptr; // [0] int sum, [1] first bad index
+    cuda_ok(cudaMallocAsync(&partial, nc * 8 + 8, s), "cudaMallocAsync");
+    cuda_ok(cudaMallocAsync(&scal, 16, s), "cudaMallocAsync");
+    const unsigned long long init[2] = {0ull, ~0ull};
+    cuda_ok(cudaMemcpyAsync(scal, init, 16, cudaMemcpyHostToDevice, s), "H2D");
+    cuda_ok(launch_integrate(ip, mode, partial, scal, scal + 1, s), "launch_integrate");
+    partials.assign(mode == QMC_ACCUM_KAHAN ? nc : 0, 0.0);
+    unsigned long long hs[2] = {0, 0};
+    if (!partials.empty())
+        cuda_ok(cudaMemcpyAsync(partials.data(), partial, nc * 8, cudaMemcpyDeviceToHost, s),
+                "D2H");
+    cuda_ok(cudaMemcpyAsync(hs, scal, 16, cudaMemcpyDeviceToHost, s), "D2H");
+    cudaFreeAsync(partial, s);
+    cudaFreeAsync(scal, s);
+    cuda_ok(cudaStreamSynchronize(s), "sync");
+    if (hs[1] != ~0ull)
+        fail(QMC_INTERNAL, std::string("integrate: non-finite value of '") + kIntegrandNames[f] +
+                               "' at index " + std::to_string(hs[1]));
+    isum = static_cast<long long>(hs[0]);
+}
+
+// CompensatedSum (quality.hpp:18-33) over values in the given order.
+double compensated_sum(const double* v, uint64_t count)
+{
+    double sum = 0.0, comp = 0.0;
+    for (uint64_t k = 0; k < count; ++k) {
+        const double t = sum + v[k];
+        if (std::fabs(sum) >= std::fabs(v[k]))
+            comp += (sum - t) + v[k];
+        else
+            comp += (v[k] - t) + sum;
+        sum = t;
+    }
+    return sum + comp;
+}
+
+} // namespace
+
+extern "C" {
+
 qmc_status qmc_integrate(qmc_sampler_kind kind, const qmc_stream_params* p,
                          qmc_integrand_kind f, uint32_t f_dims, uint64_t n, qmc_accum mode,
                          qmc_integration_row* row, qmc_stream stream)
 {
     return guard([&] {
         const auto t0 = std::chrono::steady_clock::now();
-        const cudaStream_t s = as_stream(stream);
-        if (f < 0 || f > 2)
-            fail(QMC_CONFIG, "unknown integrand");
-        if (f_dims == 0)
-            fail(QMC_INVALID_ARGUMENT, "builtin_integrands: dims must be >= 1");
-        if (mode != QMC_ACCUM_KAHAN && mode != QMC_ACCUM_INT)
-            fail(QMC_CONFIG, "accumulation mode must be 'kahan' or 'int'");
-        if (n == 0)
-            fail(QMC_INVALID_ARGUMENT, "integrate: n must be >= 1");
-        if (!p)
-            fail(QMC_INVALID_ARGUMENT, "stream params are null");
-        if (p->dims < f_dims)
-            fail(QMC_INVALID_ARGUMENT, "integrate: stream has fewer dimensions than the integrand");
-        if (f_dims > integrate_max_dims())
-            fail(QMC_INVALID_ARGUMENT, "integrate: at most 64 integrand dimensions on the device");
-        CallArgs args(s), pargs(s);
-        ResolvedStream r;
-        resolve_stream(kind, p, s, r, args, pargs);
-        // sample-time preconditions of SampleStream::sample over [0, n)
-        if (kind == QMC_KIND_SOBOL && n > (1ull << 52))
-            fail(QMC_INVALID_ARGUMENT, "sobol_component: index must be below 2^52");
-        if (kind == QMC_KIND_HALTON_HILBERT && n > p->spp)
-            fail(QMC_OUT_OF_RANGE, "SampleStream: sample index beyond the pixel block");
-        if (kind == QMC_KIND_SOBOL_XOR_TABLE && n > r.q.xor_point_count)
-            fail(QMC_OUT_OF_RANGE, "xor_table_sample: index beyond the stored point set");
-        if (kind == QMC_KIND_HALTON || kind == QMC_KIND_HALTON_HILBERT ||
-            kind == QMC_KIND_IMAGE_PLANE_HALTON)
-            for (const RadicalDim& d : r.rd)
-                if (d.mode == 1 && (d.factor == 0 || d.factor >= d.base))
-                    fail(QMC_INVALID_ARGUMENT,
-                         "radical_inverse_linscramble: factor must be in [1, base)");
-
-        const uint32_t dims_of_integrand = p->dims; // stream dims (>= f_dims)
-        IntegrateParams ip{};
-        ip.pix = r.q;
-        ip.fn = f;
-        ip.fdims = f_dims;
-        ip.n = n;
-        ip.sc = make_scene_consts();
-        if (kind == QMC_KIND_SOBOL) {
-            const auto& dev = r.matrices->on_device(dims_of_integrand);
-            ip.colsT = static_cast<const uint32_t*>(dev.colsT.get());
-            ip.mdims = dims_of_integrand;
-            ip.words = r.woff == SIZE_MAX ? nullptr : args.at<uint32_t>(r.woff);
-        }
-        const uint64_t chunks = (n + 4095) / 4096;
-        double* partial = nullptr;
-        unsigned long long* scal = nullptr; // [0] int sum, [1] first bad index
-        cuda_ok(cudaMallocAsync(&partial, chunks * 8, s), "cudaMallocAsync");
-        cuda_ok(cudaMallocAsync(&scal, 16, s), "cudaMallocAsync");
-        const unsigned long long init[2] = {0ull, ~0ull};
-        cuda_ok(cudaMemcpyAsync(scal, init, 16, cudaMemcpyHostToDevice, s), "H2D");
-        cuda_ok(launch_integrate(ip, mode, partial, scal, scal + 1, s), "launch_integrate");
-        std::vector<double> hp(mode == QMC_ACCUM_KAHAN ? chunks : 0);
-        unsigned long long hs[2] = {0, 0};
-        if (!hp.empty())
-            cuda_ok(cudaMemcpyAsync(hp.data(), partial, chunks * 8, cudaMemcpyDeviceToHost, s),
-                    "D2H");
-        cuda_ok(cudaMemcpyAsync(hs, scal, 16, cudaMemcpyDeviceToHost, s), "D2H");
-        cudaFreeAsync(partial, s);
-        cudaFreeAsync(scal, s);
-        cuda_ok(cudaStreamSynchronize(s), "sync");
-        if (hs[1] != ~0ull)
-            fail(QMC_INTERNAL, std::string("integrate: non-finite value of '") +
-                                   kIntegrandNames[f] + "' at index " + std::to_string(hs[1]));
-        double estimate;
-        if (mode == QMC_ACCUM_KAHAN) { // rank-ordered CompensatedSum, quality.cpp:262-267
-            double sum = 0.0, comp = 0.0;
-            for (double v : hp) {
-                const double t = sum + v;
-                if (std::fabs(sum) >= std::fabs(v))
-                    comp += (sum - t) + v;
-                else
-                    comp += (v - t) + sum;
-                sum = t;
-            }
-            estimate = (sum + comp) / static_cast<double>(n);
-        } else { // exact 64-bit sum, quality.cpp:268-272
-            estimate = static_cast<double>(static_cast<long long>(hs[0])) / 4294967296.0 /
-                       static_cast<double>(n);
-        }
+        std::vector<double> partials;
+        long long isum = 0;
+        integrate_chunks(kind, p, f, f_dims, n, 0, (n + 4095) / 4096, mode, as_stream(stream),
+                         partials, isum);
+        // rank-ordered CompensatedSum of the chunk partials (quality.cpp:262-267),
+        // or the exact 64-bit sum (quality.cpp:268-272)
+        const double estimate =
+            mode == QMC_ACCUM_KAHAN
+                ? compensated_sum(partials.data(), partials.size()) / static_cast<double>(n)
+                : static_cast<double>(isum) / 4294967296.0 / static_cast<double>(n);
         double exact = 1.0;
         qmc_builtin_integrand(kIntegrandNames[f], f_dims, nullptr, &exact);
         if (row) {
@@ -854,6 +885,45 @@ qmc_status qmc_integrate(qmc_sampler_kind kind, const qmc_stream_params* p,
             row->seconds =
                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         }
+    });
+}
+
+qmc_status qmc_integrate_partials(qmc_sampler_kind kind, const qmc_stream_params* p,
+                                  qmc_integrand_kind f, uint32_t f_dims, uint64_t n,
+                                  uint64_t chunk_begin, uint64_t chunk_end, qmc_accum mode,
+                                  double* partials, int64_t* int_sum, qmc_stream stream)
+{
+    return guard([&] {
+        if (mode == QMC_ACCUM_KAHAN && !partials && chunk_end > chunk_begin)
+            fail(QMC_INVALID_ARGUMENT, "partials pointer is null");
+        if (mode == QMC_ACCUM_INT && !int_sum)
+            fail(QMC_INVALID_ARGUMENT, "int_sum pointer is null");
+        std::vector<double> hp;
+        long long isum = 0;
+        integrate_chunks(kind, p, f, f_dims, n, chunk_begin, chunk_end, mode, as_stream(stream),
+                         hp, isum);
+        if (mode == QMC_ACCUM_KAHAN)
+            std::memcpy(partials, hp.data(), hp.size() * 8);
+        else
+            *int_sum = isum;
+    });
+}
+
+qmc_status qmc_reduce_deterministic(const uint64_t* ranks, const double* values, uint64_t count,
+                                    double* out)
+{
+    return guard([&] {
+        if (!out || (count && (!ranks || !values)))
+            fail(QMC_INVALID_ARGUMENT, "null pointer");
+        std::vector<uint64_t> order(count);
+        for (uint64_t k = 0; k < count; ++k)
+            order[k] = k;
+        std::stable_sort(order.begin(), order.end(),
+                         [&](uint64_t a, uint64_t b) { return ranks[a] < ranks[b]; });
+        std::vector<double> v(count);
+        for (uint64_t k = 0; k < count; ++k)
+            v[k] = values[order[k]];
+        *out = compensated_sum(v.data(), count);
     });
 }
 

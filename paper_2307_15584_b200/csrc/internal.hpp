@@ -112,8 +112,9 @@ struct IntegrateParams {
     uint64_t n;
     const uint32_t* colsT; // sobol: device [52][mdims]
     uint32_t mdims;
-    const uint32_t* words; // sobol: device XOR scrambles or null
-    SceneConsts sc;          // product-sine's sine (sin_cw)
+    const uint32_t* words;    // sobol: device XOR scrambles or null
+    SceneConsts sc;           // product-sine's sine (sin_cw)
+    uint64_t chunk0, nchunks; // this launch: 4096-index chunks [chunk0, chunk0 + nchunks)
 };
 
 // ------------------------------------------------------------ launchers

@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(kBlock)
     __shared__ uint32_t E[5][kMaxDims]; // sobol: XOR of columns 7..7+c
     __shared__ uint32_t XB[kMaxDims];   // sobol: value of `begin` (scramble included)
     __shared__ long long red[kBlock / 32];
-    const uint64_t chunk = blockIdx.x;
+    const uint64_t chunk = p.chunk0 + blockIdx.x;
     const uint64_t begin = chunk * 4096;
     const uint32_t count = static_cast<uint32_t>(p.n - begin < 4096 ? p.n - begin : 4096);
     const uint32_t dims = p.fdims;
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kBlock)
             double sum = 0.0, comp = 0.0;
             for (uint32_t k = 0; k < count; ++k)
                 neumaier_add(sum, comp, vals[k]);
-            partial[chunk] = __dadd_rn(sum, comp);
+            partial[blockIdx.x] = __dadd_rn(sum, comp);
         }
     } else {
         for (int o = 16; o; o >>= 1)
@@ -197,10 +197,11 @@ template <uint32_t KIND, uint32_t FN>
 cudaError_t integrate_kind_fn(const IntegrateParams& p, uint32_t accum, double* partial,
                               unsigned long long* isum, unsigned long long* bad, cudaStream_t s)
 {
-    const uint64_t chunks = (p.n + 4095) / 4096;
-    if (chunks > 0x7fffffffull)
+    if (p.nchunks == 0)
+        return cudaSuccess;
+    if (p.nchunks > 0x7fffffffull)
         return cudaErrorInvalidValue;
-    const unsigned grid = static_cast<unsigned>(chunks);
+    const unsigned grid = static_cast<unsigned>(p.nchunks);
     if (accum == 0)
         k_integrate<KIND, FN, 0><<<grid, kBlock, 0, s>>>(p, partial, isum, bad);
     else

@@ -12,6 +12,11 @@ Two partitionings:
   all-gather of the fp32 bands (NCCL over NVLink on a GPU box, gloo in the
   CPU tests) — assembles the image (`render_distributed`).
 
+* Integration (quality.cpp:214-282) splits the fixed 4096-index chunks into
+  contiguous rank ranges; the Kahan chunk partials are all-gathered and
+  combined by reduce_deterministic in chunk order (or the exact int64 sums
+  all-reduced), so the estimate is bit-identical to the single-GPU one
+  (`integrate_distributed`).
 * The paper's own split (`partition_by_extra_dimension`,
   imageplane.cpp:114-130): every GPU renders ALL pixels but only its residue
   class of samples, i == rev_2(rank) (mod world), into int64 accumulators;
@@ -105,3 +110,54 @@ def render_distributed(width: int, height: int, spp: int, kind: str = "pixel-shi
     else:
         band = band_renderer(r0, r1)
     return gather_bands(band, height, width, group)
+
+
+def chunk_range(n: int, world: int, rank: int) -> Tuple[int, int]:
+    """Rank's contiguous share [c0, c1) of the ceil(n / 4096) integration chunks."""
+    chunks = (n + 4095) // 4096
+    return chunks * rank // world, chunks * (rank + 1) // world
+
+
+def integrate_distributed(kind: str, integrand: str, n: int, dims: int, accum: str = "kahan",
+                          group=None, partials_fn: Optional[Callable] = None,
+                          reduce_fn: Optional[Callable] = None, **stream_kw) -> float:
+    """Multi-rank integrate(): each rank evaluates its chunk range on its GPU
+    (qmc_integrate_partials); Kahan partials are gathered to every rank (one
+    all-gather of the padded per-rank vectors) and summed in chunk order by
+    reduce_deterministic; int sums take one all-reduce. Returns the estimate,
+    bit-identical to the single-GPU qmc_integrate. `partials_fn(c0, c1)` and
+    `reduce_fn(ranks, values)` default to the CUDA path; tests inject CPU
+    stand-ins."""
+    import numpy as np
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    c0, c1 = chunk_range(n, world, rank)
+    if partials_fn is None:
+        from . import integrate_partials
+
+        def partials_fn(a, b):
+            return integrate_partials(kind, integrand, n, dims, a, b, accum, **stream_kw)
+    if reduce_fn is None:
+        from . import reduce_deterministic as reduce_fn
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else \
+        torch.device("cpu")
+    if accum == "int":
+        t = torch.tensor([int(partials_fn(c0, c1))], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)  # exact
+        return float(int(t.item())) / 4294967296.0 / n
+    mine = np.asarray(partials_fn(c0, c1), np.float64)
+    chunks = (n + 4095) // 4096
+    width = max(chunks * (r + 1) // world - chunks * r // world for r in range(world))
+    pad = torch.zeros(width, dtype=torch.float64, device=dev)
+    pad[: mine.size] = torch.from_numpy(mine).to(dev)
+    full = torch.empty(world * width, dtype=torch.float64, device=dev)
+    dist.all_gather_into_tensor(full, pad, group=group)
+    full = full.cpu().numpy()
+    ranks, values = [], []
+    for r in range(world):
+        a, b = chunk_range(n, world, r)
+        ranks.extend(range(a, b))
+        values.extend(full[r * width: r * width + (b - a)].tolist())
+    return reduce_fn(ranks, values) / n

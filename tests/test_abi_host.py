@@ -247,3 +247,15 @@ def test_hilbert_digit_reverse_lattice_shift_vs_reference(ref):
     for k, m in [(1, 33), (1, 32), (2, 32), (1 << 20, 20)]:
         assert L.qmc_lattice_shift_fixed(k, m, g.ctypes.data, 8, out.ctypes.data) == \
             ref.ref_lattice_shift_fixed(k, m, g.ctypes.data, 8, out.ctypes.data) != 0
+
+
+def test_reduce_deterministic_vs_reference(ref):
+    """reduce_deterministic (quality.cpp:158-166): rank-sorted CompensatedSum,
+    bit-identical for shuffled ranks and values spanning many magnitudes."""
+    rng = np.random.default_rng(5)
+    for n in (0, 1, 7, 1000, 20000):
+        ranks = rng.permutation(n).astype(np.uint32)
+        vals = rng.standard_normal(n) * 10.0 ** rng.integers(-12, 12, n)
+        got = q.reduce_deterministic(ranks, vals)
+        exp = ref.ref_reduce_deterministic(ranks.ctypes.data, vals.ctypes.data, n)
+        assert got == exp or (np.isnan(got) and np.isnan(exp)), n

@@ -110,3 +110,45 @@ def test_render_sample_partition_gloo(tmp_path, oracle, columns64, world):
     mp.spawn(_worker_samples, args=(world, _free_port(), w, h, spp, cols_path, out_path),
              nprocs=world, join=True)
     np.testing.assert_array_equal(np.load(out_path), full)
+
+
+def _worker_integrate(rank, world, port, n, accum, vals_path, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2307_15584_b200.distributed import integrate_distributed
+
+    vals = np.load(vals_path)  # stand-in chunk partials (kahan) / chunk int sums (int)
+
+    def partials(c0, c1):
+        return vals[c0:c1] if accum == "kahan" else int(vals[c0:c1].astype(np.int64).sum())
+
+    est = integrate_distributed("sobol", "product-sine", n, 4, accum, partials_fn=partials)
+    if rank == 0:
+        np.save(out_path, np.array([est]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("accum", ["kahan", "int"])
+def test_integrate_distributed_gloo(tmp_path, world, accum):
+    """Chunk ranges per rank + one all-gather and the rank-ordered
+    reduce_deterministic (or one int all-reduce) reproduce the single-process
+    combine exactly."""
+    import paper_2307_15584_b200 as q
+
+    n = 4096 * 37 + 5
+    chunks = (n + 4095) // 4096
+    rng = np.random.default_rng(world)
+    if accum == "kahan":
+        vals = rng.standard_normal(chunks) * 10.0 ** rng.integers(-8, 8, chunks)
+        exp = q.reduce_deterministic(np.arange(chunks), vals) / n
+    else:
+        vals = rng.integers(-2**40, 2**40, chunks).astype(np.float64)
+        exp = float(int(vals.astype(np.int64).sum())) / 4294967296.0 / n
+    vp, op = str(tmp_path / "v.npy"), str(tmp_path / "o.npy")
+    np.save(vp, vals)
+    mp.spawn(_worker_integrate, args=(world, _free_port(), n, accum, vp, op), nprocs=world,
+             join=True)
+    assert np.load(op)[0] == exp

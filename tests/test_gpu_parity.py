@@ -443,6 +443,33 @@ def test_lattice_shifted_block_identity():
         assert torch.equal(direct, shifted), (k, m)
 
 
+@pytest.mark.parametrize("kind", ["sobol", "lattice", "halton", "image-plane-halton"])
+def test_integrate_partials_split_equals_whole(kind):
+    """qmc_integrate_partials over any split of the chunk range, combined by
+    reduce_deterministic in chunk order (kahan) or summed (int), is exactly
+    qmc_integrate's estimate — the multi-GPU integrate's invariant."""
+    n, dims = 4096 * 53 + 77, 5
+    kw = {"generator": q.lfsr_generator_vector(0xACE1, dims)} if kind == "lattice" else {}
+    if kind == "image-plane-halton":
+        kw.update(width=64, height=27, pixel=(3, 4))
+    chunks = (n + 4095) // 4096
+    for accum in ("kahan", "int"):
+        whole = q.integrate(kind, "product-sine", n, dims, accum, **kw)["estimate"]
+        cuts = [0, 1, 17, 40, chunks]
+        if accum == "kahan":
+            vals = np.concatenate([q.integrate_partials(kind, "product-sine", n, dims, a, b,
+                                                        accum, **kw)
+                                   for a, b in zip(cuts, cuts[1:])])
+            est = q.reduce_deterministic(np.arange(chunks)[::-1], vals[::-1]) / n
+        else:
+            tot = sum(q.integrate_partials(kind, "product-sine", n, dims, a, b, accum, **kw)
+                      for a, b in zip(cuts, cuts[1:]))
+            est = float(tot) / 4294967296.0 / n
+        assert est == whole, (kind, accum)
+    with pytest.raises(IndexError):
+        q.integrate_partials(kind, "product-sine", n, dims, 3, chunks + 1, **kw)
+
+
 # ------------------------------------------------ full-size properties
 @pytest.mark.slow
 def test_c2_full_size_properties(oracle, columns64):
