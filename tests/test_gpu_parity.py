@@ -470,6 +470,47 @@ def test_integrate_partials_split_equals_whole(kind):
         q.integrate_partials(kind, "product-sine", n, dims, 3, chunks + 1, **kw)
 
 
+def _nccl_world1_worker(rank, port, out_path):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    from paper_2307_15584_b200.distributed import (integrate_distributed, render_distributed,
+                                                   render_distributed_samples)
+
+    a = render_distributed(96, 40, 8).cpu().numpy()
+    b = render_distributed_samples(96, 40, 8).cpu().numpy()
+    e1 = integrate_distributed("sobol", "product-sine", 4096 * 9 + 1, 4)
+    e2 = integrate_distributed("sobol", "product-sine", 4096 * 9 + 1, 4, "int")
+    np.savez(out_path, a=a, b=b, e=np.array([e1, e2]))
+    dist.destroy_process_group()
+
+
+def test_distributed_paths_on_nccl_world1(tmp_path):
+    """The multi-GPU drivers on a real NCCL group (world size 1 on this box):
+    device placement and collectives run, results equal the 1-GPU calls."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    out = str(tmp_path / "r.npz")
+    mp.spawn(_nccl_world1_worker, args=(port, out), nprocs=1, join=True)
+    r = np.load(out)
+    np.testing.assert_array_equal(r["a"], q.render(96, 40, 8).cpu().numpy())
+    np.testing.assert_array_equal(r["b"], q.render(96, 40, 8, accum="int").cpu().numpy())
+    assert r["e"][0] == q.integrate("sobol", "product-sine", 4096 * 9 + 1, 4)["estimate"]
+    assert r["e"][1] == q.integrate("sobol", "product-sine", 4096 * 9 + 1, 4, "int")["estimate"]
+
+
 # ------------------------------------------------ full-size properties
 @pytest.mark.slow
 def test_c2_full_size_properties(oracle, columns64):
