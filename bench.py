@@ -133,25 +133,60 @@ def max_over_ranks(x: float, world: int) -> float:
 
 
 # --------------------------------------------------------- reference arm
-def cpu_sobol_sample(ref, n_pts: int, threads: int, first: int = 0) -> float:
-    """Seconds for the reference qmc::sobol_component over n_pts x 32 dims."""
-    import numpy as np
+class CpuSobol:
+    """The CPU implementation timed beside the GPU (cpu_baseline and --impl
+    reference): the unmodified reference build (oracle/_ref, kind
+    "reference") on all host threads, or — if that build is absent — the C
+    restatement (oracle/, kind "port") on as many Python threads (ctypes
+    releases the GIL)."""
 
-    from oracle import ptr
+    def __init__(self):
+        from oracle import load_oracle, load_ref, ref_available
 
-    out = np.empty((n_pts, DIMS), np.float32)
-    t0 = time.perf_counter()
-    rc = ref.ref_sobol_fill(first, n_pts, DIMS, None, ptr(out), threads)
-    dt = time.perf_counter() - t0
-    if rc != 0:
-        raise RuntimeError(ref.ref_last_error().decode())
-    return dt
+        if ref_available():
+            self.kind, self.lib = "reference", load_ref()
+            self.what = "qmc::sobol_component, reference build"
+        else:
+            import numpy as np
+
+            import paper_2307_15584_b200 as q
+
+            self.kind, self.lib = "port", load_oracle()
+            self.cols = np.ascontiguousarray(q.GeneratorMatrixSet.builtin(DIMS).columns(),
+                                             dtype=np.uint32)
+            self.what = "oracle qo_sobol_fill_f32 (C restatement)"
+
+    def sample(self, n_pts: int, threads: int, first: int = 0) -> float:
+        """Seconds for n_pts x 32 dims of float Sobol' points on the CPU."""
+        import numpy as np
+
+        from oracle import ptr
+
+        out = np.empty((n_pts, DIMS), np.float32)
+        t0 = time.perf_counter()
+        if self.kind == "reference":
+            rc = self.lib.ref_sobol_fill(first, n_pts, DIMS, None, ptr(out), threads)
+            if rc != 0:
+                raise RuntimeError(self.lib.ref_last_error().decode())
+        else:
+            from concurrent.futures import ThreadPoolExecutor
+
+            cuts = [n_pts * t // threads for t in range(threads + 1)]
+
+            def run(t):
+                a, b = cuts[t], cuts[t + 1]
+                self.lib.qo_sobol_fill_f32(first + a, b - a, DIMS, ptr(self.cols), None,
+                                           out[a:].ctypes.data)
+
+            with ThreadPoolExecutor(threads) as ex:
+                list(ex.map(run, range(threads)))
+        return time.perf_counter() - t0
 
 
-def calibrate_cpu(ref, threads: int, target_s: float) -> int:
+def calibrate_cpu(cpu: "CpuSobol", threads: int, target_s: float) -> int:
     n = 1 << 16
     while True:
-        dt = cpu_sobol_sample(ref, n, threads)
+        dt = cpu.sample(n, threads)
         if dt > 0.25 or n >= (1 << 26):
             break
         n <<= 2
@@ -163,24 +198,22 @@ def run_reference(args):
     world, rank, _ = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
     if rank != 0:
         return 0
-    from oracle import load_ref
-
-    ref = load_ref()
+    cpu = CpuSobol()
     threads = os.cpu_count() or 1
-    n_pts = calibrate_cpu(ref, threads, 3.0)
+    n_pts = calibrate_cpu(cpu, threads, 3.0)
     for _ in range(args.warmup):
-        cpu_sobol_sample(ref, n_pts, threads)
-    times = [cpu_sobol_sample(ref, n_pts, threads) for _ in range(args.steps)]
+        cpu.sample(n_pts, threads)
+    times = [cpu.sample(n_pts, threads) for _ in range(args.steps)]
     sec = statistics.median(times)
     value = n_pts * DIMS / sec / 1e9
-    sample = "%d points x %d dims per step (qmc::sobol_component, %d threads)" % (n_pts, DIMS, threads)
+    sample = "%d points x %d dims per step (%s, %d threads)" % (n_pts, DIMS, cpu.what, threads)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "impl": "reference",
         "config": {"workload": WORKLOAD, "points": N_POINTS, "dims": DIMS, "sampled": True},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": cpu.kind,
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -312,17 +345,13 @@ def run_ours(args):
     cpu = None
     if rank == 0 and not args.no_cpu:
         try:
-            from oracle import load_ref, ref_available
-
-            if ref_available():
-                ref = load_ref()
-                threads = os.cpu_count() or 1
-                n_pts = calibrate_cpu(ref, threads, args.cpu_seconds)
-                sec = cpu_sobol_sample(ref, n_pts, threads)
-                cpu = {"value": n_pts * DIMS / sec / 1e9, "unit": UNIT, "cores": threads,
-                       "kind": "reference",
-                       "sample": "%d points x %d dims (qmc::sobol_component, reference build, "
-                                 "%.1f s)" % (n_pts, DIMS, sec)}
+            impl = CpuSobol()
+            threads = os.cpu_count() or 1
+            n_pts = calibrate_cpu(impl, threads, args.cpu_seconds)
+            sec = impl.sample(n_pts, threads)
+            cpu = {"value": n_pts * DIMS / sec / 1e9, "unit": UNIT, "cores": threads,
+                   "kind": impl.kind,
+                   "sample": "%d points x %d dims (%s, %.1f s)" % (n_pts, DIMS, impl.what, sec)}
         except Exception as e:  # pragma: no cover
             cpu = {"error": str(e)}
 

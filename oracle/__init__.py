@@ -63,6 +63,7 @@ def load_oracle():
         _sig(lib, "qo_build_matrices", None, u32, P, P, P, P)
         _sig(lib, "qo_sobol_component_fixed", u32, u64, P, u32)
         _sig(lib, "qo_sobol_fill_fixed", None, u64, u64, u32, P, P, P)
+        _sig(lib, "qo_sobol_fill_f32", None, u64, u64, u32, P, P, P)
         _sig(lib, "qo_owen_scramble", u32, u32, u32)
         _sig(lib, "qo_sobol_owen_fill_fixed", None, u64, u64, u32, P, P, P)
         _sig(lib, "qo_lattice_component_fixed", u32, u32, u32)

@@ -283,6 +283,20 @@ void qo_sobol_fill_fixed(uint64_t first, uint64_t n, uint32_t dims, const uint32
                                                          scrambles ? scrambles[j] : 0u);
 }
 
+/* sobol_point as floats (digitalnet.cpp:141-151 + unitfloat.hpp:34-50): the
+ * CPU "port" timing of bench.py --impl reference when the reference build is
+ * absent (the checker is never the thing measured on the GPU side). */
+void qo_sobol_fill_f32(uint64_t first, uint64_t n, uint32_t dims, const uint32_t* columns,
+                       const uint32_t* scrambles, float* out)
+{
+    for (uint64_t k = 0; k < n; ++k)
+        for (uint32_t j = 0; j < dims; ++j) {
+            const uint32_t b = qo_map_bits(qo_sobol_component_fixed(
+                first + k, columns + 52u * j, scrambles ? scrambles[j] : 0u));
+            memcpy(out + k * dims + j, &b, 4);
+        }
+}
+
 /* Hash-based Owen scrambling — BUILDER-DEFINED, no reference counterpart
  * (SPEC.md:271 lists Owen trees as a non-goal). The 32-bit
  * fixed-point value v is bit-reversed, so digit k (from the most significant

@@ -54,6 +54,8 @@ void qo_build_matrices(uint32_t dims, const uint32_t* s, const uint32_t* a,
 uint32_t qo_sobol_component_fixed(uint64_t i, const uint32_t* columns_j, uint32_t scramble);
 void qo_sobol_fill_fixed(uint64_t first, uint64_t n, uint32_t dims, const uint32_t* columns,
                          const uint32_t* scrambles, uint32_t* out);
+void qo_sobol_fill_f32(uint64_t first, uint64_t n, uint32_t dims, const uint32_t* columns,
+                       const uint32_t* scrambles, float* out);
 
 /* Builder-defined hash-based Owen scramble (no reference). */
 uint32_t qo_owen_scramble(uint32_t v, uint32_t seed);

@@ -273,3 +273,17 @@ def test_oracle_vs_ref_random_sobol(oracle, ref, columns64):
         oracle.qo_sobol_fill_fixed(i, 1, 64, ptr(columns64), None, ptr(a))
         assert ref.ref_sobol_fixed_fill(i, 1, 64, None, ptr(b), 1) == 0
         np.testing.assert_array_equal(a, b)
+
+
+def test_sobol_fill_f32_port_matches_reference(oracle, ref, columns64):
+    """qo_sobol_fill_f32 (bench.py's CPU "port" when the reference build is
+    absent) gives the reference's float points bit for bit."""
+    from oracle import ptr
+
+    n, dims = 5000, 32
+    cols = np.ascontiguousarray(columns64[:dims])
+    got = np.zeros((n, dims), np.float32)
+    exp = np.zeros((n, dims), np.float32)
+    oracle.qo_sobol_fill_f32(12345, n, dims, ptr(cols), None, ptr(got))
+    assert ref.ref_sobol_fill(12345, n, dims, None, ptr(exp), 4) == 0
+    np.testing.assert_array_equal(got.view(np.uint32), exp.view(np.uint32))
