@@ -116,35 +116,85 @@ __device__ __forceinline__ void sample2(uint32_t i, const PixelState& s, const R
     }
 }
 
+// ---- per-pixel building blocks shared by the render kernels
+
+// Pixel of band index q (row-major over rows [row_begin, row_end)).
+__device__ __forceinline__ void band_pixel(uint64_t q, const RenderParams& p, uint32_t& px,
+                                           uint32_t& py)
+{
+    py = p.row_begin + static_cast<uint32_t>(q / p.width);
+    px = static_cast<uint32_t>(q % p.width);
+}
+
+// Direct Sobol' value (both render dims) of index i (digitalnet.cpp:111-131).
+__device__ __forceinline__ void sobol_direct2(uint32_t i, const RenderParams& p, uint32_t& s0,
+                                              uint32_t& s1)
+{
+    s0 = p.scr0;
+    s1 = p.scr1;
+    for (uint32_t k = 0, v = i; v; ++k, v >>= 1)
+        if (v & 1u) {
+            s0 ^= __ldg(p.cols2 + k);
+            s1 ^= __ldg(p.cols2 + 52 + k);
+        }
+}
+
+// scene_value at sample i of the pixel (render.cpp:61-68): the two fp32
+// sample components, the sample point ((px + u) / W, (py + v) / H) in FP64
+// and the integrand. sob0/sob1: the Sobol' value of index i (KIND 0).
+template <uint32_t KIND>
+__device__ __forceinline__ double pixel_sample(uint32_t i, const PixelState& s,
+                                               const RenderParams& p, double fx, double fy,
+                                               const double2* s_poly, uint32_t sob0,
+                                               uint32_t sob1)
+{
+    uint32_t a, b;
+    sample2<KIND>(i, s, p, a, b, sob0, sob1);
+    const double u = static_cast<double>(map_u32(a));
+    const double v = static_cast<double>(map_u32(b));
+    return scene_value<true>(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
+                             __dmul_rn(__dadd_rn(fy, v), p.inv_h), p.sc, s_poly);
+}
+
+// render.cpp:72-78: llround(f * 2^32), the int accumulator's term.
+__device__ __forceinline__ long long int_term(double f)
+{
+    return llround(__dmul_rn(f, 4294967296.0));
+}
+
+// float(value() / spp) (kahan) and float(sum / 2^32 / spp) (int).
+__device__ __forceinline__ float finish_kahan(double sum, double comp, uint32_t spp)
+{
+    return __double2float_rn(__ddiv_rn(__dadd_rn(sum, comp), static_cast<double>(spp)));
+}
+__device__ __forceinline__ float finish_int(long long isum, uint32_t spp)
+{
+    return __double2float_rn(
+        __ddiv_rn(__ddiv_rn(static_cast<double>(isum), 4294967296.0), static_cast<double>(spp)));
+}
+
 template <uint32_t KIND, uint32_t ACCUM>
 __global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __restrict__ out)
 {
     __shared__ double2 s_poly[8];
     load_sin_poly(s_poly);
-    const uint32_t band = p.row_end - p.row_begin;
-    const uint64_t npix = static_cast<uint64_t>(band) * p.width;
+    const uint64_t npix = static_cast<uint64_t>(p.row_end - p.row_begin) * p.width;
     const uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= npix)
         return;
-    const uint32_t py = p.row_begin + static_cast<uint32_t>(q / p.width);
-    const uint32_t px = static_cast<uint32_t>(q % p.width);
+    uint32_t px, py;
+    band_pixel(q, p, px, py);
     const PixelState s = pixel_state<KIND>(px, py, p);
-
     uint32_t sob0 = p.scr0, sob1 = p.scr1; // sobol index 0 value
     double sum = 0.0, comp = 0.0;
     long long isum = 0;
     const double fx = static_cast<double>(px), fy = static_cast<double>(py);
     for (uint32_t i = 0; i < p.spp; ++i) {
-        uint32_t a, b;
-        sample2<KIND>(i, s, p, a, b, sob0, sob1);
-        const double u = static_cast<double>(map_u32(a));
-        const double v = static_cast<double>(map_u32(b));
-        const double f = scene_value<true>(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
-                                           __dmul_rn(__dadd_rn(fy, v), p.inv_h), p.sc, s_poly);
+        const double f = pixel_sample<KIND>(i, s, p, fx, fy, s_poly, sob0, sob1);
         if (ACCUM == 0)
             neumaier_add(sum, comp, f);
         else
-            isum += llround(__dmul_rn(f, 4294967296.0));
+            isum += int_term(f);
         if (KIND == 0) { // x(i+1) = x(i) ^ (C[0] ^ ... ^ C[ctz(i+1)])
             const uint32_t c = __ffs(static_cast<int>(i + 1)) - 1;
             for (uint32_t k = 0; k <= c; ++k) {
@@ -153,13 +203,7 @@ __global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __rest
             }
         }
     }
-    float r;
-    if (ACCUM == 0)
-        r = __double2float_rn(__ddiv_rn(__dadd_rn(sum, comp), static_cast<double>(p.spp)));
-    else
-        r = __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(isum), 4294967296.0),
-                                        static_cast<double>(p.spp)));
-    out[q] = r;
+    out[q] = ACCUM == 0 ? finish_kahan(sum, comp, p.spp) : finish_int(isum, p.spp);
 }
 
 // Few pixels, many samples (npix < kWarpPixels, spp >= 64): one warp per
@@ -173,35 +217,26 @@ __global__ void __launch_bounds__(kBlock) k_render_warp(RenderParams p, float* _
 {
     __shared__ double2 s_poly[8];
     load_sin_poly(s_poly);
-    const uint32_t band = p.row_end - p.row_begin;
-    const uint64_t npix = static_cast<uint64_t>(band) * p.width;
+    const uint64_t npix = static_cast<uint64_t>(p.row_end - p.row_begin) * p.width;
     const uint64_t q = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const uint32_t lane = threadIdx.x & 31u;
     if (q >= npix)
         return; // whole warp
-    const uint32_t py = p.row_begin + static_cast<uint32_t>(q / p.width);
-    const uint32_t px = static_cast<uint32_t>(q % p.width);
+    uint32_t px, py;
+    band_pixel(q, p, px, py);
     const PixelState s = pixel_state<KIND>(px, py, p);
     double sum = 0.0, comp = 0.0;
     long long isum = 0;
     const double fx = static_cast<double>(px), fy = static_cast<double>(py);
     for (uint32_t i = lane; i < p.spp; i += 32) {
-        uint32_t a, b, s0 = p.scr0, s1 = p.scr1;
-        if (KIND == 0) // direct Sobol' value of index i (digitalnet.cpp:111-131)
-            for (uint32_t k = 0, v = i; v; ++k, v >>= 1)
-                if (v & 1u) {
-                    s0 ^= __ldg(p.cols2 + k);
-                    s1 ^= __ldg(p.cols2 + 52 + k);
-                }
-        sample2<KIND>(i, s, p, a, b, s0, s1);
-        const double u = static_cast<double>(map_u32(a));
-        const double v = static_cast<double>(map_u32(b));
-        const double f = scene_value<true>(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
-                                           __dmul_rn(__dadd_rn(fy, v), p.inv_h), p.sc, s_poly);
+        uint32_t s0 = p.scr0, s1 = p.scr1;
+        if (KIND == 0)
+            sobol_direct2(i, p, s0, s1);
+        const double f = pixel_sample<KIND>(i, s, p, fx, fy, s_poly, s0, s1);
         if (ACCUM == 0)
             neumaier_add(sum, comp, f);
         else
-            isum += llround(__dmul_rn(f, 4294967296.0));
+            isum += int_term(f);
     }
     for (int o = 16; o; o >>= 1) {
         if (ACCUM == 0) {
@@ -214,10 +249,7 @@ __global__ void __launch_bounds__(kBlock) k_render_warp(RenderParams p, float* _
         }
     }
     if (lane == 0)
-        out[q] = ACCUM == 0
-                     ? __double2float_rn(__ddiv_rn(__dadd_rn(sum, comp), static_cast<double>(p.spp)))
-                     : __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(isum), 4294967296.0),
-                                                   static_cast<double>(p.spp)));
+        out[q] = ACCUM == 0 ? finish_kahan(sum, comp, p.spp) : finish_int(isum, p.spp);
 }
 
 // Sample-partitioned render (PAPER.md:498-509 / imageplane.cpp:114-130:
@@ -233,31 +265,20 @@ __global__ void __launch_bounds__(kBlock)
 {
     __shared__ double2 s_poly[8];
     load_sin_poly(s_poly);
-    const uint32_t band = p.row_end - p.row_begin;
-    const uint64_t npix = static_cast<uint64_t>(band) * p.width;
+    const uint64_t npix = static_cast<uint64_t>(p.row_end - p.row_begin) * p.width;
     const uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= npix)
         return;
-    const uint32_t py = p.row_begin + static_cast<uint32_t>(q / p.width);
-    const uint32_t px = static_cast<uint32_t>(q % p.width);
+    uint32_t px, py;
+    band_pixel(q, p, px, py);
     const PixelState s = pixel_state<KIND>(px, py, p);
     long long isum = 0;
     const double fx = static_cast<double>(px), fy = static_cast<double>(py);
     for (uint32_t i = first; i < p.spp; i += step) {
-        uint32_t a, b, s0 = p.scr0, s1 = p.scr1;
-        if (KIND == 0) { // direct Sobol' value of index i (digitalnet.cpp:111-131)
-            for (uint32_t k = 0, v = i; v; ++k, v >>= 1)
-                if (v & 1u) {
-                    s0 ^= __ldg(p.cols2 + k);
-                    s1 ^= __ldg(p.cols2 + 52 + k);
-                }
-        }
-        sample2<KIND>(i, s, p, a, b, s0, s1);
-        const double u = static_cast<double>(map_u32(a));
-        const double v = static_cast<double>(map_u32(b));
-        const double f = scene_value<true>(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
-                                           __dmul_rn(__dadd_rn(fy, v), p.inv_h), p.sc, s_poly);
-        isum += llround(__dmul_rn(f, 4294967296.0));
+        uint32_t s0 = p.scr0, s1 = p.scr1;
+        if (KIND == 0)
+            sobol_direct2(i, p, s0, s1);
+        isum += int_term(pixel_sample<KIND>(i, s, p, fx, fy, s_poly, s0, s1));
     }
     acc[q] = isum;
 }
@@ -268,8 +289,7 @@ __global__ void k_render_finalize(const long long* __restrict__ acc, uint64_t np
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < npix;
          k += stride)
-        out[k] = __double2float_rn(__ddiv_rn(__ddiv_rn(static_cast<double>(acc[k]), 4294967296.0),
-                                             static_cast<double>(spp)));
+        out[k] = finish_int(acc[k], spp);
 }
 
 // --------------------------------------------- stream fill of pixel kinds
