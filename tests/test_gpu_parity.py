@@ -511,6 +511,21 @@ def test_distributed_paths_on_nccl_world1(tmp_path):
     assert r["e"][1] == q.integrate("sobol", "product-sine", 4096 * 9 + 1, 4, "int")["estimate"]
 
 
+@pytest.mark.parametrize("kind", ["halton-hilbert", "image-plane-halton", "halton"])
+def test_render_4k_halton_kinds_vs_reference(ref, kind):
+    """4K renders of the Halton kinds against the reference render: every
+    phi_3 path (two table steps below 3^14, 7 + 7 + 6 digits above — the
+    halton-hilbert block indices reach 4^12 * spp) bit for bit in int mode."""
+    import os
+
+    w, h, spp = 3840, 2160, 2
+    exp = np.zeros((h, w), np.float32)
+    assert ref.ref_render(w, h, spp, kind.encode(), b"int", 0, os.cpu_count() or 1,
+                          ptr(exp)) == 0
+    got = q.render(w, h, spp, kind=kind, accum="int").cpu().numpy()
+    np.testing.assert_array_equal(got, exp)
+
+
 # ------------------------------------------------ full-size properties
 @pytest.mark.slow
 def test_c2_full_size_properties(oracle, columns64):
