@@ -526,6 +526,30 @@ def test_render_4k_halton_kinds_vs_reference(ref, kind):
     np.testing.assert_array_equal(got, exp)
 
 
+@pytest.mark.parametrize("world", [1, 2, 4, 8, 3])
+def test_fill_shards_equal_single_fill(world):
+    """SURVEY §4 plan item 5 with G logical shards: the multi-GPU partition
+    (index_shard: contiguous index ranges, no collective) gives identical
+    bytes to the single fill for every generator."""
+    import torch
+
+    from paper_2307_15584_b200.distributed import index_shard
+
+    first, n = (1 << 33) + 7, 300001
+    g = q.lfsr_generator_vector(0xACE1, 16)
+    fills = {
+        "sobol": lambda a, c: q.sobol_fill(c, 32, first=a, fixed=True),
+        "owen": lambda a, c: q.sobol_fill(c, 64, first=a, scramble="owen",
+                                          words=list(range(64)), fixed=True),
+        "lattice": lambda a, c: q.lattice_fill(c, g, first=a, shifts=list(range(16)), fixed=True),
+        "halton": lambda a, c: q.halton_fill(c, 24, first=a, scramble="faure", fixed=True),
+    }
+    for name, fill in fills.items():
+        whole = fill(first, n)
+        parts = [fill(*index_shard(first, n, world, r)) for r in range(world)]
+        assert torch.equal(torch.cat(parts, 0), whole), (name, world)
+
+
 # ------------------------------------------------ full-size properties
 @pytest.mark.slow
 def test_c2_full_size_properties(oracle, columns64):
