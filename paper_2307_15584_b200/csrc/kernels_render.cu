@@ -142,18 +142,19 @@ __device__ __forceinline__ void sobol_direct2(uint32_t i, const RenderParams& p,
 // scene_value at sample i of the pixel (render.cpp:61-68): the two fp32
 // sample components, the sample point ((px + u) / W, (py + v) / H) in FP64
 // and the integrand. sob0/sob1: the Sobol' value of index i (KIND 0).
-template <uint32_t KIND>
+template <uint32_t KIND, bool DISC_TEST = true>
 __device__ __forceinline__ double pixel_sample(uint32_t i, const PixelState& s,
                                                const RenderParams& p, double fx, double fy,
                                                const double2* s_poly, uint32_t sob0,
-                                               uint32_t sob1)
+                                               uint32_t sob1, bool inside_px = false)
 {
     uint32_t a, b;
     sample2<KIND>(i, s, p, a, b, sob0, sob1);
     const double u = static_cast<double>(map_u32(a));
     const double v = static_cast<double>(map_u32(b));
-    return scene_value<true>(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
-                             __dmul_rn(__dadd_rn(fy, v), p.inv_h), p.sc, s_poly);
+    return scene_value<true, DISC_TEST>(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
+                                        __dmul_rn(__dadd_rn(fy, v), p.inv_h), p.sc, s_poly,
+                                        inside_px);
 }
 
 // render.cpp:72-78: llround(f * 2^32), the int accumulator's term.
@@ -173,24 +174,18 @@ __device__ __forceinline__ float finish_int(long long isum, uint32_t spp)
         __ddiv_rn(__ddiv_rn(static_cast<double>(isum), 4294967296.0), static_cast<double>(spp)));
 }
 
-template <uint32_t KIND, uint32_t ACCUM>
-__global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __restrict__ out)
+// The sequential per-pixel sample loop of k_render (render.cpp:61-78).
+template <uint32_t KIND, uint32_t ACCUM, bool DISC_TEST>
+__device__ __forceinline__ float render_pixel(const PixelState& s, const RenderParams& p,
+                                              double fx, double fy, const double2* s_poly,
+                                              bool inside_px)
 {
-    __shared__ double2 s_poly[8];
-    load_sin_poly(s_poly);
-    const uint64_t npix = static_cast<uint64_t>(p.row_end - p.row_begin) * p.width;
-    const uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (q >= npix)
-        return;
-    uint32_t px, py;
-    band_pixel(q, p, px, py);
-    const PixelState s = pixel_state<KIND>(px, py, p);
     uint32_t sob0 = p.scr0, sob1 = p.scr1; // sobol index 0 value
     double sum = 0.0, comp = 0.0;
     long long isum = 0;
-    const double fx = static_cast<double>(px), fy = static_cast<double>(py);
     for (uint32_t i = 0; i < p.spp; ++i) {
-        const double f = pixel_sample<KIND>(i, s, p, fx, fy, s_poly, sob0, sob1);
+        const double f =
+            pixel_sample<KIND, DISC_TEST>(i, s, p, fx, fy, s_poly, sob0, sob1, inside_px);
         if (ACCUM == 0)
             neumaier_add(sum, comp, f);
         else
@@ -203,7 +198,28 @@ __global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __rest
             }
         }
     }
-    out[q] = ACCUM == 0 ? finish_kahan(sum, comp, p.spp) : finish_int(isum, p.spp);
+    return ACCUM == 0 ? finish_kahan(sum, comp, p.spp) : finish_int(isum, p.spp);
+}
+
+template <uint32_t KIND, uint32_t ACCUM>
+__global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __restrict__ out)
+{
+    __shared__ double2 s_poly[8];
+    load_sin_poly(s_poly);
+    const uint64_t npix = static_cast<uint64_t>(p.row_end - p.row_begin) * p.width;
+    const uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= npix)
+        return;
+    uint32_t px, py;
+    band_pixel(q, p, px, py);
+    const PixelState s = pixel_state<KIND>(px, py, p);
+    const double fx = static_cast<double>(px), fy = static_cast<double>(py);
+    // warps with no pixel on the disc's edge skip the per-sample disc test
+    const int disc = disc_class(px, py, p.inv_w, p.inv_h, p.sc.disc_r2);
+    if (__any_sync(__activemask(), disc == kDiscTest))
+        out[q] = render_pixel<KIND, ACCUM, true>(s, p, fx, fy, s_poly, false);
+    else
+        out[q] = render_pixel<KIND, ACCUM, false>(s, p, fx, fy, s_poly, disc == kDiscInside);
 }
 
 // Few pixels, many samples (npix < kWarpPixels, spp >= 64): one warp per
