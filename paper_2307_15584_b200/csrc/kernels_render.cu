@@ -11,6 +11,8 @@
 // the CPU where device sin() differs from libm's.
 #include <cstdint>
 
+#include <type_traits>
+
 #include "device.cuh"
 #include "internal.hpp"
 
@@ -183,22 +185,39 @@ __device__ __forceinline__ float render_pixel(const PixelState& s, const RenderP
     uint32_t sob0 = p.scr0, sob1 = p.scr1; // sobol index 0 value
     double sum = 0.0, comp = 0.0;
     long long isum = 0;
-    for (uint32_t i = 0; i < p.spp; ++i) {
-        const double f =
-            pixel_sample<KIND, DISC_TEST>(i, s, p, fx, fy, s_poly, sob0, sob1, inside_px);
-        if (ACCUM == 0)
-            neumaier_add(sum, comp, f);
-        else
-            isum += int_term(f);
-        if (KIND == 0) { // x(i+1) = x(i) ^ (C[0] ^ ... ^ C[ctz(i+1)])
-            const uint32_t c = __ffs(static_cast<int>(i + 1)) - 1;
-            for (uint32_t k = 0; k <= c; ++k) {
-                sob0 ^= __ldg(p.cols2 + k);
-                sob1 ^= __ldg(p.cols2 + 52 + k);
+    // BIG: Neumaier's |sum| >= |v| branch is known to hold
+    auto run = [&](uint32_t i0, uint32_t i1, auto big) {
+        for (uint32_t i = i0; i < i1; ++i) {
+            const double f =
+                pixel_sample<KIND, DISC_TEST>(i, s, p, fx, fy, s_poly, sob0, sob1, inside_px);
+            if (ACCUM != 0)
+                isum += int_term(f);
+            else if (decltype(big)::value)
+                neumaier_add_big(sum, comp, f);
+            else
+                neumaier_add(sum, comp, f);
+            if (KIND == 0) { // x(i+1) = x(i) ^ (C[0] ^ ... ^ C[ctz(i+1)])
+                const uint32_t c = __ffs(static_cast<int>(i + 1)) - 1;
+                for (uint32_t k = 0; k <= c; ++k) {
+                    sob0 ^= __ldg(p.cols2 + k);
+                    sob1 ^= __ldg(p.cols2 + 52 + k);
+                }
             }
         }
+    };
+    if (ACCUM != 0) {
+        run(0, p.spp, std::false_type{});
+        return finish_int(isum, p.spp);
     }
-    return ACCUM == 0 ? finish_kahan(sum, comp, p.spp) : finish_int(isum, p.spp);
+    // scene_value lies in [0, 1.25] and the sum never decreases, so once the
+    // whole warp has sum >= 1.25 every later step takes the first branch
+    const uint32_t k0 = p.spp < 8u ? p.spp : 8u;
+    run(0, k0, std::false_type{});
+    if (__all_sync(__activemask(), sum >= 1.25))
+        run(k0, p.spp, std::true_type{});
+    else
+        run(k0, p.spp, std::false_type{});
+    return finish_kahan(sum, comp, p.spp);
 }
 
 template <uint32_t KIND, uint32_t ACCUM>
