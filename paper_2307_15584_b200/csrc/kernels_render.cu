@@ -309,12 +309,21 @@ __global__ void __launch_bounds__(kBlock)
     const PixelState s = pixel_state<KIND>(px, py, p);
     long long isum = 0;
     const double fx = static_cast<double>(px), fy = static_cast<double>(py);
-    for (uint32_t i = first; i < p.spp; i += step) {
-        uint32_t s0 = p.scr0, s1 = p.scr1;
-        if (KIND == 0)
-            sobol_direct2(i, p, s0, s1);
-        isum += int_term(pixel_sample<KIND>(i, s, p, fx, fy, s_poly, s0, s1));
-    }
+    auto run = [&](auto test, bool inside_px) {
+        for (uint32_t i = first; i < p.spp; i += step) {
+            uint32_t s0 = p.scr0, s1 = p.scr1;
+            if (KIND == 0)
+                sobol_direct2(i, p, s0, s1);
+            isum += int_term(pixel_sample<KIND, decltype(test)::value>(i, s, p, fx, fy, s_poly,
+                                                                       s0, s1, inside_px));
+        }
+    };
+    // warps with no pixel on the disc's edge skip the per-sample disc test
+    const int disc = disc_class(px, py, p.inv_w, p.inv_h, p.sc.disc_r2);
+    if (__any_sync(__activemask(), disc == kDiscTest))
+        run(std::true_type{}, false);
+    else
+        run(std::false_type{}, disc == kDiscInside);
     acc[q] = isum;
 }
 
