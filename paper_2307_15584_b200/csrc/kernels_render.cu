@@ -144,19 +144,20 @@ __device__ __forceinline__ void sobol_direct2(uint32_t i, const RenderParams& p,
 // scene_value at sample i of the pixel (render.cpp:61-68): the two fp32
 // sample components, the sample point ((px + u) / W, (py + v) / H) in FP64
 // and the integrand. sob0/sob1: the Sobol' value of index i (KIND 0).
-template <uint32_t KIND, bool DISC_TEST = true>
+template <uint32_t KIND, bool DISC_TEST = true, bool FIXED_Q = false>
 __device__ __forceinline__ double pixel_sample(uint32_t i, const PixelState& s,
                                                const RenderParams& p, double fx, double fy,
                                                const double2* s_poly, uint32_t sob0,
-                                               uint32_t sob1, bool inside_px = false)
+                                               uint32_t sob1, bool inside_px = false, int qx = 0,
+                                               int qy = 0)
 {
     uint32_t a, b;
     sample2<KIND>(i, s, p, a, b, sob0, sob1);
     const double u = static_cast<double>(map_u32(a));
     const double v = static_cast<double>(map_u32(b));
-    return scene_value<true, DISC_TEST>(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
-                                        __dmul_rn(__dadd_rn(fy, v), p.inv_h), p.sc, s_poly,
-                                        inside_px);
+    return scene_value<true, DISC_TEST, FIXED_Q>(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
+                                                 __dmul_rn(__dadd_rn(fy, v), p.inv_h), p.sc,
+                                                 s_poly, inside_px, qx, qy);
 }
 
 // render.cpp:72-78: llround(f * 2^32), the int accumulator's term.
@@ -177,10 +178,10 @@ __device__ __forceinline__ float finish_int(long long isum, uint32_t spp)
 }
 
 // The sequential per-pixel sample loop of k_render (render.cpp:61-78).
-template <uint32_t KIND, uint32_t ACCUM, bool DISC_TEST>
+template <uint32_t KIND, uint32_t ACCUM, bool DISC_TEST, bool FIXED_Q>
 __device__ __forceinline__ float render_pixel(const PixelState& s, const RenderParams& p,
                                               double fx, double fy, const double2* s_poly,
-                                              bool inside_px)
+                                              bool inside_px, int qx, int qy)
 {
     uint32_t sob0 = p.scr0, sob1 = p.scr1; // sobol index 0 value
     double sum = 0.0, comp = 0.0;
@@ -188,8 +189,8 @@ __device__ __forceinline__ float render_pixel(const PixelState& s, const RenderP
     // BIG: Neumaier's |sum| >= |v| branch is known to hold
     auto run = [&](uint32_t i0, uint32_t i1, auto big) {
         for (uint32_t i = i0; i < i1; ++i) {
-            const double f =
-                pixel_sample<KIND, DISC_TEST>(i, s, p, fx, fy, s_poly, sob0, sob1, inside_px);
+            const double f = pixel_sample<KIND, DISC_TEST, FIXED_Q>(i, s, p, fx, fy, s_poly, sob0,
+                                                                    sob1, inside_px, qx, qy);
             if (ACCUM != 0)
                 isum += int_term(f);
             else if (decltype(big)::value)
@@ -233,12 +234,25 @@ __global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __rest
     band_pixel(q, p, px, py);
     const PixelState s = pixel_state<KIND>(px, py, p);
     const double fx = static_cast<double>(px), fy = static_cast<double>(py);
-    // warps with no pixel on the disc's edge skip the per-sample disc test
+    // warps with no pixel on the disc's edge skip the per-sample disc test;
+    // warps whose footprints each keep one sine quadrant per axis skip the
+    // per-sample quadrant count (both choices warp-uniform)
     const int disc = disc_class(px, py, p.inv_w, p.inv_h, p.sc.disc_r2);
-    if (__any_sync(__activemask(), disc == kDiscTest))
-        out[q] = render_pixel<KIND, ACCUM, true>(s, p, fx, fy, s_poly, false);
-    else
-        out[q] = render_pixel<KIND, ACCUM, false>(s, p, fx, fy, s_poly, disc == kDiscInside);
+    int qx, qy;
+    const bool fixed = sin_fixed_quadrant(fx * p.inv_w, (fx + 1.0) * p.inv_w, p.sc, qx) &&
+                       sin_fixed_quadrant(fy * p.inv_h, (fy + 1.0) * p.inv_h, p.sc, qy);
+    const unsigned mask = __activemask();
+    const bool test = __any_sync(mask, disc == kDiscTest);
+    const bool inside = disc == kDiscInside;
+    if (__all_sync(mask, fixed)) {
+        out[q] = test ? render_pixel<KIND, ACCUM, true, true>(s, p, fx, fy, s_poly, false, qx, qy)
+                      : render_pixel<KIND, ACCUM, false, true>(s, p, fx, fy, s_poly, inside, qx,
+                                                                qy);
+    } else {
+        out[q] = test ? render_pixel<KIND, ACCUM, true, false>(s, p, fx, fy, s_poly, false, 0, 0)
+                      : render_pixel<KIND, ACCUM, false, false>(s, p, fx, fy, s_poly, inside, 0,
+                                                                 0);
+    }
 }
 
 // Few pixels, many samples (npix < kWarpPixels, spp >= 64): one warp per
