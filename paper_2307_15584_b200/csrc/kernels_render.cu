@@ -323,21 +323,33 @@ __global__ void __launch_bounds__(kBlock)
     const PixelState s = pixel_state<KIND>(px, py, p);
     long long isum = 0;
     const double fx = static_cast<double>(px), fy = static_cast<double>(py);
-    auto run = [&](auto test, bool inside_px) {
+    auto run = [&](auto test, auto fixed, bool inside_px, int qx, int qy) {
         for (uint32_t i = first; i < p.spp; i += step) {
             uint32_t s0 = p.scr0, s1 = p.scr1;
             if (KIND == 0)
                 sobol_direct2(i, p, s0, s1);
-            isum += int_term(pixel_sample<KIND, decltype(test)::value>(i, s, p, fx, fy, s_poly,
-                                                                       s0, s1, inside_px));
+            isum += int_term(pixel_sample<KIND, decltype(test)::value, decltype(fixed)::value>(
+                i, s, p, fx, fy, s_poly, s0, s1, inside_px, qx, qy));
         }
     };
-    // warps with no pixel on the disc's edge skip the per-sample disc test
+    // the same warp-uniform skips as k_render (disc_class, sin_fixed_quadrant)
     const int disc = disc_class(px, py, p.inv_w, p.inv_h, p.sc.disc_r2);
-    if (__any_sync(__activemask(), disc == kDiscTest))
-        run(std::true_type{}, false);
-    else
-        run(std::false_type{}, disc == kDiscInside);
+    int qx, qy;
+    const bool fixed = sin_fixed_quadrant(fx * p.inv_w, (fx + 1.0) * p.inv_w, p.sc, qx) &&
+                       sin_fixed_quadrant(fy * p.inv_h, (fy + 1.0) * p.inv_h, p.sc, qy);
+    const unsigned mask = __activemask();
+    const bool test = __any_sync(mask, disc == kDiscTest), inside = disc == kDiscInside;
+    if (__all_sync(mask, fixed)) {
+        if (test)
+            run(std::true_type{}, std::true_type{}, false, qx, qy);
+        else
+            run(std::false_type{}, std::true_type{}, inside, qx, qy);
+    } else {
+        if (test)
+            run(std::true_type{}, std::false_type{}, false, 0, 0);
+        else
+            run(std::false_type{}, std::false_type{}, inside, 0, 0);
+    }
     acc[q] = isum;
 }
 
