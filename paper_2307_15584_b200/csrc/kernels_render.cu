@@ -234,6 +234,10 @@ __global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __rest
     band_pixel(q, p, px, py);
     const PixelState s = pixel_state<KIND>(px, py, p);
     const double fx = static_cast<double>(px), fy = static_cast<double>(py);
+    if (p.spp < 8) { // too few samples to repay the per-pixel classification
+        out[q] = render_pixel<KIND, ACCUM, true, false>(s, p, fx, fy, s_poly, false, 0, 0);
+        return;
+    }
     // warps with no pixel on the disc's edge skip the per-sample disc test;
     // warps whose footprints each keep one sine quadrant per axis skip the
     // per-sample quadrant count (both choices warp-uniform)

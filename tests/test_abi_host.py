@@ -259,3 +259,28 @@ def test_reduce_deterministic_vs_reference(ref):
         got = q.reduce_deterministic(ranks, vals)
         exp = ref.ref_reduce_deterministic(ranks.ctypes.data, vals.ctypes.data, n)
         assert got == exp or (np.isnan(got) and np.isnan(exp)), n
+
+
+def test_hilbert_state_tables_match_generator():
+    """device.cuh's kHilbert3 / kHilbert1 are the state machine that
+    tools/gen_hilbert_table.py derives from hilbert.hpp's per-level rule (and
+    checks against it); the library's hilbert_index is compared with the
+    reference in test_hilbert_digit_reverse_lattice_shift_vs_reference."""
+    import importlib.util
+    import re
+
+    spec = importlib.util.spec_from_file_location(
+        "gen_hilbert_table", os.path.join(ROOT, "tools", "gen_hilbert_table.py"))
+    g = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(g)
+    t3, t1 = g.tables()
+    src = open(os.path.join(ROOT, "paper_2307_15584_b200", "csrc", "device.cuh")).read()
+    block = src[src.index("#define QMC_HILBERT3"):src.index("#define QMC_HILBERT1")]
+    assert [int(v) for v in re.findall(r"\b\d+\b", block.split("{", 1)[1])] == t3
+    m = re.search(r"#define QMC_HILBERT1 \{([^}]*)\}", src)
+    assert [int(v) for v in m.group(1).split(",")] == t1
+    rng = np.random.default_rng(3)
+    for order in (1, 3, 4, 7, 12, 13, 31):
+        n = 1 << order
+        for x, y in rng.integers(0, n, (200, 2), dtype=np.uint64):
+            assert g.fast_index(int(x), int(y), order, t3, t1) == g.ref_index(int(x), int(y), order)
