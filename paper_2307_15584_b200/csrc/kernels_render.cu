@@ -181,7 +181,8 @@ __device__ __forceinline__ float finish_int(long long isum, uint32_t spp)
 template <uint32_t KIND, uint32_t ACCUM, bool DISC_TEST, bool FIXED_Q>
 __device__ __forceinline__ float render_pixel(const PixelState& s, const RenderParams& p,
                                               double fx, double fy, const double2* s_poly,
-                                              bool inside_px, int qx, int qy)
+                                              const uint32_t* sob_d, bool inside_px, int qx,
+                                              int qy)
 {
     uint32_t sob0 = p.scr0, sob1 = p.scr1; // sobol index 0 value
     double sum = 0.0, comp = 0.0;
@@ -197,12 +198,10 @@ __device__ __forceinline__ float render_pixel(const PixelState& s, const RenderP
                 neumaier_add_big(sum, comp, f);
             else
                 neumaier_add(sum, comp, f);
-            if (KIND == 0) { // x(i+1) = x(i) ^ (C[0] ^ ... ^ C[ctz(i+1)])
+            if (KIND == 0) { // x(i+1) = x(i) ^ D[ctz(i+1)], D[c] = C[0] ^ ... ^ C[c]
                 const uint32_t c = __ffs(static_cast<int>(i + 1)) - 1;
-                for (uint32_t k = 0; k <= c; ++k) {
-                    sob0 ^= __ldg(p.cols2 + k);
-                    sob1 ^= __ldg(p.cols2 + 52 + k);
-                }
+                sob0 ^= sob_d[c];
+                sob1 ^= sob_d[32 + c];
             }
         }
     };
@@ -225,7 +224,15 @@ template <uint32_t KIND, uint32_t ACCUM>
 __global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __restrict__ out)
 {
     __shared__ double2 s_poly[8];
-    load_sin_poly(s_poly);
+    __shared__ uint32_t s_sob_d[KIND == 0 ? 64 : 1]; // sobol: prefix XORs of the columns
+    if (KIND == 0 && threadIdx.x < 64) {
+        const uint32_t dim = threadIdx.x >> 5, c = threadIdx.x & 31u;
+        uint32_t d = 0;
+        for (uint32_t k = 0; k <= c; ++k)
+            d ^= __ldg(p.cols2 + 52 * dim + k);
+        s_sob_d[threadIdx.x] = d;
+    }
+    load_sin_poly(s_poly); // includes the barrier
     const uint64_t npix = static_cast<uint64_t>(p.row_end - p.row_begin) * p.width;
     const uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= npix)
@@ -235,7 +242,7 @@ __global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __rest
     const PixelState s = pixel_state<KIND>(px, py, p);
     const double fx = static_cast<double>(px), fy = static_cast<double>(py);
     if (p.spp < 8) { // too few samples to repay the per-pixel classification
-        out[q] = render_pixel<KIND, ACCUM, true, false>(s, p, fx, fy, s_poly, false, 0, 0);
+        out[q] = render_pixel<KIND, ACCUM, true, false>(s, p, fx, fy, s_poly, s_sob_d, false, 0, 0);
         return;
     }
     // warps with no pixel on the disc's edge skip the per-sample disc test;
@@ -249,13 +256,13 @@ __global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __rest
     const bool test = __any_sync(mask, disc == kDiscTest);
     const bool inside = disc == kDiscInside;
     if (__all_sync(mask, fixed)) {
-        out[q] = test ? render_pixel<KIND, ACCUM, true, true>(s, p, fx, fy, s_poly, false, qx, qy)
-                      : render_pixel<KIND, ACCUM, false, true>(s, p, fx, fy, s_poly, inside, qx,
-                                                                qy);
+        out[q] = test ? render_pixel<KIND, ACCUM, true, true>(s, p, fx, fy, s_poly, s_sob_d, false, qx, qy)
+                      : render_pixel<KIND, ACCUM, false, true>(s, p, fx, fy, s_poly, s_sob_d, inside,
+                                                                qx, qy);
     } else {
-        out[q] = test ? render_pixel<KIND, ACCUM, true, false>(s, p, fx, fy, s_poly, false, 0, 0)
-                      : render_pixel<KIND, ACCUM, false, false>(s, p, fx, fy, s_poly, inside, 0,
-                                                                 0);
+        out[q] = test ? render_pixel<KIND, ACCUM, true, false>(s, p, fx, fy, s_poly, s_sob_d, false, 0, 0)
+                      : render_pixel<KIND, ACCUM, false, false>(s, p, fx, fy, s_poly, s_sob_d, inside,
+                                                                 0, 0);
     }
 }
 
