@@ -79,17 +79,18 @@ __device__ __forceinline__ uint32_t rad2(uint32_t i) { return brev32(i & 0x7ffff
 
 // Component j in {0,1} of sample i (SampleStream::sample, imageplane.cpp:
 // 427-461) at the integer stage, for the render's 2-dim streams.
-template <uint32_t KIND>
+// SMEM_T3: t3 is a shared-memory copy of the 3^7-entry phi_3 table.
+template <uint32_t KIND, bool SMEM_T3 = false>
 __device__ __forceinline__ void sample2(uint32_t i, const PixelState& s, const RenderParams& p,
                                         uint32_t& x0, uint32_t& x1, uint32_t& sob0,
-                                        uint32_t& sob1)
+                                        uint32_t& sob1, const uint32_t* t3)
 {
     if (KIND == 0) { // sobol: natural-order incremental, caller advances
         x0 = sob0;
         x1 = sob1;
     } else if (KIND == 1) { // halton (plain)
         x0 = rad2(i);
-        x1 = phi3_fixed(i, p.tab3);
+        x1 = phi3_fixed<SMEM_T3>(i, t3);
     } else if (KIND == 2) { // lattice
         const uint32_t b = brev32(i);
         x0 = b * p.g0;
@@ -97,7 +98,7 @@ __device__ __forceinline__ void sample2(uint32_t i, const PixelState& s, const R
     } else if (KIND == 3) { // halton_hilbert
         const uint32_t gi = static_cast<uint32_t>(s.block + i);
         x0 = rad2(gi);
-        x1 = phi3_fixed(gi, p.tab3);
+        x1 = phi3_fixed<SMEM_T3>(gi, t3);
     } else if (KIND == 4) { // pixel_shifted_lattice (Eq. 3)
         const uint32_t b = brev32(i) + s.shift;
         x0 = b * p.g0;
@@ -108,7 +109,7 @@ __device__ __forceinline__ void sample2(uint32_t i, const PixelState& s, const R
         x1 = b * s.g1;
     } else if (KIND == 6) { // image_plane_halton: (offset + i*stride)>>a, / 3^b
         x0 = rad2(s.ipx0 + i * p.scale_y);
-        x1 = phi3_fixed(s.ipy0 + i * p.scale_x, p.tab3);
+        x1 = phi3_fixed<SMEM_T3>(s.ipy0 + i * p.scale_x, t3);
     } else { // sobol_xor_table, imageplane.cpp:231-243
         const uint32_t k = i ^ __ldg(p.xor_reorder + s.cell);
         const uint64_t pk = static_cast<uint64_t>(k) * p.xor_dims;
@@ -144,15 +145,15 @@ __device__ __forceinline__ void sobol_direct2(uint32_t i, const RenderParams& p,
 // scene_value at sample i of the pixel (render.cpp:61-68): the two fp32
 // sample components, the sample point ((px + u) / W, (py + v) / H) in FP64
 // and the integrand. sob0/sob1: the Sobol' value of index i (KIND 0).
-template <uint32_t KIND, bool DISC_TEST = true, bool FIXED_Q = false>
+template <uint32_t KIND, bool DISC_TEST = true, bool FIXED_Q = false, bool SMEM_T3 = false>
 __device__ __forceinline__ double pixel_sample(uint32_t i, const PixelState& s,
                                                const RenderParams& p, double fx, double fy,
                                                const double2* s_poly, uint32_t sob0,
                                                uint32_t sob1, bool inside_px = false, int qx = 0,
-                                               int qy = 0)
+                                               int qy = 0, const uint32_t* s_tab3 = nullptr)
 {
     uint32_t a, b;
-    sample2<KIND>(i, s, p, a, b, sob0, sob1);
+    sample2<KIND, SMEM_T3>(i, s, p, a, b, sob0, sob1, SMEM_T3 ? s_tab3 : p.tab3);
     const double u = static_cast<double>(map_u32(a));
     const double v = static_cast<double>(map_u32(b));
     return scene_value<true, DISC_TEST, FIXED_Q>(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
@@ -182,16 +183,17 @@ template <uint32_t KIND, uint32_t ACCUM, bool DISC_TEST, bool FIXED_Q>
 __device__ __forceinline__ float render_pixel(const PixelState& s, const RenderParams& p,
                                               double fx, double fy, const double2* s_poly,
                                               const uint32_t* sob_d, bool inside_px, int qx,
-                                              int qy)
+                                              int qy, const uint32_t* s_tab3)
 {
+    constexpr bool kSmemT3 = KIND == 1 || KIND == 3 || KIND == 6;
     uint32_t sob0 = p.scr0, sob1 = p.scr1; // sobol index 0 value
     double sum = 0.0, comp = 0.0;
     long long isum = 0;
     // BIG: Neumaier's |sum| >= |v| branch is known to hold
     auto run = [&](uint32_t i0, uint32_t i1, auto big) {
         for (uint32_t i = i0; i < i1; ++i) {
-            const double f = pixel_sample<KIND, DISC_TEST, FIXED_Q>(i, s, p, fx, fy, s_poly, sob0,
-                                                                    sob1, inside_px, qx, qy);
+            const double f = pixel_sample<KIND, DISC_TEST, FIXED_Q, kSmemT3>(
+                i, s, p, fx, fy, s_poly, sob0, sob1, inside_px, qx, qy, s_tab3);
             if (ACCUM != 0)
                 isum += int_term(f);
             else if (decltype(big)::value)
@@ -232,6 +234,12 @@ __global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __rest
             d ^= __ldg(p.cols2 + 52 * dim + k);
         s_sob_d[threadIdx.x] = d;
     }
+    // halton kinds: the phi_3 table (3^7 words) staged in shared memory
+    constexpr bool kSmemT3 = KIND == 1 || KIND == 3 || KIND == 6;
+    __shared__ uint32_t s_tab3[kSmemT3 ? 2187 : 1];
+    if (kSmemT3)
+        for (uint32_t e = threadIdx.x; e < 2187; e += blockDim.x)
+            s_tab3[e] = __ldg(p.tab3 + e);
     load_sin_poly(s_poly); // includes the barrier
     const uint64_t npix = static_cast<uint64_t>(p.row_end - p.row_begin) * p.width;
     const uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -242,7 +250,8 @@ __global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __rest
     const PixelState s = pixel_state<KIND>(px, py, p);
     const double fx = static_cast<double>(px), fy = static_cast<double>(py);
     if (p.spp < 8) { // too few samples to repay the per-pixel classification
-        out[q] = render_pixel<KIND, ACCUM, true, false>(s, p, fx, fy, s_poly, s_sob_d, false, 0, 0);
+        out[q] = render_pixel<KIND, ACCUM, true, false>(s, p, fx, fy, s_poly, s_sob_d, false, 0,
+                                                         0, s_tab3);
         return;
     }
     // warps with no pixel on the disc's edge skip the per-sample disc test;
@@ -256,13 +265,15 @@ __global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __rest
     const bool test = __any_sync(mask, disc == kDiscTest);
     const bool inside = disc == kDiscInside;
     if (__all_sync(mask, fixed)) {
-        out[q] = test ? render_pixel<KIND, ACCUM, true, true>(s, p, fx, fy, s_poly, s_sob_d, false, qx, qy)
-                      : render_pixel<KIND, ACCUM, false, true>(s, p, fx, fy, s_poly, s_sob_d, inside,
-                                                                qx, qy);
+        out[q] = test ? render_pixel<KIND, ACCUM, true, true>(s, p, fx, fy, s_poly, s_sob_d, false,
+                                                               qx, qy, s_tab3)
+                      : render_pixel<KIND, ACCUM, false, true>(s, p, fx, fy, s_poly, s_sob_d,
+                                                                inside, qx, qy, s_tab3);
     } else {
-        out[q] = test ? render_pixel<KIND, ACCUM, true, false>(s, p, fx, fy, s_poly, s_sob_d, false, 0, 0)
-                      : render_pixel<KIND, ACCUM, false, false>(s, p, fx, fy, s_poly, s_sob_d, inside,
-                                                                 0, 0);
+        out[q] = test ? render_pixel<KIND, ACCUM, true, false>(s, p, fx, fy, s_poly, s_sob_d,
+                                                                false, 0, 0, s_tab3)
+                      : render_pixel<KIND, ACCUM, false, false>(s, p, fx, fy, s_poly, s_sob_d,
+                                                                 inside, 0, 0, s_tab3);
     }
 }
 
