@@ -287,7 +287,22 @@ template <uint32_t KIND, uint32_t ACCUM>
 __global__ void __launch_bounds__(kBlock) k_render_warp(RenderParams p, float* __restrict__ out)
 {
     __shared__ double2 s_poly[8];
-    load_sin_poly(s_poly);
+    // sobol: D32[c] = C[5] ^ ... ^ C[5 + c] per dim (lane l takes samples
+    // l + 32 m: X = X(l) ^ X(32 m), and m -> m + 1 flips X(32 m) by D32)
+    __shared__ uint32_t s_d32[KIND == 0 ? 64 : 1];
+    constexpr bool kSmemT3 = KIND == 1 || KIND == 3 || KIND == 6;
+    __shared__ uint32_t s_tab3[kSmemT3 ? 2187 : 1];
+    if (KIND == 0 && threadIdx.x < 64) {
+        const uint32_t dim = threadIdx.x >> 5, c = threadIdx.x & 31u;
+        uint32_t d = 0;
+        for (uint32_t k = 0; k <= c && 5 + k < 52; ++k)
+            d ^= __ldg(p.cols2 + 52 * dim + 5 + k);
+        s_d32[threadIdx.x] = d;
+    }
+    if (kSmemT3)
+        for (uint32_t e = threadIdx.x; e < 2187; e += blockDim.x)
+            s_tab3[e] = __ldg(p.tab3 + e);
+    load_sin_poly(s_poly); // includes the barrier
     const uint64_t npix = static_cast<uint64_t>(p.row_end - p.row_begin) * p.width;
     const uint64_t q = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const uint32_t lane = threadIdx.x & 31u;
@@ -299,15 +314,42 @@ __global__ void __launch_bounds__(kBlock) k_render_warp(RenderParams p, float* _
     double sum = 0.0, comp = 0.0;
     long long isum = 0;
     const double fx = static_cast<double>(px), fy = static_cast<double>(py);
-    for (uint32_t i = lane; i < p.spp; i += 32) {
-        uint32_t s0 = p.scr0, s1 = p.scr1;
-        if (KIND == 0)
-            sobol_direct2(i, p, s0, s1);
-        const double f = pixel_sample<KIND>(i, s, p, fx, fy, s_poly, s0, s1);
-        if (ACCUM == 0)
-            neumaier_add(sum, comp, f);
+    uint32_t xl0 = p.scr0, xl1 = p.scr1; // sobol: scramble ^ X(lane)
+    if (KIND == 0)
+        sobol_direct2(lane, p, xl0, xl1);
+    auto run = [&](auto test, auto fixed, bool inside_px, int qx, int qy) {
+        uint32_t h0 = 0, h1 = 0; // sobol: X(32 m)
+        for (uint32_t m = 0, i = lane; i < p.spp; ++m, i += 32) {
+            const double f = pixel_sample<KIND, decltype(test)::value, decltype(fixed)::value,
+                                          kSmemT3>(i, s, p, fx, fy, s_poly, xl0 ^ h0, xl1 ^ h1,
+                                                   inside_px, qx, qy, s_tab3);
+            if (ACCUM == 0)
+                neumaier_add(sum, comp, f);
+            else
+                isum += int_term(f);
+            if (KIND == 0) {
+                const uint32_t c = __ffs(static_cast<int>(m + 1)) - 1;
+                h0 ^= s_d32[c];
+                h1 ^= s_d32[32 + c];
+            }
+        }
+    };
+    // one pixel per warp: the disc and quadrant classifications are uniform
+    const int disc = disc_class(px, py, p.inv_w, p.inv_h, p.sc.disc_r2);
+    int qx, qy;
+    const bool fixed = sin_fixed_quadrant(fx * p.inv_w, (fx + 1.0) * p.inv_w, p.sc, qx) &&
+                       sin_fixed_quadrant(fy * p.inv_h, (fy + 1.0) * p.inv_h, p.sc, qy);
+    const bool inside = disc == kDiscInside;
+    if (fixed) {
+        if (disc == kDiscTest)
+            run(std::true_type{}, std::true_type{}, false, qx, qy);
         else
-            isum += int_term(f);
+            run(std::false_type{}, std::true_type{}, inside, qx, qy);
+    } else {
+        if (disc == kDiscTest)
+            run(std::true_type{}, std::false_type{}, false, 0, 0);
+        else
+            run(std::false_type{}, std::false_type{}, inside, 0, 0);
     }
     for (int o = 16; o; o >>= 1) {
         if (ACCUM == 0) {
