@@ -377,7 +377,24 @@ __global__ void __launch_bounds__(kBlock)
     k_render_partial(RenderParams p, uint32_t first, uint32_t step, long long* __restrict__ acc)
 {
     __shared__ double2 s_poly[8];
-    load_sin_poly(s_poly);
+    // sobol: the part's samples first + step * m (step = 2^lp, first < step)
+    // are X(first) ^ X(step * m); m -> m + 1 flips X(step * m) by
+    // D[c] = C[lp] ^ ... ^ C[lp + c]
+    __shared__ uint32_t s_dp[KIND == 0 ? 64 : 1];
+    constexpr bool kSmemT3 = KIND == 1 || KIND == 3 || KIND == 6;
+    __shared__ uint32_t s_tab3[kSmemT3 ? 2187 : 1];
+    if (KIND == 0 && threadIdx.x < 64) {
+        const uint32_t dim = threadIdx.x >> 5, c = threadIdx.x & 31u;
+        const uint32_t lp = __ffs(static_cast<int>(step)) - 1;
+        uint32_t d = 0;
+        for (uint32_t k = 0; k <= c && lp + k < 52; ++k)
+            d ^= __ldg(p.cols2 + 52 * dim + lp + k);
+        s_dp[threadIdx.x] = d;
+    }
+    if (kSmemT3)
+        for (uint32_t e = threadIdx.x; e < 2187; e += blockDim.x)
+            s_tab3[e] = __ldg(p.tab3 + e);
+    load_sin_poly(s_poly); // includes the barrier
     const uint64_t npix = static_cast<uint64_t>(p.row_end - p.row_begin) * p.width;
     const uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= npix)
@@ -387,13 +404,20 @@ __global__ void __launch_bounds__(kBlock)
     const PixelState s = pixel_state<KIND>(px, py, p);
     long long isum = 0;
     const double fx = static_cast<double>(px), fy = static_cast<double>(py);
+    uint32_t xf0 = p.scr0, xf1 = p.scr1; // sobol: scramble ^ X(first)
+    if (KIND == 0)
+        sobol_direct2(first, p, xf0, xf1);
     auto run = [&](auto test, auto fixed, bool inside_px, int qx, int qy) {
-        for (uint32_t i = first; i < p.spp; i += step) {
-            uint32_t s0 = p.scr0, s1 = p.scr1;
-            if (KIND == 0)
-                sobol_direct2(i, p, s0, s1);
-            isum += int_term(pixel_sample<KIND, decltype(test)::value, decltype(fixed)::value>(
-                i, s, p, fx, fy, s_poly, s0, s1, inside_px, qx, qy));
+        uint32_t h0 = 0, h1 = 0; // sobol: X(step * m)
+        for (uint32_t m = 0, i = first; i < p.spp; ++m, i += step) {
+            isum += int_term(pixel_sample<KIND, decltype(test)::value, decltype(fixed)::value,
+                                          kSmemT3>(i, s, p, fx, fy, s_poly, xf0 ^ h0, xf1 ^ h1,
+                                                   inside_px, qx, qy, s_tab3));
+            if (KIND == 0) {
+                const uint32_t c = __ffs(static_cast<int>(m + 1)) - 1;
+                h0 ^= s_dp[c];
+                h1 ^= s_dp[32 + c];
+            }
         }
     };
     // the same warp-uniform skips as k_render (disc_class, sin_fixed_quadrant)
