@@ -191,6 +191,7 @@ __device__ __forceinline__ float render_pixel(const PixelState& s, const RenderP
     long long isum = 0;
     // BIG: Neumaier's |sum| >= |v| branch is known to hold
     auto run = [&](uint32_t i0, uint32_t i1, auto big) {
+#pragma unroll 2
         for (uint32_t i = i0; i < i1; ++i) {
             const double f = pixel_sample<KIND, DISC_TEST, FIXED_Q, kSmemT3>(
                 i, s, p, fx, fy, s_poly, sob0, sob1, inside_px, qx, qy, s_tab3);
