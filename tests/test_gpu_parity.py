@@ -577,6 +577,36 @@ def test_c2_full_size_properties(oracle, columns64):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("dims,n", [(48, 1 << 27), (12, 1 << 30), (24, (1 << 28) + 12345)])
+def test_generic_dims_full_size(oracle, columns64, dims, n):
+    """The element-wise Sobol' kernel (dims not dividing 256) and the Halton
+    fill at tens of GiB (more than 2^32 output words): random rows against
+    the oracle / the per-index reference, F2-linearity, and stratification
+    of one dimension at m = log2(n) where n is a power of two."""
+    x = q.sobol_fill(n, dims, first=7 if n & (n - 1) else 0, fixed=True)
+    rng = np.random.default_rng(dims)
+    rows = torch.from_numpy(rng.integers(0, n, 2048)).cuda()
+    sample = u32(x[rows]).reshape(-1, dims)
+    cols = np.ascontiguousarray(columns64[:dims])
+    first = 7 if n & (n - 1) else 0
+    for k, i in enumerate(rows.cpu().tolist()):
+        exp = np.zeros(dims, np.uint32)
+        oracle.qo_sobol_fill_fixed(first + i, 1, dims, ptr(cols), None, ptr(exp))
+        np.testing.assert_array_equal(sample[k], exp)
+    if first == 0:
+        a = torch.from_numpy(rng.integers(0, n, 1 << 20)).cuda()
+        b = torch.from_numpy(rng.integers(0, n, 1 << 20)).cuda()
+        np.testing.assert_array_equal(u32(x[a ^ b]), u32(x[a] ^ x[b]))
+        m = n.bit_length() - 1
+        col = x[:, dims - 1].to(torch.int64) & 0xFFFFFFFF
+        strata = torch.bincount(col >> (32 - m), minlength=1 << m)
+        assert int(strata.min()) == 1 and int(strata.max()) == 1
+        del col, strata
+    del x
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("dims", [8, 100, 128, 129, 200, 256, 300])
 def test_large_dims_args_paths(oracle, dims):
     """Per-dim word arrays beyond the by-value parameter block (dims > 256)
