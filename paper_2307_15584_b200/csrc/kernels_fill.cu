@@ -856,6 +856,10 @@ template <bool U32OUT>
 __global__ void __launch_bounds__(kBlock)
     k_vdc(uint64_t first, uint64_t n, uint32_t* __restrict__ out)
 {
+    // programmatic dependent launch: let the next kernel in the stream start
+    // its launch now, and wait for the previous grid (its stores) before ours
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint64_t quads = (n + 3) / 4;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     const bool aligned = (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
@@ -1404,11 +1408,18 @@ cudaError_t launch_vdc(bool u32, const FillRange& r, cudaStream_t s)
     const uint64_t quads = (r.n + 3) / 4;
     const unsigned grid = static_cast<unsigned>(
         std::min<uint64_t>((quads + kBlock - 1) / kBlock, static_cast<uint64_t>(sm_count()) * 16));
-    if (u32)
-        k_vdc<true><<<grid, kBlock, 0, s>>>(r.first, r.n, static_cast<uint32_t*>(r.out));
-    else
-        k_vdc<false><<<grid, kBlock, 0, s>>>(r.first, r.n, static_cast<uint32_t*>(r.out));
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kBlock);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    uint32_t* out = static_cast<uint32_t*>(r.out);
+    return u32 ? cudaLaunchKernelEx(&cfg, k_vdc<true>, r.first, r.n, out)
+               : cudaLaunchKernelEx(&cfg, k_vdc<false>, r.first, r.n, out);
 }
 
 } // namespace qmcgpu
