@@ -43,6 +43,8 @@ elif a.config == "halton":
     n, d = 1 << 24, 32
     out = torch.empty((n, d), dtype=torch.float32, device="cuda")
     fn = lambda: q.halton_fill(n, d, scramble="linear", out=out)  # noqa: E731
+elif a.config == "integrate":
+    fn = lambda: q.integrate("sobol", "product-sine", 1 << 26, 8, "kahan")  # noqa: E731
 elif a.config.startswith("c5"):
     spp = int(a.config[2:] or 64)
     out = torch.empty((2160, 3840), dtype=torch.float32, device="cuda")
