@@ -37,7 +37,7 @@ __all__ = [
     "min_toroidal_distance", "check_1d_stratification", "XorTables", "render_partial",
     "render_finalize", "load_generator_vector", "load_linear_factors", "fnv1a64", "write_pnm",
     "write_points_csv", "hilbert_index", "hilbert_xy", "digit_reverse", "lattice_shift_fixed",
-    "integrate_partials", "reduce_deterministic",
+    "integrate_partials", "reduce_deterministic", "sampler_kind_name", "status_string",
     "SAMPLER_KINDS",
 ]
 
@@ -98,6 +98,8 @@ def lib():
         f.restype, f.argtypes = res, list(args)
 
     sig("qmc_last_error", C.c_char_p)
+    sig("qmc_status_string", C.c_char_p, i32)
+    sig("qmc_sampler_kind_name", C.c_char_p, i32)
     sig("qmc_abi_version", i32)
     sig("qmc_map_u32_to_unifloat", i32, P, P, u64, P)
     sig("qmc_map_selfcheck", i32, C.POINTER(u64), P)
@@ -302,6 +304,16 @@ def sampler_kind_from_name(name: str) -> int:
     o = i32()
     _check(lib().qmc_sampler_kind_from_name(name.encode(), C.byref(o)))
     return o.value
+
+
+def sampler_kind_name(kind: int) -> str:
+    """sampler_kind_name (imageplane.cpp:273-284); "" for an unknown value."""
+    return lib().qmc_sampler_kind_name(kind).decode()
+
+
+def status_string(status: int) -> str:
+    """Human-readable name of a qmc_status code."""
+    return lib().qmc_status_string(status).decode()
 
 
 class GeneratorMatrixSet:

@@ -106,6 +106,9 @@ def test_matrices(golden_arrays, golden, ref):
 def test_sampler_names():
     for k, name in enumerate(q.SAMPLER_KINDS):
         assert q.sampler_kind_from_name(name) == k
+        assert q.sampler_kind_name(k) == name
+    assert q.sampler_kind_name(99) == ""
+    assert q.status_string(0) == "ok" and q.status_string(1) == "config error"
     with pytest.raises(q.ConfigError):
         q.sampler_kind_from_name("sobol2")
 
