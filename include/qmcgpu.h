@@ -93,6 +93,9 @@ qmc_status qmc_partition_by_extra_dimension(uint32_t part, uint32_t parts, uint3
 /* hilbert.hpp:39-56: invalid_argument unless order in [1, 31], out_of_range
  * for a pixel outside the 2^order grid */
 qmc_status qmc_hilbert_index(uint32_t x, uint32_t y, uint32_t order, uint64_t* out);
+/* hilbert_phi3_fixed (imageplane.cpp:16-21): phi_3 of the pixel's Hilbert
+ * index at the integer stage — the pixel-shifted lattice's shift */
+qmc_status qmc_hilbert_phi3_fixed(uint32_t x, uint32_t y, uint32_t order, uint32_t* out);
 /* hilbert.hpp:59-78: the inverse (same orientation) */
 qmc_status qmc_hilbert_xy(uint64_t d, uint32_t order, uint32_t* x, uint32_t* y);
 /* imageplane.cpp:43-51: the `digits` least significant base-b digits of v,

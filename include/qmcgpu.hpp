@@ -362,6 +362,12 @@ inline std::uint64_t hilbert_index(const PixelCoord& p) // hilbert.hpp:39-56
     check(qmc_hilbert_index(p.x, p.y, p.order, &d));
     return d;
 }
+inline std::uint32_t hilbert_phi3_fixed(const PixelCoord& p) // imageplane.cpp:16-21
+{
+    std::uint32_t v = 0;
+    check(qmc_hilbert_phi3_fixed(p.x, p.y, p.order, &v));
+    return v;
+}
 inline PixelCoord hilbert_xy(std::uint64_t d, std::uint32_t order) // hilbert.hpp:59-78
 {
     PixelCoord p{0, 0, order};

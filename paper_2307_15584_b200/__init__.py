@@ -36,7 +36,7 @@ __all__ = [
     "integrate", "builtin_integrand", "write_probe", "l2_star_discrepancy",
     "min_toroidal_distance", "check_1d_stratification", "XorTables", "render_partial",
     "render_finalize", "load_generator_vector", "load_linear_factors", "fnv1a64", "write_pnm",
-    "write_points_csv", "hilbert_index", "hilbert_xy", "digit_reverse", "lattice_shift_fixed",
+    "write_points_csv", "hilbert_index", "hilbert_xy", "hilbert_phi3_fixed", "digit_reverse", "lattice_shift_fixed",
     "integrate_partials", "reduce_deterministic", "sampler_kind_name", "status_string",
     "SAMPLER_KINDS",
 ]
@@ -117,6 +117,7 @@ def lib():
         P, C.POINTER(C.c_int64), P)
     sig("qmc_reduce_deterministic", i32, P, P, u64, C.POINTER(f64))
     sig("qmc_hilbert_xy", i32, u64, u32, C.POINTER(u32), C.POINTER(u32))
+    sig("qmc_hilbert_phi3_fixed", i32, u32, u32, u32, C.POINTER(u32))
     sig("qmc_digit_reverse", u64, u64, u32, u32)
     sig("qmc_lattice_shift_fixed", i32, u32, u32, P, u32, P)
     sig("qmc_halton_pixel_enumeration", i32, u32, u32, u32, u32, C.POINTER(HaltonEnumeration),
@@ -270,6 +271,13 @@ def hilbert_index(x: int, y: int, order: int) -> int:
     d = u64()
     _check(lib().qmc_hilbert_index(x, y, order, C.byref(d)))
     return d.value
+
+
+def hilbert_phi3_fixed(x: int, y: int, order: int) -> int:
+    """hilbert_phi3_fixed(PixelCoord{x, y, order}) (imageplane.cpp:16-21)."""
+    o = u32()
+    _check(lib().qmc_hilbert_phi3_fixed(x, y, order, C.byref(o)))
+    return o.value
 
 
 def hilbert_xy(d: int, order: int):

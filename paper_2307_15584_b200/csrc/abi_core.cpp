@@ -280,6 +280,28 @@ qmc_status qmc_hilbert_index(uint32_t x, uint32_t y, uint32_t order, uint64_t* o
     });
 }
 
+qmc_status qmc_hilbert_phi3_fixed(uint32_t x, uint32_t y, uint32_t order, uint32_t* out)
+{
+    return guard([&] {
+        uint64_t h = 0;
+        const qmc_status st = qmc_hilbert_index(x, y, order, &h);
+        if (st != QMC_OK)
+            fail(st, last_error());
+        // radical_inverse_tabled_fixed(h, 3, base3_four_digit_table()) ==
+        // radical_inverse_fixed(h, 1): i %= 3^20, reversed digits / 3^digits
+        uint32_t i = static_cast<uint32_t>(h) % 3486784401u;
+        uint64_t acc = 0, scale = 1;
+        do {
+            acc = acc * 3 + i % 3;
+            i /= 3;
+            scale *= 3;
+        } while (i != 0);
+        if (!out)
+            fail(QMC_INVALID_ARGUMENT, "output pointer is null");
+        *out = static_cast<uint32_t>((acc << 32) / scale);
+    });
+}
+
 qmc_status qmc_hilbert_xy(uint64_t d, uint32_t order, uint32_t* x, uint32_t* y)
 {
     return guard([&] {

@@ -56,6 +56,9 @@ static int host_checks()
     const qmcgpu::HaltonPixelEnumeration e(3840, 2160);
     EXPECT(e.stride() == 8957952u && e.scale_x() == 4096 && e.scale_y() == 2187);
     EXPECT(qmcgpu::hilbert_index({0, 1, 1}) == 1 && qmcgpu::hilbert_index({1, 0, 1}) == 3);
+    // SURVEY §4 goldens
+    EXPECT(qmcgpu::hilbert_phi3_fixed({1, 0, 12}) == 0x55555555u);
+    EXPECT(qmcgpu::hilbert_phi3_fixed({0, 1, 12}) == 0x1c71c71cu);
     const auto hp = qmcgpu::hilbert_xy(qmcgpu::hilbert_index({5, 9, 4}), 4);
     EXPECT(hp.x == 5 && hp.y == 9);
     EXPECT(throws<std::invalid_argument>([] { qmcgpu::hilbert_index({0, 0, 0}); }));

@@ -287,3 +287,21 @@ def test_hilbert_state_tables_match_generator():
         n = 1 << order
         for x, y in rng.integers(0, n, (200, 2), dtype=np.uint64):
             assert g.fast_index(int(x), int(y), order, t3, t1) == g.ref_index(int(x), int(y), order)
+
+
+def test_hilbert_phi3_fixed_vs_reference(ref, golden):
+    """hilbert_phi3_fixed (imageplane.cpp:16-21) at random pixels of every
+    order, including indices past 3^20 (the table's index modulus)."""
+    import ctypes as C
+
+    rng = np.random.default_rng(9)
+    for order in (1, 2, 5, 12, 16, 17, 24, 31):
+        n = 1 << order
+        for x, y in rng.integers(0, n, (100, 2), dtype=np.uint64):
+            e = C.c_uint32()
+            assert ref.ref_hilbert_phi3_fixed(int(x), int(y), order, C.byref(e)) == 0
+            assert q.hilbert_phi3_fixed(int(x), int(y), order) == e.value
+    with pytest.raises(ValueError):
+        q.hilbert_phi3_fixed(0, 0, 0)
+    with pytest.raises(IndexError):
+        q.hilbert_phi3_fixed(4, 0, 2)
