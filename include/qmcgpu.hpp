@@ -209,6 +209,65 @@ inline std::vector<float> halton_points(std::uint64_t first, std::uint64_t n, st
     return v;
 }
 
+inline std::vector<std::uint32_t> default_linear_factors(std::uint32_t dims); // below
+
+// Faure permutations for the first dims prime bases (radical.hpp:80-89).
+class FaurePermutations {
+public:
+    explicit FaurePermutations(std::uint32_t dims)
+    {
+        for (std::uint32_t j = 0; j < dims; ++j)
+            perms_.push_back(faure_permutation(prime(j)));
+    }
+    std::uint32_t dims() const { return static_cast<std::uint32_t>(perms_.size()); }
+    const std::vector<std::uint32_t>& for_prime_index(std::uint32_t j) const { return perms_.at(j); }
+
+private:
+    std::vector<std::vector<std::uint32_t>> perms_;
+};
+
+// TabledHalton (radical.hpp:110-121): linearly scrambled Halton. The
+// reference evaluates it through per-base multi-digit tables; the values
+// equal the single-digit linear scramble, which the GPU fill computes.
+class TabledHalton {
+public:
+    explicit TabledHalton(std::uint32_t dims, std::vector<std::uint32_t> linear_factors = {})
+        : dims_(dims), factors_(linear_factors.empty() ? default_linear_factors(dims)
+                                                         : std::move(linear_factors))
+    {
+        if (factors_.size() < dims_)
+            throw std::invalid_argument("TabledHalton: linear factor list shorter than dims");
+    }
+    std::uint32_t dims() const { return dims_; }
+    // rows [first, first + n) x dims, row-major
+    std::vector<float> points(std::uint64_t first, std::uint64_t n) const
+    {
+        std::vector<float> v(n * dims_);
+        check(qmc_halton_fill(first, n, dims_, QMC_RADICAL_LINEAR, factors_.data(), QMC_OUT_F32,
+                              v.data(), nullptr));
+        return v;
+    }
+    std::uint32_t component_fixed(std::uint32_t i, std::uint32_t j) const
+    {
+        if (j >= dims_)
+            throw std::out_of_range("TabledHalton: dimension out of range");
+        std::vector<std::uint32_t> v(dims_);
+        check(qmc_halton_fill(i, 1, dims_, QMC_RADICAL_LINEAR, factors_.data(), QMC_OUT_U32,
+                              v.data(), nullptr));
+        return v[j];
+    }
+    float component(std::uint32_t i, std::uint32_t j) const
+    {
+        if (j >= dims_)
+            throw std::out_of_range("TabledHalton: dimension out of range");
+        return points(i, 1)[j];
+    }
+
+private:
+    std::uint32_t dims_;
+    std::vector<std::uint32_t> factors_;
+};
+
 // ------------------------------------------------ render.hpp:31-54
 struct ImageBuffer { // image.hpp:13-23
     std::uint32_t width = 0, height = 0;

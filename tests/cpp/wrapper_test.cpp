@@ -123,6 +123,13 @@ int main(int argc, char** argv)
     for (int k = 0; k < 50; ++k)
         EXPECT(hal[k * 5 + 3] == rad[k]);
 
+    // TabledHalton equals the linearly scrambled Halton; Faure tables
+    const qmcgpu::TabledHalton th(5);
+    EXPECT(th.points(100, 50) == hal);
+    EXPECT(th.component(107, 3) == hal[7 * 5 + 3]);
+    const qmcgpu::FaurePermutations fp(4);
+    EXPECT(fp.dims() == 4 && fp.for_prime_index(2) == qmcgpu::faure_permutation(5));
+
     // make_stream / SampleStream: the halton kind equals halton_point
     qmcgpu::StreamParams sp;
     sp.dims = 5;
