@@ -329,6 +329,14 @@ typedef struct qmc_render_job { /* RenderJob, render.hpp:31-47 */
 qmc_status qmc_render(const qmc_render_job* job, uint32_t row_begin, uint32_t row_end, float* out,
                       qmc_stream stream);
 
+/* render(job) across several GPUs of one process (no collective): the rows
+ * are split into n_devices bands, one host thread per device renders its
+ * band with qmc_render and copies it into its rows of `out` (HOST memory,
+ * pinned or pageable). Each pixel keeps the single-GPU summation order, so
+ * the image is bit-identical to a one-device render. A device may repeat. */
+qmc_status qmc_render_devices(const qmc_render_job* job, const int* devices, uint32_t n_devices,
+                              float* out);
+
 /* Sample-partitioned render (the paper's parallelization by an extra
  * radical-inverse dimension; partition_by_extra_dimension,
  * imageplane.cpp:114-130): part `part` of `parts` (a power of two) owns the

@@ -299,6 +299,25 @@ inline ImageBuffer render(const RenderJob& job)
     return img;
 }
 
+// render(job) across several GPUs of this process (row bands; host image).
+inline ImageBuffer render_devices(const RenderJob& job, const std::vector<int>& devices)
+{
+    qmc_render_job j{};
+    j.width = job.width;
+    j.height = job.height;
+    j.spp = job.spp;
+    j.kind = job.kind;
+    j.accum = job.accum;
+    j.seed = job.seed;
+    j.generator = job.generator.g.empty() ? nullptr : job.generator.g.data();
+    j.generator_dims = job.generator.dims();
+    ImageBuffer img{job.width, job.height,
+                    std::vector<float>(static_cast<size_t>(job.width) * job.height)};
+    check(qmc_render_devices(&j, devices.data(), static_cast<std::uint32_t>(devices.size()),
+                             img.values.data()));
+    return img;
+}
+
 inline qmc_sampler_kind sampler_kind_from_name(const std::string& name)
 {
     qmc_sampler_kind k{};

@@ -37,7 +37,7 @@ __all__ = [
     "min_toroidal_distance", "check_1d_stratification", "XorTables", "render_partial",
     "render_finalize", "load_generator_vector", "load_linear_factors", "fnv1a64", "write_pnm",
     "write_points_csv", "hilbert_index", "hilbert_xy", "hilbert_phi3_fixed", "digit_reverse", "lattice_shift_fixed",
-    "integrate_partials", "reduce_deterministic", "sampler_kind_name", "status_string",
+    "integrate_partials", "reduce_deterministic", "render_devices", "sampler_kind_name", "status_string",
     "SAMPLER_KINDS",
 ]
 
@@ -113,6 +113,7 @@ def lib():
     sig("qmc_hilbert_order_for", u32, u32, u32)
     sig("qmc_partition_by_extra_dimension", i32, u32, u32, u32, C.POINTER(u64), C.POINTER(u64))
     sig("qmc_hilbert_index", i32, u32, u32, u32, C.POINTER(u64))
+    sig("qmc_render_devices", i32, C.POINTER(RenderJob), P, u32, P)
     sig("qmc_integrate_partials", i32, i32, C.POINTER(StreamParams), i32, u32, u64, u64, u64, i32,
         P, C.POINTER(C.c_int64), P)
     sig("qmc_reduce_deterministic", i32, P, P, u64, C.POINTER(f64))
@@ -700,6 +701,21 @@ def _render_job(width, height, spp, kind, accum, seed, generator, matrices, tabl
     if tables is not None:
         job.tables = tables.handle
     return job, keep
+
+
+def render_devices(width: int, height: int, spp: int, devices, kind: str = "pixel-shifted-lattice",
+                   accum: str = "kahan", seed: int = 0, generator=None,
+                   matrices: Optional[GeneratorMatrixSet] = None,
+                   tables: Optional[XorTables] = None, out=None) -> np.ndarray:
+    """render(RenderJob) across the GPUs `devices` of this process (row bands,
+    one host thread per device; qmc_render_devices). Returns a host
+    [height, width] float32 array, bit-identical to a one-device render."""
+    job, keep = _render_job(width, height, spp, kind, accum, seed, generator, matrices, tables)
+    devs = np.ascontiguousarray(devices, dtype=np.int32)
+    if out is None:
+        out = np.empty((height, width), np.float32)
+    _check(lib().qmc_render_devices(C.byref(job), devs.ctypes.data, devs.size, _ptr(out)))
+    return out
 
 
 def render_partial(width: int, height: int, spp: int, part: int, parts: int,

@@ -3,6 +3,10 @@
 // qmc_render_finalize, and qmc_scene_value.
 #include "objects.hpp"
 
+#include <string>
+#include <thread>
+#include <vector>
+
 using namespace qmcgpu;
 using namespace qmcgpu::host;
 
@@ -172,6 +176,57 @@ qmc_status qmc_render_finalize(const int64_t* accum, uint64_t npix, uint32_t spp
         cuda_ok(launch_render_finalize(reinterpret_cast<const long long*>(accum), npix, spp, out,
                                        as_stream(stream)),
                 "launch_render_finalize");
+    });
+}
+
+qmc_status qmc_render_devices(const qmc_render_job* job, const int* devices, uint32_t n_devices,
+                              float* out)
+{
+    return guard([&] {
+        if (!job)
+            fail(QMC_INVALID_ARGUMENT, "render job is null");
+        if (!devices || n_devices == 0)
+            fail(QMC_INVALID_ARGUMENT, "qmc_render_devices: the device list is empty");
+        if (!out)
+            fail(QMC_INVALID_ARGUMENT, "output pointer is null");
+        if (is_device_pointer(out))
+            fail(QMC_INVALID_ARGUMENT, "qmc_render_devices: out must be host memory");
+        int prev = 0;
+        cuda_ok(cudaGetDevice(&prev), "cudaGetDevice");
+        // one host thread per device renders its row band (the single-GPU
+        // per-pixel order, so the assembled image is bit-identical) and
+        // copies it into its rows of `out`
+        std::vector<qmc_status> st(n_devices, QMC_OK);
+        std::vector<std::string> msg(n_devices);
+        std::vector<std::thread> workers;
+        for (uint32_t k = 0; k < n_devices; ++k) {
+            const uint32_t r0 = static_cast<uint32_t>(uint64_t(job->height) * k / n_devices);
+            const uint32_t r1 = static_cast<uint32_t>(uint64_t(job->height) * (k + 1) / n_devices);
+            workers.emplace_back([&, k, r0, r1] {
+                if (cudaSetDevice(devices[k]) != cudaSuccess) {
+                    st[k] = QMC_CUDA;
+                    msg[k] = "qmc_render_devices: cudaSetDevice failed";
+                    return;
+                }
+                cudaStream_t s = nullptr;
+                if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+                    st[k] = QMC_CUDA;
+                    msg[k] = "qmc_render_devices: cudaStreamCreate failed";
+                    return;
+                }
+                st[k] = qmc_render(job, r0, r1, out + uint64_t(r0) * job->width, s);
+                if (st[k] != QMC_OK)
+                    msg[k] = qmc_last_error();
+                cudaStreamSynchronize(s);
+                cudaStreamDestroy(s);
+            });
+        }
+        for (auto& w : workers)
+            w.join();
+        cudaSetDevice(prev);
+        for (uint32_t k = 0; k < n_devices; ++k)
+            if (st[k] != QMC_OK)
+                fail(st[k], msg[k]);
     });
 }
 

@@ -110,6 +110,8 @@ int main(int argc, char** argv)
     job.spp = 16;
     const auto img = qmcgpu::render(job);
     EXPECT(fnv(img.values.data(), img.values.size() * 4) == want_render);
+    const auto img3 = qmcgpu::render_devices(job, {0, 0, 0}); // row bands, one thread each
+    EXPECT(img3.values == img.values);
     EXPECT(throws<qmcgpu::ConfigError>([] { qmcgpu::GeneratorMatrixSet::builtin(65); }));
     EXPECT(throws<std::invalid_argument>([&] { qmcgpu::sobol_points(m, (1ull << 52) - 1, 2, 4); }));
 

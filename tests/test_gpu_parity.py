@@ -550,6 +550,28 @@ def test_fill_shards_equal_single_fill(world):
         assert torch.equal(torch.cat(parts, 0), whole), (name, world)
 
 
+def test_render_devices_bands_equal_one_device():
+    """qmc_render_devices: row bands on a device list (here device 0 three
+    times, one host thread each) assemble the one-device image bit for bit,
+    into pinned and pageable host memory; errors as documented."""
+    import torch
+
+    for kind, accum in [("pixel-shifted-lattice", "kahan"), ("sobol", "int"),
+                        ("image-plane-halton", "kahan")]:
+        full = q.render(300, 77, 16, kind=kind, accum=accum).cpu().numpy()
+        got = q.render_devices(300, 77, 16, [0, 0, 0], kind=kind, accum=accum)
+        np.testing.assert_array_equal(got, full)
+        pinned = torch.empty((77, 300), dtype=torch.float32, pin_memory=True).numpy()
+        q.render_devices(300, 77, 16, [0] * 5, kind=kind, accum=accum, out=pinned)
+        np.testing.assert_array_equal(pinned, full)
+    with pytest.raises(ValueError):
+        q.render_devices(300, 77, 16, [])
+    with pytest.raises(ValueError):
+        q.render_devices(300, 77, 16, [0], out=torch.empty((77, 300), device="cuda"))
+    with pytest.raises(q.ConfigError):
+        q.render_devices(300, 77, 0, [0, 0])
+
+
 # ------------------------------------------------ full-size properties
 @pytest.mark.slow
 def test_c2_full_size_properties(oracle, columns64):
