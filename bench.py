@@ -315,7 +315,9 @@ def run_ours(args):
     # every step = device fill + D2H of the step's points.
     e2e = None
     if not args.no_e2e:
-        e2e_pts = min(N_POINTS, args.e2e_points)
+        # the job's host image stays ~8.6 GB however many ranks share it
+        # (each rank pins only its slab)
+        e2e_pts = max(1 << 20, min(N_POINTS, args.e2e_points) // world)
         host = torch.empty((e2e_pts, DIMS), dtype=torch.float32, pin_memory=True)
         hn = host.numpy()
         for _ in range(2):
