@@ -18,7 +18,16 @@ namespace qmcgpu {
 namespace {
 
 constexpr uint32_t kMaxDims = 64; // local sample-state capacity per thread
-constexpr int kBlock = 128;
+// Threads per chunk CTA: 256 (16 samples per thread) for every kind but
+// Sobol', whose per-thread state array (local memory) prefers 128 threads.
+template <uint32_t KIND>
+struct ChunkShape {
+    static constexpr uint32_t kLogBlock = KIND == 0 ? 7 : 8;
+    static constexpr uint32_t kBlock = 1u << kLogBlock;
+    static constexpr uint32_t kLogSteps = 12 - kLogBlock; // 4096 = block * steps
+    static constexpr uint32_t kSteps = 1u << kLogSteps;
+};
+constexpr int kBlockMax = 256;
 
 __device__ __forceinline__ uint32_t rad2(uint32_t i) { return brev32(i & 0x7fffffffu); }
 
@@ -50,22 +59,24 @@ __device__ __forceinline__ bool factor(float xs, double& v, const SceneConsts& s
     return true;
 }
 
-// One CTA per 4096-index chunk. Phase 1: the 128 threads evaluate the
-// integrand at indices begin + t + 128*m (m < 32) into shared memory — all
+// One CTA per 4096-index chunk. Phase 1: the B threads (ChunkShape) evaluate
+// the integrand at indices begin + t + B*m (m < 4096/B) into shared memory — all
 // the sampling and FP64 math, fully parallel. Phase 2 (kahan): one thread
 // runs the reference's sequential Neumaier sum over the 4096 values in index
 // order, so the chunk partial is bit-identical to chunk_sum_kahan
 // (quality.cpp:180-194); (int) the llround(v*2^32) terms are exactly
 // associative, so the CTA reduces them in any order (quality.cpp:196-210).
 template <uint32_t KIND, uint32_t FN, uint32_t ACCUM>
-__global__ void __launch_bounds__(kBlock)
+__global__ void __launch_bounds__(ChunkShape<KIND>::kBlock)
     k_integrate(IntegrateParams p, double* __restrict__ partial,
                 unsigned long long* __restrict__ isum, unsigned long long* __restrict__ bad)
 {
     __shared__ double vals[4096];
-    __shared__ uint32_t E[5][kMaxDims]; // sobol: XOR of columns 7..7+c
+    constexpr uint32_t kBlock = ChunkShape<KIND>::kBlock, kLogBlock = ChunkShape<KIND>::kLogBlock;
+    constexpr uint32_t kSteps = ChunkShape<KIND>::kSteps, kLogSteps = ChunkShape<KIND>::kLogSteps;
+    __shared__ uint32_t E[kLogSteps][kMaxDims]; // sobol: XOR of columns kLogBlock..+c
     __shared__ uint32_t XB[kMaxDims];   // sobol: value of `begin` (scramble included)
-    __shared__ long long red[kBlock / 32];
+    __shared__ long long red[kBlockMax / 32];
     const uint64_t chunk = p.chunk0 + blockIdx.x;
     const uint64_t begin = chunk * 4096;
     const uint32_t count = static_cast<uint32_t>(p.n - begin < 4096 ? p.n - begin : 4096);
@@ -91,7 +102,7 @@ __global__ void __launch_bounds__(kBlock)
         cell = (q.px % 128u) + (q.py % 128u) * 128u;
     const RadicalDim* rd = static_cast<const RadicalDim*>(q.radical_dims);
 
-    // Sobol' state: x(begin + t + 128 m) = XB ^ X(t) ^ X(128 m); m advances
+    // Sobol' state: x(begin + t + B m) = XB ^ X(t) ^ X(B m); m advances
     // with x ^= E[ctz(m+1)].
     uint32_t sob[kMaxDims];
     if (KIND == 0) {
@@ -103,15 +114,15 @@ __global__ void __launch_bounds__(kBlock)
                     x ^= __ldg(p.colsT + k * p.mdims + j);
             XB[j] = x;
             uint32_t e = 0;
-            for (uint32_t c = 0; c < 5; ++c) {
-                e ^= __ldg(p.colsT + (7 + c) * p.mdims + j);
+            for (uint32_t c = 0; c < kLogSteps; ++c) {
+                e ^= __ldg(p.colsT + (kLogBlock + c) * p.mdims + j);
                 E[c][j] = e;
             }
         }
         __syncthreads();
         for (uint32_t j = 0; j < dims; ++j) {
             uint32_t x = XB[j];
-            for (uint32_t k = 0; k < 7; ++k)
+            for (uint32_t k = 0; k < kLogBlock; ++k)
                 if ((t >> k) & 1u)
                     x ^= __ldg(p.colsT + k * p.mdims + j);
             sob[j] = x;
@@ -120,8 +131,8 @@ __global__ void __launch_bounds__(kBlock)
 
     bool finite = true;
     long long acc = 0;
-    for (uint32_t m = 0; m < 32; ++m) {
-        const uint32_t local = t + 128 * m;
+    for (uint32_t m = 0; m < kSteps; ++m) {
+        const uint32_t local = t + kBlock * m;
         if (local < count) {
             const uint64_t idx = begin + local;
             const uint32_t i = static_cast<uint32_t>(idx);
@@ -163,7 +174,7 @@ __global__ void __launch_bounds__(kBlock)
             else
                 acc += llround(__dmul_rn(v, 4294967296.0));
         }
-        if (KIND == 0 && m < 31) {
+        if (KIND == 0 && m + 1 < kSteps) {
             const uint32_t c = __ffs(static_cast<int>(m + 1)) - 1;
             for (uint32_t j = 0; j < dims; ++j)
                 sob[j] ^= E[c][j];
@@ -202,10 +213,8 @@ cudaError_t integrate_kind_fn(const IntegrateParams& p, uint32_t accum, double* 
     if (p.nchunks > 0x7fffffffull)
         return cudaErrorInvalidValue;
     const unsigned grid = static_cast<unsigned>(p.nchunks);
-    if (accum == 0)
-        k_integrate<KIND, FN, 0><<<grid, kBlock, 0, s>>>(p, partial, isum, bad);
-    else
-        k_integrate<KIND, FN, 1><<<grid, kBlock, 0, s>>>(p, partial, isum, bad);
+    auto kern = accum == 0 ? k_integrate<KIND, FN, 0> : k_integrate<KIND, FN, 1>;
+    kern<<<grid, ChunkShape<KIND>::kBlock, 0, s>>>(p, partial, isum, bad);
     return cudaGetLastError();
 }
 
