@@ -337,6 +337,17 @@ qmc_status qmc_render(const qmc_render_job* job, uint32_t row_begin, uint32_t ro
 qmc_status qmc_render_devices(const qmc_render_job* job, const int* devices, uint32_t n_devices,
                               float* out);
 
+/* The paper's sample partition across several GPUs of one process, with
+ * the reduction fused into the render: part k of n (a power of two; samples
+ * i == rev_2(k) mod n, partition_by_extra_dimension) runs on devices[k] and
+ * its kernel atomically adds the int64 partial sums straight into one
+ * accumulator on devices[0] — through NVLink peer access when the devices
+ * differ — so no separate collective runs. The finalized image goes to
+ * `out` (HOST memory) and is bit-identical to the one-device int render.
+ * Int accumulator only (job->accum == QMC_ACCUM_INT). A device may repeat. */
+qmc_status qmc_render_samples_devices(const qmc_render_job* job, const int* devices,
+                                      uint32_t n_devices, float* out);
+
 /* Sample-partitioned render (the paper's parallelization by an extra
  * radical-inverse dimension; partition_by_extra_dimension,
  * imageplane.cpp:114-130): part `part` of `parts` (a power of two) owns the

@@ -318,6 +318,28 @@ inline ImageBuffer render_devices(const RenderJob& job, const std::vector<int>& 
     return img;
 }
 
+// The paper's sample partition across GPUs of this process, with the int64
+// reduction fused into the render kernels (atomic adds into one accumulator
+// over peer access). Int accumulator; a power-of-two device count.
+inline ImageBuffer render_samples_devices(const RenderJob& job, const std::vector<int>& devices)
+{
+    qmc_render_job j{};
+    j.width = job.width;
+    j.height = job.height;
+    j.spp = job.spp;
+    j.kind = job.kind;
+    j.accum = QMC_ACCUM_INT;
+    j.seed = job.seed;
+    j.generator = job.generator.g.empty() ? nullptr : job.generator.g.data();
+    j.generator_dims = job.generator.dims();
+    ImageBuffer img{job.width, job.height,
+                    std::vector<float>(static_cast<size_t>(job.width) * job.height)};
+    check(qmc_render_samples_devices(&j, devices.data(),
+                                     static_cast<std::uint32_t>(devices.size()),
+                                     img.values.data()));
+    return img;
+}
+
 inline qmc_sampler_kind sampler_kind_from_name(const std::string& name)
 {
     qmc_sampler_kind k{};

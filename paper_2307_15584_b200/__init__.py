@@ -37,7 +37,7 @@ __all__ = [
     "min_toroidal_distance", "check_1d_stratification", "XorTables", "render_partial",
     "render_finalize", "load_generator_vector", "load_linear_factors", "fnv1a64", "write_pnm",
     "write_points_csv", "hilbert_index", "hilbert_xy", "hilbert_phi3_fixed", "digit_reverse", "lattice_shift_fixed",
-    "integrate_partials", "reduce_deterministic", "render_devices", "sampler_kind_name", "status_string",
+    "integrate_partials", "reduce_deterministic", "render_devices", "render_samples_devices", "sampler_kind_name", "status_string",
     "SAMPLER_KINDS",
 ]
 
@@ -114,6 +114,7 @@ def lib():
     sig("qmc_partition_by_extra_dimension", i32, u32, u32, u32, C.POINTER(u64), C.POINTER(u64))
     sig("qmc_hilbert_index", i32, u32, u32, u32, C.POINTER(u64))
     sig("qmc_render_devices", i32, C.POINTER(RenderJob), P, u32, P)
+    sig("qmc_render_samples_devices", i32, C.POINTER(RenderJob), P, u32, P)
     sig("qmc_integrate_partials", i32, i32, C.POINTER(StreamParams), i32, u32, u64, u64, u64, i32,
         P, C.POINTER(C.c_int64), P)
     sig("qmc_reduce_deterministic", i32, P, P, u64, C.POINTER(f64))
@@ -715,6 +716,23 @@ def render_devices(width: int, height: int, spp: int, devices, kind: str = "pixe
     if out is None:
         out = np.empty((height, width), np.float32)
     _check(lib().qmc_render_devices(C.byref(job), devs.ctypes.data, devs.size, _ptr(out)))
+    return out
+
+
+def render_samples_devices(width: int, height: int, spp: int, devices,
+                           kind: str = "pixel-shifted-lattice", seed: int = 0, generator=None,
+                           matrices: Optional[GeneratorMatrixSet] = None,
+                           tables: Optional[XorTables] = None, out=None) -> np.ndarray:
+    """The paper's sample partition over `devices` (a power-of-two count) with
+    the int64 reduction fused into the render kernels (atomic adds into one
+    accumulator on devices[0], peer access across GPUs). Returns the host
+    [height, width] image, bit-identical to render(..., accum="int")."""
+    job, keep = _render_job(width, height, spp, kind, "int", seed, generator, matrices, tables)
+    devs = np.ascontiguousarray(devices, dtype=np.int32)
+    if out is None:
+        out = np.empty((height, width), np.float32)
+    _check(lib().qmc_render_samples_devices(C.byref(job), devs.ctypes.data, devs.size,
+                                            _ptr(out)))
     return out
 
 

@@ -230,6 +230,123 @@ qmc_status qmc_render_devices(const qmc_render_job* job, const int* devices, uin
     });
 }
 
+namespace {
+
+// RAII: a non-blocking stream on the current device, destroyed last.
+struct OwnedStream {
+    cudaStream_t s = nullptr;
+    OwnedStream() { cuda_ok(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate"); }
+    ~OwnedStream()
+    {
+        if (s) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    }
+    OwnedStream(const OwnedStream&) = delete;
+    OwnedStream& operator=(const OwnedStream&) = delete;
+};
+
+// RAII: restores the calling thread's current device.
+struct DeviceRestore {
+    int prev = 0;
+    DeviceRestore() { cuda_ok(cudaGetDevice(&prev), "cudaGetDevice"); }
+    ~DeviceRestore() { cudaSetDevice(prev); }
+};
+
+} // namespace
+
+qmc_status qmc_render_samples_devices(const qmc_render_job* job, const int* devices,
+                                      uint32_t n_devices, float* out)
+{
+    return guard([&] {
+        if (!job)
+            fail(QMC_INVALID_ARGUMENT, "render job is null");
+        if (job->accum != QMC_ACCUM_INT)
+            fail(QMC_INVALID_ARGUMENT,
+                 "render_samples: sample partitions need the int accumulator (exactly associative)");
+        if (!devices || n_devices == 0 || (n_devices & (n_devices - 1)) != 0)
+            fail(QMC_INVALID_ARGUMENT,
+                 "qmc_render_samples_devices: the device count must be a power of two");
+        if (!out)
+            fail(QMC_INVALID_ARGUMENT, "output pointer is null");
+        if (is_device_pointer(out))
+            fail(QMC_INVALID_ARGUMENT, "qmc_render_samples_devices: out must be host memory");
+        const DeviceRestore restore;
+        const int home = devices[0];
+        cuda_ok(cudaSetDevice(home), "cudaSetDevice");
+        const OwnedStream hs; // declared first: destroyed after everything below
+        uint64_t npix = 0;
+        {
+            CallArgs hargs(hs.s);
+            ResolvedRender hr; // validates the job
+            resolve_render(job, 0, job->height, hs.s, hargs, hr);
+            npix = hr.npix;
+            cuda_ok(cudaStreamSynchronize(hs.s), "sync");
+        }
+        if (npix == 0)
+            return;
+        // the one accumulator, on the first device
+        long long* acc = nullptr;
+        cuda_ok(cudaMalloc(&acc, npix * 8 + 8), "cudaMalloc");
+        const std::unique_ptr<long long, DevFree> acc_own(acc);
+        cuda_ok(cudaMemset(acc, 0, npix * 8), "cudaMemset");
+        // part k of n (samples i == rev_2(k) mod n) on devices[k]: one kernel
+        // renders and atomically adds its int64 partials into the
+        // accumulator — over NVLink peer access when the device differs
+        std::vector<qmc_status> st(n_devices, QMC_OK);
+        std::vector<std::string> msg(n_devices);
+        std::vector<std::thread> workers;
+        for (uint32_t k = 0; k < n_devices; ++k) {
+            workers.emplace_back([&, k] {
+                st[k] = guard([&] {
+                    cuda_ok(cudaSetDevice(devices[k]), "cudaSetDevice");
+                    if (devices[k] != home) {
+                        int can = 0;
+                        cuda_ok(cudaDeviceCanAccessPeer(&can, devices[k], home),
+                                "cudaDeviceCanAccessPeer");
+                        if (!can)
+                            fail(QMC_CUDA, "qmc_render_samples_devices: no peer access to the "
+                                           "accumulator's device");
+                        const cudaError_t e = cudaDeviceEnablePeerAccess(home, 0);
+                        if (e == cudaErrorPeerAccessAlreadyEnabled)
+                            cudaGetLastError(); // clear
+                        else
+                            cuda_ok(e, "cudaDeviceEnablePeerAccess");
+                    }
+                    uint64_t rem = 0, mod = 1;
+                    const qmc_status ps =
+                        qmc_partition_by_extra_dimension(k, n_devices, 2, &rem, &mod);
+                    if (ps != QMC_OK)
+                        fail(ps, last_error());
+                    const OwnedStream s;
+                    CallArgs args(s.s);
+                    ResolvedRender rr;
+                    resolve_render(job, 0, job->height, s.s, args, rr);
+                    cuda_ok(launch_render_partial(rr.p, job->kind, static_cast<uint32_t>(rem),
+                                                  static_cast<uint32_t>(mod), acc, s.s, true),
+                            "launch_render_partial");
+                    cuda_ok(cudaStreamSynchronize(s.s), "sync");
+                });
+                if (st[k] != QMC_OK)
+                    msg[k] = qmc_last_error();
+            });
+        }
+        for (auto& w : workers)
+            w.join();
+        for (uint32_t k = 0; k < n_devices; ++k)
+            if (st[k] != QMC_OK)
+                fail(st[k], msg[k]);
+        cuda_ok(cudaSetDevice(home), "cudaSetDevice");
+        float* d = nullptr;
+        cuda_ok(cudaMalloc(&d, npix * 4 + 4), "cudaMalloc");
+        const DevPtr d_own(d);
+        cuda_ok(launch_render_finalize(acc, npix, job->spp, d, hs.s), "launch_render_finalize");
+        cuda_ok(cudaMemcpyAsync(out, d, npix * 4, cudaMemcpyDeviceToHost, hs.s), "D2H");
+        cuda_ok(cudaStreamSynchronize(hs.s), "sync");
+    });
+}
+
 qmc_status qmc_scene_value(const double* xy, double* out, uint64_t n, qmc_stream stream)
 {
     return guard([&] {

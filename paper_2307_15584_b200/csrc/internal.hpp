@@ -149,7 +149,8 @@ cudaError_t launch_render(const RenderParams& p, uint32_t kind, uint32_t accum, 
 // Int-mode partial render over samples first, first+step, ... (< spp):
 // int64 per pixel of the band; finalize: float(sum / 2^32 / spp).
 cudaError_t launch_render_partial(const RenderParams& p, uint32_t kind, uint32_t first,
-                                  uint32_t step, long long* acc, cudaStream_t s);
+                                  uint32_t step, long long* acc, cudaStream_t s,
+                                  bool add = false);
 cudaError_t launch_render_finalize(const long long* acc, uint64_t npix, uint32_t spp, float* out,
                                    cudaStream_t s);
 

@@ -373,7 +373,11 @@ __global__ void __launch_bounds__(kBlock) k_render_warp(RenderParams p, float* _
 // int64, render.cpp:72-78) is exactly associative, so summing the partials
 // of all parts (one NCCL all-reduce across GPUs) and finalizing is
 // bit-identical to the single-GPU int render.
-template <uint32_t KIND>
+// ADD: atomically add into acc instead of storing — the fused reduction of
+// qmc_render_samples_devices, where acc may be another GPU's memory (peer
+// access over NVLink): every part's kernel adds its int64 partials straight
+// into the one accumulator, no separate collective.
+template <uint32_t KIND, bool ADD = false>
 __global__ void __launch_bounds__(kBlock)
     k_render_partial(RenderParams p, uint32_t first, uint32_t step, long long* __restrict__ acc)
 {
@@ -439,7 +443,11 @@ __global__ void __launch_bounds__(kBlock)
         else
             run(std::false_type{}, std::false_type{}, inside, 0, 0);
     }
-    acc[q] = isum;
+    if (ADD)
+        atomicAdd(reinterpret_cast<unsigned long long*>(acc) + q,
+                  static_cast<unsigned long long>(isum)); // two's complement: exact
+    else
+        acc[q] = isum;
 }
 
 __global__ void k_render_finalize(const long long* __restrict__ acc, uint64_t npix, uint32_t spp,
@@ -629,28 +637,31 @@ cudaError_t launch_render(const RenderParams& p, uint32_t kind, uint32_t accum, 
 
 template <uint32_t KIND>
 cudaError_t render_partial_kind(const RenderParams& p, uint32_t first, uint32_t step,
-                                long long* acc, cudaStream_t s)
+                                long long* acc, bool add, cudaStream_t s)
 {
     const uint64_t npix = static_cast<uint64_t>(p.row_end - p.row_begin) * p.width;
-    k_render_partial<KIND><<<static_cast<unsigned>((npix + kBlock - 1) / kBlock), kBlock, 0, s>>>(
-        p, first, step, acc);
+    const unsigned grid = static_cast<unsigned>((npix + kBlock - 1) / kBlock);
+    if (add)
+        k_render_partial<KIND, true><<<grid, kBlock, 0, s>>>(p, first, step, acc);
+    else
+        k_render_partial<KIND, false><<<grid, kBlock, 0, s>>>(p, first, step, acc);
     return cudaGetLastError();
 }
 
 cudaError_t launch_render_partial(const RenderParams& p, uint32_t kind, uint32_t first,
-                                  uint32_t step, long long* acc, cudaStream_t s)
+                                  uint32_t step, long long* acc, cudaStream_t s, bool add)
 {
     if (p.row_end <= p.row_begin || p.width == 0)
         return cudaSuccess;
     switch (kind) {
-    case 0: return render_partial_kind<0>(p, first, step, acc, s);
-    case 1: return render_partial_kind<1>(p, first, step, acc, s);
-    case 2: return render_partial_kind<2>(p, first, step, acc, s);
-    case 3: return render_partial_kind<3>(p, first, step, acc, s);
-    case 4: return render_partial_kind<4>(p, first, step, acc, s);
-    case 5: return render_partial_kind<5>(p, first, step, acc, s);
-    case 6: return render_partial_kind<6>(p, first, step, acc, s);
-    case 7: return render_partial_kind<7>(p, first, step, acc, s);
+    case 0: return render_partial_kind<0>(p, first, step, acc, add, s);
+    case 1: return render_partial_kind<1>(p, first, step, acc, add, s);
+    case 2: return render_partial_kind<2>(p, first, step, acc, add, s);
+    case 3: return render_partial_kind<3>(p, first, step, acc, add, s);
+    case 4: return render_partial_kind<4>(p, first, step, acc, add, s);
+    case 5: return render_partial_kind<5>(p, first, step, acc, add, s);
+    case 6: return render_partial_kind<6>(p, first, step, acc, add, s);
+    case 7: return render_partial_kind<7>(p, first, step, acc, add, s);
     }
     return cudaErrorInvalidValue;
 }

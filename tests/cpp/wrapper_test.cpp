@@ -112,6 +112,11 @@ int main(int argc, char** argv)
     EXPECT(fnv(img.values.data(), img.values.size() * 4) == want_render);
     const auto img3 = qmcgpu::render_devices(job, {0, 0, 0}); // row bands, one thread each
     EXPECT(img3.values == img.values);
+    qmcgpu::RenderJob ijob = job;
+    ijob.accum = QMC_ACCUM_INT;
+    const auto iimg = qmcgpu::render(ijob);
+    const auto iimg4 = qmcgpu::render_samples_devices(ijob, {0, 0, 0, 0}); // fused reduction
+    EXPECT(iimg4.values == iimg.values);
     EXPECT(throws<qmcgpu::ConfigError>([] { qmcgpu::GeneratorMatrixSet::builtin(65); }));
     EXPECT(throws<std::invalid_argument>([&] { qmcgpu::sobol_points(m, (1ull << 52) - 1, 2, 4); }));
 

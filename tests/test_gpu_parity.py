@@ -572,6 +572,23 @@ def test_render_devices_bands_equal_one_device():
         q.render_devices(300, 77, 0, [0, 0])
 
 
+def test_render_samples_devices_fused_reduction():
+    """qmc_render_samples_devices: parts k of n (the paper's sample partition)
+    atomically add their int64 partials into one accumulator from their own
+    kernels (here all on device 0; across GPUs through peer access) — the
+    finalized image equals the one-device int render bit for bit."""
+    for kind in ("pixel-shifted-lattice", "sobol", "image-plane-halton", "halton-hilbert"):
+        full = q.render(200, 61, 24, kind=kind, accum="int").cpu().numpy()
+        for n in (1, 2, 4, 8):
+            got = q.render_samples_devices(200, 61, 24, [0] * n, kind=kind)
+            np.testing.assert_array_equal(got, full, err_msg=f"{kind} n={n}")
+    with pytest.raises(ValueError):
+        q.render_samples_devices(200, 61, 24, [0, 0, 0])
+    job_err = pytest.raises(ValueError)
+    with job_err:
+        q.render_samples_devices(200, 61, 24, [])
+
+
 # ------------------------------------------------ full-size properties
 @pytest.mark.slow
 def test_c2_full_size_properties(oracle, columns64):
