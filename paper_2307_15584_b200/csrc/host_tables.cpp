@@ -4,6 +4,7 @@
 // function cites the reference file:line it restates.
 #include "host.hpp"
 
+#include <cstdlib>
 #include <map>
 #include <sstream>
 #include <tuple>

@@ -13,8 +13,12 @@
 //     lattice update is one IMAD with a compile-time brev constant;
 //   * the float map is 9 full-rate ops (device.cuh map_u32).
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <type_traits>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "device.cuh"
 #include "internal.hpp"
@@ -901,7 +905,7 @@ __device__ __forceinline__ void sts32(uint32_t addr, uint32_t v)
 // One warp, one dimension, `cnt` consecutive indices from i0 into the
 // padded tile column at shared address col (row stride ld words). `st` (or
 // null) carries the incremental state from the previous contiguous run.
-template <bool U32OUT>
+template <bool U32OUT, int UNR = 4>
 __device__ __forceinline__ void halton_run(const RadicalDim& r, uint32_t i0, uint32_t cnt,
                                            uint32_t lane, uint32_t col, uint32_t ld,
                                            HaltonState* st)
@@ -945,6 +949,7 @@ __device__ __forceinline__ void halton_run(const RadicalDim& r, uint32_t i0, uin
             // steps whose 32 indices all lie in h's block: one record
             const uint32_t nf = min(steps - s, (G - lob) >> 5);
             const uint32_t* tab = r.ftable + lob + lane;
+#pragma unroll(UNR)
             for (uint32_t e = 0; e < nf; ++e) {
                 const uint32_t acc = __ldg(tab) * r0.mul + r0.acc;
                 const uint32_t x = frac_div_magic(acc, r0.scale, r0.mlo, r0.mhi);
@@ -973,7 +978,7 @@ __device__ __forceinline__ void halton_run(const RadicalDim& r, uint32_t i0, uin
                 hi_advance(h1, r1, g0, mulg, r);
             }
         }
-        if (st && lane == 0) {
+        if (st) { // every lane: the state may live in registers (k_halton_runs)
             st->next = i0 + (steps << 5);
             st->lob = lob;
             st->h1 = h1;
@@ -1006,7 +1011,7 @@ __global__ void __launch_bounds__(kBlock)
                    uint64_t first, uint64_t n, uint64_t ntiles, uint32_t* __restrict__ out)
 {
     extern __shared__ __align__(16) uint32_t tile[];
-    const uint32_t ld = dims + 1;
+    const uint32_t ld = dims | 1u; // odd row stride: a column store hits 32 banks
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, nwarps = blockDim.x >> 5;
     const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(tile));
     // (dim, point run) work items: several warps share a dimension when
@@ -1037,6 +1042,186 @@ __global__ void __launch_bounds__(kBlock)
         tile_store_rows(tile, ld, dims, div_dims, 0, cnt, out + p0 * dims);
         __syncthreads();
     }
+}
+
+__device__ __forceinline__ void bar_named(uint32_t id, uint32_t threads)
+{
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// Prime-base Halton for dims <= 32, one dimension per warp for the whole
+// launch: a CTA of runs x dims warps (runs = min(15, 32 / dims)) owns a
+// contiguous range of sub-tiles of `chunk` points; run r walks its own
+// contiguous part of that range, one sub-tile at a time, so every warp's
+// incremental state (HaltonState) stays in registers from sub-tile to
+// sub-tile and each warp step is just the table lookup, IMAD, magic division
+// and map. A run's dims warps fill its padded [chunk][dims | 1] sub-tile,
+// meet at their own named barrier, and write it out as consecutive words
+// (each thread keeps a fixed column and a fixed shared-memory stride), so
+// runs never wait for each other.
+template <bool U32OUT, int UNR>
+__global__ void __launch_bounds__(1024, 1)
+    k_halton_runs(const RadicalDim* __restrict__ rd, uint32_t dims, uint32_t runs, uint32_t chunk,
+                  uint64_t first, uint64_t n, uint64_t nsub, uint32_t* __restrict__ out, int skip)
+{
+    extern __shared__ __align__(16) uint32_t tile[];
+    const uint32_t ld = dims | 1u; // odd row stride: a column store hits 32 banks
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint32_t run = warp / dims, j = warp - run * dims;
+    const uint32_t nthr = dims * 32, tid = threadIdx.x - run * nthr;
+    const uint32_t* sub = tile + static_cast<size_t>(run) * chunk * ld;
+    const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(sub));
+    // balanced split of the sub-tiles over the CTAs, then over the runs
+    const uint64_t s0 = nsub * blockIdx.x / gridDim.x, s1 = nsub * (blockIdx.x + 1) / gridDim.x;
+    const uint64_t q = (s1 - s0 + runs - 1) / runs;
+    const uint64_t r0 = s0 + run * q, r1 = min(s1, r0 + q);
+    // store mapping: thread tid owns the quads at words 4*tid + k*4*nthr of a
+    // sub-tile, i.e. a fixed column and rows advancing by 128 (4*nthr =
+    // 128*dims). Sub-tiles start on multiples of 32 points, so with out
+    // 16-B aligned every quad is a 16-B store; its words sit at fixed offsets
+    // from the row start (offk: +1 per row wrap when dims % 4 != 0).
+    const bool vec = (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+    const uint32_t e0 = vec ? tid * 4 : tid, row0 = e0 / dims, col0 = e0 - row0 * dims;
+    const uint32_t pad = ld - dims;
+    const uint32_t off1 = 1 + (col0 + 1) / dims * pad, off2 = 2 + (col0 + 2) / dims * pad,
+                   off3 = 3 + (col0 + 3) / dims * pad;
+    HaltonState st;
+    st.live = 0;
+    for (uint64_t s = r0; s < r1; ++s) {
+        const uint64_t p0 = s * chunk;
+        const uint32_t cnt = static_cast<uint32_t>(n - p0 < chunk ? n - p0 : chunk);
+        if (!(skip & 2))
+        halton_run<U32OUT, UNR>(rd[j], static_cast<uint32_t>(first + p0), cnt, lane, sbase + j * 4,
+                                ld, &st);
+        bar_named(1 + run, nthr);
+        if (skip & 1) { bar_named(1 + run, nthr); continue; }
+        const uint32_t words = cnt * dims;
+        uint32_t* o = out + p0 * dims;
+        const uint32_t* src = sub + row0 * ld + col0;
+        uint32_t e = e0;
+        if (!vec) {
+#pragma unroll 4
+            for (; e < words; e += nthr, src += 32 * ld)
+                __stcs(o + e, *src);
+        } else if ((dims & 3u) == 0) {
+#pragma unroll 2
+            for (; e < words; e += 4 * nthr, src += 128 * ld)
+                __stcs(reinterpret_cast<uint4*>(o + e), make_uint4(src[0], src[1], src[2], src[3]));
+        } else {
+#pragma unroll 2
+            for (; e + 4 <= words; e += 4 * nthr, src += 128 * ld)
+                __stcs(reinterpret_cast<uint4*>(o + e),
+                       make_uint4(src[0], src[off1], src[off2], src[off3]));
+            if (e < words) { // the ragged end of the last sub-tile: < 4 words
+                o[e] = src[0];
+                if (e + 1 < words)
+                    o[e + 1] = src[off1];
+                if (e + 2 < words)
+                    o[e + 2] = src[off2];
+            }
+        }
+        bar_named(1 + run, nthr);
+    }
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(addr), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t addr)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity)
+{
+    uint32_t ok;
+    do {
+        asm volatile("{\n\t.reg .pred p;\n\t"
+                     "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(ok)
+                     : "r"(addr), "r"(parity)
+                     : "memory");
+    } while (!ok);
+}
+
+// Prime-base Halton, dims == 32, stored by TMA: the k_halton_runs walk (one
+// dimension per warp, state in registers) into a ring of nbuf sub-tiles of
+// `rows` points laid out exactly as the output rows (128 B each) with the
+// 128-B swizzle, so a column store by 32 lanes is a 4-way bank conflict
+// instead of 32-way, and the tensor-map store (cp.async.bulk.tensor, boxes of
+// 256 rows) runs asynchronously while the warps walk the next sub-tiles.
+// full[b]: the 32 warps have written sub-tile b (count 32); empty[b]: its
+// bulk store has finished reading shared memory (count 1, warp 0 lane 0,
+// which also issues the stores: it walks base 2, the cheapest dimension).
+template <bool U32OUT>
+__global__ void __launch_bounds__(1024, 1)
+    k_halton_tma(const __grid_constant__ CUtensorMap tmap, const RadicalDim* __restrict__ rd,
+                 uint32_t rows, uint32_t nbuf, uint64_t first, uint64_t n, uint64_t nsub, int skip)
+{
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    __shared__ __align__(8) uint64_t bars[16];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint32_t base = (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + 1023u) & ~1023u;
+    const uint32_t bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
+    const uint32_t buf_bytes = rows * 128;
+    if (threadIdx.x == 0) {
+        for (uint32_t b = 0; b < nbuf; ++b) {
+            mbar_init(bar0 + 8 * b, 32);             // full[b]
+            mbar_init(bar0 + 8 * (8 + b), 1);        // empty[b]
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // lane l writes rows l + 32 s: row & 7 == l & 7, so the swizzled column
+    // offset of dimension `warp` is fixed per lane
+    const uint32_t col = (((warp >> 2) ^ (lane & 7u)) << 4) + (warp & 3u) * 4 - lane * 128;
+    const uint64_t s0 = nsub * blockIdx.x / gridDim.x, s1 = nsub * (blockIdx.x + 1) / gridDim.x;
+    const bool issuer = threadIdx.x == 0;
+    HaltonState st;
+    st.live = 0;
+    uint32_t b = 0, k = 0;
+    for (uint64_t s = s0; s < s1; ++s) {
+        const uint64_t p0 = s * rows;
+        const uint32_t cnt = static_cast<uint32_t>(n - p0 < rows ? n - p0 : rows);
+        const uint32_t buf = base + b * buf_bytes;
+        if (k > 0)
+            mbar_wait(bar0 + 8 * (8 + b), (k - 1) & 1u);
+        if (!(skip & 2))
+            halton_run<U32OUT>(rd[warp], static_cast<uint32_t>(first + p0), cnt, lane,
+                               buf + lane * 128 + col, 32, &st);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0)
+            mbar_arrive(bar0 + 8 * b);
+        if (issuer) {
+            mbar_wait(bar0 + 8 * b, k & 1u);
+            if (!(skip & 1)) {
+                for (uint32_t r = 0; r < cnt; r += 256) {
+                    const int32_t y = static_cast<int32_t>(p0 + r);
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                            reinterpret_cast<uint64_t>(&tmap)),
+                        "r"(buf + r * 128), "r"(0), "r"(y)
+                        : "memory");
+                }
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            // the previous sub-tile's store has read its buffer: release it
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            if (s > s0)
+                mbar_arrive(bar0 + 8 * (8 + (b == 0 ? nbuf - 1 : b - 1)));
+        }
+        __syncwarp();
+        if (++b == nbuf) {
+            b = 0;
+            ++k;
+        }
+    }
+    if (issuer)
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // ------------------------------------------------------------- launching
@@ -1371,15 +1556,96 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
 {
     if (r.n == 0)
         return cudaSuccess;
+    static const int kSkip = [] {
+        const char* e = getenv("QMC_HALTON_SKIP");
+        return e ? atoi(e) : 0;
+    }();
+    static const int kTma = [] {
+        const char* e = getenv("QMC_HALTON_TMA");
+        return e ? atoi(e) : 1;
+    }();
+    if (dims == 32 && kTma && (reinterpret_cast<uintptr_t>(r.out) & 15u) == 0 &&
+        r.n < (1ull << 31)) {
+        static PFN_cuTensorMapEncodeTiled encode = [] {
+            void* fn = nullptr;
+            cudaDriverEntryPointQueryResult q{};
+            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+                    cudaSuccess ||
+                q != cudaDriverEntryPointSuccess)
+                fn = nullptr;
+            return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+        }();
+        static const uint32_t kRows = [] {
+            const char* e = getenv("QMC_HALTON_TMA_ROWS");
+            return e ? static_cast<uint32_t>(atoi(e)) : 512u;
+        }();
+        static const uint32_t kBufs = [] {
+            const char* e = getenv("QMC_HALTON_TMA_NB");
+            return e ? static_cast<uint32_t>(atoi(e)) : 3u;
+        }();
+        if (encode) {
+            CUtensorMap tmap;
+            const cuuint64_t gdim[2] = {32, r.n};
+            const cuuint64_t gstride[1] = {128};
+            const cuuint32_t box[2] = {32, 256};
+            const cuuint32_t estride[2] = {1, 1};
+            if (encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, r.out, gdim, gstride, box, estride,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                       CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+                const size_t smem = static_cast<size_t>(kRows) * 128 * kBufs + 1024;
+                auto kern = u32 ? k_halton_tma<true> : k_halton_tma<false>;
+                const cudaError_t e = cudaFuncSetAttribute(
+                    kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+                if (e != cudaSuccess)
+                    return e;
+                const uint64_t nsub = (r.n + kRows - 1) / kRows;
+                const unsigned grid = static_cast<unsigned>(
+                    std::min<uint64_t>(nsub, static_cast<uint64_t>(sm_count())));
+                kern<<<grid, 1024, smem, s>>>(tmap, static_cast<const RadicalDim*>(rd), kRows,
+                                              kBufs, r.first, r.n, nsub, kSkip);
+                return cudaGetLastError();
+            }
+        }
+    }
+    if (dims <= 32) {
+        // one CTA per SM, runs x dims warps, sub-tiles sharing ~kRunsTileWords
+        const uint32_t runs = std::min(15u, 32u / dims), ld = dims | 1u;
+        static const uint32_t kRunsTileWords = [] {
+            const char* e = getenv("QMC_HALTON_TILE_WORDS");
+            return e ? static_cast<uint32_t>(atoi(e)) : 49152u;
+        }();
+        uint32_t chunk = (kRunsTileWords / (runs * ld)) & ~31u;
+        if (chunk < 32)
+            chunk = 32;
+        const size_t smem = static_cast<size_t>(chunk) * ld * runs * 4;
+        static const int kUnr = [] {
+            const char* e = getenv("QMC_HALTON_UNROLL");
+            return e ? atoi(e) : 4;
+        }();
+        auto kern = kUnr == 8 ? (u32 ? k_halton_runs<true, 8> : k_halton_runs<false, 8>)
+                              : (u32 ? k_halton_runs<true, 4> : k_halton_runs<false, 4>);
+        const cudaError_t e =
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess)
+            return e;
+        const uint64_t nsub = (r.n + chunk - 1) / chunk;
+        const unsigned grid =
+            static_cast<unsigned>(std::min<uint64_t>(nsub, static_cast<uint64_t>(sm_count())));
+        kern<<<grid, runs * dims * 32, smem, s>>>(static_cast<const RadicalDim*>(rd), dims, runs,
+                                                   chunk, r.first, r.n, nsub,
+                                                   static_cast<uint32_t*>(r.out), kSkip);
+        return cudaGetLastError();
+    }
     // tile of tp points x (dims + 1) padded words: <= 48 KB, >= 32 points;
     // then 64 B of carried state per dimension when dims >= warps per CTA
     // 48 KB tiles: 4 CTAs (32 warps) per SM; larger tiles amortise the
     // per-(tile, dimension) bookkeeping better but lose more to latency
     // (measured 8-32K words at 8-64 dims, tools/exp_halton.py)
-    uint32_t tp = (12288u / (dims + 1)) & ~31u;
+    uint32_t tp = (12288u / (dims | 1u)) & ~31u;
     if (tp < 32)
         tp = 32;
-    const size_t tile_words = (static_cast<size_t>(tp) * (dims + 1) + 15) & ~size_t(15);
+    const size_t tile_words = (static_cast<size_t>(tp) * (dims | 1u) + 15) & ~size_t(15);
     const size_t smem = tile_words * 4 + (dims >= kBlock / 32 ? size_t(dims) * 64 : 0);
     auto kern = u32 ? k_halton_tiled<true> : k_halton_tiled<false>;
     if (smem > 48 * 1024) {

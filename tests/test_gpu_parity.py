@@ -156,6 +156,22 @@ def test_halton_fill_long_runs_vs_reference(ref, mode, first):
         np.testing.assert_array_equal(got[:, j], exp, err_msg=f"dim={j}")
 
 
+@pytest.mark.parametrize("dims", [1, 2, 3, 5, 8, 13, 16, 20, 31, 32])
+def test_halton_fill_runs_all_small_dims_vs_reference(ref, dims):
+    """dims <= 32 (k_halton_runs: runs x dims warps, state in registers):
+    enough points for several sub-tiles per run on every SM, uneven runs, a
+    ragged last sub-tile, and a start just below the base-3 prime_max_power."""
+    n = 148 * 4 * 1500 + 777
+    for first, mode in [(3486784401 - 100000, "linear"), (12345, "faure")]:
+        got = u32(q.halton_fill(n, dims, first=first, scramble=mode, fixed=True)).reshape(n, dims)
+        for j in range(dims):
+            b = q.prime(j)
+            exp = np.zeros(n, np.uint32)
+            assert ref.ref_radical_fixed_fill(first, n, j, _MODE[mode], b - 1 if b > 2 else 1,
+                                              ptr(exp)) == 0
+            np.testing.assert_array_equal(got[:, j], exp, err_msg=f"first={first} dim={j}")
+
+
 # ---------------------------------------------------------------- Sobol'
 def test_sobol_vs_golden(golden_arrays, golden, oracle):
     got = u32(q.sobol_fill(1024, 64, fixed=True))
