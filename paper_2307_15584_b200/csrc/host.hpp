@@ -126,6 +126,8 @@ void hilbert_xy_host(uint64_t d, uint32_t order, uint32_t& x, uint32_t& y); // h
 struct DigitTable {
     const uint32_t* ptr = nullptr;
     uint32_t group = 0;
+    // with_quotients: {floor(T * 2^32 / group), T * 2^32 mod group} per entry
+    const uint32_t* qr = nullptr;
 };
 
 // Widest b^d-entry table (b^d <= max_entries) inverting d >= min_digits
@@ -135,7 +137,7 @@ struct DigitTable {
 constexpr uint32_t kDigitTableMax = 4096;
 constexpr uint32_t kFillTableMax = 65536;
 DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor, uint32_t min_digits = 2,
-                       uint32_t max_entries = kDigitTableMax);
+                       uint32_t max_entries = kDigitTableMax, bool with_quotients = false);
 // floor(2^64 / b^D) for D = 0..32 (0 where b^D >= 2^32), on the current device
 const uint64_t* pow_magic(uint32_t b);
 std::vector<RadicalDim> radical_dims(uint32_t dims, uint32_t first_prime, qmc_radical_scramble sc,

@@ -273,12 +273,14 @@ uint64_t digit_reverse_host(uint64_t v, uint32_t base, uint32_t digits)
 // L1-resident), entry v = the d digits of v permuted by sigma and mirrored.
 // Built once per (device, base, scramble) and kept for the process.
 DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor, uint32_t min_digits,
-                       uint32_t max_entries)
+                       uint32_t max_entries, bool with_quotients)
 {
+    struct Slot {
+        DevPtr t, qr;
+        uint32_t group = 0;
+    };
     static std::mutex mu;
-    static std::map<std::tuple<int, uint32_t, uint32_t, uint32_t, uint32_t>,
-                    std::pair<DevPtr, uint32_t>>
-        cache;
+    static std::map<std::tuple<int, uint32_t, uint32_t, uint32_t, uint32_t, bool>, Slot> cache;
     uint32_t d = 0, group = 1;
     while (static_cast<uint64_t>(group) * b <= max_entries) {
         group *= b;
@@ -288,8 +290,8 @@ DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor, uint32_t min_
         return {};
     const int dev = current_device();
     std::lock_guard<std::mutex> lk(mu);
-    auto& slot = cache[{dev, b, mode, factor, max_entries}];
-    if (!slot.first) {
+    auto& slot = cache[{dev, b, mode, factor, max_entries, with_quotients}];
+    if (!slot.t) {
         std::vector<uint32_t> sigma(b);
         if (mode == 2) {
             sigma = faure(b);
@@ -306,10 +308,22 @@ DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor, uint32_t min_
             }
             t[v] = out;
         }
-        slot.first = dev_upload(t.data(), t.size() * 4);
-        slot.second = group;
+        if (with_quotients) {
+            // T * 2^32 = q * group + r: the contiguous fill adds the
+            // warp-uniform quotient of the high digits and a carry (r >= thr)
+            std::vector<uint32_t> qr(2 * (group + 8), 0u);
+            for (uint32_t v = 0; v < group; ++v) {
+                const uint64_t num = static_cast<uint64_t>(t[v]) << 32;
+                qr[2 * v] = static_cast<uint32_t>(num / group);
+                qr[2 * v + 1] = static_cast<uint32_t>(num % group);
+            }
+            slot.qr = dev_upload(qr.data(), qr.size() * 4);
+        }
+        slot.t = dev_upload(t.data(), t.size() * 4);
+        slot.group = group;
     }
-    return {static_cast<const uint32_t*>(slot.first.get()), slot.second};
+    return {static_cast<const uint32_t*>(slot.t.get()), slot.group,
+            static_cast<const uint32_t*>(slot.qr.get())};
 }
 
 const uint64_t* pow_magic(uint32_t b)
@@ -364,6 +378,7 @@ std::vector<RadicalDim> radical_dims(uint32_t dims, uint32_t first_prime, qmc_ra
             r.mode = 2;
         }
         r.ftable = nullptr;
+        r.fqr = nullptr;
         r.magic = nullptr;
         r.gdigits = r.fgroup = r.fdigits = r.himod = 0;
         r.fdivg = Div32{0, 0};
@@ -377,9 +392,10 @@ std::vector<RadicalDim> radical_dims(uint32_t dims, uint32_t first_prime, qmc_ra
                 for (uint32_t g = t.group; g > 1; g /= b)
                     ++r.gdigits;
             }
-            const DigitTable f = digit_table(b, r.mode, r.factor, 1, kFillTableMax);
+            const DigitTable f = digit_table(b, r.mode, r.factor, 1, kFillTableMax, true);
             if (f.ptr) {
                 r.ftable = f.ptr;
+                r.fqr = reinterpret_cast<const uint2*>(f.qr);
                 r.fgroup = f.group;
                 r.fdivg = make_div32(f.group);
                 for (uint32_t g = f.group; g > 1; g /= b)

@@ -886,14 +886,14 @@ __global__ void __launch_bounds__(kBlock)
     }
 }
 
-// Continuation state of one dimension's incremental walk (shared memory,
-// 16 words): valid when `live` and the next run starts at index `next`.
+// Continuation state of one dimension's incremental walk (shared memory or
+// registers, 20 words): valid when `live` and the next run starts at index `next`.
 struct HaltonState {
     uint32_t next, lob, h1, live;
     HiRecord r0, r1;
     uint32_t g0, mulg; // hi_advance state of r1
 };
-static_assert(sizeof(HaltonState) == 64, "HaltonState is 16 words");
+static_assert(sizeof(HaltonState) % 16 == 0, "HaltonState is whole 16-B units");
 
 // No memory clobber: the tile is only read back after __syncthreads(), and
 // leaving it out lets the table loads of later steps move ahead of the stores.
@@ -905,7 +905,7 @@ __device__ __forceinline__ void sts32(uint32_t addr, uint32_t v)
 // One warp, one dimension, `cnt` consecutive indices from i0 into the
 // padded tile column at shared address col (row stride ld words). `st` (or
 // null) carries the incremental state from the previous contiguous run.
-template <bool U32OUT, int UNR = 4>
+template <bool U32OUT>
 __device__ __forceinline__ void halton_run(const RadicalDim& r, uint32_t i0, uint32_t cnt,
                                            uint32_t lane, uint32_t col, uint32_t ld,
                                            HaltonState* st)
@@ -948,11 +948,11 @@ __device__ __forceinline__ void halton_run(const RadicalDim& r, uint32_t i0, uin
         for (uint32_t s = 0; s < steps;) {
             // steps whose 32 indices all lie in h's block: one record
             const uint32_t nf = min(steps - s, (G - lob) >> 5);
-            const uint32_t* tab = r.ftable + lob + lane;
-#pragma unroll(UNR)
+            const uint2* tab = r.fqr + lob + lane;
+#pragma unroll 4
             for (uint32_t e = 0; e < nf; ++e) {
-                const uint32_t acc = __ldg(tab) * r0.mul + r0.acc;
-                const uint32_t x = frac_div_magic(acc, r0.scale, r0.mlo, r0.mhi);
+                const uint2 v = __ldg(tab);
+                const uint32_t x = v.x + r0.qa + (v.y >= r0.thr ? 1u : 0u);
                 sts32(addr, U32OUT ? x : map_bits(x));
                 addr += stride;
                 tab += 32;
@@ -963,10 +963,8 @@ __device__ __forceinline__ void halton_run(const RadicalDim& r, uint32_t i0, uin
                 uint32_t lo = lob + lane;
                 const bool up = lo >= G;
                 lo = up ? lo - G : lo;
-                const uint32_t acc =
-                    __ldg(r.ftable + lo) * (up ? r1.mul : r0.mul) + (up ? r1.acc : r0.acc);
-                const uint32_t x = frac_div_magic(acc, up ? r1.scale : r0.scale,
-                                                  up ? r1.mlo : r0.mlo, up ? r1.mhi : r0.mhi);
+                const uint2 v = __ldg(r.fqr + lo);
+                const uint32_t x = v.x + (up ? r1.qa : r0.qa) + (v.y >= (up ? r1.thr : r0.thr) ? 1u : 0u);
                 sts32(addr, U32OUT ? x : map_bits(x));
                 addr += stride;
                 lob += 32;
@@ -1059,10 +1057,10 @@ __device__ __forceinline__ void bar_named(uint32_t id, uint32_t threads)
 // meet at their own named barrier, and write it out as consecutive words
 // (each thread keeps a fixed column and a fixed shared-memory stride), so
 // runs never wait for each other.
-template <bool U32OUT, int UNR>
+template <bool U32OUT>
 __global__ void __launch_bounds__(1024, 1)
     k_halton_runs(const RadicalDim* __restrict__ rd, uint32_t dims, uint32_t runs, uint32_t chunk,
-                  uint64_t first, uint64_t n, uint64_t nsub, uint32_t* __restrict__ out, int skip)
+                  uint64_t first, uint64_t n, uint64_t nsub, uint32_t* __restrict__ out)
 {
     extern __shared__ __align__(16) uint32_t tile[];
     const uint32_t ld = dims | 1u; // odd row stride: a column store hits 32 banks
@@ -1090,11 +1088,9 @@ __global__ void __launch_bounds__(1024, 1)
     for (uint64_t s = r0; s < r1; ++s) {
         const uint64_t p0 = s * chunk;
         const uint32_t cnt = static_cast<uint32_t>(n - p0 < chunk ? n - p0 : chunk);
-        if (!(skip & 2))
-        halton_run<U32OUT, UNR>(rd[j], static_cast<uint32_t>(first + p0), cnt, lane, sbase + j * 4,
-                                ld, &st);
+        halton_run<U32OUT>(rd[j], static_cast<uint32_t>(first + p0), cnt, lane, sbase + j * 4, ld,
+                           &st);
         bar_named(1 + run, nthr);
-        if (skip & 1) { bar_named(1 + run, nthr); continue; }
         const uint32_t words = cnt * dims;
         uint32_t* o = out + p0 * dims;
         const uint32_t* src = sub + row0 * ld + col0;
@@ -1159,7 +1155,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity)
 template <bool U32OUT>
 __global__ void __launch_bounds__(1024, 1)
     k_halton_tma(const __grid_constant__ CUtensorMap tmap, const RadicalDim* __restrict__ rd,
-                 uint32_t rows, uint32_t nbuf, uint64_t first, uint64_t n, uint64_t nsub, int skip)
+                 uint32_t rows, uint32_t nbuf, uint64_t first, uint64_t n, uint64_t nsub)
 {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t bars[16];
@@ -1189,24 +1185,21 @@ __global__ void __launch_bounds__(1024, 1)
         const uint32_t buf = base + b * buf_bytes;
         if (k > 0)
             mbar_wait(bar0 + 8 * (8 + b), (k - 1) & 1u);
-        if (!(skip & 2))
-            halton_run<U32OUT>(rd[warp], static_cast<uint32_t>(first + p0), cnt, lane,
-                               buf + lane * 128 + col, 32, &st);
+        halton_run<U32OUT>(rd[warp], static_cast<uint32_t>(first + p0), cnt, lane,
+                           buf + lane * 128 + col, 32, &st);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0)
             mbar_arrive(bar0 + 8 * b);
         if (issuer) {
             mbar_wait(bar0 + 8 * b, k & 1u);
-            if (!(skip & 1)) {
-                for (uint32_t r = 0; r < cnt; r += 256) {
-                    const int32_t y = static_cast<int32_t>(p0 + r);
-                    asm volatile(
-                        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                            reinterpret_cast<uint64_t>(&tmap)),
-                        "r"(buf + r * 128), "r"(0), "r"(y)
-                        : "memory");
-                }
+            for (uint32_t r = 0; r < cnt; r += 256) {
+                const int32_t y = static_cast<int32_t>(p0 + r);
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                        reinterpret_cast<uint64_t>(&tmap)),
+                    "r"(buf + r * 128), "r"(0), "r"(y)
+                    : "memory");
             }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             // the previous sub-tile's store has read its buffer: release it
@@ -1556,15 +1549,7 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
 {
     if (r.n == 0)
         return cudaSuccess;
-    static const int kSkip = [] {
-        const char* e = getenv("QMC_HALTON_SKIP");
-        return e ? atoi(e) : 0;
-    }();
-    static const int kTma = [] {
-        const char* e = getenv("QMC_HALTON_TMA");
-        return e ? atoi(e) : 1;
-    }();
-    if (dims == 32 && kTma && (reinterpret_cast<uintptr_t>(r.out) & 15u) == 0 &&
+    if (dims == 32 && (reinterpret_cast<uintptr_t>(r.out) & 15u) == 0 &&
         r.n < (1ull << 31)) {
         static PFN_cuTensorMapEncodeTiled encode = [] {
             void* fn = nullptr;
@@ -1575,14 +1560,7 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
                 fn = nullptr;
             return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
         }();
-        static const uint32_t kRows = [] {
-            const char* e = getenv("QMC_HALTON_TMA_ROWS");
-            return e ? static_cast<uint32_t>(atoi(e)) : 512u;
-        }();
-        static const uint32_t kBufs = [] {
-            const char* e = getenv("QMC_HALTON_TMA_NB");
-            return e ? static_cast<uint32_t>(atoi(e)) : 3u;
-        }();
+        constexpr uint32_t kRows = 512, kBufs = 3; // 192 KB ring, 16 warp steps per sub-tile
         if (encode) {
             CUtensorMap tmap;
             const cuuint64_t gdim[2] = {32, r.n};
@@ -1603,7 +1581,7 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
                 const unsigned grid = static_cast<unsigned>(
                     std::min<uint64_t>(nsub, static_cast<uint64_t>(sm_count())));
                 kern<<<grid, 1024, smem, s>>>(tmap, static_cast<const RadicalDim*>(rd), kRows,
-                                              kBufs, r.first, r.n, nsub, kSkip);
+                                              kBufs, r.first, r.n, nsub);
                 return cudaGetLastError();
             }
         }
@@ -1611,20 +1589,12 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
     if (dims <= 32) {
         // one CTA per SM, runs x dims warps, sub-tiles sharing ~kRunsTileWords
         const uint32_t runs = std::min(15u, 32u / dims), ld = dims | 1u;
-        static const uint32_t kRunsTileWords = [] {
-            const char* e = getenv("QMC_HALTON_TILE_WORDS");
-            return e ? static_cast<uint32_t>(atoi(e)) : 49152u;
-        }();
+        constexpr uint32_t kRunsTileWords = 49152; // 192 KB
         uint32_t chunk = (kRunsTileWords / (runs * ld)) & ~31u;
         if (chunk < 32)
             chunk = 32;
         const size_t smem = static_cast<size_t>(chunk) * ld * runs * 4;
-        static const int kUnr = [] {
-            const char* e = getenv("QMC_HALTON_UNROLL");
-            return e ? atoi(e) : 4;
-        }();
-        auto kern = kUnr == 8 ? (u32 ? k_halton_runs<true, 8> : k_halton_runs<false, 8>)
-                              : (u32 ? k_halton_runs<true, 4> : k_halton_runs<false, 4>);
+        auto kern = u32 ? k_halton_runs<true> : k_halton_runs<false>;
         const cudaError_t e =
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess)
@@ -1634,7 +1604,7 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
             static_cast<unsigned>(std::min<uint64_t>(nsub, static_cast<uint64_t>(sm_count())));
         kern<<<grid, runs * dims * 32, smem, s>>>(static_cast<const RadicalDim*>(rd), dims, runs,
                                                    chunk, r.first, r.n, nsub,
-                                                   static_cast<uint32_t*>(r.out), kSkip);
+                                                   static_cast<uint32_t*>(r.out));
         return cudaGetLastError();
     }
     // tile of tp points x (dims + 1) padded words: <= 48 KB, >= 32 points;
@@ -1646,7 +1616,7 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
     if (tp < 32)
         tp = 32;
     const size_t tile_words = (static_cast<size_t>(tp) * (dims | 1u) + 15) & ~size_t(15);
-    const size_t smem = tile_words * 4 + (dims >= kBlock / 32 ? size_t(dims) * 64 : 0);
+    const size_t smem = tile_words * 4 + (dims >= kBlock / 32 ? size_t(dims) * sizeof(HaltonState) : 0);
     auto kern = u32 ? k_halton_tiled<true> : k_halton_tiled<false>;
     if (smem > 48 * 1024) {
         const cudaError_t e =

@@ -172,6 +172,22 @@ def test_halton_fill_runs_all_small_dims_vs_reference(ref, dims):
             np.testing.assert_array_equal(got[:, j], exp, err_msg=f"first={first} dim={j}")
 
 
+def test_halton_fill_32_dims_small_and_ragged_vs_reference(ref):
+    """dims == 32 (k_halton_tma: TMA boxes of 256 rows clipped at n) for
+    counts below one box, one sub-tile and one CTA's share, u32 and f32."""
+    for n, first in [(1, 0), (100, 7), (257, 2**32 - 100), (513, 1000), (148 * 512 + 33, 99)]:
+        got = u32(q.halton_fill(n, 32, first=first, scramble="linear", fixed=True)).reshape(n, 32)
+        f = q.halton_fill(n, 32, first=first, scramble="linear").cpu().numpy().reshape(n, 32)
+        for j in range(32):
+            b = q.prime(j)
+            exp = np.zeros(n, np.uint32)
+            assert ref.ref_radical_fixed_fill(first, n, j, 1, b - 1 if b > 2 else 1, ptr(exp)) == 0
+            np.testing.assert_array_equal(got[:, j], exp, err_msg=f"n={n} dim={j}")
+            mapped = np.zeros(n, np.uint32)
+            ref.ref_map_bulk(ptr(exp), ptr(mapped), n)
+            np.testing.assert_array_equal(f[:, j].view(np.uint32), mapped, err_msg=f"n={n} dim={j}")
+
+
 # ---------------------------------------------------------------- Sobol'
 def test_sobol_vs_golden(golden_arrays, golden, oracle):
     got = u32(q.sobol_fill(1024, 64, fixed=True))
