@@ -496,7 +496,7 @@ def run_extra(q, stream, peak, args):
         rh = measure_fill("halton linear 2^24 x 32",
                           lambda: q.halton_fill(nh, 32, scramble="linear", out=oh), nh * 32, steps,
                           warm, peak, stream)
-        rh["roofline"]["bound"] = "issue (table load + magic division + map per sample)"
+        rh["roofline"]["bound"] = "issue (quotient-table load + 3 integer ops + map per sample; TMA store)"
         res["halton_linear_2^24x32"] = rh
 
     def c3():
