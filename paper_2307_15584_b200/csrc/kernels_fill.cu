@@ -1143,19 +1143,21 @@ __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity)
     } while (!ok);
 }
 
-// Prime-base Halton, dims == 32, stored by TMA: the k_halton_runs walk (one
-// dimension per warp, state in registers) into a ring of nbuf sub-tiles of
-// `rows` points laid out exactly as the output rows (128 B each) with the
+// Prime-base Halton, dims % 32 == 0, stored by TMA: the k_halton_runs walk
+// (one dimension of a 32-dimension column block per warp, state in
+// registers) into a ring of nbuf sub-tiles of `rows` points laid out exactly
+// as the block's 128-B output row segments (whole cache lines) with the
 // 128-B swizzle, so a column store by 32 lanes is a 4-way bank conflict
 // instead of 32-way, and the tensor-map store (cp.async.bulk.tensor, boxes of
 // 256 rows) runs asynchronously while the warps walk the next sub-tiles.
 // full[b]: the 32 warps have written sub-tile b (count 32); empty[b]: its
 // bulk store has finished reading shared memory (count 1, warp 0 lane 0,
-// which also issues the stores: it walks base 2, the cheapest dimension).
+// which also issues the stores; in block 0 it walks base 2, the cheapest).
 template <bool U32OUT>
 __global__ void __launch_bounds__(1024, 1)
     k_halton_tma(const __grid_constant__ CUtensorMap tmap, const RadicalDim* __restrict__ rd,
-                 uint32_t rows, uint32_t nbuf, uint64_t first, uint64_t n, uint64_t nsub)
+                 uint32_t rows, uint32_t nbuf, uint32_t ncb, uint64_t first, uint64_t n,
+                 uint64_t nsub)
 {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t bars[16];
@@ -1174,18 +1176,28 @@ __global__ void __launch_bounds__(1024, 1)
     // lane l writes rows l + 32 s: row & 7 == l & 7, so the swizzled column
     // offset of dimension `warp` is fixed per lane
     const uint32_t col = (((warp >> 2) ^ (lane & 7u)) << 4) + (warp & 3u) * 4 - lane * 128;
-    const uint64_t s0 = nsub * blockIdx.x / gridDim.x, s1 = nsub * (blockIdx.x + 1) / gridDim.x;
+    // work units (column block cb of 32 dimensions, sub-tile s), cb-major:
+    // a CTA's contiguous range mostly stays in one column block
+    const uint64_t units = nsub * ncb;
+    const uint64_t u0 = units * blockIdx.x / gridDim.x, u1 = units * (blockIdx.x + 1) / gridDim.x;
     const bool issuer = threadIdx.x == 0;
     HaltonState st;
     st.live = 0;
     uint32_t b = 0, k = 0;
-    for (uint64_t s = s0; s < s1; ++s) {
+    uint32_t cb = static_cast<uint32_t>(u0 / nsub);
+    uint64_t s = u0 - static_cast<uint64_t>(cb) * nsub;
+    for (uint64_t u = u0; u < u1; ++u, ++s) {
+        if (s == nsub) { // next column block: other dimensions, fresh walk
+            s = 0;
+            ++cb;
+            st.live = 0;
+        }
         const uint64_t p0 = s * rows;
         const uint32_t cnt = static_cast<uint32_t>(n - p0 < rows ? n - p0 : rows);
         const uint32_t buf = base + b * buf_bytes;
         if (k > 0)
             mbar_wait(bar0 + 8 * (8 + b), (k - 1) & 1u);
-        halton_run<U32OUT>(rd[warp], static_cast<uint32_t>(first + p0), cnt, lane,
+        halton_run<U32OUT>(rd[cb * 32 + warp], static_cast<uint32_t>(first + p0), cnt, lane,
                            buf + lane * 128 + col, 32, &st);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
@@ -1198,13 +1210,13 @@ __global__ void __launch_bounds__(1024, 1)
                 asm volatile(
                     "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                         reinterpret_cast<uint64_t>(&tmap)),
-                    "r"(buf + r * 128), "r"(0), "r"(y)
+                    "r"(buf + r * 128), "r"(cb * 32), "r"(y)
                     : "memory");
             }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             // the previous sub-tile's store has read its buffer: release it
             asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-            if (s > s0)
+            if (u > u0)
                 mbar_arrive(bar0 + 8 * (8 + (b == 0 ? nbuf - 1 : b - 1)));
         }
         __syncwarp();
@@ -1549,7 +1561,7 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
 {
     if (r.n == 0)
         return cudaSuccess;
-    if (dims == 32 && (reinterpret_cast<uintptr_t>(r.out) & 15u) == 0 &&
+    if (dims % 32 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 15u) == 0 &&
         r.n < (1ull << 31)) {
         static PFN_cuTensorMapEncodeTiled encode = [] {
             void* fn = nullptr;
@@ -1563,8 +1575,8 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
         constexpr uint32_t kRows = 512, kBufs = 3; // 192 KB ring, 16 warp steps per sub-tile
         if (encode) {
             CUtensorMap tmap;
-            const cuuint64_t gdim[2] = {32, r.n};
-            const cuuint64_t gstride[1] = {128};
+            const cuuint64_t gdim[2] = {dims, r.n};
+            const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(dims) * 4};
             const cuuint32_t box[2] = {32, 256};
             const cuuint32_t estride[2] = {1, 1};
             if (encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, r.out, gdim, gstride, box, estride,
@@ -1578,10 +1590,11 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
                 if (e != cudaSuccess)
                     return e;
                 const uint64_t nsub = (r.n + kRows - 1) / kRows;
+                const uint32_t ncb = dims / 32;
                 const unsigned grid = static_cast<unsigned>(
-                    std::min<uint64_t>(nsub, static_cast<uint64_t>(sm_count())));
+                    std::min<uint64_t>(nsub * ncb, static_cast<uint64_t>(sm_count())));
                 kern<<<grid, 1024, smem, s>>>(tmap, static_cast<const RadicalDim*>(rd), kRows,
-                                              kBufs, r.first, r.n, nsub);
+                                              kBufs, ncb, r.first, r.n, nsub);
                 return cudaGetLastError();
             }
         }

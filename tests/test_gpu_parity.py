@@ -188,6 +188,21 @@ def test_halton_fill_32_dims_small_and_ragged_vs_reference(ref):
             np.testing.assert_array_equal(f[:, j].view(np.uint32), mapped, err_msg=f"n={n} dim={j}")
 
 
+@pytest.mark.parametrize("dims", [64, 96, 256])
+def test_halton_fill_column_blocks_vs_reference(ref, dims):
+    """dims % 32 == 0 (k_halton_tma over 32-dimension column blocks: a CTA's
+    unit range crosses block boundaries, TMA boxes at column offset 32*cb)."""
+    n = 148 * 512 + 1000
+    for first, mode in [(3486784401 - 20000, "linear"), (5, "faure")]:
+        got = u32(q.halton_fill(n, dims, first=first, scramble=mode, fixed=True)).reshape(n, dims)
+        for j in list(range(0, dims, 5)) + [31, 32, dims - 1]:
+            b = q.prime(j)
+            exp = np.zeros(n, np.uint32)
+            assert ref.ref_radical_fixed_fill(first, n, j, _MODE[mode], b - 1 if b > 2 else 1,
+                                              ptr(exp)) == 0
+            np.testing.assert_array_equal(got[:, j], exp, err_msg=f"first={first} dim={j}")
+
+
 # ---------------------------------------------------------------- Sobol'
 def test_sobol_vs_golden(golden_arrays, golden, oracle):
     got = u32(q.sobol_fill(1024, 64, fixed=True))
