@@ -1024,8 +1024,7 @@ def test_fills_write_exactly_their_range(dims):
                                    matrices=q.GeneratorMatrixSet.from_columns(
                                        np.arange(dims * 52, dtype=np.uint32).reshape(dims, 52))),
             lambda o: q.lattice_fill(n, [2 * k + 1 for k in range(dims)], first=first, out=o),
-            lambda o: q.halton_fill(n, min(dims, 100), first=first,
-                                    out=o[: n * min(dims, 100)]),
+            lambda o: q.halton_fill(n, dims, first=first, out=o),
         ):
             buf, mid = _guarded(n * dims)
             call(mid)

@@ -15,6 +15,13 @@ for dims in (1, 3, 4, 8, 16, 32, 48, 64):
     g = [2 * k + 1 for k in range(dims)]
     q.lattice_fill(999, g, first=(1 << 32) - 100, shifts=list(range(dims)))
     q.halton_fill(333, dims, first=77, scramble="faure")
+for n, dims in ((148 * 512 * 2 + 77, 32), (3000, 64), (5000, 96), (70000, 31), (9000, 2)):
+    q.halton_fill(n, dims, first=3486784401 - 2000, scramble="linear")  # runs / TMA column blocks
+    q.halton_fill(n, dims, first=5, fixed=True)
+if os.environ.get("QMC_SANITIZE_HALTON_ONLY"):
+    torch.cuda.synchronize()
+    print("sanitize smoke done")
+    sys.exit(0)
 q.radical_inverse_fill(1001, 0)
 q.radical_inverse_fill(1001, 5, scramble="linear", factor=3)
 q.map_u32_to_unifloat(torch.arange(1000, dtype=torch.int32, device="cuda"))
