@@ -129,6 +129,41 @@ __global__ void __launch_bounds__(ChunkShape<KIND>::kBlock)
         }
     }
 
+    // Halton kinds: when every index of the chunk (mod prime_max_power) lies
+    // in the fill-table blocks h0 and h0 + 1 of a dimension, its inverse is
+    // the quotient-table form of the contiguous fill (device.cuh: hi_split):
+    // one coalesced 8-B load and three integer ops instead of the digit loop.
+    __shared__ const uint2* HTAB[kMaxDims];
+    __shared__ uint32_t HG[kMaxDims], HLO[kMaxDims], HQ0[kMaxDims], HT0[kMaxDims], HQ1[kMaxDims],
+        HT1[kMaxDims];
+    if (KIND == 1 || KIND == 3) {
+        const uint32_t ib = static_cast<uint32_t>(KIND == 3 ? block + begin : begin);
+        for (uint32_t j = t; j < dims; j += kBlock) {
+            const RadicalDim& r = rd[j];
+            const uint2* tab = nullptr;
+            if (r.fqr && ib <= 0xffffffffu - count) {
+                const uint32_t ir = ib - div32(ib, r.divmp) * r.maxpow;
+                const uint32_t G = r.fgroup, h0 = div32(ir, r.fdivg), lo0 = ir - h0 * G;
+                if (static_cast<uint64_t>(ir) + count <= r.maxpow && lo0 + count <= 2 * G) {
+                    uint32_t g0, mulg, h = h0;
+                    const HiRecord a = hi_record(h0, r, g0, mulg);
+                    HiRecord b = a;
+                    if (lo0 + count > G)
+                        hi_advance(h, b, g0, mulg, r);
+                    HG[j] = G;
+                    HLO[j] = lo0;
+                    HQ0[j] = a.qa;
+                    HT0[j] = a.thr;
+                    HQ1[j] = b.qa;
+                    HT1[j] = b.thr;
+                    tab = r.fqr;
+                }
+            }
+            HTAB[j] = tab;
+        }
+        __syncthreads();
+    }
+
     bool finite = true;
     long long acc = 0;
     for (uint32_t m = 0; m < kSteps; ++m) {
@@ -142,12 +177,20 @@ __global__ void __launch_bounds__(ChunkShape<KIND>::kBlock)
                 uint32_t x;
                 if (KIND == 0)
                     x = sob[j];
-                else if (KIND == 1)
-                    x = radical_fixed(i, rd[j]);
-                else if (KIND == 2)
+                else if (KIND == 1 || KIND == 3) {
+                    const uint2* tab = HTAB[j];
+                    if (tab) {
+                        const uint32_t G = HG[j];
+                        uint32_t lo = HLO[j] + local;
+                        const bool up = lo >= G;
+                        lo = up ? lo - G : lo;
+                        const uint2 e = __ldg(tab + lo);
+                        x = e.x + (up ? HQ1[j] : HQ0[j]) + (e.y >= (up ? HT1[j] : HT0[j]) ? 1u : 0u);
+                    } else {
+                        x = radical_fixed(KIND == 1 ? i : static_cast<uint32_t>(block + idx), rd[j]);
+                    }
+                } else if (KIND == 2)
                     x = brev32(i) * __ldg(q.generator + j);
-                else if (KIND == 3)
-                    x = radical_fixed(static_cast<uint32_t>(block + idx), rd[j]);
                 else if (KIND == 4)
                     x = (brev32(i) + shift) * __ldg(q.generator + j);
                 else if (KIND == 5)

@@ -814,6 +814,21 @@ def test_integrate_pixel_kinds_vs_reference(ref):
             assert abs(row["estimate"] - e.value) <= 1e-12 * abs(e.value)
 
 
+@pytest.mark.parametrize("accum", ["int", "kahan"])
+def test_integrate_halton_quotient_tables_vs_reference(ref, accum):
+    """Halton integration over 2^20 points x 12 dims: the chunks that take the
+    quotient-table path (fill-table blocks h0, h0 + 1, incl. the ones that
+    straddle a block) and the digit-loop fallback give the reference's
+    estimate bit for bit (product-poly: exact FP64 products)."""
+    import ctypes as C
+    n, dims = (1 << 20) + 123, 12
+    e = C.c_double()
+    assert ref.ref_integrate(b"halton", dims, 0, b"product-poly", n, accum.encode(), 8,
+                             C.byref(e)) == 0
+    row = q.integrate("halton", "product-poly", n, dims, accum)
+    assert row["estimate"] == e.value
+
+
 @pytest.mark.parametrize("scramble", ["plain", "faure", "linear"])
 @pytest.mark.parametrize("kind", ["halton", "halton-hilbert"])
 def test_halton_streams_scrambles_vs_reference(ref, kind, scramble):
