@@ -976,7 +976,7 @@ __device__ __forceinline__ void halton_run(const RadicalDim& r, uint32_t i0, uin
                 hi_advance(h1, r1, g0, mulg, r);
             }
         }
-        if (st) { // every lane: the state may live in registers (k_halton_runs)
+        if (st) { // every lane: the state may live in registers (k_runs, k_tma)
             st->next = i0 + (steps << 5);
             st->lob = lob;
             st->h1 = h1;
@@ -1042,6 +1042,97 @@ __global__ void __launch_bounds__(kBlock)
     }
 }
 
+// Column walkers for the one-dimension-per-warp fills (k_runs, k_tma): a
+// warp writes `cnt` consecutive points (from index i0) of dimension j into
+// the shared column at address col, row stride ld words, carrying State from
+// one call to the next (in registers); wsm is the warp's 32-word scratch.
+template <bool U32OUT>
+struct HaltonWalk {
+    const RadicalDim* rd;
+    using State = HaltonState;
+    __device__ __forceinline__ void reset(State& st) const { st.live = 0; }
+    __device__ __forceinline__ void run(uint32_t j, uint64_t i0, uint32_t cnt, uint32_t lane,
+                                        uint32_t col, uint32_t ld, State& st, uint32_t*) const
+    {
+        halton_run<U32OUT>(rd[j], static_cast<uint32_t>(i0), cnt, lane, col, ld, &st);
+    }
+};
+
+// Sobol' (digitalnet.cpp:96-110) from a 32-aligned i0: with i = 32 H + l and
+// H = 32 b + t (disjoint index bits) the point is X(1024 b) ^ X(32 t) ^ X(l):
+// X(l) stays in a register per lane, X(32 t) for t < 32 sits in the warp's
+// scratch (one broadcast load per step) and X(1024 b) (with the XOR word)
+// advances once per 32 steps by the columns of the bits that change.
+// MODE 2: cols are bit-reversed, finished by brev(owen_lk(., seed)).
+template <int MODE, bool U32OUT>
+struct SobolWalk {
+    const uint32_t* cols; // [52][dims]
+    uint32_t dims;
+    SmallArgs words;
+    struct State {
+        uint64_t next, h;
+        uint32_t xq, xl, live, pad;
+    };
+    __device__ __forceinline__ void reset(State& st) const { st.live = 0; }
+    __device__ __forceinline__ uint32_t col(uint32_t k, uint32_t j) const
+    {
+        return __ldg(cols + static_cast<size_t>(k) * dims + j);
+    }
+    __device__ __forceinline__ void run(uint32_t j, uint64_t i0, uint32_t cnt, uint32_t lane,
+                                        uint32_t colad, uint32_t ld, State& st,
+                                        uint32_t* wsm) const
+    {
+        const uint32_t* w = small_a(words);
+        const uint32_t seed = MODE == 2 && w ? w[j] : 0u;
+        if (!st.live || st.next != i0) {
+            uint32_t xl = 0, xt = 0;
+            for (uint32_t k = 0; k < 5; ++k)
+                if ((lane >> k) & 1u) {
+                    xl ^= col(k, j);
+                    xt ^= col(5 + k, j);
+                }
+            __syncwarp();
+            wsm[lane] = xt;
+            uint32_t xb = MODE == 0 && w ? w[j] : 0u;
+            for (uint64_t b = (i0 >> 10) << 10; b; b &= b - 1)
+                xb ^= col(__ffsll(static_cast<long long>(b)) - 1, j);
+            st.h = i0 >> 5;
+            st.xl = xl;
+            st.xq = xb ^ xl;
+            st.live = 1;
+        }
+        __syncwarp();
+        const uint32_t row = ld * 4, stride = 32 * row;
+        uint32_t addr = colad + lane * row;
+        uint64_t h = st.h;
+        uint32_t xq = st.xq;
+        const uint32_t steps = (cnt + 31) >> 5;
+        for (uint32_t s = 0; s < steps;) {
+            const uint32_t t0 = static_cast<uint32_t>(h) & 31u;
+            const uint32_t m = min(steps - s, 32u - t0);
+#pragma unroll 4
+            for (uint32_t e = 0; e < m; ++e) {
+                uint32_t v = xq ^ wsm[t0 + e];
+                if (MODE == 2)
+                    v = brev32(owen_lk(v, seed));
+                sts32(addr, U32OUT ? v : map_bits(v));
+                addr += stride;
+            }
+            s += m;
+            h += m;
+            if ((static_cast<uint32_t>(h) & 31u) == 0) { // next 1024-block: bits 10.. change
+                const uint64_t b = h >> 5;
+                const int cz = __ffsll(static_cast<long long>(b)) - 1;
+                for (int k = 0; k <= cz; ++k)
+                    xq ^= col(10 + k, j);
+            }
+        }
+        st.h = h;
+        st.xq = xq;
+        st.next = i0 + (static_cast<uint64_t>(steps) << 5);
+    }
+};
+
 __device__ __forceinline__ void bar_named(uint32_t id, uint32_t threads)
 {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
@@ -1057,10 +1148,10 @@ __device__ __forceinline__ void bar_named(uint32_t id, uint32_t threads)
 // meet at their own named barrier, and write it out as consecutive words
 // (each thread keeps a fixed column and a fixed shared-memory stride), so
 // runs never wait for each other.
-template <bool U32OUT>
+template <class W>
 __global__ void __launch_bounds__(1024, 1)
-    k_halton_runs(const RadicalDim* __restrict__ rd, uint32_t dims, uint32_t runs, uint32_t chunk,
-                  uint64_t first, uint64_t n, uint64_t nsub, uint32_t* __restrict__ out)
+    k_runs(const __grid_constant__ W w, uint32_t dims, uint32_t runs, uint32_t chunk,
+           uint64_t first, uint64_t n, uint64_t nsub, uint32_t* __restrict__ out)
 {
     extern __shared__ __align__(16) uint32_t tile[];
     const uint32_t ld = dims | 1u; // odd row stride: a column store hits 32 banks
@@ -1083,13 +1174,13 @@ __global__ void __launch_bounds__(1024, 1)
     const uint32_t pad = ld - dims;
     const uint32_t off1 = 1 + (col0 + 1) / dims * pad, off2 = 2 + (col0 + 2) / dims * pad,
                    off3 = 3 + (col0 + 3) / dims * pad;
-    HaltonState st;
-    st.live = 0;
+    uint32_t* wsm = tile + static_cast<size_t>(runs) * chunk * ld + warp * 32;
+    typename W::State st;
+    w.reset(st);
     for (uint64_t s = r0; s < r1; ++s) {
         const uint64_t p0 = s * chunk;
         const uint32_t cnt = static_cast<uint32_t>(n - p0 < chunk ? n - p0 : chunk);
-        halton_run<U32OUT>(rd[j], static_cast<uint32_t>(first + p0), cnt, lane, sbase + j * 4, ld,
-                           &st);
+        w.run(j, first + p0, cnt, lane, sbase + j * 4, ld, st, wsm);
         bar_named(1 + run, nthr);
         const uint32_t words = cnt * dims;
         uint32_t* o = out + p0 * dims;
@@ -1143,7 +1234,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity)
     } while (!ok);
 }
 
-// Prime-base Halton, dims % 32 == 0, stored by TMA: the k_halton_runs walk
+// Fills with dims % 32 == 0, stored by TMA: the k_runs walk
 // (one dimension of a 32-dimension column block per warp, state in
 // registers) into a ring of nbuf sub-tiles of `rows` points laid out exactly
 // as the block's 128-B output row segments (whole cache lines) with the
@@ -1153,14 +1244,14 @@ __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity)
 // full[b]: the 32 warps have written sub-tile b (count 32); empty[b]: its
 // bulk store has finished reading shared memory (count 1, warp 0 lane 0,
 // which also issues the stores; in block 0 it walks base 2, the cheapest).
-template <bool U32OUT>
+template <class W>
 __global__ void __launch_bounds__(1024, 1)
-    k_halton_tma(const __grid_constant__ CUtensorMap tmap, const RadicalDim* __restrict__ rd,
-                 uint32_t rows, uint32_t nbuf, uint32_t ncb, uint64_t first, uint64_t n,
-                 uint64_t nsub)
+    k_tma(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ W w, uint32_t rows,
+          uint32_t nbuf, uint32_t ncb, uint64_t first, uint64_t n, uint64_t nsub)
 {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t bars[16];
+    __shared__ uint32_t scratch[32 * 32];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint32_t base = (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + 1023u) & ~1023u;
     const uint32_t bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
@@ -1181,8 +1272,8 @@ __global__ void __launch_bounds__(1024, 1)
     const uint64_t units = nsub * ncb;
     const uint64_t u0 = units * blockIdx.x / gridDim.x, u1 = units * (blockIdx.x + 1) / gridDim.x;
     const bool issuer = threadIdx.x == 0;
-    HaltonState st;
-    st.live = 0;
+    typename W::State st;
+    w.reset(st);
     uint32_t b = 0, k = 0;
     uint32_t cb = static_cast<uint32_t>(u0 / nsub);
     uint64_t s = u0 - static_cast<uint64_t>(cb) * nsub;
@@ -1190,15 +1281,15 @@ __global__ void __launch_bounds__(1024, 1)
         if (s == nsub) { // next column block: other dimensions, fresh walk
             s = 0;
             ++cb;
-            st.live = 0;
+            w.reset(st);
         }
         const uint64_t p0 = s * rows;
         const uint32_t cnt = static_cast<uint32_t>(n - p0 < rows ? n - p0 : rows);
         const uint32_t buf = base + b * buf_bytes;
         if (k > 0)
             mbar_wait(bar0 + 8 * (8 + b), (k - 1) & 1u);
-        halton_run<U32OUT>(rd[cb * 32 + warp], static_cast<uint32_t>(first + p0), cnt, lane,
-                           buf + lane * 128 + col, 32, &st);
+        w.run(cb * 32 + warp, first + p0, cnt, lane, buf + lane * 128 + col, 32, st,
+              scratch + warp * 32);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0)
@@ -1453,6 +1544,71 @@ cudaError_t launch_map_selfcheck(unsigned long long* count, cudaStream_t s)
     return cudaGetLastError();
 }
 
+// One-dimension-per-warp fills (k_tma / k_runs) over a column walker W.
+// TMA: dims % 32 == 0, out 16-B aligned, n < 2^31; returns false otherwise.
+template <class W>
+bool launch_tma_fill(const W& w, uint32_t dims, const FillRange& r, cudaStream_t s,
+                     cudaError_t* err)
+{
+    if (dims % 32 != 0 || (reinterpret_cast<uintptr_t>(r.out) & 15u) != 0 || r.n >= (1ull << 31))
+        return false;
+    static PFN_cuTensorMapEncodeTiled encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+    }();
+    if (!encode)
+        return false;
+    constexpr uint32_t kRows = 512, kBufs = 3; // 192 KB ring, 16 warp steps per sub-tile
+    CUtensorMap tmap;
+    const cuuint64_t gdim[2] = {dims, r.n};
+    const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(dims) * 4};
+    const cuuint32_t box[2] = {32, 256};
+    const cuuint32_t estride[2] = {1, 1};
+    if (encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, r.out, gdim, gstride, box, estride,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    const size_t smem = static_cast<size_t>(kRows) * 128 * kBufs + 1024;
+    *err = cudaFuncSetAttribute(k_tma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (*err != cudaSuccess)
+        return true;
+    const uint64_t nsub = (r.n + kRows - 1) / kRows;
+    const uint32_t ncb = dims / 32;
+    const unsigned grid = static_cast<unsigned>(
+        std::min<uint64_t>(nsub * ncb, static_cast<uint64_t>(sm_count())));
+    k_tma<W><<<grid, 1024, smem, s>>>(tmap, w, kRows, kBufs, ncb, r.first, r.n, nsub);
+    *err = cudaGetLastError();
+    return true;
+}
+
+// dims <= 32: one CTA per SM, runs x dims warps, sub-tiles sharing ~192 KB,
+// plus a 32-word scratch per warp
+template <class W>
+cudaError_t launch_runs_fill(const W& w, uint32_t dims, const FillRange& r, cudaStream_t s)
+{
+    const uint32_t runs = std::min(15u, 32u / dims), ld = dims | 1u;
+    constexpr uint32_t kRunsTileWords = 49152;
+    uint32_t chunk = (kRunsTileWords / (runs * ld)) & ~31u;
+    if (chunk < 32)
+        chunk = 32;
+    const size_t smem = (static_cast<size_t>(chunk) * ld * runs + runs * dims * 32) * 4;
+    const cudaError_t e =
+        cudaFuncSetAttribute(k_runs<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess)
+        return e;
+    const uint64_t nsub = (r.n + chunk - 1) / chunk;
+    const unsigned grid =
+        static_cast<unsigned>(std::min<uint64_t>(nsub, static_cast<uint64_t>(sm_count())));
+    k_runs<W><<<grid, runs * dims * 32, smem, s>>>(w, dims, runs, chunk, r.first, r.n, nsub,
+                                                    static_cast<uint32_t*>(r.out));
+    return cudaGetLastError();
+}
+
 cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const SmallArgs& words,
                          uint32_t dims, int mode, bool u32, const FillRange& r, cudaStream_t s)
 {
@@ -1479,6 +1635,35 @@ cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const
                                 : launch_tiled(k_sobol_narrow<2, 2, false>, kLogTp2, r, s, cols, words))
                          : (u32 ? launch_tiled(k_sobol_narrow<2, 0, true>, kLogTp2, r, s, cols, words)
                                 : launch_tiled(k_sobol_narrow<2, 0, false>, kLogTp2, r, s, cols, words));
+    }
+    // one dimension per warp (k_tma for dims % 32 == 0, else k_runs for dims
+    // <= 32) from a 32-aligned index; the few points before it go through
+    // the element-wise / tiled paths below
+    if ((dims <= 32 || dims % 32 == 0) && r.n >= 64) {
+        const uint64_t head = (32u - static_cast<uint32_t>(r.first & 31u)) & 31u;
+        const FillRange main{r.first + head, r.n - head,
+                             static_cast<uint32_t*>(r.out) + head * dims};
+        const bool tma = dims % 32 == 0 && (reinterpret_cast<uintptr_t>(main.out) & 15u) == 0 &&
+                         main.n < (1ull << 31);
+        if (dims <= 32 || tma) {
+            if (head) {
+                const cudaError_t e = launch_sobol(colsT, colsT_rev, words, dims, mode, u32,
+                                                   FillRange{r.first, head, r.out}, s);
+                if (e != cudaSuccess)
+                    return e;
+            }
+            auto go = [&](auto w) {
+                cudaError_t err = cudaSuccess;
+                if (tma && launch_tma_fill(w, dims, main, s, &err))
+                    return err;
+                return launch_runs_fill(w, dims, main, s);
+            };
+            if (mode == 2)
+                return u32 ? go(SobolWalk<2, true>{cols, dims, words})
+                           : go(SobolWalk<2, false>{cols, dims, words});
+            return u32 ? go(SobolWalk<0, true>{cols, dims, words})
+                       : go(SobolWalk<0, false>{cols, dims, words});
+        }
     }
     if (dims <= kElemMaxDims) {
         // element-wise path: chunks of <= 1022 points (two 1024-point tiles)
@@ -1561,65 +1746,14 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
 {
     if (r.n == 0)
         return cudaSuccess;
-    if (dims % 32 == 0 && (reinterpret_cast<uintptr_t>(r.out) & 15u) == 0 &&
-        r.n < (1ull << 31)) {
-        static PFN_cuTensorMapEncodeTiled encode = [] {
-            void* fn = nullptr;
-            cudaDriverEntryPointQueryResult q{};
-            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
-                    cudaSuccess ||
-                q != cudaDriverEntryPointSuccess)
-                fn = nullptr;
-            return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
-        }();
-        constexpr uint32_t kRows = 512, kBufs = 3; // 192 KB ring, 16 warp steps per sub-tile
-        if (encode) {
-            CUtensorMap tmap;
-            const cuuint64_t gdim[2] = {dims, r.n};
-            const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(dims) * 4};
-            const cuuint32_t box[2] = {32, 256};
-            const cuuint32_t estride[2] = {1, 1};
-            if (encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, r.out, gdim, gstride, box, estride,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                       CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
-                const size_t smem = static_cast<size_t>(kRows) * 128 * kBufs + 1024;
-                auto kern = u32 ? k_halton_tma<true> : k_halton_tma<false>;
-                const cudaError_t e = cudaFuncSetAttribute(
-                    kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-                if (e != cudaSuccess)
-                    return e;
-                const uint64_t nsub = (r.n + kRows - 1) / kRows;
-                const uint32_t ncb = dims / 32;
-                const unsigned grid = static_cast<unsigned>(
-                    std::min<uint64_t>(nsub * ncb, static_cast<uint64_t>(sm_count())));
-                kern<<<grid, 1024, smem, s>>>(tmap, static_cast<const RadicalDim*>(rd), kRows,
-                                              kBufs, ncb, r.first, r.n, nsub);
-                return cudaGetLastError();
-            }
-        }
-    }
-    if (dims <= 32) {
-        // one CTA per SM, runs x dims warps, sub-tiles sharing ~kRunsTileWords
-        const uint32_t runs = std::min(15u, 32u / dims), ld = dims | 1u;
-        constexpr uint32_t kRunsTileWords = 49152; // 192 KB
-        uint32_t chunk = (kRunsTileWords / (runs * ld)) & ~31u;
-        if (chunk < 32)
-            chunk = 32;
-        const size_t smem = static_cast<size_t>(chunk) * ld * runs * 4;
-        auto kern = u32 ? k_halton_runs<true> : k_halton_runs<false>;
-        const cudaError_t e =
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess)
-            return e;
-        const uint64_t nsub = (r.n + chunk - 1) / chunk;
-        const unsigned grid =
-            static_cast<unsigned>(std::min<uint64_t>(nsub, static_cast<uint64_t>(sm_count())));
-        kern<<<grid, runs * dims * 32, smem, s>>>(static_cast<const RadicalDim*>(rd), dims, runs,
-                                                   chunk, r.first, r.n, nsub,
-                                                   static_cast<uint32_t*>(r.out));
-        return cudaGetLastError();
-    }
+    const RadicalDim* rdv = static_cast<const RadicalDim*>(rd);
+    cudaError_t err = cudaSuccess;
+    if (u32 ? launch_tma_fill(HaltonWalk<true>{rdv}, dims, r, s, &err)
+            : launch_tma_fill(HaltonWalk<false>{rdv}, dims, r, s, &err))
+        return err;
+    if (dims <= 32)
+        return u32 ? launch_runs_fill(HaltonWalk<true>{rdv}, dims, r, s)
+                   : launch_runs_fill(HaltonWalk<false>{rdv}, dims, r, s);
     // tile of tp points x (dims + 1) padded words: <= 48 KB, >= 32 points;
     // then 64 B of carried state per dimension when dims >= warps per CTA
     // 48 KB tiles: 4 CTAs (32 warps) per SM; larger tiles amortise the

@@ -255,6 +255,37 @@ def test_sobol_owen_vs_oracle(oracle, columns64, golden_arrays, mapv, dims):
     np.testing.assert_array_equal(f.reshape(n, dims)[::37], mapv(exp[::37]))
 
 
+@pytest.mark.parametrize("dims", [3, 5, 7, 12, 24, 31, 96, 160])
+@pytest.mark.parametrize("scramble", ["none", "xor", "owen"])
+def test_sobol_walk_dims_vs_oracle(oracle, columns64, dims, scramble):
+    """One dimension per warp (k_runs for dims <= 32, k_tma column blocks for
+    dims % 32 == 0): several sub-tiles per run, the 1024-index block steps,
+    an unaligned first (head through the element-wise path), a ragged end."""
+    rng = np.random.default_rng(dims)
+    if dims <= 64:
+        cols = np.ascontiguousarray(columns64[:dims])
+        m = None
+    else:
+        cols = rng.integers(0, 2**32, (dims, 52), dtype=np.uint64).astype(np.uint32)
+        m = q.GeneratorMatrixSet.from_columns(cols)
+    words = [int(w) for w in rng.integers(0, 2**32, dims, dtype=np.uint64)]
+    n = 148 * 1536 + 777
+    for first in [0, 77, (1 << 40) + 3]:
+        exp = np.zeros((n, dims), np.uint32)
+        kw = {"matrices": m} if m is not None else {}
+        if scramble == "owen":
+            seeds = np.array(words, np.uint32)
+            oracle.qo_sobol_owen_fill_fixed(first, n, dims, ptr(cols), ptr(seeds), ptr(exp))
+            kw.update(scramble="owen", words=words)
+        else:
+            sw = np.array(words, np.uint32) if scramble == "xor" else None
+            oracle.qo_sobol_fill_fixed(first, n, dims, ptr(cols), ptr(sw), ptr(exp))
+            if scramble == "xor":
+                kw.update(scramble="xor", words=words)
+        got = u32(q.sobol_fill(n, dims, first=first, fixed=True, **kw)).reshape(n, dims)
+        np.testing.assert_array_equal(got, exp, err_msg=f"first={first}")
+
+
 # --------------------------------------------------------------- lattice
 def test_lattice_vs_golden(golden_arrays, golden, oracle):
     g = golden_arrays["lfsr_ace1_16"]
