@@ -1148,7 +1148,7 @@ __device__ __forceinline__ void bar_named(uint32_t id, uint32_t threads)
 // meet at their own named barrier, and write it out as consecutive words
 // (each thread keeps a fixed column and a fixed shared-memory stride), so
 // runs never wait for each other.
-template <class W>
+template <class W, int DPW>
 __global__ void __launch_bounds__(1024, 1)
     k_runs(const __grid_constant__ W w, uint32_t dims, uint32_t runs, uint32_t chunk,
            uint64_t first, uint64_t n, uint64_t nsub, uint32_t* __restrict__ out)
@@ -1156,8 +1156,11 @@ __global__ void __launch_bounds__(1024, 1)
     extern __shared__ __align__(16) uint32_t tile[];
     const uint32_t ld = dims | 1u; // odd row stride: a column store hits 32 banks
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    const uint32_t run = warp / dims, j = warp - run * dims;
-    const uint32_t nthr = dims * 32, tid = threadIdx.x - run * nthr;
+    // DPW dimensions per warp (dims % DPW == 0): warp j of a run walks
+    // dimensions j, j + wpr, ...
+    const uint32_t wpr = dims / DPW;
+    const uint32_t run = warp / wpr, j = warp - run * wpr;
+    const uint32_t nthr = wpr * 32, tid = threadIdx.x - run * nthr;
     const uint32_t* sub = tile + static_cast<size_t>(run) * chunk * ld;
     const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(sub));
     // balanced split of the sub-tiles over the CTAs, then over the runs
@@ -1165,8 +1168,8 @@ __global__ void __launch_bounds__(1024, 1)
     const uint64_t q = (s1 - s0 + runs - 1) / runs;
     const uint64_t r0 = s0 + run * q, r1 = min(s1, r0 + q);
     // store mapping: thread tid owns the quads at words 4*tid + k*4*nthr of a
-    // sub-tile, i.e. a fixed column and rows advancing by 128 (4*nthr =
-    // 128*dims). Sub-tiles start on multiples of 32 points, so with out
+    // sub-tile, i.e. a fixed column and rows advancing by 128 / DPW (4*nthr =
+    // 128*dims/DPW). Sub-tiles start on multiples of 32 points, so with out
     // 16-B aligned every quad is a 16-B store; its words sit at fixed offsets
     // from the row start (offk: +1 per row wrap when dims % 4 != 0).
     const bool vec = (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
@@ -1174,13 +1177,18 @@ __global__ void __launch_bounds__(1024, 1)
     const uint32_t pad = ld - dims;
     const uint32_t off1 = 1 + (col0 + 1) / dims * pad, off2 = 2 + (col0 + 2) / dims * pad,
                    off3 = 3 + (col0 + 3) / dims * pad;
-    uint32_t* wsm = tile + static_cast<size_t>(runs) * chunk * ld + warp * 32;
-    typename W::State st;
-    w.reset(st);
+    uint32_t* wsm = tile + static_cast<size_t>(runs) * chunk * ld + warp * 32 * DPW;
+    typename W::State st[DPW];
+#pragma unroll
+    for (int k = 0; k < DPW; ++k)
+        w.reset(st[k]);
     for (uint64_t s = r0; s < r1; ++s) {
         const uint64_t p0 = s * chunk;
         const uint32_t cnt = static_cast<uint32_t>(n - p0 < chunk ? n - p0 : chunk);
-        w.run(j, first + p0, cnt, lane, sbase + j * 4, ld, st, wsm);
+#pragma unroll
+        for (int k = 0; k < DPW; ++k)
+            w.run(j + k * wpr, first + p0, cnt, lane, sbase + (j + k * wpr) * 4, ld, st[k],
+                  wsm + 32 * k);
         bar_named(1 + run, nthr);
         const uint32_t words = cnt * dims;
         uint32_t* o = out + p0 * dims;
@@ -1188,15 +1196,15 @@ __global__ void __launch_bounds__(1024, 1)
         uint32_t e = e0;
         if (!vec) {
 #pragma unroll 4
-            for (; e < words; e += nthr, src += 32 * ld)
+            for (; e < words; e += nthr, src += 32 / DPW * ld)
                 __stcs(o + e, *src);
         } else if ((dims & 3u) == 0) {
 #pragma unroll 2
-            for (; e < words; e += 4 * nthr, src += 128 * ld)
+            for (; e < words; e += 4 * nthr, src += 128 / DPW * ld)
                 __stcs(reinterpret_cast<uint4*>(o + e), make_uint4(src[0], src[1], src[2], src[3]));
         } else {
 #pragma unroll 2
-            for (; e + 4 <= words; e += 4 * nthr, src += 128 * ld)
+            for (; e + 4 <= words; e += 4 * nthr, src += 128 / DPW * ld)
                 __stcs(reinterpret_cast<uint4*>(o + e),
                        make_uint4(src[0], src[off1], src[off2], src[off3]));
             if (e < words) { // the ragged end of the last sub-tile: < 4 words
@@ -1588,24 +1596,24 @@ bool launch_tma_fill(const W& w, uint32_t dims, const FillRange& r, cudaStream_t
 
 // dims <= 32: one CTA per SM, runs x dims warps, sub-tiles sharing ~192 KB,
 // plus a 32-word scratch per warp
-template <class W>
+template <class W, int DPW = 1>
 cudaError_t launch_runs_fill(const W& w, uint32_t dims, const FillRange& r, cudaStream_t s)
 {
-    const uint32_t runs = std::min(15u, 32u / dims), ld = dims | 1u;
+    const uint32_t runs = std::min(15u, 32u * DPW / dims), ld = dims | 1u;
     constexpr uint32_t kRunsTileWords = 49152;
     uint32_t chunk = (kRunsTileWords / (runs * ld)) & ~31u;
     if (chunk < 32)
         chunk = 32;
     const size_t smem = (static_cast<size_t>(chunk) * ld * runs + runs * dims * 32) * 4;
-    const cudaError_t e =
-        cudaFuncSetAttribute(k_runs<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    const cudaError_t e = cudaFuncSetAttribute(k_runs<W, DPW>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess)
         return e;
     const uint64_t nsub = (r.n + chunk - 1) / chunk;
     const unsigned grid =
         static_cast<unsigned>(std::min<uint64_t>(nsub, static_cast<uint64_t>(sm_count())));
-    k_runs<W><<<grid, runs * dims * 32, smem, s>>>(w, dims, runs, chunk, r.first, r.n, nsub,
-                                                    static_cast<uint32_t*>(r.out));
+    k_runs<W, DPW><<<grid, runs * dims / DPW * 32, smem, s>>>(w, dims, runs, chunk, r.first, r.n,
+                                                               nsub, static_cast<uint32_t*>(r.out));
     return cudaGetLastError();
 }
 
@@ -1639,13 +1647,14 @@ cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const
     // one dimension per warp (k_tma for dims % 32 == 0, else k_runs for dims
     // <= 32) from a 32-aligned index; the few points before it go through
     // the element-wise / tiled paths below
-    if ((dims <= 32 || dims % 32 == 0) && r.n >= 64) {
+    const int dpw = dims <= 32 ? 1 : (dims <= 64 && dims % 2 == 0) ? 2 : (dims <= 128 && dims % 4 == 0) ? 4 : 0;
+    if ((dpw || dims % 32 == 0) && r.n >= 64) {
         const uint64_t head = (32u - static_cast<uint32_t>(r.first & 31u)) & 31u;
         const FillRange main{r.first + head, r.n - head,
                              static_cast<uint32_t*>(r.out) + head * dims};
         const bool tma = dims % 32 == 0 && (reinterpret_cast<uintptr_t>(main.out) & 15u) == 0 &&
                          main.n < (1ull << 31);
-        if (dims <= 32 || tma) {
+        if (dpw || tma) {
             if (head) {
                 const cudaError_t e = launch_sobol(colsT, colsT_rev, words, dims, mode, u32,
                                                    FillRange{r.first, head, r.out}, s);
@@ -1656,7 +1665,9 @@ cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const
                 cudaError_t err = cudaSuccess;
                 if (tma && launch_tma_fill(w, dims, main, s, &err))
                     return err;
-                return launch_runs_fill(w, dims, main, s);
+                return dpw == 4 ? launch_runs_fill<decltype(w), 4>(w, dims, main, s)
+                       : dpw == 2 ? launch_runs_fill<decltype(w), 2>(w, dims, main, s)
+                                  : launch_runs_fill<decltype(w), 1>(w, dims, main, s);
             };
             if (mode == 2)
                 return u32 ? go(SobolWalk<2, true>{cols, dims, words})
