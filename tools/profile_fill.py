@@ -43,6 +43,13 @@ elif a.config == "halton":
     n, d = 1 << 24, 32
     out = torch.empty((n, d), dtype=torch.float32, device="cuda")
     fn = lambda: q.halton_fill(n, d, scramble="linear", out=out)  # noqa: E731
+elif a.config in ("sobolowen12", "sobolowen256"):
+    d = 12 if a.config.endswith("12") else 256
+    n = (1 << 30) // d
+    out = torch.empty((n, d), dtype=torch.float32, device="cuda")
+    m = q.GeneratorMatrixSet.builtin(min(d, 64)) if d <= 64 else q.GeneratorMatrixSet.from_columns(
+        __import__("numpy").arange(d * 52, dtype="uint32").reshape(d, 52) | 1)
+    fn = lambda: q.sobol_fill(n, d, matrices=m, scramble="owen", words=list(range(d)), out=out)  # noqa: E731
 elif a.config == "integrate":
     fn = lambda: q.integrate("sobol", "product-sine", 1 << 26, 8, "kahan")  # noqa: E731
 elif a.config.startswith("c5"):
