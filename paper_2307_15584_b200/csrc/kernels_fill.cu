@@ -1328,6 +1328,81 @@ __global__ void __launch_bounds__(1024, 1)
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Odd dims <= 31: the padded sub-tile of k_runs has an odd row stride, so
+// with no padding at all (ld == dims) it is already conflict-free and laid
+// out exactly as the output — so each run keeps a ring of nbuf dense
+// sub-tiles and one bulk copy (cp.async.bulk, 16-B multiple; the < 16-B
+// tail by plain stores) writes a sub-tile while the warps walk the next.
+// Per run r: full[b] (count dims: every warp wrote sub-tile b), empty[b]
+// (count 1: the copy has read it), signalled by warp 0 lane 0 of the run.
+template <class W>
+__global__ void __launch_bounds__(1024, 1)
+    k_bulk(const __grid_constant__ W w, uint32_t dims, uint32_t runs, uint32_t rows,
+           uint32_t nbuf, uint64_t first, uint64_t n, uint64_t nsub, uint32_t* __restrict__ out)
+{
+    extern __shared__ __align__(128) uint32_t ring[];
+    __shared__ __align__(8) uint64_t bars[15][8];
+    __shared__ uint32_t scratch[32 * 32];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint32_t run = warp / dims, j = warp - run * dims;
+    const uint32_t buf_words = rows * dims;
+    const uint32_t ring0 = static_cast<uint32_t>(__cvta_generic_to_shared(ring)) +
+                           run * nbuf * buf_words * 4;
+    const uint32_t bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(bars[run]));
+    const bool issuer = j == 0 && lane == 0;
+    if (issuer) {
+        for (uint32_t b = 0; b < nbuf; ++b) {
+            mbar_init(bar0 + 8 * b, dims);    // full[b]
+            mbar_init(bar0 + 8 * (4 + b), 1); // empty[b]
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint64_t s0 = nsub * blockIdx.x / gridDim.x, s1 = nsub * (blockIdx.x + 1) / gridDim.x;
+    const uint64_t q = (s1 - s0 + runs - 1) / runs;
+    const uint64_t r0 = s0 + run * q, r1 = min(s1, r0 + q);
+    typename W::State st;
+    w.reset(st);
+    uint32_t b = 0, k = 0;
+    for (uint64_t s = r0; s < r1; ++s) {
+        const uint64_t p0 = s * rows;
+        const uint32_t cnt = static_cast<uint32_t>(n - p0 < rows ? n - p0 : rows);
+        const uint32_t buf = ring0 + b * buf_words * 4;
+        if (k > 0)
+            mbar_wait(bar0 + 8 * (4 + b), (k - 1) & 1u);
+        w.run(j, first + p0, cnt, lane, buf + j * 4, dims, st, scratch + warp * 32);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0)
+            mbar_arrive(bar0 + 8 * b);
+        if (issuer) {
+            mbar_wait(bar0 + 8 * b, k & 1u);
+            const uint32_t words = cnt * dims, w16 = words & ~3u;
+            uint32_t* o = out + p0 * dims;
+            if (w16)
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(o),
+                             "r"(buf), "r"(w16 * 4)
+                             : "memory");
+            for (uint32_t e = w16; e < words; ++e) {
+                uint32_t v;
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(buf + e * 4));
+                o[e] = v;
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            if (s > r0)
+                mbar_arrive(bar0 + 8 * (4 + (b == 0 ? nbuf - 1 : b - 1)));
+        }
+        __syncwarp();
+        if (++b == nbuf) {
+            b = 0;
+            ++k;
+        }
+    }
+    if (issuer)
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // ------------------------------------------------------------- launching
 
 template <typename K>
@@ -1617,6 +1692,31 @@ cudaError_t launch_runs_fill(const W& w, uint32_t dims, const FillRange& r, cuda
     return cudaGetLastError();
 }
 
+// Odd dims <= 31 with out 16-B aligned: k_bulk; returns false otherwise.
+template <class W>
+bool launch_bulk_fill(const W& w, uint32_t dims, const FillRange& r, cudaStream_t s,
+                      cudaError_t* err)
+{
+    if (dims > 31 || (dims & 1u) == 0 || (reinterpret_cast<uintptr_t>(r.out) & 15u) != 0)
+        return false;
+    const uint32_t runs = std::min(15u, 32u / dims), nbuf = 3;
+    constexpr uint32_t kRingWords = 47104; // 184 KB over all runs
+    uint32_t rows = (kRingWords / (runs * nbuf * dims)) & ~31u;
+    if (rows < 32)
+        rows = 32;
+    const size_t smem = static_cast<size_t>(rows) * dims * runs * nbuf * 4;
+    *err = cudaFuncSetAttribute(k_bulk<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (*err != cudaSuccess)
+        return true;
+    const uint64_t nsub = (r.n + rows - 1) / rows;
+    const unsigned grid =
+        static_cast<unsigned>(std::min<uint64_t>(nsub, static_cast<uint64_t>(sm_count())));
+    k_bulk<W><<<grid, runs * dims * 32, smem, s>>>(w, dims, runs, rows, nbuf, r.first, r.n, nsub,
+                                                    static_cast<uint32_t*>(r.out));
+    *err = cudaGetLastError();
+    return true;
+}
+
 cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const SmallArgs& words,
                          uint32_t dims, int mode, bool u32, const FillRange& r, cudaStream_t s)
 {
@@ -1761,6 +1861,12 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
     cudaError_t err = cudaSuccess;
     if (u32 ? launch_tma_fill(HaltonWalk<true>{rdv}, dims, r, s, &err)
             : launch_tma_fill(HaltonWalk<false>{rdv}, dims, r, s, &err))
+        return err;
+    // odd dims >= 5: bulk-copy ring (the walk is the bottleneck and warp 0,
+    // the issuer, walks base 2); the Sobol' walk is too cheap to spare the
+    // issuer's waits, and 3 dims measured no better
+    if (dims >= 5 && (u32 ? launch_bulk_fill(HaltonWalk<true>{rdv}, dims, r, s, &err)
+                          : launch_bulk_fill(HaltonWalk<false>{rdv}, dims, r, s, &err)))
         return err;
     if (dims <= 32)
         return u32 ? launch_runs_fill(HaltonWalk<true>{rdv}, dims, r, s)
