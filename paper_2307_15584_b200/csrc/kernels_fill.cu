@@ -1341,7 +1341,7 @@ __global__ void __launch_bounds__(1024, 1)
            uint32_t nbuf, uint64_t first, uint64_t n, uint64_t nsub, uint32_t* __restrict__ out)
 {
     extern __shared__ __align__(128) uint32_t ring[];
-    __shared__ __align__(8) uint64_t bars[15][8];
+    __shared__ __align__(8) uint64_t bars[32][8];
     __shared__ uint32_t scratch[32 * 32];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint32_t run = warp / dims, j = warp - run * dims;
@@ -1699,7 +1699,8 @@ bool launch_bulk_fill(const W& w, uint32_t dims, const FillRange& r, cudaStream_
 {
     if (dims > 31 || (dims & 1u) == 0 || (reinterpret_cast<uintptr_t>(r.out) & 15u) != 0)
         return false;
-    const uint32_t runs = std::min(15u, 32u / dims), nbuf = 3;
+    // mbarriers, not named barriers, so a CTA may hold 32 one-warp runs
+    const uint32_t runs = dims == 1 ? 32u : std::min(15u, 32u / dims), nbuf = 3;
     constexpr uint32_t kRingWords = 47104; // 184 KB over all runs
     uint32_t rows = (kRingWords / (runs * nbuf * dims)) & ~31u;
     if (rows < 32)
@@ -1864,8 +1865,9 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
         return err;
     // odd dims >= 5: bulk-copy ring (the walk is the bottleneck and warp 0,
     // the issuer, walks base 2); the Sobol' walk is too cheap to spare the
-    // issuer's waits, and 3 dims measured no better
-    if (dims >= 5 && (u32 ? launch_bulk_fill(HaltonWalk<true>{rdv}, dims, r, s, &err)
+    // issuer's waits, and 3 dims measured no better. dims == 1 (a single
+    // radical inverse): 32 one-warp runs per CTA instead of k_runs' 15
+    if ((dims >= 5 || dims == 1) && (u32 ? launch_bulk_fill(HaltonWalk<true>{rdv}, dims, r, s, &err)
                           : launch_bulk_fill(HaltonWalk<false>{rdv}, dims, r, s, &err)))
         return err;
     if (dims <= 32)
