@@ -1003,8 +1003,8 @@ __device__ __forceinline__ void halton_run(const RadicalDim& r, uint32_t i0, uin
 // per dimension the same warp owns a dimension in every tile, so its
 // incremental state carries over from tile to tile (HaltonState, after the
 // tile in shared memory).
-template <bool U32OUT>
-__global__ void __launch_bounds__(kBlock)
+template <bool U32OUT, int BLOCK>
+__global__ void __launch_bounds__(BLOCK)
     k_halton_tiled(const RadicalDim* __restrict__ rd, uint32_t dims, Div32 div_dims, uint32_t tp,
                    uint64_t first, uint64_t n, uint64_t ntiles, uint32_t* __restrict__ out)
 {
@@ -1879,17 +1879,23 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
     if (dims <= 32)
         return u32 ? launch_runs_fill(HaltonWalk<true>{rdv}, dims, r, s)
                    : launch_runs_fill(HaltonWalk<false>{rdv}, dims, r, s);
-    // tile of tp points x (dims + 1) padded words: <= 48 KB, >= 32 points;
-    // then 64 B of carried state per dimension when dims >= warps per CTA
-    // 48 KB tiles: 4 CTAs (32 warps) per SM; larger tiles amortise the
-    // per-(tile, dimension) bookkeeping better but lose more to latency
-    // (measured 8-32K words at 8-64 dims, tools/exp_halton.py)
-    uint32_t tp = (12288u / (dims | 1u)) & ~31u;
+    // dims > 32 (not a multiple of 32): shared-memory walk state per
+    // dimension. One CTA of 1024 threads per SM with a ~190 KB tile (minus
+    // the states) makes each (tile, dimension) run 3-5x longer than 48 KB
+    // tiles at 4 CTAs per SM, which pays for the per-run state load/store
+    const bool wide = dims > 32;
+    const uint32_t block = wide ? 1024u : static_cast<uint32_t>(kBlock);
+    const size_t state_bytes =
+        dims >= block / 32 ? static_cast<size_t>(dims) * sizeof(HaltonState) : 0;
+    const uint32_t budget =
+        wide ? static_cast<uint32_t>((196608 - std::min<size_t>(state_bytes, 98304)) / 4) : 12288u;
+    uint32_t tp = (budget / (dims | 1u)) & ~31u;
     if (tp < 32)
         tp = 32;
     const size_t tile_words = (static_cast<size_t>(tp) * (dims | 1u) + 15) & ~size_t(15);
-    const size_t smem = tile_words * 4 + (dims >= kBlock / 32 ? size_t(dims) * sizeof(HaltonState) : 0);
-    auto kern = u32 ? k_halton_tiled<true> : k_halton_tiled<false>;
+    const size_t smem = tile_words * 4 + state_bytes;
+    auto kern = wide ? (u32 ? k_halton_tiled<true, 1024> : k_halton_tiled<false, 1024>)
+                     : (u32 ? k_halton_tiled<true, kBlock> : k_halton_tiled<false, kBlock>);
     if (smem > 48 * 1024) {
         const cudaError_t e =
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -1897,15 +1903,15 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
             return e;
     }
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, smem) != cudaSuccess ||
         per_sm < 1)
         per_sm = 1;
     const uint64_t ntiles = (r.n + tp - 1) / tp;
     const uint64_t cap = static_cast<uint64_t>(sm_count()) * per_sm;
     const unsigned grid = static_cast<unsigned>(ntiles < cap ? ntiles : cap);
     const Div32 dd = dims >= 2 ? make_div32(dims) : Div32{0, 0};
-    kern<<<grid, kBlock, smem, s>>>(static_cast<const RadicalDim*>(rd), dims, dd, tp, r.first,
-                                    r.n, ntiles, static_cast<uint32_t*>(r.out));
+    kern<<<grid, block, smem, s>>>(static_cast<const RadicalDim*>(rd), dims, dd, tp, r.first, r.n,
+                                   ntiles, static_cast<uint32_t*>(r.out));
     return cudaGetLastError();
 }
 
