@@ -472,8 +472,34 @@ __global__ void __launch_bounds__(kBlock)
 // chain (one LDS + XOR per sample); X(p0) advances from tile to tile through
 // the index bits that change. The padded [tp][dims+1] tile is then written
 // out with tile_store_rows.
+// Sobol' with more dimensions than any shared-memory tile holds (direction
+// number files reach tens of thousands): element-wise over the output words,
+// each point component the XOR of the columns of its index's set bits
+// (digitalnet.cpp:96-110) — correct at any dims, not a fast path.
 template <int MODE, bool U32OUT>
 __global__ void __launch_bounds__(kBlock)
+    k_sobol_huge(const uint32_t* __restrict__ colsT, const __grid_constant__ SmallArgs args,
+                 uint32_t dims, Div32 div_dims, uint64_t first, uint64_t n,
+                 uint32_t* __restrict__ out)
+{
+    const uint32_t* words = small_a(args);
+    const uint64_t total = n * dims;
+    for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t p = e / dims;
+        const uint32_t j = static_cast<uint32_t>(e - p * dims);
+        uint32_t x = (MODE == 0 && words) ? words[j] : 0u;
+        for (uint64_t b = first + p; b; b &= b - 1)
+            x ^= __ldg(colsT + static_cast<size_t>(__ffsll(static_cast<long long>(b)) - 1) * dims + j);
+        if (MODE == 2)
+            x = brev32(owen_lk(x, words ? words[j] : 0u));
+        out[e] = U32OUT ? x : map_bits(x);
+    }
+    (void)div_dims;
+}
+
+template <int MODE, bool U32OUT, int BLOCK>
+__global__ void __launch_bounds__(BLOCK)
     k_sobol_tiled(const uint32_t* __restrict__ colsT, const __grid_constant__ SmallArgs args,
                   uint32_t dims, Div32 div_dims, uint32_t tp, uint64_t first, uint64_t n,
                   uint64_t tile0, uint64_t ntiles, uint32_t* __restrict__ out)
@@ -483,8 +509,7 @@ __global__ void __launch_bounds__(kBlock)
     const uint32_t mt = tp / 32; // m steps per tile
     uint32_t* tile = smem;
     uint32_t* T = smem + static_cast<size_t>(tp) * ld; // [dims][mt]: X(32 m)
-    uint32_t* L = T + static_cast<size_t>(dims) * mt;  // [dims][32]: X(lane)
-    uint32_t* XP = L + static_cast<size_t>(dims) * 32; // [dims]: words ^ X(p0)
+    uint32_t* XP = T + static_cast<size_t>(dims) * mt; // [dims]: words ^ X(p0)
     const uint32_t* words = small_a(args);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, nwarps = blockDim.x >> 5;
     auto col = [&](uint32_t k, uint32_t j) {
@@ -497,14 +522,6 @@ __global__ void __launch_bounds__(kBlock)
             if ((m >> k) & 1u)
                 x ^= col(5 + k, j);
         T[e] = x;
-    }
-    for (uint32_t e = threadIdx.x; e < dims * 32; e += blockDim.x) {
-        const uint32_t j = e >> 5, l = e & 31u;
-        uint32_t x = 0;
-        for (uint32_t k = 0; k < 5; ++k)
-            if ((l >> k) & 1u)
-                x ^= col(k, j);
-        L[e] = x;
     }
     // a contiguous range of tiles per CTA: X(p0) advances incrementally
     // (only the index bits that change between consecutive tiles), and
@@ -538,7 +555,10 @@ __global__ void __launch_bounds__(kBlock)
             const uint32_t j = runs == 1 ? item : item % dims;
             const uint32_t mb = (runs == 1 ? 0u : item / dims) * mchunk;
             const uint32_t me = min(mt, mb + mchunk);
-            const uint32_t x = XP[j] ^ L[j * 32 + lane];
+            uint32_t x = XP[j]; // ^ X(lane), from the columns (no table: dims can be large)
+            for (uint32_t k = 0; k < 5; ++k)
+                if ((lane >> k) & 1u)
+                    x ^= col(k, j);
             const uint32_t seed = (MODE == 2 && words) ? words[j] : 0u;
             const uint32_t* Tj = T + j * mt;
             for (uint32_t m = mb; m < me; ++m) {
@@ -1804,14 +1824,42 @@ cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const
                                         static_cast<uint32_t*>(r.out));
         return cudaGetLastError();
     }
-    // shared-memory tiled path: tp = 2^k points with tp*(dims+1) <= 8192 words
+    // shared-memory tiled path: tp = 2^k points. dims > 128: one 1024-thread
+    // CTA per SM with up to ~190 KB of tile + tables (longer runs per
+    // dimension); else tp*(dims+1) <= 8192 words at several CTAs per SM
+    const bool wide = dims > 128;
+    const uint32_t block = wide ? 1024u : static_cast<uint32_t>(kBlock);
+    auto words_for = [&](uint32_t t) {
+        return static_cast<size_t>(t) * (dims + 1) + static_cast<size_t>(dims) * (t / 32 + 1);
+    };
+    if (words_for(32) > 56000u) { // thousands of dims: no tile fits, per-element path
+        const unsigned grid = static_cast<unsigned>(sm_count()) * 8;
+        const Div32 d = make_div32(dims);
+        if (mode == 2)
+            u32 ? k_sobol_huge<2, true><<<grid, kBlock, 0, s>>>(cols, words, dims, d, r.first, r.n,
+                                                                static_cast<uint32_t*>(r.out))
+                : k_sobol_huge<2, false><<<grid, kBlock, 0, s>>>(cols, words, dims, d, r.first, r.n,
+                                                                 static_cast<uint32_t*>(r.out));
+        else
+            u32 ? k_sobol_huge<0, true><<<grid, kBlock, 0, s>>>(cols, words, dims, d, r.first, r.n,
+                                                                static_cast<uint32_t*>(r.out))
+                : k_sobol_huge<0, false><<<grid, kBlock, 0, s>>>(cols, words, dims, d, r.first, r.n,
+                                                                 static_cast<uint32_t*>(r.out));
+        return cudaGetLastError();
+    }
     uint32_t tp = 32;
-    while (tp * 2 * (dims + 1) <= 8192u)
-        tp *= 2;
-    const size_t smem = (static_cast<size_t>(tp) * (dims + 1) +
-                         static_cast<size_t>(dims) * (tp / 32 + 33)) * 4;
-    auto kern = mode == 2 ? (u32 ? k_sobol_tiled<2, true> : k_sobol_tiled<2, false>)
-                          : (u32 ? k_sobol_tiled<0, true> : k_sobol_tiled<0, false>);
+    if (wide) {
+        while (words_for(tp * 2) <= 48000u)
+            tp *= 2;
+    } else {
+        while (tp * 2 * (dims + 1) <= 8192u)
+            tp *= 2;
+    }
+    const size_t smem = words_for(tp) * 4;
+    auto kern = wide ? (mode == 2 ? (u32 ? k_sobol_tiled<2, true, 1024> : k_sobol_tiled<2, false, 1024>)
+                                  : (u32 ? k_sobol_tiled<0, true, 1024> : k_sobol_tiled<0, false, 1024>))
+                     : (mode == 2 ? (u32 ? k_sobol_tiled<2, true, kBlock> : k_sobol_tiled<2, false, kBlock>)
+                                  : (u32 ? k_sobol_tiled<0, true, kBlock> : k_sobol_tiled<0, false, kBlock>));
     if (smem > 48 * 1024) {
         const cudaError_t e =
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -1819,7 +1867,7 @@ cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const
             return e;
     }
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, smem) != cudaSuccess ||
         per_sm < 1)
         per_sm = 1;
     const uint64_t tile0 = r.first / tp;
@@ -1827,8 +1875,8 @@ cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const
     const uint64_t cap = static_cast<uint64_t>(sm_count()) * per_sm;
     const unsigned grid = static_cast<unsigned>(ntiles < cap ? ntiles : cap);
     const Div32 d = dims >= 2 ? make_div32(dims) : Div32{0, 0};
-    kern<<<grid, kBlock, smem, s>>>(cols, words, dims, d, tp, r.first, r.n, tile0, ntiles,
-                                    static_cast<uint32_t*>(r.out));
+    kern<<<grid, block, smem, s>>>(cols, words, dims, d, tp, r.first, r.n, tile0, ntiles,
+                                   static_cast<uint32_t*>(r.out));
     return cudaGetLastError();
 }
 

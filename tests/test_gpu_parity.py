@@ -286,6 +286,27 @@ def test_sobol_walk_dims_vs_oracle(oracle, columns64, dims, scramble):
         np.testing.assert_array_equal(got, exp, err_msg=f"first={first}")
 
 
+@pytest.mark.parametrize("dims", [200, 700, 1000, 2500])
+@pytest.mark.parametrize("scramble", ["xor", "owen"])
+def test_sobol_many_dims_vs_oracle(oracle, dims, scramble):
+    """Direction-number sets with hundreds to thousands of dimensions: the
+    1024-thread tiled path and, past what a tile holds, the per-element path."""
+    rng = np.random.default_rng(dims)
+    cols = rng.integers(0, 2**32, (dims, 52), dtype=np.uint64).astype(np.uint32)
+    m = q.GeneratorMatrixSet.from_columns(cols)
+    words = [int(w) for w in rng.integers(0, 2**32, dims, dtype=np.uint64)]
+    n, first = 1500, 4096 * 5 + 77
+    exp = np.zeros((n, dims), np.uint32)
+    wa = np.array(words, np.uint32)
+    if scramble == "owen":
+        oracle.qo_sobol_owen_fill_fixed(first, n, dims, ptr(cols), ptr(wa), ptr(exp))
+    else:
+        oracle.qo_sobol_fill_fixed(first, n, dims, ptr(cols), ptr(wa), ptr(exp))
+    got = u32(q.sobol_fill(n, dims, first=first, fixed=True, matrices=m, scramble=scramble,
+                           words=words)).reshape(n, dims)
+    np.testing.assert_array_equal(got, exp)
+
+
 # --------------------------------------------------------------- lattice
 def test_lattice_vs_golden(golden_arrays, golden, oracle):
     g = golden_arrays["lfsr_ace1_16"]

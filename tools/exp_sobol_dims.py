@@ -14,7 +14,8 @@ def t(fn, B, k=5):
 x = torch.empty(1 << 30, device="cuda")
 for _ in range(200): x.fill_(1)
 del x
-for dims in (2, 3, 4, 5, 6, 7, 8, 10, 12, 16, 20, 24, 31, 32, 40, 48, 64, 96, 100, 128, 200, 256):
+DIMS = [int(a) for a in sys.argv[1].split(",")] if len(sys.argv) > 1 else [2, 3, 4, 5, 6, 7, 8, 10, 12, 16, 20, 24, 31, 32, 40, 48, 64, 96, 100, 128, 200, 256]
+for dims in DIMS:
     n = (1 << 30) // dims // 4 * 4
     m = q.GeneratorMatrixSet.builtin(min(dims, 64)) if dims <= 64 else q.GeneratorMatrixSet.from_columns(
         np.arange(dims * 52, dtype="uint32").reshape(dims, 52) | 1)
