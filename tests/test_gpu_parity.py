@@ -307,6 +307,21 @@ def test_sobol_many_dims_vs_oracle(oracle, dims, scramble):
     np.testing.assert_array_equal(got, exp)
 
 
+def test_max_dims_fills_vs_oracle(oracle):
+    """The widest fills: Halton at the prime table's 1000 dims (shared-memory
+    state for every dimension) and a 3000-dim lattice."""
+    n, first = 700, 123457
+    got = u32(q.halton_fill(n, 1000, first=first, fixed=True)).reshape(n, 1000)
+    for j in (0, 1, 499, 998, 999):
+        for k in (0, 1, 350, 699):
+            assert got[k, j] == oracle.qo_radical_inverse_fixed(first + k, j)
+    g = [2 * k + 1 for k in range(3000)]
+    lat = u32(q.lattice_fill(n, g, first=first, fixed=True)).reshape(n, 3000)
+    for j in (0, 1777, 2999):
+        for k in (0, 699):
+            assert lat[k, j] == oracle.qo_lattice_component_fixed(first + k, g[j])
+
+
 # --------------------------------------------------------------- lattice
 def test_lattice_vs_golden(golden_arrays, golden, oracle):
     g = golden_arrays["lfsr_ace1_16"]
