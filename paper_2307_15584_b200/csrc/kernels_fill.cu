@@ -1239,6 +1239,39 @@ __global__ void __launch_bounds__(1024, 1)
     }
 }
 
+// dims 33..32*DMAX with no exact per-warp split: one run of 32 warps per
+// CTA, warp j walking dims j, j + 32, ... (< dims), the padded sub-tile
+// written with the generic row copy (tile_store_rows, any dims).
+template <class W, int DMAX>
+__global__ void __launch_bounds__(1024, 1)
+    k_runs_wide(const __grid_constant__ W w, uint32_t dims, Div32 div_dims, uint32_t chunk,
+                uint64_t first, uint64_t n, uint64_t nsub, uint32_t* __restrict__ out)
+{
+    extern __shared__ __align__(16) uint32_t tile[];
+    const uint32_t ld = dims | 1u;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(tile));
+    uint32_t* wsm = tile + static_cast<size_t>(chunk) * ld + warp * 32 * DMAX;
+    const uint64_t s0 = nsub * blockIdx.x / gridDim.x, s1 = nsub * (blockIdx.x + 1) / gridDim.x;
+    typename W::State st[DMAX];
+#pragma unroll
+    for (int k = 0; k < DMAX; ++k)
+        w.reset(st[k]);
+    for (uint64_t s = s0; s < s1; ++s) {
+        const uint64_t p0 = s * chunk;
+        const uint32_t cnt = static_cast<uint32_t>(n - p0 < chunk ? n - p0 : chunk);
+#pragma unroll
+        for (int k = 0; k < DMAX; ++k) {
+            const uint32_t j = warp + 32 * k;
+            if (j < dims)
+                w.run(j, first + p0, cnt, lane, sbase + j * 4, ld, st[k], wsm + 32 * k);
+        }
+        __syncthreads();
+        tile_store_rows(tile, ld, dims, div_dims, 0, cnt, out + p0 * dims);
+        __syncthreads();
+    }
+}
+
 __device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count)
 {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(addr), "r"(count) : "memory");
@@ -1712,6 +1745,24 @@ cudaError_t launch_runs_fill(const W& w, uint32_t dims, const FillRange& r, cuda
     return cudaGetLastError();
 }
 
+template <class W, int DMAX>
+cudaError_t launch_runs_wide(const W& w, uint32_t dims, const FillRange& r, cudaStream_t s)
+{
+    const uint32_t ld = dims | 1u;
+    uint32_t chunk = (49152u / ld) & ~31u;
+    const size_t smem = (static_cast<size_t>(chunk) * ld + 32 * 32 * DMAX) * 4;
+    const cudaError_t e = cudaFuncSetAttribute(k_runs_wide<W, DMAX>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess)
+        return e;
+    const uint64_t nsub = (r.n + chunk - 1) / chunk;
+    const unsigned grid =
+        static_cast<unsigned>(std::min<uint64_t>(nsub, static_cast<uint64_t>(sm_count())));
+    k_runs_wide<W, DMAX><<<grid, 1024, smem, s>>>(w, dims, make_div32(dims), chunk, r.first, r.n,
+                                                  nsub, static_cast<uint32_t*>(r.out));
+    return cudaGetLastError();
+}
+
 // Odd dims <= 31 with out 16-B aligned: k_bulk; returns false otherwise.
 template <class W>
 bool launch_bulk_fill(const W& w, uint32_t dims, const FillRange& r, cudaStream_t s,
@@ -1771,9 +1822,12 @@ cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const
     // dimensions per warp: two for even dims 10-64 (more independent runs
     // per CTA for dims <= 32, measured +2-20 %), four for dims <= 128
     // divisible by 4
+    // (-1: Owen at the other dims 33-128, k_runs_wide: +3-19 % over the
+    // element-wise kernel, where plain Sobol' measured 1-13 % slower)
     const int dpw = (dims <= 8 || (dims <= 32 && dims % 2 != 0)) ? 1
                     : (dims <= 64 && dims % 2 == 0)              ? 2
                     : (dims <= 128 && dims % 4 == 0)             ? 4
+                    : (dims <= 128 && mode == 2)                 ? -1
                                                                   : 0;
     if ((dpw || dims % 32 == 0) && r.n >= 64) {
         const uint64_t head = (32u - static_cast<uint32_t>(r.first & 31u)) & 31u;
@@ -1792,6 +1846,9 @@ cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const
                 cudaError_t err = cudaSuccess;
                 if (tma && launch_tma_fill(w, dims, main, s, &err))
                     return err;
+                if (dpw < 0)
+                    return dims <= 64 ? launch_runs_wide<decltype(w), 2>(w, dims, main, s)
+                                      : launch_runs_wide<decltype(w), 4>(w, dims, main, s);
                 return dpw == 4 ? launch_runs_fill<decltype(w), 4>(w, dims, main, s)
                        : dpw == 2 ? launch_runs_fill<decltype(w), 2>(w, dims, main, s)
                                   : launch_runs_fill<decltype(w), 1>(w, dims, main, s);

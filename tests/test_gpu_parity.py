@@ -255,7 +255,7 @@ def test_sobol_owen_vs_oracle(oracle, columns64, golden_arrays, mapv, dims):
     np.testing.assert_array_equal(f.reshape(n, dims)[::37], mapv(exp[::37]))
 
 
-@pytest.mark.parametrize("dims", [3, 5, 7, 12, 24, 31, 40, 62, 100, 96, 160])
+@pytest.mark.parametrize("dims", [3, 5, 7, 12, 24, 31, 33, 40, 62, 63, 99, 100, 96, 127, 160])
 @pytest.mark.parametrize("scramble", ["none", "xor", "owen"])
 def test_sobol_walk_dims_vs_oracle(oracle, columns64, dims, scramble):
     """One dimension per warp (k_runs for dims <= 32, k_tma column blocks for
