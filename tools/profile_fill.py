@@ -52,6 +52,9 @@ elif a.config in ("sobolowen12", "sobolowen256"):
     fn = lambda: q.sobol_fill(n, d, matrices=m, scramble="owen", words=list(range(d)), out=out)  # noqa: E731
 elif a.config == "integrate":
     fn = lambda: q.integrate("sobol", "product-sine", 1 << 26, 8, "kahan")  # noqa: E731
+elif a.config == "c5iph":
+    out = torch.empty((2160, 3840), dtype=torch.float32, device="cuda")
+    fn = lambda: q.render(3840, 2160, 64, kind="image-plane-halton", out=out)  # noqa: E731
 elif a.config.startswith("c5"):
     spp = int(a.config[2:] or 64)
     out = torch.empty((2160, 3840), dtype=torch.float32, device="cuda")
