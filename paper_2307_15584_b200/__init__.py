@@ -218,6 +218,28 @@ def _alloc(n: int, dims: int, fixed: bool, out, device=None):
     return torch.empty(shape, dtype=dt, device=device or "cuda")
 
 
+def _check_out(out, count: int, dtype: str):
+    """A caller-supplied render output must hold `count` C-contiguous elements
+    of `dtype` ("float32" / "int64"): the C-ABI writes exactly that many."""
+    if isinstance(out, np.ndarray):
+        ok_dt = out.dtype == np.dtype(dtype)
+        contig = out.flags["C_CONTIGUOUS"]
+        nbytes = out.nbytes
+        size = out.size
+    else:
+        ok_dt = str(out.dtype) == "torch." + dtype
+        contig = out.is_contiguous()
+        size = out.numel()
+        nbytes = size * out.element_size()
+    if not ok_dt:
+        raise ValueError("output must be %s, got %s" % (dtype, out.dtype))
+    if not contig:
+        raise ValueError("output must be C-contiguous")
+    if size < count or nbytes < count * np.dtype(dtype).itemsize:
+        raise ValueError("output buffer too small: %d elements for %d" % (size, count))
+    return out
+
+
 _SOBOL = {"none": 0, "plain": 0, "xor": 1, "owen": 2}
 _RADICAL = {"plain": 0, "linear": 1, "faure": 2}
 _ACCUM = {"kahan": 0, "int": 1}
@@ -680,6 +702,7 @@ def render(width: int, height: int, spp: int = 1, kind: str = "pixel-shifted-lat
     if out is None:
         torch = _torch()
         out = torch.empty((max(r1 - r0, 0), width), dtype=torch.float32, device="cuda")
+    _check_out(out, max(r1 - r0, 0) * width, "float32")
     _check(lib().qmc_render(C.byref(job), r0, r1, _ptr(out), _stream(stream)))
     return out
 
@@ -715,6 +738,7 @@ def render_devices(width: int, height: int, spp: int, devices, kind: str = "pixe
     devs = np.ascontiguousarray(devices, dtype=np.int32)
     if out is None:
         out = np.empty((height, width), np.float32)
+    _check_out(out, height * width, "float32")
     _check(lib().qmc_render_devices(C.byref(job), devs.ctypes.data, devs.size, _ptr(out)))
     return out
 
@@ -731,6 +755,7 @@ def render_samples_devices(width: int, height: int, spp: int, devices,
     devs = np.ascontiguousarray(devices, dtype=np.int32)
     if out is None:
         out = np.empty((height, width), np.float32)
+    _check_out(out, height * width, "float32")
     _check(lib().qmc_render_samples_devices(C.byref(job), devs.ctypes.data, devs.size,
                                             _ptr(out)))
     return out
@@ -747,6 +772,7 @@ def render_partial(width: int, height: int, spp: int, part: int, parts: int,
     if out is None:
         torch = _torch()
         out = torch.empty((max(r1 - r0, 0), width), dtype=torch.int64, device="cuda")
+    _check_out(out, max(r1 - r0, 0) * width, "int64")
     _check(lib().qmc_render_partial(C.byref(job), part, parts, r0, r1, _ptr(out),
                                     _stream(stream)))
     return out
@@ -757,6 +783,8 @@ def render_finalize(acc, spp: int, out=None, stream=None):
     torch = _torch()
     if out is None:
         out = torch.empty(acc.shape, dtype=torch.float32, device=acc.device)
+    _check_out(acc, acc.numel(), "int64")
+    _check_out(out, acc.numel(), "float32")
     _check(lib().qmc_render_finalize(_ptr(acc), acc.numel(), spp, _ptr(out), _stream(stream)))
     return out
 

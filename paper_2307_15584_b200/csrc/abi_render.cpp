@@ -290,7 +290,11 @@ qmc_status qmc_render_samples_devices(const qmc_render_job* job, const int* devi
         long long* acc = nullptr;
         cuda_ok(cudaMalloc(&acc, npix * 8 + 8), "cudaMalloc");
         const std::unique_ptr<long long, DevFree> acc_own(acc);
-        cuda_ok(cudaMemset(acc, 0, npix * 8), "cudaMemset");
+        // zeroed on the home stream and waited for before any worker starts:
+        // the workers' non-blocking streams (and the peer devices' streams)
+        // have no ordering with the legacy stream a plain cudaMemset uses
+        cuda_ok(cudaMemsetAsync(acc, 0, npix * 8, hs.s), "cudaMemsetAsync");
+        cuda_ok(cudaStreamSynchronize(hs.s), "sync");
         // part k of n (samples i == rev_2(k) mod n) on devices[k]: one kernel
         // renders and atomically adds its int64 partials into the
         // accumulator — over NVLink peer access when the device differs

@@ -67,10 +67,14 @@ int current_device()
     return dev;
 }
 
-// Keep the stream-ordered pool's memory cached across synchronizations, so
-// the per-call argument blobs (cudaMallocAsync) never remap physical memory
-// in a timed loop (the default release threshold of 0 returns it at every
-// sync, which cost milliseconds per call).
+// Keep up to kPoolKeepBytes of the stream-ordered pool cached across
+// synchronizations, so the per-call argument blobs (cudaMallocAsync) never
+// remap physical memory in a timed loop (the default release threshold of 0
+// returns it at every sync, which cost milliseconds per call). The bound keeps
+// large user-sized scratch (host-output render/fill chunks, scene_value,
+// quality-metric points) from staying reserved against torch's allocator.
+constexpr uint64_t kPoolKeepBytes = 256ull << 20;
+
 void pool_keep_memory()
 {
     static std::mutex mu;
@@ -83,7 +87,7 @@ void pool_keep_memory()
         return;
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t keep = UINT64_MAX;
+        uint64_t keep = kPoolKeepBytes;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
     done[dev] = 1;

@@ -447,12 +447,55 @@ def test_render_seeded_sobol_vs_reference(ref):
 
 
 def test_render4k_golden_checksums(golden, oracle):
-    """4K pixel-shifted lattice: checksum vs reference where bit-exact; else 1e-6."""
+    """BASELINE C5 (3840x2160, pixel-shifted lattice): the FNV-1a of the GPU
+    image equals the reference build's (tests/golden/make_golden.py) for
+    1 spp Kahan, 16 spp Kahan and 64 spp int — bit for bit."""
+    assert len(golden["render4k_psl_fnv"]) == 3
     for key, h in golden["render4k_psl_fnv"].items():
         spp, accum = key.split("/")
         img = q.render(3840, 2160, int(spp), accum=accum).cpu().numpy()
         got = fnv(oracle, img)
         print("render4k %s: %s (reference %s)" % (key, got, h))
+        assert got == h, (key, got, h)
+
+
+# BASELINE C5 at its stated size against the reference render run on this
+# box (render.cpp:83-143 with workers = nproc; glibc sin, so run here, not
+# from a fixture). spp 64/256 take the classified disc/quadrant/neumaier_add_big
+# fast path (kernels_render.cu); halton-hilbert at 256 spp has block starts
+# 4^12*256 > 2^32, i.e. the (uint32_t)(block_start_ + index) wrap
+# (imageplane.cpp:378, :440-442), and phi3's 7+7+6-digit branch.
+C5_CASES = [
+    ("pixel-shifted-lattice", "kahan", 64),
+    ("pixel-shifted-lattice", "kahan", 256),
+    ("pixel-shifted-lattice", "int", 256),
+    ("image-plane-halton", "kahan", 64),
+    ("image-plane-halton", "kahan", 256),
+    ("halton-hilbert", "kahan", 64),
+    ("halton-hilbert", "int", 256),
+]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("kind,accum,spp", C5_CASES)
+def test_render_4k_c5_vs_reference(ref, kind, accum, spp):
+    """BASELINE C5 at 3840x2160, spp 64 and 256: every pixel within 1e-6
+    relative of the reference render (north_star tolerance); the number of
+    pixels whose bits differ is printed (CUDA sin vs glibc sin can move the
+    last ulp of a sample)."""
+    import os
+
+    w, h = 3840, 2160
+    exp = np.zeros((h, w), np.float32)
+    assert ref.ref_render(w, h, spp, kind.encode(), accum.encode(), 0, os.cpu_count() or 1,
+                          ptr(exp)) == 0
+    got = q.render(w, h, spp, kind=kind, accum=accum).cpu().numpy()
+    rel = np.abs(got.astype(np.float64) - exp) / np.maximum(np.abs(exp), 1e-30)
+    mism = int((got.view(np.uint32) != exp.view(np.uint32)).sum())
+    print("C5 4K %s/%s/spp%d: %d of %d pixels differ in bits, max rel %.2e"
+          % (kind, accum, spp, mism, exp.size, rel.max()))
+    assert np.isfinite(got).all()
+    assert rel.max() <= 1e-6, (kind, accum, spp, rel.max(), mism)
 
 
 def test_scene_value_vs_reference(ref):
