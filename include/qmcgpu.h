@@ -363,6 +363,74 @@ qmc_status qmc_render_partial(const qmc_render_job* job, uint32_t part, uint32_t
 qmc_status qmc_render_finalize(const int64_t* accum, uint64_t npix, uint32_t spp, float* out,
                                qmc_stream stream);
 
+/* ------------------------------------- component-generation benchmark
+ * run_bench_kernel (bench.cpp:79-150; `qmckit bench`, SPEC acceptance 9) on
+ * the device: the same walk (128x128 tile, 16 indices per pixel, `dims`
+ * components each), the same kernels ("sobol", "halton", "halton-tabled",
+ * "lattice", "pixel-shifted-lattice", "pixel-random-lattice") and the same
+ * Sink checksum (rotl 7 fold of the float bits), so `checksum` equals the
+ * reference's for the same (kernel, count, dims). One warm-up walk of
+ * count / 8, then the timed walk (CUDA events on `stream`); synchronous. */
+typedef struct qmc_bench_result {
+    uint64_t evaluations;
+    double seconds;
+    double components_per_second;
+    uint64_t checksum;
+} qmc_bench_result;
+qmc_status qmc_run_bench_kernel(const char* kernel, uint64_t count, uint32_t dims,
+                                qmc_bench_result* out, qmc_stream stream);
+
+/* Diagnostic: dense FP64 FMA throughput of this GPU (one wave of CTAs, 8
+ * independent DFMA chains per thread; 2 flops per DFMA), the roofline
+ * denominator of the render's FP64 integrand. Synchronous. */
+qmc_status qmc_fp64_probe(uint32_t iters, double* flops_per_second, qmc_stream stream);
+
+/* ------------------------------------------ multi-GPU render over NCCL
+ * The one collective of the path, inside the library. It
+ * replaces the reference's host worker pool (render.cpp:114-139) across
+ * GPUs. NCCL is loaded on first use (an already-loaded libnccl.so.2 is
+ * preferred; QMC_NCCL_LIBRARY=<path> overrides); without it these calls fail
+ * with QMC_NCCL. */
+typedef struct qmc_comm qmc_comm; /* wraps an ncclComm_t */
+#define QMC_COMM_UNIQUE_ID_BYTES 128
+
+typedef enum qmc_partition {
+    /* row bands of ceil(H / nranks) rows + one ncclAllGather of the fp32
+     * bands: every pixel keeps the one-GPU order (bit-identical image) */
+    QMC_PARTITION_ROWS = 0,
+    /* the paper's sample partition (rank r owns samples i == rev_2(r) mod
+     * nranks, imageplane.cpp:114-130) + one ncclAllReduce(sum) of the int64
+     * accumulators + finalize: int accumulator, power-of-two rank count,
+     * bit-identical to the one-GPU int render */
+    QMC_PARTITION_SAMPLES = 1
+} qmc_partition;
+
+/* ncclGetVersion of the NCCL the library bound. */
+qmc_status qmc_nccl_version(int* version);
+/* ncclGetUniqueId into id[QMC_COMM_UNIQUE_ID_BYTES] (rank 0; the caller
+ * ships it to the other ranks over its own transport). */
+qmc_status qmc_comm_unique_id(void* id);
+/* ncclCommInitRank on the calling thread's current device. */
+qmc_status qmc_comm_init_rank(const void* id, int nranks, int rank, qmc_comm** out);
+/* ncclCommInitAll: one communicator per device of this process, out[n]. */
+qmc_status qmc_comm_init_all(const int* devices, int n, qmc_comm** out);
+/* Borrows an existing ncclComm_t (not destroyed by qmc_comm_destroy). */
+qmc_status qmc_comm_from_nccl(void* nccl_comm, qmc_comm** out);
+qmc_status qmc_comm_info(const qmc_comm* comm, int* rank, int* nranks, int* device);
+void qmc_comm_destroy(qmc_comm* comm);
+
+/* render(job) by every rank of `comm` (collective: all ranks call it with
+ * the same job): this rank's share, then the collective, on `stream`; the
+ * whole [height][width] image lands in `out` (device memory of the
+ * communicator's GPU) on every rank. Asynchronous like qmc_render. */
+qmc_status qmc_render_nccl(const qmc_render_job* job, const qmc_comm* comm, qmc_partition mode,
+                           float* out, qmc_stream stream);
+/* The same across `devices` of one process (ncclCommInitAll, one NCCL group
+ * call for the collectives); the image goes to `out` (HOST memory). Devices
+ * must be distinct (an NCCL communicator holds each GPU once). */
+qmc_status qmc_render_nccl_devices(const qmc_render_job* job, const int* devices,
+                                   uint32_t n_devices, qmc_partition mode, float* out);
+
 /* scene_value (render.cpp:17-26) evaluated on the device for n (x, y)
  * pairs (device or host arrays of doubles) — integrand parity probe. */
 qmc_status qmc_scene_value(const double* xy, double* out, uint64_t n, qmc_stream stream);

@@ -340,6 +340,29 @@ inline ImageBuffer render_samples_devices(const RenderJob& job, const std::vecto
     return img;
 }
 
+// render(job) across distinct GPUs of this process over NCCL, inside the
+// library (qmc_render_nccl_devices): row bands + ncclAllGather
+// (QMC_PARTITION_ROWS) or the sample partition + int64 ncclAllReduce
+// (QMC_PARTITION_SAMPLES, int accumulator). Host image.
+inline ImageBuffer render_nccl_devices(const RenderJob& job, const std::vector<int>& devices,
+                                       qmc_partition mode = QMC_PARTITION_ROWS)
+{
+    qmc_render_job j{};
+    j.width = job.width;
+    j.height = job.height;
+    j.spp = job.spp;
+    j.kind = job.kind;
+    j.accum = job.accum;
+    j.seed = job.seed;
+    j.generator = job.generator.g.empty() ? nullptr : job.generator.g.data();
+    j.generator_dims = job.generator.dims();
+    ImageBuffer img{job.width, job.height,
+                    std::vector<float>(static_cast<size_t>(job.width) * job.height)};
+    check(qmc_render_nccl_devices(&j, devices.data(), static_cast<std::uint32_t>(devices.size()),
+                                  mode, img.values.data()));
+    return img;
+}
+
 inline qmc_sampler_kind sampler_kind_from_name(const std::string& name)
 {
     qmc_sampler_kind k{};

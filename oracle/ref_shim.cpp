@@ -425,6 +425,35 @@ int ref_integrate(const char* kind, std::uint32_t dims, std::uint32_t seed, cons
             qmc::integrate(s, f, n, qmc::accum_mode_from_name(accum), workers).estimate;
     });
 }
+// integrate over a Sobol' stream with caller direction numbers (any dims the
+// text defines; parse_direction_numbers + build_matrices, digitalnet.cpp:23-109).
+int ref_integrate_sobol_text(const char* text, std::uint32_t dims, const char* integrand,
+                             std::uint64_t n, const char* accum, std::uint32_t workers,
+                             double* estimate)
+{
+    return guard([&] {
+        qmc::StreamParams p;
+        p.dims = dims;
+        p.matrices = std::make_shared<qmc::GeneratorMatrixSet>(
+            qmc::build_matrices(qmc::parse_direction_numbers(std::string(text)), dims));
+        const qmc::SampleStream s = qmc::make_stream(qmc::SamplerKind::sobol, std::move(p));
+        const auto f = qmc::builtin_integrand(integrand, dims);
+        *estimate =
+            qmc::integrate(s, f, n, qmc::accum_mode_from_name(accum), workers).estimate;
+    });
+}
+// CPU float radical inverse fill through the public API (qmc::radical_inverse,
+// radical.cpp:210-213) on `threads` threads — config C1's timed CPU baseline.
+int ref_radical_fill(std::uint64_t first, std::uint64_t n, std::uint32_t prime_index, float* out,
+                     int threads)
+{
+    return guard([&] {
+        parallel_ranges(n, threads, [&](std::uint64_t b, std::uint64_t e) {
+            for (std::uint64_t k = b; k < e; ++k)
+                out[k] = qmc::radical_inverse(static_cast<std::uint32_t>(first + k), prime_index);
+        });
+    });
+}
 int ref_l2_star(const float* pts, std::uint64_t n, std::uint32_t dims, double* out)
 {
     return guard([&] {

@@ -38,7 +38,7 @@ __all__ = [
     "render_finalize", "load_generator_vector", "load_linear_factors", "fnv1a64", "write_pnm",
     "write_points_csv", "hilbert_index", "hilbert_xy", "hilbert_phi3_fixed", "digit_reverse", "lattice_shift_fixed",
     "integrate_partials", "reduce_deterministic", "render_devices", "render_samples_devices", "sampler_kind_name", "status_string",
-    "SAMPLER_KINDS",
+    "SAMPLER_KINDS", "run_bench_kernel", "fp64_probe", "Comm", "nccl_version", "render_nccl", "render_nccl_devices",
 ]
 
 
@@ -72,6 +72,11 @@ class RenderJob(C.Structure):
 
 class IntegrationRow(C.Structure):
     _fields_ = [("n", u64), ("estimate", f64), ("abs_error", f64), ("seconds", f64)]
+
+
+class BenchResult(C.Structure):
+    _fields_ = [("evaluations", u64), ("seconds", f64), ("components_per_second", f64),
+                ("checksum", u64)]
 
 
 class HaltonEnumeration(C.Structure):
@@ -158,6 +163,17 @@ def lib():
     sig("qmc_builtin_integrand", i32, C.c_char_p, u32, C.POINTER(i32), C.POINTER(f64))
     sig("qmc_integrate", i32, i32, C.POINTER(StreamParams), i32, u32, u64, i32,
         C.POINTER(IntegrationRow), P)
+    sig("qmc_run_bench_kernel", i32, C.c_char_p, u64, u32, C.POINTER(BenchResult), P)
+    sig("qmc_fp64_probe", i32, u32, C.POINTER(f64), P)
+    sig("qmc_nccl_version", i32, C.POINTER(i32))
+    sig("qmc_comm_unique_id", i32, P)
+    sig("qmc_comm_init_rank", i32, P, i32, i32, C.POINTER(P))
+    sig("qmc_comm_init_all", i32, P, i32, P)
+    sig("qmc_comm_from_nccl", i32, P, C.POINTER(P))
+    sig("qmc_comm_info", i32, P, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32))
+    sig("qmc_comm_destroy", None, P)
+    sig("qmc_render_nccl", i32, C.POINTER(RenderJob), P, i32, P, P)
+    sig("qmc_render_nccl_devices", i32, C.POINTER(RenderJob), P, u32, i32, P)
     _lib = L
     return L
 
@@ -845,4 +861,155 @@ def scene_value(xy, out=None, stream=None):
         torch = _torch()
         out = torch.empty(xy.shape[0], dtype=torch.float64, device=xy.device) if out is None else out
     _check(lib().qmc_scene_value(_ptr(xy), _ptr(out), xy.shape[0], _stream(stream)))
+    return out
+
+
+def run_bench_kernel(kernel: str, count: int, dims: int, stream=None) -> dict:
+    """run_bench_kernel (bench.cpp:79-150) on the device: the BenchResult
+    fields; `checksum` equals the reference's for the same arguments."""
+    r = BenchResult()
+    _check(lib().qmc_run_bench_kernel(kernel.encode(), count, dims, C.byref(r), _stream(stream)))
+    return {"kernel": kernel, "evaluations": r.evaluations, "seconds": r.seconds,
+            "components_per_second": r.components_per_second, "checksum": r.checksum}
+
+
+def fp64_probe(iters: int = 4096, stream=None) -> float:
+    """Measured dense FP64 FMA throughput of the current GPU, flop/s."""
+    v = f64()
+    _check(lib().qmc_fp64_probe(iters, C.byref(v), _stream(stream)))
+    return v.value
+
+
+# ------------------------------------------------ multi-GPU render over NCCL
+_PARTITION = {"rows": 0, "samples": 1}
+
+
+def _prefer_process_nccl() -> None:
+    """Point the library's lazy NCCL load at the copy PyTorch uses (the
+    nvidia-nccl wheel), so one process never maps two NCCL builds; an explicit
+    QMC_NCCL_LIBRARY wins."""
+    if os.environ.get("QMC_NCCL_LIBRARY"):
+        return
+    try:
+        import nvidia.nccl as nn
+
+        for base in nn.__path__:
+            cand = os.path.join(base, "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["QMC_NCCL_LIBRARY"] = cand
+                return
+    except ImportError:
+        pass
+
+
+def nccl_version() -> int:
+    """NCCL_VERSION_CODE of the NCCL the library bound (e.g. 22809)."""
+    _prefer_process_nccl()
+    v = i32()
+    _check(lib().qmc_nccl_version(C.byref(v)))
+    return v.value
+
+
+class Comm:
+    """An NCCL communicator owned by libqmcgpu (qmc_comm)."""
+
+    def __init__(self, handle: int):
+        self._h = handle
+
+    @staticmethod
+    def unique_id() -> bytes:
+        """ncclGetUniqueId (rank 0), to ship to the other ranks."""
+        _prefer_process_nccl()
+        buf = C.create_string_buffer(128)
+        _check(lib().qmc_comm_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def init_rank(cls, uid: bytes, nranks: int, rank: int) -> "Comm":
+        """ncclCommInitRank on the current CUDA device."""
+        _prefer_process_nccl()
+        if len(uid) != 128:
+            raise ValueError("unique id must be 128 bytes")
+        h = P()
+        _check(lib().qmc_comm_init_rank(C.c_char_p(uid), nranks, rank, C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def init_all(cls, devices) -> list:
+        """ncclCommInitAll: one communicator per device of this process."""
+        _prefer_process_nccl()
+        devs = np.ascontiguousarray(devices, dtype=np.int32)
+        hs = (P * max(devs.size, 1))()
+        _check(lib().qmc_comm_init_all(devs.ctypes.data, devs.size, hs))
+        return [cls(hs[k]) for k in range(devs.size)]
+
+    @classmethod
+    def from_torch_group(cls, group=None) -> "Comm":
+        """A library communicator spanning the ranks of a torch.distributed
+        group: rank 0's unique id travels over the group, then every rank
+        calls ncclCommInitRank on its current device."""
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls.init_rank(obj[0], world, rank)
+
+    def info(self):
+        r, n, d = i32(), i32(), i32()
+        _check(lib().qmc_comm_info(self._h, C.byref(r), C.byref(n), C.byref(d)))
+        return {"rank": r.value, "nranks": n.value, "device": d.value}
+
+    @property
+    def handle(self) -> int:
+        return self._h
+
+    def destroy(self) -> None:
+        if self._h:
+            lib().qmc_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:  # pragma: no cover - interpreter teardown
+            pass
+
+
+def render_nccl(width: int, height: int, spp: int, comm: Comm, mode: str = "rows",
+                kind: str = "pixel-shifted-lattice", accum: str = "kahan", seed: int = 0,
+                generator=None, matrices: Optional[GeneratorMatrixSet] = None,
+                tables: Optional[XorTables] = None, out=None, stream=None):
+    """render(RenderJob) by every rank of `comm` (qmc_render_nccl): row bands +
+    ncclAllGather ("rows") or the paper's sample partition + int64
+    ncclAllReduce ("samples", int accumulator). Every rank gets the whole
+    [height, width] float32 image on its device."""
+    if mode not in _PARTITION:
+        raise ValueError("mode must be 'rows' or 'samples'")
+    job, keep = _render_job(width, height, spp, kind, accum, seed, generator, matrices, tables)
+    if out is None:
+        torch = _torch()
+        out = torch.empty((height, width), dtype=torch.float32, device="cuda")
+    _check_out(out, height * width, "float32")
+    _check(lib().qmc_render_nccl(C.byref(job), comm.handle, _PARTITION[mode], _ptr(out),
+                                 _stream(stream)))
+    return out
+
+
+def render_nccl_devices(width: int, height: int, spp: int, devices, mode: str = "rows",
+                        kind: str = "pixel-shifted-lattice", accum: str = "kahan", seed: int = 0,
+                        generator=None, matrices: Optional[GeneratorMatrixSet] = None,
+                        tables: Optional[XorTables] = None, out=None) -> np.ndarray:
+    """The NCCL render across distinct `devices` of this process
+    (qmc_render_nccl_devices); returns the host [height, width] image."""
+    if mode not in _PARTITION:
+        raise ValueError("mode must be 'rows' or 'samples'")
+    _prefer_process_nccl()
+    job, keep = _render_job(width, height, spp, kind, accum, seed, generator, matrices, tables)
+    devs = np.ascontiguousarray(devices, dtype=np.int32)
+    if out is None:
+        out = np.empty((height, width), np.float32)
+    _check_out(out, height * width, "float32")
+    _check(lib().qmc_render_nccl_devices(C.byref(job), devs.ctypes.data, devs.size,
+                                         _PARTITION[mode], _ptr(out)))
     return out

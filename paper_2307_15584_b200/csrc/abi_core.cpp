@@ -176,6 +176,7 @@ int qmc_abi_version(void) { return QMCGPU_ABI_VERSION; }
 qmc_status qmc_map_u32_to_unifloat(const uint32_t* in, float* out, uint64_t n, qmc_stream stream)
 {
     return guard([&] {
+        const NvtxRange nvtx("qmc_map_u32_to_unifloat");
         if (n == 0)
             return;
         const cudaStream_t s = as_stream(stream);
@@ -434,6 +435,7 @@ qmc_status qmc_sobol_fill(const qmc_matrices* m, uint64_t first_index, uint64_t 
                           void* out, qmc_stream stream)
 {
     return guard([&] {
+        const NvtxRange nvtx("qmc_sobol_fill");
         sobol_fill_impl(const_cast<qmc_matrices*>(m), first_index, n, dims, scramble, words, kind,
                         out, as_stream(stream));
     });
@@ -481,6 +483,7 @@ qmc_status qmc_halton_fill(uint64_t first_index, uint64_t n, uint32_t dims,
                            qmc_output kind, void* out, qmc_stream stream)
 {
     return guard([&] {
+        const NvtxRange nvtx("qmc_halton_fill");
         if (dims > kPrimes)
             fail(QMC_INVALID_ARGUMENT, "halton_point: dims beyond the prime table");
         halton_fill_impl(first_index, n, dims, 0, scramble, factors, kind, out,
@@ -493,6 +496,7 @@ qmc_status qmc_radical_inverse_fill(uint64_t first_index, uint64_t n, uint32_t p
                                     qmc_output kind, void* out, qmc_stream stream)
 {
     return guard([&] {
+        const NvtxRange nvtx("qmc_radical_inverse_fill");
         prime_at(prime_index); // out_of_range like prime()
         halton_fill_impl(first_index, n, 1, prime_index, scramble, &factor, kind, out,
                          as_stream(stream));
@@ -526,6 +530,7 @@ qmc_status qmc_lattice_fill(const uint32_t* g, const uint32_t* shifts, uint32_t 
                             qmc_stream stream)
 {
     return guard([&] {
+        const NvtxRange nvtx("qmc_lattice_fill");
         lattice_fill_impl(g, shifts, dims, first_index, n, kind, out, as_stream(stream));
     });
 }
@@ -705,6 +710,7 @@ qmc_status qmc_stream_fill(qmc_sampler_kind kind, const qmc_stream_params* p,
                            qmc_stream stream)
 {
     return guard([&] {
+        const NvtxRange nvtx("qmc_stream_fill");
         const cudaStream_t s = as_stream(stream);
         if (!p)
             fail(QMC_INVALID_ARGUMENT, "stream params are null");
@@ -803,8 +809,6 @@ void integrate_chunks(qmc_sampler_kind kind, const qmc_stream_params* p, qmc_int
         fail(QMC_INVALID_ARGUMENT, "stream params are null");
     if (p->dims < f_dims)
         fail(QMC_INVALID_ARGUMENT, "integrate: stream has fewer dimensions than the integrand");
-    if (f_dims > integrate_max_dims())
-        fail(QMC_INVALID_ARGUMENT, "integrate: at most 64 integrand dimensions on the device");
     const uint64_t chunks = (n + 4095) / 4096;
     if (c0 > c1 || c1 > chunks)
         fail(QMC_OUT_OF_RANGE, "integrate: chunk range outside [0, ceil(n / 4096))");
@@ -887,6 +891,7 @@ qmc_status qmc_integrate(qmc_sampler_kind kind, const qmc_stream_params* p,
                          qmc_integration_row* row, qmc_stream stream)
 {
     return guard([&] {
+        const NvtxRange nvtx("qmc_integrate");
         const auto t0 = std::chrono::steady_clock::now();
         std::vector<double> partials;
         long long isum = 0;
@@ -916,6 +921,7 @@ qmc_status qmc_integrate_partials(qmc_sampler_kind kind, const qmc_stream_params
                                   double* partials, int64_t* int_sum, qmc_stream stream)
 {
     return guard([&] {
+        const NvtxRange nvtx("qmc_integrate_partials");
         if (mode == QMC_ACCUM_KAHAN && !partials && chunk_end > chunk_begin)
             fail(QMC_INVALID_ARGUMENT, "partials pointer is null");
         if (mode == QMC_ACCUM_INT && !int_sum)
@@ -1062,6 +1068,7 @@ qmc_status qmc_l2_star_discrepancy(const float* points, uint64_t n, uint32_t dim
                                    qmc_stream stream)
 {
     return guard([&] {
+        const NvtxRange nvtx("qmc_l2_star_discrepancy");
         if (n == 0 || dims == 0)
             fail(QMC_INVALID_ARGUMENT, "l2_star_discrepancy: empty point set");
         if (!points || !out)
@@ -1074,6 +1081,7 @@ qmc_status qmc_min_toroidal_distance(const float* points, uint64_t n, uint32_t d
                                      qmc_stream stream)
 {
     return guard([&] {
+        const NvtxRange nvtx("qmc_min_toroidal_distance");
         if (n < 2)
             fail(QMC_INVALID_ARGUMENT, "min_toroidal_distance: need at least two points");
         if (!points || !out)

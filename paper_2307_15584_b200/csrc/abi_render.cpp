@@ -111,6 +111,7 @@ qmc_status qmc_render(const qmc_render_job* job, uint32_t row_begin, uint32_t ro
                       qmc_stream stream)
 {
     return guard([&] {
+        const NvtxRange nvtx("qmc_render");
         const cudaStream_t s = as_stream(stream);
         CallArgs args(s);
         ResolvedRender rr;
@@ -139,6 +140,7 @@ qmc_status qmc_render_partial(const qmc_render_job* job, uint32_t part, uint32_t
                               qmc_stream stream)
 {
     return guard([&] {
+        const NvtxRange nvtx("qmc_render_partial");
         const cudaStream_t s = as_stream(stream);
         if (job && job->accum != QMC_ACCUM_INT)
             fail(QMC_INVALID_ARGUMENT,
@@ -167,6 +169,7 @@ qmc_status qmc_render_finalize(const int64_t* accum, uint64_t npix, uint32_t spp
                                qmc_stream stream)
 {
     return guard([&] {
+        const NvtxRange nvtx("qmc_render_finalize");
         if (spp == 0)
             fail(QMC_CONFIG, "render: spp must be >= 1");
         if (npix == 0)
@@ -183,6 +186,7 @@ qmc_status qmc_render_devices(const qmc_render_job* job, const int* devices, uin
                               float* out)
 {
     return guard([&] {
+        const NvtxRange nvtx("qmc_render_devices");
         if (!job)
             fail(QMC_INVALID_ARGUMENT, "render job is null");
         if (!devices || n_devices == 0)
@@ -260,6 +264,7 @@ qmc_status qmc_render_samples_devices(const qmc_render_job* job, const int* devi
                                       uint32_t n_devices, float* out)
 {
     return guard([&] {
+        const NvtxRange nvtx("qmc_render_samples_devices");
         if (!job)
             fail(QMC_INVALID_ARGUMENT, "render job is null");
         if (job->accum != QMC_ACCUM_INT)

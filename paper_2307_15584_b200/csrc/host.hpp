@@ -17,6 +17,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "device.cuh" // RadicalDim (host-visible layout)
 #include "internal.hpp"
@@ -157,6 +158,24 @@ int current_device();
 void pool_keep_memory();
 bool is_device_pointer(const void* p);
 inline cudaStream_t as_stream(qmc_stream s) { return static_cast<cudaStream_t>(s); }
+
+// NVTX range around a C-ABI entry point (SURVEY §5 tracing): visible in
+// Nsight Systems / ncu --nvtx; header-only NVTX3, no cost without a tool.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
+// RAII: restores the calling thread's current device.
+struct DeviceRestoreGuard {
+    int prev = 0;
+    DeviceRestoreGuard() { cuda_ok(cudaGetDevice(&prev), "cudaGetDevice"); }
+    ~DeviceRestoreGuard() { cudaSetDevice(prev); }
+    DeviceRestoreGuard(const DeviceRestoreGuard&) = delete;
+    DeviceRestoreGuard& operator=(const DeviceRestoreGuard&) = delete;
+};
 
 // Small per-call parameter arrays, uploaded with one stream-ordered copy
 // and released stream-ordered after the launches.

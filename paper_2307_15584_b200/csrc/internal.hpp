@@ -117,6 +117,25 @@ struct IntegrateParams {
     uint64_t chunk0, nchunks; // this launch: 4096-index chunks [chunk0, chunk0 + nchunks)
 };
 
+// run_bench_kernel (bench.cpp:79-150) on the device: kernel ids, and the
+// tables the components read.
+enum BenchKind : uint32_t {
+    QMC_BENCH_SOBOL = 0,
+    QMC_BENCH_HALTON = 1,
+    QMC_BENCH_HALTON_TABLED = 2,
+    QMC_BENCH_LATTICE = 3,
+    QMC_BENCH_PIXEL_SHIFTED_LATTICE = 4,
+    QMC_BENCH_PIXEL_RANDOM_LATTICE = 5,
+};
+struct BenchParams {
+    uint64_t count;
+    uint32_t dims, kind;
+    const uint32_t* colsT; // sobol: device [52][dims]
+    const void* rd;        // halton kinds: device RadicalDim[dims]
+    const uint32_t* g;     // lattice kinds: device generator vector
+    const uint32_t* tab3;  // phi_3 7-digit table (pixel shift)
+};
+
 // ------------------------------------------------------------ launchers
 // All launchers write DEVICE memory and are asynchronous on `s`.
 cudaError_t launch_map(const uint32_t* in, float* out, uint64_t n, cudaStream_t s);
@@ -167,7 +186,6 @@ cudaError_t launch_write_probe(void* out, uint64_t bytes, int mode, cudaStream_t
 // (int); bad: first index with a non-finite integrand value (~0 if none).
 cudaError_t launch_integrate(const IntegrateParams& p, uint32_t accum, double* partial,
                              unsigned long long* isum, unsigned long long* bad, cudaStream_t s);
-uint32_t integrate_max_dims();
 
 // Quality metrics (quality.cpp:76-156). scratch: device, 2n doubles.
 cudaError_t launch_l2star(const float* pts, uint64_t n, uint32_t dims, double* scratch,
@@ -177,6 +195,13 @@ cudaError_t launch_mindist(const float* pts, uint64_t n, uint32_t dims, double* 
 cudaError_t launch_stratification(const float* v, uint32_t m, uint32_t dims, uint32_t j,
                                   uint32_t* hist, unsigned int* bad, cudaStream_t s);
 uint32_t quality_max_dims();
+
+// result: device u64, zeroed by the caller; receives the Sink checksum.
+cudaError_t launch_bench(const BenchParams& p, unsigned long long* result, cudaStream_t s);
+// FP64 probe: threads = one full wave of resident CTAs; out has `threads` doubles.
+uint64_t fp64_probe_threads();
+cudaError_t launch_fp64_probe(double* out, uint64_t threads, uint32_t iters, cudaStream_t s);
+uint64_t fp64_probe_flops(uint64_t threads, uint32_t iters);
 
 // Number of SMs of the current device (cached).
 int sm_count();

@@ -17,7 +17,12 @@ namespace qmcgpu {
 
 namespace {
 
-constexpr uint32_t kMaxDims = 64; // local sample-state capacity per thread
+// Per-dimension incremental state (Sobol' register/local words, Halton
+// quotient-table records) covers the first kStateDims integrand dimensions;
+// dimensions beyond take the direct per-sample form (Sobol': XOR of the
+// columns of the index's set bits; Halton: the digit loop), so any dims the
+// stream allows integrate (quality.cpp:214-282 has no cap).
+constexpr uint32_t kStateDims = 64;
 // Threads per chunk CTA: 256 (16 samples per thread) for every kind but
 // Sobol', whose per-thread state array (local memory) prefers 128 threads.
 template <uint32_t KIND>
@@ -30,6 +35,16 @@ struct ChunkShape {
 constexpr int kBlockMax = 256;
 
 __device__ __forceinline__ uint32_t rad2(uint32_t i) { return brev32(i & 0x7fffffffu); }
+
+// sobol_component_fixed (digitalnet.cpp:111-131) of dimension j at idx.
+__device__ __forceinline__ uint32_t sobol_direct(uint64_t idx, uint32_t j, const IntegrateParams& p)
+{
+    uint32_t x = p.words ? __ldg(p.words + j) : 0u;
+    for (uint32_t k = 0; idx; ++k, idx >>= 1)
+        if (idx & 1u)
+            x ^= __ldg(p.colsT + k * p.mdims + j);
+    return x;
+}
 
 __device__ __forceinline__ uint64_t digit_reverse3(uint64_t v, uint32_t digits)
 {
@@ -74,13 +89,14 @@ __global__ void __launch_bounds__(ChunkShape<KIND>::kBlock)
     __shared__ double vals[4096];
     constexpr uint32_t kBlock = ChunkShape<KIND>::kBlock, kLogBlock = ChunkShape<KIND>::kLogBlock;
     constexpr uint32_t kSteps = ChunkShape<KIND>::kSteps, kLogSteps = ChunkShape<KIND>::kLogSteps;
-    __shared__ uint32_t E[kLogSteps][kMaxDims]; // sobol: XOR of columns kLogBlock..+c
-    __shared__ uint32_t XB[kMaxDims];   // sobol: value of `begin` (scramble included)
+    __shared__ uint32_t E[kLogSteps][kStateDims]; // sobol: XOR of columns kLogBlock..+c
+    __shared__ uint32_t XB[kStateDims];   // sobol: value of `begin` (scramble included)
     __shared__ long long red[kBlockMax / 32];
     const uint64_t chunk = p.chunk0 + blockIdx.x;
     const uint64_t begin = chunk * 4096;
     const uint32_t count = static_cast<uint32_t>(p.n - begin < 4096 ? p.n - begin : 4096);
     const uint32_t dims = p.fdims;
+    const uint32_t sdims = dims < kStateDims ? dims : kStateDims; // dims with incremental state
     const uint32_t t = threadIdx.x;
     const PixelStreamParams& q = p.pix;
 
@@ -104,9 +120,9 @@ __global__ void __launch_bounds__(ChunkShape<KIND>::kBlock)
 
     // Sobol' state: x(begin + t + B m) = XB ^ X(t) ^ X(B m); m advances
     // with x ^= E[ctz(m+1)].
-    uint32_t sob[kMaxDims];
+    uint32_t sob[kStateDims];
     if (KIND == 0) {
-        for (uint32_t j = t; j < dims; j += kBlock) {
+        for (uint32_t j = t; j < sdims; j += kBlock) {
             uint32_t x = p.words ? p.words[j] : 0u;
             uint64_t b = begin;
             for (uint32_t k = 0; b; ++k, b >>= 1)
@@ -120,7 +136,7 @@ __global__ void __launch_bounds__(ChunkShape<KIND>::kBlock)
             }
         }
         __syncthreads();
-        for (uint32_t j = 0; j < dims; ++j) {
+        for (uint32_t j = 0; j < sdims; ++j) {
             uint32_t x = XB[j];
             for (uint32_t k = 0; k < kLogBlock; ++k)
                 if ((t >> k) & 1u)
@@ -133,12 +149,12 @@ __global__ void __launch_bounds__(ChunkShape<KIND>::kBlock)
     // in the fill-table blocks h0 and h0 + 1 of a dimension, its inverse is
     // the quotient-table form of the contiguous fill (device.cuh: hi_split):
     // one coalesced 8-B load and three integer ops instead of the digit loop.
-    __shared__ const uint2* HTAB[kMaxDims];
-    __shared__ uint32_t HG[kMaxDims], HLO[kMaxDims], HQ0[kMaxDims], HT0[kMaxDims], HQ1[kMaxDims],
-        HT1[kMaxDims];
+    __shared__ const uint2* HTAB[kStateDims];
+    __shared__ uint32_t HG[kStateDims], HLO[kStateDims], HQ0[kStateDims], HT0[kStateDims],
+        HQ1[kStateDims], HT1[kStateDims];
     if (KIND == 1 || KIND == 3) {
         const uint32_t ib = static_cast<uint32_t>(KIND == 3 ? block + begin : begin);
-        for (uint32_t j = t; j < dims; j += kBlock) {
+        for (uint32_t j = t; j < sdims; j += kBlock) {
             const RadicalDim& r = rd[j];
             const uint2* tab = nullptr;
             if (r.fqr && ib <= 0xffffffffu - count) {
@@ -176,9 +192,9 @@ __global__ void __launch_bounds__(ChunkShape<KIND>::kBlock)
             for (uint32_t j = 0; j < dims && alive; ++j) {
                 uint32_t x;
                 if (KIND == 0)
-                    x = sob[j];
+                    x = j < kStateDims ? sob[j] : sobol_direct(idx, j, p);
                 else if (KIND == 1 || KIND == 3) {
-                    const uint2* tab = HTAB[j];
+                    const uint2* tab = j < kStateDims ? HTAB[j] : nullptr;
                     if (tab) {
                         const uint32_t G = HG[j];
                         uint32_t lo = HLO[j] + local;
@@ -219,7 +235,7 @@ __global__ void __launch_bounds__(ChunkShape<KIND>::kBlock)
         }
         if (KIND == 0 && m + 1 < kSteps) {
             const uint32_t c = __ffs(static_cast<int>(m + 1)) - 1;
-            for (uint32_t j = 0; j < dims; ++j)
+            for (uint32_t j = 0; j < sdims; ++j)
                 sob[j] ^= E[c][j];
         }
     }
@@ -274,8 +290,6 @@ cudaError_t integrate_kind(const IntegrateParams& p, uint32_t accum, double* par
 }
 
 } // namespace
-
-uint32_t integrate_max_dims() { return kMaxDims; }
 
 cudaError_t launch_integrate(const IntegrateParams& p, uint32_t accum, double* partial,
                              unsigned long long* isum, unsigned long long* bad, cudaStream_t s)

@@ -8,6 +8,7 @@
 #include "qmcgpu.hpp"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <sstream>
@@ -117,6 +118,18 @@ int main(int argc, char** argv)
     const auto iimg = qmcgpu::render(ijob);
     const auto iimg4 = qmcgpu::render_samples_devices(ijob, {0, 0, 0, 0}); // fused reduction
     EXPECT(iimg4.values == iimg.values);
+    // the collective inside the library: NCCL communicator over device 0
+    // (world size 1 on a one-GPU box; every distinct GPU on a bigger one)
+    const int ndev = argc > 3 ? std::atoi(argv[3]) : 1;
+    std::vector<int> devs;
+    for (int d = 0; d < ndev && d < 8; ++d)
+        devs.push_back(d);
+    const auto nimg = qmcgpu::render_nccl_devices(job, devs, QMC_PARTITION_ROWS);
+    EXPECT(nimg.values == img.values);
+    if ((devs.size() & (devs.size() - 1)) == 0) {
+        const auto nimg2 = qmcgpu::render_nccl_devices(ijob, devs, QMC_PARTITION_SAMPLES);
+        EXPECT(nimg2.values == iimg.values);
+    }
     EXPECT(throws<qmcgpu::ConfigError>([] { qmcgpu::GeneratorMatrixSet::builtin(65); }));
     EXPECT(throws<std::invalid_argument>([&] { qmcgpu::sobol_points(m, (1ull << 52) - 1, 2, 4); }));
 

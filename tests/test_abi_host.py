@@ -305,3 +305,28 @@ def test_hilbert_phi3_fixed_vs_reference(ref, golden):
         q.hilbert_phi3_fixed(0, 0, 0)
     with pytest.raises(IndexError):
         q.hilbert_phi3_fixed(4, 0, 2)
+
+
+def test_nccl_loads_lazily_without_a_gpu():
+    """The library binds NCCL on first use (no link-time dependency): the
+    version query works here; communicator calls fail with a status, not a
+    crash, when no GPU is present."""
+    v = q.nccl_version()
+    assert v >= 22700, v
+    with pytest.raises((q.CudaError, RuntimeError)):
+        q.Comm.init_all([0])
+    with pytest.raises(ValueError):
+        q.Comm.init_rank(b"x" * 7, 1, 0)
+
+
+def test_render_output_validation():
+    """Caller-supplied render outputs are checked before the C-ABI writes
+    rows * width elements (dtype, size, contiguity)."""
+    with pytest.raises(ValueError):
+        q.render_devices(8, 4, 1, [0], out=np.empty((3, 8), np.float32))
+    with pytest.raises(ValueError):
+        q.render_devices(8, 4, 1, [0], out=np.empty((4, 8), np.float64))
+    with pytest.raises(ValueError):
+        q.render_samples_devices(8, 4, 1, [0], out=np.empty((8, 8), np.float32)[:, ::2])
+    with pytest.raises(ValueError):
+        q.render_nccl_devices(8, 4, 1, [0], out=np.empty(31, np.float32))

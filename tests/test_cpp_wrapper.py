@@ -35,6 +35,7 @@ def test_wrapper_runs_on_gpu(tmp_path, golden):
         pytest.skip("needs a GPU")
     exe = _build(tmp_path)
     r = subprocess.run([exe, golden["sobol_f32_65536x32_fnv"],
-                        golden["render64_spp16_fnv"]["pixel-shifted-lattice/kahan"]],
+                        golden["render64_spp16_fnv"]["pixel-shifted-lattice/kahan"],
+                        str(torch.cuda.device_count())],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr

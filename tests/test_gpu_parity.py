@@ -2,6 +2,7 @@
 reference build and the golden fixtures. Bit-exact for every integer / float
 point set; <= 1e-6 relative for the render (north_star tolerance)."""
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
@@ -1238,3 +1239,184 @@ def test_write_pnm_matches_reference(ref):
         assert ref.ref_write_pnm(ptr(host), 57, 31, p6, ptr(buf), C.byref(n)) == 0
         assert q.write_pnm(host, ch) == buf.tobytes()
         assert q.write_pnm(torch.from_numpy(host).cuda(), ch) == buf.tobytes()
+
+
+# ------------------------------------------ the collective inside the library
+def test_render_nccl_devices_world1_equals_render():
+    """qmc_render_nccl_devices on a one-GPU NCCL communicator
+    (ncclCommInitAll): row bands + ncclAllGather and the sample partition +
+    int64 ncclAllReduce reproduce the one-GPU render bit for bit."""
+    for kind in ("pixel-shifted-lattice", "image-plane-halton", "sobol"):
+        full = q.render(300, 77, 16, kind=kind).cpu().numpy()
+        np.testing.assert_array_equal(q.render_nccl_devices(300, 77, 16, [0], kind=kind), full)
+        ifull = q.render(300, 77, 16, kind=kind, accum="int").cpu().numpy()
+        got = q.render_nccl_devices(300, 77, 16, [0], mode="samples", kind=kind, accum="int")
+        np.testing.assert_array_equal(got, ifull)
+    with pytest.raises(ValueError):  # sample partitions need the int accumulator
+        q.render_nccl_devices(300, 77, 16, [0], mode="samples")
+    with pytest.raises(ValueError):
+        q.render_nccl_devices(300, 77, 16, [])
+
+
+def _comm_world1_worker(rank, port, out_path):
+    import torch
+
+    torch.cuda.set_device(0)
+    comm = q.Comm.init_rank(q.Comm.unique_id(), 1, 0)
+    info = comm.info()
+    a = q.render_nccl(3840, 2160, 4, comm).cpu().numpy()
+    b = q.render_nccl(3840, 2160, 4, comm, mode="samples", accum="int").cpu().numpy()
+    c = q.render_nccl(97, 31, 9, comm, kind="halton-hilbert").cpu().numpy()
+    comm.destroy()
+    np.savez(out_path, a=a, b=b, c=c, info=np.array([info["rank"], info["nranks"],
+                                                     info["device"]]))
+
+
+def test_render_nccl_comm_init_rank_world1(tmp_path):
+    """qmc_comm_unique_id + qmc_comm_init_rank + qmc_render_nccl in a fresh
+    process (the torchrun shape at world size 1): the 4K image equals the
+    one-GPU render bit for bit in both partition modes."""
+    import torch.multiprocessing as mp
+
+    out = str(tmp_path / "c.npz")
+    mp.spawn(_comm_world1_worker, args=(0, out), nprocs=1, join=True)
+    r = np.load(out)
+    assert list(r["info"]) == [0, 1, 0]
+    np.testing.assert_array_equal(r["a"], q.render(3840, 2160, 4).cpu().numpy())
+    np.testing.assert_array_equal(r["b"], q.render(3840, 2160, 4, accum="int").cpu().numpy())
+    np.testing.assert_array_equal(r["c"], q.render(97, 31, 9, kind="halton-hilbert").cpu().numpy())
+
+
+def _two_gpus():
+    import torch
+
+    return torch.cuda.device_count() >= 2
+
+
+@pytest.mark.skipif(not _two_gpus(), reason="needs >= 2 GPUs")
+def test_multi_gpu_renders_distinct_devices_4k():
+    """Distinct GPUs: the peer-atomic sample partition, the row
+    bands and the NCCL paths at 4K against the one-device render, including
+    a device count that does not divide the height (scratch all-gather)."""
+    import torch
+
+    n = torch.cuda.device_count()
+    devs = list(range(min(n, 8)))
+    pow2 = devs[: 1 << (len(devs).bit_length() - 1)]
+    full = q.render(3840, 2160, 8).cpu().numpy()
+    ifull = q.render(3840, 2160, 8, accum="int").cpu().numpy()
+    np.testing.assert_array_equal(q.render_devices(3840, 2160, 8, devs), full)
+    np.testing.assert_array_equal(q.render_samples_devices(3840, 2160, 8, pow2), ifull)
+    np.testing.assert_array_equal(q.render_nccl_devices(3840, 2160, 8, devs), full)
+    np.testing.assert_array_equal(
+        q.render_nccl_devices(3840, 2160, 8, pow2, mode="samples", accum="int"), ifull)
+    odd = q.render(3840, 2161, 8).cpu().numpy()
+    np.testing.assert_array_equal(q.render_nccl_devices(3840, 2161, 8, devs[:3] or devs), odd)
+
+
+# ------------------------------- run_bench_kernel (SPEC acceptance 9's walk)
+BENCH_KERNELS = ["sobol", "halton", "halton-tabled", "lattice", "pixel-shifted-lattice",
+                 "pixel-random-lattice"]
+
+
+@pytest.mark.parametrize("kernel", BENCH_KERNELS)
+def test_bench_kernel_checksums_vs_golden(golden, kernel):
+    """qmc_run_bench_kernel folds the same components in the same walk into
+    the same Sink checksum as the reference's run_bench_kernel
+    (bench.cpp:23-150): 65536 evaluations x 32 dims, golden from the
+    reference build."""
+    r = q.run_bench_kernel(kernel, 65536, 32)
+    assert "%016x" % r["checksum"] == golden["bench_checksums_65536x32"][kernel]
+    assert r["evaluations"] == 65536 and r["seconds"] > 0
+
+
+@pytest.mark.parametrize("kernel", BENCH_KERNELS)
+@pytest.mark.parametrize("count,dims", [(1, 1), (1000003, 7), (2621440, 32), (300001, 100)])
+def test_bench_kernel_vs_reference(ref, kernel, count, dims):
+    """Ragged counts (a partial last index), other dims and walks past one
+    128x128 tile (py wraps) against the reference build's checksum."""
+    import ctypes as C
+
+    if kernel == "sobol" and dims > 64:
+        with pytest.raises(q.ConfigError):
+            q.run_bench_kernel(kernel, count, dims)
+        return
+    cps, ck = C.c_double(), C.c_uint64()
+    assert ref.ref_run_bench_kernel(kernel.encode(), count, dims, C.byref(cps), C.byref(ck)) == 0
+    assert q.run_bench_kernel(kernel, count, dims)["checksum"] == ck.value
+
+
+def test_bench_kernel_errors():
+    with pytest.raises(q.ConfigError):
+        q.run_bench_kernel("nope", 10, 2)
+    with pytest.raises(q.ConfigError):
+        q.run_bench_kernel("lattice", 0, 2)
+    with pytest.raises(q.ConfigError):
+        q.run_bench_kernel("lattice", 10, 0)
+
+
+def test_fp64_probe_reports_a_plausible_peak():
+    tf = q.fp64_probe(2048) / 1e12
+    print("fp64 probe: %.2f TFLOP/s" % tf)
+    assert 5.0 < tf < 200.0
+
+
+# --------------------------------------------- integrate beyond 64 dimensions
+@pytest.mark.parametrize("kind,dims,integrand,accum", [
+    ("halton", 100, "product-poly", "kahan"),
+    ("halton", 100, "product-poly", "int"),
+    ("halton", 500, "product-poly", "kahan"),
+    ("halton", 500, "indicator", "int"),
+    ("lattice", 200, "product-poly", "kahan"),
+    ("lattice", 200, "indicator", "int"),
+])
+def test_integrate_high_dims_vs_reference(ref, kind, dims, integrand, accum):
+    """integrate() (quality.cpp:214-282) has no dimension cap: Halton at 100
+    and 500 dims (the first 64 dims on the quotient-table state, the rest on
+    the digit loop) and lattice at 200 dims equal the reference bit for bit."""
+    import ctypes as C
+
+    n = 3 * 4096 + 77
+    e = C.c_double()
+    assert ref.ref_integrate(kind.encode(), dims, 0, integrand.encode(), n, accum.encode(), 8,
+                             C.byref(e)) == 0
+    kw = {"generator": q.lfsr_generator_vector(0xACE1, dims)} if kind == "lattice" else {}
+    row = q.integrate(kind, integrand, n, dims, accum, **kw)
+    assert row["estimate"] == e.value, (row["estimate"], e.value)
+
+
+def _direction_text(dims, seed=5):
+    """A valid direction-number file (the builtin 63 Joe-Kuo rows, then
+    synthetic rows obeying parse_direction_numbers' grammar)."""
+    import json
+
+    rows = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))[
+        "direction_numbers"]
+    rng = np.random.default_rng(seed)
+    lines = ["d s a m_i"]
+    for d in range(2, dims + 1):
+        if d - 2 < len(rows):
+            _, s, a, ms = rows[d - 2]
+        else:
+            s = int(rng.integers(3, 12))
+            a = int(rng.integers(0, 1 << (s - 1)))
+            ms = [int(rng.integers(0, 1 << (k - 1))) * 2 + 1 for k in range(1, s + 1)]
+        lines.append(" ".join(str(v) for v in [d, s, a] + list(ms)))
+    return "\n".join(lines) + "\n"
+
+
+@pytest.mark.parametrize("accum", ["kahan", "int"])
+def test_integrate_sobol_beyond_64_dims_vs_reference(ref, accum):
+    """Sobol' integration over caller direction numbers with 130 dims: the
+    first 64 on the incremental state, the rest XOR the columns per sample —
+    bit for bit with the reference."""
+    import ctypes as C
+
+    dims, n = 130, 2 * 4096 + 5
+    text = _direction_text(dims)
+    e = C.c_double()
+    assert ref.ref_integrate_sobol_text(text.encode(), dims, b"product-poly", n, accum.encode(), 8,
+                                        C.byref(e)) == 0, ref.ref_last_error()
+    m = q.GeneratorMatrixSet.from_text(text, dims)
+    row = q.integrate("sobol", "product-poly", n, dims, accum, matrices=m)
+    assert row["estimate"] == e.value, (row["estimate"], e.value)
