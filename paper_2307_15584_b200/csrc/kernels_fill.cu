@@ -1458,6 +1458,23 @@ __global__ void __launch_bounds__(1024, 1)
 
 // ------------------------------------------------------------- launching
 
+// Lets `kernel` launch with any dynamic shared memory size the device allows
+// (the opt-in maximum). The attribute is per function and process-wide, so
+// it is set to one fixed value: setting it to each call's own size raced
+// between host threads launching the same kernel with different sizes (one
+// thread's smaller setting made another's launch fail with invalid argument).
+template <typename K>
+cudaError_t allow_dynamic_smem(K kernel)
+{
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    const cudaError_t e =
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e != cudaSuccess)
+        return e;
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+}
+
 template <typename K>
 int blocks_per_sm(K kernel)
 {
@@ -1710,7 +1727,7 @@ bool launch_tma_fill(const W& w, uint32_t dims, const FillRange& r, cudaStream_t
                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
     const size_t smem = static_cast<size_t>(kRows) * 128 * kBufs + 1024;
-    *err = cudaFuncSetAttribute(k_tma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    *err = allow_dynamic_smem(k_tma<W>);
     if (*err != cudaSuccess)
         return true;
     const uint64_t nsub = (r.n + kRows - 1) / kRows;
@@ -1733,8 +1750,7 @@ cudaError_t launch_runs_fill(const W& w, uint32_t dims, const FillRange& r, cuda
     if (chunk < 32)
         chunk = 32;
     const size_t smem = (static_cast<size_t>(chunk) * ld * runs + runs * dims * 32) * 4;
-    const cudaError_t e = cudaFuncSetAttribute(k_runs<W, DPW>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    const cudaError_t e = allow_dynamic_smem(k_runs<W, DPW>);
     if (e != cudaSuccess)
         return e;
     const uint64_t nsub = (r.n + chunk - 1) / chunk;
@@ -1751,8 +1767,7 @@ cudaError_t launch_runs_wide(const W& w, uint32_t dims, const FillRange& r, cuda
     const uint32_t ld = dims | 1u;
     uint32_t chunk = (49152u / ld) & ~31u;
     const size_t smem = (static_cast<size_t>(chunk) * ld + 32 * 32 * DMAX) * 4;
-    const cudaError_t e = cudaFuncSetAttribute(k_runs_wide<W, DMAX>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    const cudaError_t e = allow_dynamic_smem(k_runs_wide<W, DMAX>);
     if (e != cudaSuccess)
         return e;
     const uint64_t nsub = (r.n + chunk - 1) / chunk;
@@ -1777,7 +1792,7 @@ bool launch_bulk_fill(const W& w, uint32_t dims, const FillRange& r, cudaStream_
     if (rows < 32)
         rows = 32;
     const size_t smem = static_cast<size_t>(rows) * dims * runs * nbuf * 4;
-    *err = cudaFuncSetAttribute(k_bulk<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    *err = allow_dynamic_smem(k_bulk<W>);
     if (*err != cudaSuccess)
         return true;
     const uint64_t nsub = (r.n + rows - 1) / rows;
@@ -1918,8 +1933,7 @@ cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const
                      : (mode == 2 ? (u32 ? k_sobol_tiled<2, true, kBlock> : k_sobol_tiled<2, false, kBlock>)
                                   : (u32 ? k_sobol_tiled<0, true, kBlock> : k_sobol_tiled<0, false, kBlock>));
     if (smem > 48 * 1024) {
-        const cudaError_t e =
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        const cudaError_t e = allow_dynamic_smem(kern);
         if (e != cudaSuccess)
             return e;
     }
@@ -2002,8 +2016,7 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
     auto kern = wide ? (u32 ? k_halton_tiled<true, 1024> : k_halton_tiled<false, 1024>)
                      : (u32 ? k_halton_tiled<true, kBlock> : k_halton_tiled<false, kBlock>);
     if (smem > 48 * 1024) {
-        const cudaError_t e =
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        const cudaError_t e = allow_dynamic_smem(kern);
         if (e != cudaSuccess)
             return e;
     }
