@@ -427,6 +427,16 @@ def measure_fill(name, fn, samples_per_step, steps, warmup, peak, stream, betwee
                                              "unit": "GB/s", "frac": gbs / peak}}
 
 
+def host_ram() -> str:
+    try:
+        import psutil
+
+        vm = psutil.virtual_memory()
+        return "%.0f GiB total, %.0f GiB available" % (vm.total / 2**30, vm.available / 2**30)
+    except Exception:
+        return "unknown"
+
+
 def host_bytes_ok(nbytes: int) -> bool:
     try:
         import psutil
@@ -521,7 +531,8 @@ def run_ours(args):
                "sample": "%d points x %d dims per rank per step into pinned host memory "
                          "(C-ABI qmc_sobol_fill, chunked D2H pipeline)%s"
                          % (e2e_pts, DIMS, "" if e2e_pts == N_POINTS else
-                            "; full 2^28 skipped: host RAM"),
+                            "; the full 2^28 x 32 (32 GiB pinned) skipped: host RAM %s"
+                            % host_ram()),
                "full_config": e2e_pts == N_POINTS}
         del host, hn
 
@@ -666,16 +677,17 @@ def run_extra(q, stream, peak, args):
 
     def c1():
         # van der Corput 2^24 x 1 (launch-bound parity config). Timed per
-        # launch with an untimed 256 MiB write between launches (L2 flush:
-        # the launch finds L2 full of other dirty lines); the CUDA-graph
-        # replay of 12 launches over 4 rotating buffers is reported beside it.
+        # launch with an untimed 512 MiB read between launches (L2 flush: the
+        # previous output is written back during the flush and the launch
+        # finds L2 full of clean lines); the CUDA-graph replay of 12 launches
+        # over 4 rotating buffers is reported beside it.
         n1 = 1 << 24
         o1 = [torch.empty(n1, dtype=torch.float32, device="cuda") for _ in range(4)]
-        flush = torch.empty(1 << 28, dtype=torch.uint8, device="cuda")
+        flush = torch.ones(1 << 27, dtype=torch.float32, device="cuda")
         r1 = measure_fill("vdc 2^24 x 1, one launch per step, L2 flushed between steps",
                           lambda: q.radical_inverse_fill(n1, 0, out=o1[0]), n1, 20, 5, peak,
-                          stream, between=lambda: q.write_probe(flush))
-        r1["l2"] = "256 MiB write (qmc_write_probe) before every timed launch"
+                          stream, between=lambda: flush.sum())
+        r1["l2"] = "512 MiB read (torch.sum) before every timed launch"
         g1 = torch.cuda.CUDAGraph()
         cap = torch.cuda.Stream()
         with torch.cuda.graph(g1, stream=cap):

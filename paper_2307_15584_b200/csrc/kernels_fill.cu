@@ -1459,20 +1459,25 @@ __global__ void __launch_bounds__(1024, 1)
 // ------------------------------------------------------------- launching
 
 // Lets `kernel` launch with any dynamic shared memory size the device allows
-// (the opt-in maximum). The attribute is per function and process-wide, so
-// it is set to one fixed value: setting it to each call's own size raced
-// between host threads launching the same kernel with different sizes (one
-// thread's smaller setting made another's launch fail with invalid argument).
+// (the opt-in maximum less the kernel's static shared memory). The attribute
+// is per function and process-wide, so it is set to one fixed value: setting
+// it to each call's own size raced between host threads launching the same
+// kernel with different sizes (one thread's smaller setting made another's
+// launch fail with invalid argument).
 template <typename K>
 cudaError_t allow_dynamic_smem(K kernel)
 {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
-    const cudaError_t e =
-        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (e != cudaSuccess)
         return e;
-    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    cudaFuncAttributes fa{};
+    e = cudaFuncGetAttributes(&fa, kernel);
+    if (e != cudaSuccess)
+        return e;
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                optin - static_cast<int>(fa.sharedSizeBytes));
 }
 
 template <typename K>
