@@ -745,6 +745,22 @@ qmc_status qmc_stream_fill(qmc_sampler_kind kind, const qmc_stream_params* p,
             fail(QMC_OUT_OF_RANGE, "xor_table_sample: index beyond the stored point set");
         if (n == 0)
             return;
+        if (kind == QMC_KIND_PIXEL_SHIFTED_LATTICE) {
+            // (brev(i) + shift) * g_j == brev(i) * g_j + shift * g_j (mod 2^32):
+            // the pixel's stream is the CP-rotated lattice with integer
+            // shifts s_j = shift * g_j (imageplane.hpp:26-31), so it takes
+            // the HBM-bound lattice fill
+            uint32_t shift = 0;
+            const qmc_status st = qmc_hilbert_phi3_fixed(p->px, p->py, p->order, &shift);
+            if (st != QMC_OK)
+                fail(st, last_error());
+            std::vector<uint32_t> sh(dims);
+            for (uint32_t j = 0; j < dims; ++j)
+                sh[j] = shift * p->generator[j];
+            lattice_fill_impl(p->generator, sh.data(), dims, first_index, n, out_kind, out, s);
+            cuda_ok(cudaStreamSynchronize(s), "sync");
+            return;
+        }
         if (kind == QMC_KIND_HALTON_HILBERT) {
             // sample(i, j) = halton_component(u32(block_start + i), j)
             // (imageplane.cpp:378, :439-442): the contiguous Halton fill

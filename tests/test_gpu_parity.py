@@ -1420,3 +1420,29 @@ def test_integrate_sobol_beyond_64_dims_vs_reference(ref, accum):
     m = q.GeneratorMatrixSet.from_text(text, dims)
     row = q.integrate("sobol", "product-poly", n, dims, accum, matrices=m)
     assert row["estimate"] == e.value, (row["estimate"], e.value)
+
+
+@pytest.mark.parametrize("dims", [1, 2, 3, 16, 32, 64, 300])
+@pytest.mark.parametrize("first", [0, (1 << 32) - 5000, (1 << 33) + 17])
+def test_pixel_shifted_lattice_stream_as_cp_lattice_vs_reference(ref, dims, first):
+    """The pixel-shifted lattice stream goes through the lattice fill with
+    integer shifts s_j = shift * g_j ((brev(i) + shift) * g_j mod 2^32,
+    imageplane.hpp:26-31): every dims path (fast 256-bit, generic, > 256 dims
+    device args), windows across the u32 index wrap, fixed and float — equal
+    to SampleStream::sample of the reference."""
+    px, py, order, n = 3001, 1777, 12, 9000
+    g = q.lfsr_generator_vector(0xACE1, max(dims, 2))
+    got = u32(q.stream_fill("pixel-shifted-lattice", n, dims, first=first, generator=g,
+                            pixel=(px, py), order=order)).reshape(n, dims)
+    exp = np.zeros((n, dims), np.uint32)
+    assert ref.ref_stream_fill(b"pixel-shifted-lattice", dims, 0, b"plain", px, py, order, 1, 0, 0,
+                               first, n, ptr(exp)) == 0, ref.ref_last_error()
+    np.testing.assert_array_equal(got, exp)
+    fx = u32(q.stream_fill("pixel-shifted-lattice", n, dims, first=first, generator=g,
+                           pixel=(px, py), order=order, fixed=True)).reshape(n, dims)
+    shift = q.hilbert_phi3_fixed(px, py, order)
+    i = (np.arange(first, first + n, dtype=np.uint64) & 0xFFFFFFFF).astype(np.uint32)
+    br = np.array([int("{:032b}".format(int(v))[::-1], 2) for v in i], np.uint64)
+    ga = np.array(g[:dims], np.uint64)
+    np.testing.assert_array_equal(
+        fx, (((br[:, None] + shift) & 0xFFFFFFFF) * ga[None, :] & 0xFFFFFFFF).astype(np.uint32))
