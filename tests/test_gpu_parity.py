@@ -1446,3 +1446,37 @@ def test_pixel_shifted_lattice_stream_as_cp_lattice_vs_reference(ref, dims, firs
     ga = np.array(g[:dims], np.uint64)
     np.testing.assert_array_equal(
         fx, (((br[:, None] + shift) & 0xFFFFFFFF) * ga[None, :] & 0xFFFFFFFF).astype(np.uint32))
+
+
+@pytest.mark.parametrize("mode", ["plain", "linear", "faure"])
+@pytest.mark.parametrize("first", [0, 3486784401 - (1 << 18), 2**31 - (1 << 18) - 3,
+                                   2**32 - (1 << 18) + 5, 2**33 + 5])
+def test_halton_fill_q4_long_runs_vs_reference(ref, mode, first):
+    """k_halton_q4 (dims % 32 == 0): 2^19 + 77 points x 32 dims carried
+    across sub-tiles, across the base-3 prime_max_power boundary, the base-2
+    2^31 reduction and the u32 index wrap (the per-sample fallback units)."""
+    n, dims = (1 << 19) + 77, 32
+    got = u32(q.halton_fill(n, dims, first=first, scramble=mode, fixed=True)).reshape(n, dims)
+    for j in range(dims):
+        b = q.prime(j)
+        exp = np.zeros(n, np.uint32)
+        assert ref.ref_radical_fixed_fill(first & 0xFFFFFFFF, n, j, _MODE[mode],
+                                          b - 1 if (mode == "linear" and b > 2) else 1,
+                                          ptr(exp)) == 0
+        np.testing.assert_array_equal(got[:, j], exp, err_msg=f"dim={j}")
+
+
+@pytest.mark.parametrize("dims", [64, 160])
+def test_halton_fill_q4_many_blocks_vs_reference(ref, dims):
+    """Column blocks past the first (bases up to 941 at 160 dims, fill tables
+    of one or two digits with G >= 257): every dimension against the
+    reference, f32 output through the map."""
+    n, first = 40000 + 3, 123456789
+    got = q.halton_fill(n, dims, first=first, scramble="linear").cpu().numpy().reshape(n, dims)
+    for j in range(dims):
+        b = q.prime(j)
+        exp = np.zeros(n, np.uint32)
+        assert ref.ref_radical_fixed_fill(first, n, j, 1, b - 1 if b > 2 else 1, ptr(exp)) == 0
+        mapped = np.zeros(n, np.uint32)
+        ref.ref_map_bulk(ptr(exp), ptr(mapped), n)
+        np.testing.assert_array_equal(got[:, j].view(np.uint32), mapped, err_msg=f"dim={j}")
