@@ -129,18 +129,7 @@ struct DigitTable {
     uint32_t group = 0;
     // with_quotients: {floor(T * 2^32 / group), T * 2^32 mod group} per entry
     const uint32_t* qr = nullptr;
-    // with_quotients: qx[lo] = floor(T[lo mod group] * 2^32 / group) for
-    // lo < group + kQxExt (the remainder is -qx * group mod 2^32)
-    const uint32_t* qx = nullptr;
 };
-
-// Extension of the quotient-only fill tables past `group` entries, so a
-// warp's run of positions lo .. lo + kQxExt - 1 (lo < group) reads one
-// contiguous span across the block boundary.
-constexpr uint32_t kQxExt = 256;
-// qx for base 2 (group 2^16, every scramble the identity): qx[lo] =
-// brev16(lo mod 2^16) << 16, on the current device
-const uint32_t* base2_fill_qx();
 
 // Widest b^d-entry table (b^d <= max_entries) inverting d >= min_digits
 // digits per step with the digit permutation of `mode`; cached per device.

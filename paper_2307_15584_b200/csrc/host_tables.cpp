@@ -276,7 +276,7 @@ DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor, uint32_t min_
                        uint32_t max_entries, bool with_quotients)
 {
     struct Slot {
-        DevPtr t, qr, qx;
+        DevPtr t, qr;
         uint32_t group = 0;
     };
     static std::mutex mu;
@@ -318,33 +318,12 @@ DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor, uint32_t min_
                 qr[2 * v + 1] = static_cast<uint32_t>(num % group);
             }
             slot.qr = dev_upload(qr.data(), qr.size() * 4);
-            std::vector<uint32_t> qx(group + kQxExt);
-            for (uint32_t v = 0; v < group + kQxExt; ++v)
-                qx[v] = qr[2 * (v % group)];
-            slot.qx = dev_upload(qx.data(), qx.size() * 4);
         }
         slot.t = dev_upload(t.data(), t.size() * 4);
         slot.group = group;
     }
     return {static_cast<const uint32_t*>(slot.t.get()), slot.group,
-            static_cast<const uint32_t*>(slot.qr.get()),
-            static_cast<const uint32_t*>(slot.qx.get())};
-}
-
-const uint32_t* base2_fill_qx()
-{
-    static std::mutex mu;
-    static std::map<int, DevPtr> cache;
-    const int dev = current_device();
-    std::lock_guard<std::mutex> lk(mu);
-    auto& slot = cache[dev];
-    if (!slot) {
-        std::vector<uint32_t> qx(65536 + kQxExt);
-        for (uint32_t v = 0; v < qx.size(); ++v)
-            qx[v] = brev_host(v & 0xffffu); // = brev16(v mod 2^16) << 16
-        slot = dev_upload(qx.data(), qx.size() * 4);
-    }
-    return static_cast<const uint32_t*>(slot.get());
+            static_cast<const uint32_t*>(slot.qr.get())};
 }
 
 const uint64_t* pow_magic(uint32_t b)
@@ -400,7 +379,6 @@ std::vector<RadicalDim> radical_dims(uint32_t dims, uint32_t first_prime, qmc_ra
         }
         r.ftable = nullptr;
         r.fqr = nullptr;
-        r.fqx = b == 2 ? base2_fill_qx() : nullptr;
         r.magic = nullptr;
         r.gdigits = r.fgroup = r.fdigits = r.himod = 0;
         r.fdivg = Div32{0, 0};
@@ -418,7 +396,6 @@ std::vector<RadicalDim> radical_dims(uint32_t dims, uint32_t first_prime, qmc_ra
             if (f.ptr) {
                 r.ftable = f.ptr;
                 r.fqr = reinterpret_cast<const uint2*>(f.qr);
-                r.fqx = f.qx;
                 r.fgroup = f.group;
                 r.fdivg = make_div32(f.group);
                 for (uint32_t g = f.group; g > 1; g /= b)

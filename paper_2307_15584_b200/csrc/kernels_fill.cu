@@ -1381,284 +1381,6 @@ __global__ void __launch_bounds__(1024, 1)
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-// Prime-base Halton with dims % 32 == 0, stored by TMA (k_halton_q4): per
-// 32-dimension column block, a CTA walks sub-tiles of kQ4Rows points. Warp w
-// owns dimensions 4g .. 4g + 3 (g = w & 7) of the block for the rows
-// [R q, R q + R) of a sub-tile (q = w >> 3, R = kQ4WarpRows); lane
-// (d = lane & 3, p = lane >> 2) computes dimension 4g + d at rows
-// R q + p + 8 s, s < kQ4Steps. In the 128-B swizzled sub-tile (exactly the output's
-// 128-B row segments) row & 7 == p, so a lane's 16-B chunk g lands at
-// chunk g ^ p of every row it writes: the 32 lanes hit 32 distinct banks
-// (the one-dimension-per-warp column store of k_tma is 4-way conflicted).
-//
-// Per sample: one entry of the dimension's quotient-only fill table qx
-// (RadicalDim::fqx, prefetched into registers a whole sub-tile ahead), then
-// x = qx + qa + (rT >= thr) with rT = -qx * G mod 2^32 (see HiRecord) —
-// one IMAD, a shift and an add — and the map. Every lane keeps the records
-// of its block h and of h + 1 (a lane's R positions cross at most one
-// block boundary, G >= 257); a record is rebuilt (hi_record) only when the
-// walk enters a new block.
-//
-// Thread 0 issues the TMA stores without waiting for the other warps: it
-// polls the sub-tiles' full barriers (test_wait) whenever it reaches a
-// buffer wait of its own, so warp 0 walks like every other warp.
-constexpr uint32_t kQ4Rows = 256;  // points per sub-tile (32 KB)
-constexpr uint32_t kQ4Bufs = 6;
-constexpr uint32_t kQ4Steps = 8;  // 8 rows per step
-constexpr uint32_t kQ4WarpRows = 8 * kQ4Steps; // a warp's rows of a sub-tile (kQ4Rows / 4)
-static_assert(kQ4WarpRows * 4 == kQ4Rows, "four row quarters per sub-tile");
-
-struct Q4Rec {
-    uint32_t qa1, thr; // qa + 1, thr
-};
-
-// Out of line: it runs once per block a lane enters (rare), and inlined its
-// digit loops' temporaries pushed the walk's prefetch registers to the stack.
-__device__ __noinline__ Q4Rec q4_record(uint32_t h, const RadicalDim* r)
-{
-    if (r->base == 2) // x = (brev16(lo) << 16) + brev32(h << 16), never a carry (thr = G)
-        return {brev32(h << 16) + 1u, 65536u};
-    uint32_t g0, mulg;
-    const HiRecord rec = hi_record(h, *r, g0, mulg);
-    return {rec.qa + 1u, rec.thr};
-}
-
-// A lane's walk of one dimension: table position lo of its first row, the
-// block h of that position and the records of h and h + 1.
-struct Q4Walk {
-    const uint32_t* qx;
-    uint32_t lo, G, h, himod;
-    Q4Rec r0, r1;
-};
-
-__device__ __forceinline__ uint32_t q4_next_block(const Q4Walk& w)
-{
-    return w.h + 1 == w.himod ? 0u : w.h + 1;
-}
-
-// Walk state at u32 index i (radical_inverse reduces i mod prime_max_power,
-// radical.cpp:133; base 2: brev32(i & 0x7fffffff)).
-__device__ __forceinline__ void q4_setup(Q4Walk& w, const RadicalDim& r, uint32_t i)
-{
-    w.qx = r.fqx;
-    if (r.base == 2) {
-        const uint32_t ir = i & 0x7fffffffu;
-        w.G = 65536u;
-        w.himod = 1u << 15;
-        w.h = ir >> 16;
-        w.lo = ir & 0xffffu;
-    } else {
-        const uint32_t ir = i - div32(i, r.divmp) * r.maxpow;
-        w.G = r.fgroup;
-        w.himod = r.himod;
-        w.h = div32(ir, r.fdivg);
-        w.lo = ir - w.h * w.G;
-    }
-    w.r0 = q4_record(w.h, &r);
-    w.r1 = q4_record(q4_next_block(w), &r);
-}
-
-// lo += step within the same contiguous index range (maxpow wraps included)
-__device__ __forceinline__ void q4_advance(Q4Walk& w, const RadicalDim& r, uint32_t step)
-{
-    w.lo += step;
-    while (w.lo >= w.G) {
-        w.lo -= w.G;
-        w.h = q4_next_block(w);
-        w.r0 = w.r1;
-        w.r1 = q4_record(q4_next_block(w), &r);
-    }
-}
-
-__device__ __forceinline__ bool mbar_test(uint32_t addr, uint32_t parity)
-{
-    uint32_t ok;
-    asm volatile("{\n\t.reg .pred p;\n\t"
-                 "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-                 "selp.u32 %0, 1, 0, p;\n\t}"
-                 : "=r"(ok)
-                 : "r"(addr), "r"(parity)
-                 : "memory");
-    return ok != 0;
-}
-
-template <bool U32OUT>
-__device__ __forceinline__ uint32_t q4_out(uint32_t x)
-{
-    return U32OUT ? x : map_bits(x);
-}
-
-template <bool U32OUT>
-__global__ void __launch_bounds__(1024, 1)
-    k_halton_q4(const __grid_constant__ CUtensorMap tmap, const RadicalDim* __restrict__ rd,
-                uint32_t ncb, uint64_t first, uint64_t n, uint64_t nsub)
-{
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    __shared__ __align__(8) uint64_t bars[2 * kQ4Bufs];
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    const uint32_t g = warp & 7u, quarter = warp >> 3, d = lane & 3u, p = lane >> 2;
-    const uint32_t base = (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + 1023u) & ~1023u;
-    const uint32_t bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
-    constexpr uint32_t kBufBytes = kQ4Rows * 128;
-    auto full = [&](uint32_t b) { return bar0 + 8 * b; };
-    auto empty = [&](uint32_t b) { return bar0 + 8 * (kQ4Bufs + b); };
-    if (threadIdx.x == 0) {
-        for (uint32_t b = 0; b < kQ4Bufs; ++b) {
-            mbar_init(full(b), 32);
-            mbar_init(empty(b), 1);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const uint32_t lane_off = (kQ4WarpRows * quarter + p) * 128u + ((g ^ p) << 4) + d * 4u;
-    const uint64_t units = nsub * ncb;
-    const uint64_t u0 = units * blockIdx.x / gridDim.x, u1 = units * (blockIdx.x + 1) / gridDim.x;
-    const bool issuer = threadIdx.x == 0;
-    uint64_t issued = u0; // issuer: the next unit whose store to issue
-
-    // issuer: store every finished sub-tile of units < upto, in order; after
-    // each store, the previous one has finished reading its buffer (it was
-    // issued a unit earlier) and that buffer is released
-    auto issue_ready = [&](uint64_t upto, bool block) {
-        while (issued < upto) {
-            const uint64_t v = issued - u0;
-            const uint32_t b = static_cast<uint32_t>(v % kQ4Bufs);
-            const uint32_t ph = static_cast<uint32_t>(v / kQ4Bufs) & 1u;
-            if (block)
-                mbar_wait(full(b), ph);
-            else if (!mbar_test(full(b), ph))
-                return;
-            const uint64_t vu = issued;
-            const uint32_t vcb = static_cast<uint32_t>(vu / nsub);
-            const uint64_t vp0 = (vu - static_cast<uint64_t>(vcb) * nsub) * kQ4Rows;
-            for (uint32_t r = 0; r < kQ4Rows && vp0 + r < n; r += 256) {
-                const int32_t y = static_cast<int32_t>(vp0 + r);
-                asm volatile(
-                    "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                        reinterpret_cast<uint64_t>(&tmap)),
-                    "r"(base + b * kBufBytes + r * 128), "r"(vcb * 32), "r"(y)
-                    : "memory");
-            }
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-            if (issued > u0)
-                mbar_arrive(empty(static_cast<uint32_t>((v + kQ4Bufs - 1) % kQ4Bufs)));
-            ++issued;
-        }
-    };
-
-    Q4Walk w{};
-    bool live = false;         // w describes the lane's first row of unit u
-    uint32_t cur[kQ4Steps];    // table entries of unit u (when prefetched)
-    bool have_cur = false;
-    uint32_t cb = static_cast<uint32_t>(u0 / nsub);
-    uint64_t s = u0 - static_cast<uint64_t>(cb) * nsub;
-    for (uint64_t u = u0; u < u1; ++u) {
-        const uint32_t j = cb * 32 + 4 * g + d;
-        const RadicalDim* rj = rd + j;
-        const uint64_t i64 = first + s * kQ4Rows + kQ4WarpRows * quarter + p; // lane's first row
-        const uint32_t i = static_cast<uint32_t>(i64);
-        const bool no_wrap = i <= 0xffffffffu - 8 * (kQ4Steps - 1);
-        const bool tab = rj->fqx != nullptr && no_wrap;
-        if (tab && !live) {
-            q4_setup(w, *rj, i);
-            live = true;
-            have_cur = false;
-        }
-        const bool fast = __all_sync(0xffffffffu, tab);
-        if (fast && !have_cur) {
-#pragma unroll
-            for (uint32_t k = 0; k < kQ4Steps; ++k)
-                cur[k] = __ldg(w.qx + w.lo + 8 * k);
-        }
-        // the next unit: contiguous (same column block, no u32 wrap) ->
-        // prefetch its entries now, a whole sub-tile ahead
-        uint32_t cb_n = cb;
-        uint64_t s_n = s + 1;
-        if (s_n == nsub) {
-            s_n = 0;
-            ++cb_n;
-        }
-        const bool contiguous = fast && u + 1 < u1 && cb_n == cb &&
-                                i <= 0xffffffffu - kQ4Rows - 8 * (kQ4Steps - 1);
-        uint32_t nxt[kQ4Steps];
-        if (contiguous) {
-            uint32_t lo_n = w.lo + kQ4Rows;
-            while (lo_n >= w.G)
-                lo_n -= w.G;
-#pragma unroll
-            for (uint32_t k = 0; k < kQ4Steps; ++k)
-                nxt[k] = __ldg(w.qx + lo_n + 8 * k);
-        }
-        // the ring buffer of unit u
-        const uint64_t v = u - u0;
-        const uint32_t b = static_cast<uint32_t>(v % kQ4Bufs);
-        if (v >= kQ4Bufs) {
-            const uint32_t ph = static_cast<uint32_t>(v / kQ4Bufs - 1) & 1u;
-            if (issuer) {
-                while (!mbar_test(empty(b), ph))
-                    issue_ready(u, false);
-            } else {
-                mbar_wait(empty(b), ph);
-            }
-            __syncwarp();
-        }
-        const uint32_t addr = base + b * kBufBytes + lane_off;
-        if (fast) {
-            const uint32_t negG = 0u - w.G;
-            const bool cross = __any_sync(0xffffffffu, w.lo + 8 * (kQ4Steps - 1) >= w.G);
-            if (!cross) {
-#pragma unroll
-                for (uint32_t k = 0; k < kQ4Steps; ++k) {
-                    const uint32_t e = cur[k];
-                    const uint32_t x = e + w.r0.qa1 +
-                                       static_cast<uint32_t>(static_cast<int32_t>(e * negG - w.r0.thr) >> 31);
-                    sts32(addr + k * 1024, q4_out<U32OUT>(x));
-                }
-            } else {
-#pragma unroll
-                for (uint32_t k = 0; k < kQ4Steps; ++k) {
-                    const uint32_t e = cur[k];
-                    const bool up = w.lo + 8 * k >= w.G;
-                    const uint32_t qa1 = up ? w.r1.qa1 : w.r0.qa1, thr = up ? w.r1.thr : w.r0.thr;
-                    const uint32_t x =
-                        e + qa1 + static_cast<uint32_t>(static_cast<int32_t>(e * negG - thr) >> 31);
-                    sts32(addr + k * 1024, q4_out<U32OUT>(x));
-                }
-            }
-        } else { // a u32 index wrap (or no table): the digit loop per sample
-            for (uint32_t k = 0; k < kQ4Steps; ++k) {
-                const uint32_t ik = i + 8 * k;
-                const uint32_t x = rj->base == 2 ? brev32(ik & 0x7fffffffu) : radical_fixed(ik, *rj);
-                sts32(addr + k * 1024, q4_out<U32OUT>(x));
-            }
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0)
-            mbar_arrive(full(b));
-        if (issuer)
-            issue_ready(u + 1, false);
-        // advance the walk to the next unit
-        if (contiguous) {
-            q4_advance(w, *rj, kQ4Rows);
-#pragma unroll
-            for (uint32_t k = 0; k < kQ4Steps; ++k)
-                cur[k] = nxt[k];
-            have_cur = true;
-        } else {
-            live = false;
-            have_cur = false;
-        }
-        cb = cb_n;
-        s = s_n;
-    }
-    if (issuer) {
-        issue_ready(u1, true);
-        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    }
-}
-
 // Odd dims <= 31: the padded sub-tile of k_runs has an odd row stride, so
 // with no padding at all (ld == dims) it is already conflict-free and laid
 // out exactly as the output — so each run keeps a ring of nbuf dense
@@ -2261,46 +1983,6 @@ cudaError_t launch_lattice(const SmallArgs& args, uint32_t dims, bool u32, const
     });
 }
 
-// dims % 32 == 0, out 16-B aligned, n < 2^31: k_halton_q4; false otherwise.
-bool launch_halton_q4(const RadicalDim* rd, uint32_t dims, bool u32, const FillRange& r,
-                      cudaStream_t s, cudaError_t* err)
-{
-    if (dims % 32 != 0 || (reinterpret_cast<uintptr_t>(r.out) & 15u) != 0 || r.n >= (1ull << 31))
-        return false;
-    static PFN_cuTensorMapEncodeTiled encode = [] {
-        void* fn = nullptr;
-        cudaDriverEntryPointQueryResult q{};
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
-                cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            fn = nullptr;
-        return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
-    }();
-    if (!encode)
-        return false;
-    CUtensorMap tmap;
-    const cuuint64_t gdim[2] = {dims, r.n};
-    const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(dims) * 4};
-    const cuuint32_t box[2] = {32, 256};
-    const cuuint32_t estride[2] = {1, 1};
-    if (encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, r.out, gdim, gstride, box, estride,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return false;
-    const size_t smem = static_cast<size_t>(kQ4Rows) * 128 * kQ4Bufs + 1024;
-    auto kern = u32 ? k_halton_q4<true> : k_halton_q4<false>;
-    *err = allow_dynamic_smem(kern);
-    if (*err != cudaSuccess)
-        return true;
-    const uint64_t nsub = (r.n + kQ4Rows - 1) / kQ4Rows;
-    const uint32_t ncb = dims / 32;
-    const unsigned grid = static_cast<unsigned>(
-        std::min<uint64_t>(nsub * ncb, static_cast<uint64_t>(sm_count())));
-    kern<<<grid, 1024, smem, s>>>(tmap, rd, ncb, r.first, r.n, nsub);
-    *err = cudaGetLastError();
-    return true;
-}
-
 cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRange& r,
                           cudaStream_t s)
 {
@@ -2308,8 +1990,6 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
         return cudaSuccess;
     const RadicalDim* rdv = static_cast<const RadicalDim*>(rd);
     cudaError_t err = cudaSuccess;
-    if (launch_halton_q4(rdv, dims, u32, r, s, &err))
-        return err;
     if (u32 ? launch_tma_fill(HaltonWalk<true>{rdv}, dims, r, s, &err)
             : launch_tma_fill(HaltonWalk<false>{rdv}, dims, r, s, &err))
         return err;

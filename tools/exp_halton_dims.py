@@ -1,4 +1,4 @@
-"""Probe: Halton fills on the k_halton_q4 path (dims % 32 == 0), Gsamples/s
+"""Probe: Halton fills with dims % 32 == 0 (k_tma<HaltonWalk>), Gsamples/s
 and fraction of the measured HBM copy peak."""
 import json
 import os
