@@ -1824,7 +1824,11 @@ cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const
         return by_log_pps<4>(dims, [&](auto lp) {
             return sobol_fast_dispatch<4, decltype(lp)::value>(cols, words, mode, u32, r, s);
         });
-    if ((dims == 1 || dims == 2) && (reinterpret_cast<uintptr_t>(r.out) & 31u) == 0) {
+    // the narrow kernels' interior tiles store 8 words (32 B) per lane at
+    // out + (p - first) * dims with p a multiple of 8 / dims: first must be
+    // too, or those stores are misaligned
+    if ((dims == 1 || dims == 2) && (reinterpret_cast<uintptr_t>(r.out) & 31u) == 0 &&
+        (r.first & (8u / dims - 1u)) == 0) {
         constexpr int kLogTp1 = 13, kLogTp2 = 12; // 8192 / D points per tile
         if (dims == 1)
             return mode == 2 ? (u32 ? launch_tiled(k_sobol_narrow<1, 2, true>, kLogTp1, r, s, cols, words)
@@ -1970,7 +1974,8 @@ cudaError_t launch_lattice(const SmallArgs& args, uint32_t dims, bool u32, const
         return by_log_pps<4>(dims, [&](auto lp) {
             return lattice_fast_dispatch<4, decltype(lp)::value>(args, u32, r, s);
         });
-    if ((dims == 1 || dims == 2) && (reinterpret_cast<uintptr_t>(r.out) & 31u) == 0) {
+    if ((dims == 1 || dims == 2) && (reinterpret_cast<uintptr_t>(r.out) & 31u) == 0 &&
+        (r.first & (8u / dims - 1u)) == 0) { // see launch_sobol
         if (dims == 1)
             return u32 ? launch_tiled(k_lattice_narrow<1, true>, 13, r, s, nullptr, args)
                        : launch_tiled(k_lattice_narrow<1, false>, 13, r, s, nullptr, args);

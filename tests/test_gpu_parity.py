@@ -1480,3 +1480,33 @@ def test_halton_fill_q4_many_blocks_vs_reference(ref, dims):
         mapped = np.zeros(n, np.uint32)
         ref.ref_map_bulk(ptr(exp), ptr(mapped), n)
         np.testing.assert_array_equal(got[:, j].view(np.uint32), mapped, err_msg=f"dim={j}")
+
+
+@pytest.mark.parametrize("dims", [1, 2])
+@pytest.mark.parametrize("first", [77, 4 * 1000 + 2, (1 << 33) + 17, (1 << 32) - 70001])
+def test_narrow_fills_unaligned_first_vs_oracle(oracle, columns64, dims, first):
+    """dims 1 and 2 over several 8192-point tiles from a first index that is
+    not a multiple of 8 / dims (the narrow kernels' interior tiles use 32-B
+    stores at out + (i - first) * dims): Sobol' (plain, XOR, Owen) and the
+    CP lattice against the oracle."""
+    n = 70001
+    for sc in ("none", "xor", "owen"):
+        words = [0x9E3779B9 * (j + 1) & 0xFFFFFFFF for j in range(dims)] if sc != "none" else None
+        got = u32(q.sobol_fill(n, dims, first=first, scramble=sc, words=words, fixed=True))
+        exp = np.zeros((n, dims), np.uint32)
+        w = np.ascontiguousarray(words if words else [0] * dims, np.uint32)
+        cols = np.ascontiguousarray(columns64[:dims])
+        if sc == "owen":
+            oracle.qo_sobol_owen_fill_fixed(first, n, dims, ptr(cols), ptr(w), ptr(exp))
+        else:
+            oracle.qo_sobol_fill_fixed(first, n, dims, ptr(cols), ptr(w) if words else None,
+                                       ptr(exp))
+        np.testing.assert_array_equal(got.reshape(n, dims), exp, err_msg=sc)
+    g = q.lfsr_generator_vector(0xACE1, max(dims, 2))[:dims]
+    sh = [0x12345 * (j + 3) & 0xFFFFFFFF for j in range(dims)]
+    got = u32(q.lattice_fill(n, g, first=first, shifts=sh, fixed=True)).reshape(n, dims)
+    i = (np.arange(first, first + n, dtype=np.uint64) & 0xFFFFFFFF).astype(np.uint32)
+    br = np.array([int("{:032b}".format(int(v))[::-1], 2) for v in i], np.uint64)
+    exp = ((br[:, None] * np.array(g, np.uint64)[None, :] + np.array(sh, np.uint64)[None, :])
+           & 0xFFFFFFFF).astype(np.uint32)
+    np.testing.assert_array_equal(got, exp)
