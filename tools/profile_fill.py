@@ -50,6 +50,9 @@ elif a.config in ("sobolowen12", "sobolowen256"):
     m = q.GeneratorMatrixSet.builtin(min(d, 64)) if d <= 64 else q.GeneratorMatrixSet.from_columns(
         __import__("numpy").arange(d * 52, dtype="uint32").reshape(d, 52) | 1)
     fn = lambda: q.sobol_fill(n, d, matrices=m, scramble="owen", words=list(range(d)), out=out)  # noqa: E731
+elif a.config.startswith("bench-"):
+    kern = a.config[len("bench-"):]
+    fn = lambda: q.run_bench_kernel(kern, 1 << 28, 32)  # noqa: E731
 elif a.config == "integrate":
     fn = lambda: q.integrate("sobol", "product-sine", 1 << 26, 8, "kahan")  # noqa: E731
 elif a.config == "c5iph":
