@@ -71,6 +71,9 @@ struct RenderParams {
     const uint32_t* xor_points;   // device, point_count*xor_dims
     uint32_t xor_point_count, xor_dims;
     const uint32_t* tab3;         // device phi_3 7-digit table (or null)
+    Div32 divw;                   // exact division by width (width >= 2)
+    uint32_t small_band;          // rows * width < 2^32: 32-bit pixel indexing
+    double inv_spp;               // 1 / spp when spp is a power of two (exact), else 0
 };
 
 // Per-stream (one pixel context) parameters for qmc_stream_fill kinds that

@@ -125,6 +125,13 @@ __device__ __forceinline__ void sample2(uint32_t i, const PixelState& s, const R
 __device__ __forceinline__ void band_pixel(uint64_t q, const RenderParams& p, uint32_t& px,
                                            uint32_t& py)
 {
+    if (p.small_band) { // a 32-bit multiply-high instead of a 64-bit division
+        const uint32_t q32 = static_cast<uint32_t>(q);
+        const uint32_t r = p.width == 1 ? q32 : div32(q32, p.divw);
+        py = p.row_begin + r;
+        px = q32 - r * p.width;
+        return;
+    }
     py = p.row_begin + static_cast<uint32_t>(q / p.width);
     px = static_cast<uint32_t>(q % p.width);
 }
@@ -168,14 +175,22 @@ __device__ __forceinline__ long long int_term(double f)
 }
 
 // float(value() / spp) (kahan) and float(sum / 2^32 / spp) (int).
-__device__ __forceinline__ float finish_kahan(double sum, double comp, uint32_t spp)
+// x / spp; when spp is a power of two the quotient is exact, so the product
+// with the exact reciprocal inv_spp is the same double without a DDIV
+__device__ __forceinline__ double div_spp(double x, uint32_t spp, double inv_spp)
 {
-    return __double2float_rn(__ddiv_rn(__dadd_rn(sum, comp), static_cast<double>(spp)));
+    return inv_spp != 0.0 ? __dmul_rn(x, inv_spp) : __ddiv_rn(x, static_cast<double>(spp));
 }
-__device__ __forceinline__ float finish_int(long long isum, uint32_t spp)
+__device__ __forceinline__ float finish_kahan(double sum, double comp, uint32_t spp,
+                                              double inv_spp = 0.0)
 {
+    return __double2float_rn(div_spp(__dadd_rn(sum, comp), spp, inv_spp));
+}
+__device__ __forceinline__ float finish_int(long long isum, uint32_t spp, double inv_spp = 0.0)
+{
+    // / 2^32 is exact (a power of two)
     return __double2float_rn(
-        __ddiv_rn(__ddiv_rn(static_cast<double>(isum), 4294967296.0), static_cast<double>(spp)));
+        div_spp(__dmul_rn(static_cast<double>(isum), 0x1p-32), spp, inv_spp));
 }
 
 // The sequential per-pixel sample loop of k_render (render.cpp:61-78).
@@ -210,7 +225,7 @@ __device__ __forceinline__ float render_pixel(const PixelState& s, const RenderP
     };
     if (ACCUM != 0) {
         run(0, p.spp, std::false_type{});
-        return finish_int(isum, p.spp);
+        return finish_int(isum, p.spp, p.inv_spp);
     }
     // scene_value lies in [0, 1.25] and the sum never decreases, so once the
     // whole warp has sum >= 1.25 every later step takes the first branch
@@ -220,7 +235,7 @@ __device__ __forceinline__ float render_pixel(const PixelState& s, const RenderP
         run(k0, p.spp, std::true_type{});
     else
         run(k0, p.spp, std::false_type{});
-    return finish_kahan(sum, comp, p.spp);
+    return finish_kahan(sum, comp, p.spp, p.inv_spp);
 }
 
 // Low-spp grid-stride rendering for the kinds that stage tables per CTA
@@ -384,7 +399,8 @@ __global__ void __launch_bounds__(kBlock) k_render_warp(RenderParams p, float* _
         }
     }
     if (lane == 0)
-        out[q] = ACCUM == 0 ? finish_kahan(sum, comp, p.spp) : finish_int(isum, p.spp);
+        out[q] = ACCUM == 0 ? finish_kahan(sum, comp, p.spp, p.inv_spp)
+                            : finish_int(isum, p.spp, p.inv_spp);
 }
 
 // Sample-partitioned render (PAPER.md:498-509 / imageplane.cpp:114-130:

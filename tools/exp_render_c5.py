@@ -28,7 +28,8 @@ def t(fn, px, k=5):
 
 
 row = []
-for kind, spp, acc in [("pixel-shifted-lattice", 16, "kahan"), ("pixel-shifted-lattice", 64, "kahan"),
+for kind, spp, acc in [("pixel-shifted-lattice", 1, "kahan"), ("sobol", 1, "kahan"),
+                       ("pixel-shifted-lattice", 16, "kahan"), ("pixel-shifted-lattice", 64, "kahan"),
                        ("pixel-shifted-lattice", 256, "kahan"), ("pixel-shifted-lattice", 64, "int"),
                        ("image-plane-halton", 64, "kahan"), ("sobol", 64, "kahan")]:
     row.append("%s/%d/%s=%s" % (kind[:5], spp, acc, t(lambda: q.render(3840, 2160, spp, kind=kind, accum=acc, out=img), 3840 * 2160 * spp)))
