@@ -127,8 +127,9 @@ void hilbert_xy_host(uint64_t d, uint32_t order, uint32_t& x, uint32_t& y); // h
 struct DigitTable {
     const uint32_t* ptr = nullptr;
     uint32_t group = 0;
-    // with_quotients: {floor(T * 2^32 / group), T * 2^32 mod group} per entry
-    const uint32_t* qr = nullptr;
+    // with_quotients: floor(T * 2^32 / group) per entry (the remainder
+    // T * 2^32 mod group is -q * group mod 2^32)
+    const uint32_t* qx = nullptr;
 };
 
 // Widest b^d-entry table (b^d <= max_entries) inverting d >= min_digits

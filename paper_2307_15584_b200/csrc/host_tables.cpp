@@ -276,7 +276,7 @@ DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor, uint32_t min_
                        uint32_t max_entries, bool with_quotients)
 {
     struct Slot {
-        DevPtr t, qr;
+        DevPtr t, qx;
         uint32_t group = 0;
     };
     static std::mutex mu;
@@ -311,19 +311,16 @@ DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor, uint32_t min_
         if (with_quotients) {
             // T * 2^32 = q * group + r: the contiguous fill adds the
             // warp-uniform quotient of the high digits and a carry (r >= thr)
-            std::vector<uint32_t> qr(2 * (group + 8), 0u);
-            for (uint32_t v = 0; v < group; ++v) {
-                const uint64_t num = static_cast<uint64_t>(t[v]) << 32;
-                qr[2 * v] = static_cast<uint32_t>(num / group);
-                qr[2 * v + 1] = static_cast<uint32_t>(num % group);
-            }
-            slot.qr = dev_upload(qr.data(), qr.size() * 4);
+            std::vector<uint32_t> qx(group + 8, 0u);
+            for (uint32_t v = 0; v < group; ++v)
+                qx[v] = static_cast<uint32_t>((static_cast<uint64_t>(t[v]) << 32) / group);
+            slot.qx = dev_upload(qx.data(), qx.size() * 4);
         }
         slot.t = dev_upload(t.data(), t.size() * 4);
         slot.group = group;
     }
     return {static_cast<const uint32_t*>(slot.t.get()), slot.group,
-            static_cast<const uint32_t*>(slot.qr.get())};
+            static_cast<const uint32_t*>(slot.qx.get())};
 }
 
 const uint64_t* pow_magic(uint32_t b)
@@ -378,7 +375,7 @@ std::vector<RadicalDim> radical_dims(uint32_t dims, uint32_t first_prime, qmc_ra
             r.mode = 2;
         }
         r.ftable = nullptr;
-        r.fqr = nullptr;
+        r.fqx = nullptr;
         r.magic = nullptr;
         r.gdigits = r.fgroup = r.fdigits = r.himod = 0;
         r.fdivg = Div32{0, 0};
@@ -395,7 +392,7 @@ std::vector<RadicalDim> radical_dims(uint32_t dims, uint32_t first_prime, qmc_ra
             const DigitTable f = digit_table(b, r.mode, r.factor, 1, kFillTableMax, true);
             if (f.ptr) {
                 r.ftable = f.ptr;
-                r.fqr = reinterpret_cast<const uint2*>(f.qr);
+                r.fqx = f.qx;
                 r.fgroup = f.group;
                 r.fdivg = make_div32(f.group);
                 for (uint32_t g = f.group; g > 1; g /= b)

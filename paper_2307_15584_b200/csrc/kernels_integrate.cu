@@ -149,15 +149,15 @@ __global__ void __launch_bounds__(ChunkShape<KIND>::kBlock)
     // in the fill-table blocks h0 and h0 + 1 of a dimension, its inverse is
     // the quotient-table form of the contiguous fill (device.cuh: hi_split):
     // one coalesced 8-B load and three integer ops instead of the digit loop.
-    __shared__ const uint2* HTAB[kStateDims];
+    __shared__ const uint32_t* HTAB[kStateDims];
     __shared__ uint32_t HG[kStateDims], HLO[kStateDims], HQ0[kStateDims], HT0[kStateDims],
         HQ1[kStateDims], HT1[kStateDims];
     if (KIND == 1 || KIND == 3) {
         const uint32_t ib = static_cast<uint32_t>(KIND == 3 ? block + begin : begin);
         for (uint32_t j = t; j < sdims; j += kBlock) {
             const RadicalDim& r = rd[j];
-            const uint2* tab = nullptr;
-            if (r.fqr && ib <= 0xffffffffu - count) {
+            const uint32_t* tab = nullptr;
+            if (r.fqx && ib <= 0xffffffffu - count) {
                 const uint32_t ir = ib - div32(ib, r.divmp) * r.maxpow;
                 const uint32_t G = r.fgroup, h0 = div32(ir, r.fdivg), lo0 = ir - h0 * G;
                 if (static_cast<uint64_t>(ir) + count <= r.maxpow && lo0 + count <= 2 * G) {
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(ChunkShape<KIND>::kBlock)
                     HT0[j] = a.thr;
                     HQ1[j] = b.qa;
                     HT1[j] = b.thr;
-                    tab = r.fqr;
+                    tab = r.fqx;
                 }
             }
             HTAB[j] = tab;
@@ -194,14 +194,14 @@ __global__ void __launch_bounds__(ChunkShape<KIND>::kBlock)
                 if (KIND == 0)
                     x = j < kStateDims ? sob[j] : sobol_direct(idx, j, p);
                 else if (KIND == 1 || KIND == 3) {
-                    const uint2* tab = j < kStateDims ? HTAB[j] : nullptr;
+                    const uint32_t* tab = j < kStateDims ? HTAB[j] : nullptr;
                     if (tab) {
                         const uint32_t G = HG[j];
                         uint32_t lo = HLO[j] + local;
                         const bool up = lo >= G;
                         lo = up ? lo - G : lo;
-                        const uint2 e = __ldg(tab + lo);
-                        x = e.x + (up ? HQ1[j] : HQ0[j]) + (e.y >= (up ? HT1[j] : HT0[j]) ? 1u : 0u);
+                        const uint32_t e = __ldg(tab + lo); // rT = -qT * G mod 2^32
+                        x = e + (up ? HQ1[j] : HQ0[j]) + (e * (0u - G) >= (up ? HT1[j] : HT0[j]) ? 1u : 0u);
                     } else {
                         x = radical_fixed(KIND == 1 ? i : static_cast<uint32_t>(block + idx), rd[j]);
                     }
