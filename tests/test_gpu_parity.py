@@ -76,7 +76,7 @@ def test_vdc_vs_reference(ref):
     for first, n in [(0, 4099), (2**31 - 7, 100), (2**32 - 50, 50), (123456789, 1000),
                      (2**31 - 8 * 4000, 70003), (2**32 - 8 * 5000, 80005), (2**33 + 8, 65541)]:
         exp = np.zeros(n, np.uint32)
-        assert ref.ref_radical_fixed_fill(first, n, 0, 0, 0, ptr(exp)) == 0
+        assert ref.ref_radical_fixed_fill(first & 0xFFFFFFFF, n, 0, 0, 0, ptr(exp)) == 0
         np.testing.assert_array_equal(u32(q.radical_inverse_fill(n, 0, first=first, fixed=True)), exp)
 
 
