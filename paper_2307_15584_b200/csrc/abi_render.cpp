@@ -51,6 +51,7 @@ void resolve_render(const qmc_render_job* job, uint32_t row_begin, uint32_t row_
     p.divw = job->width >= 2 ? make_div32(job->width) : Div32{0, 0};
     p.small_band = static_cast<uint64_t>(row_end - row_begin) * job->width < (1ull << 32) ? 1u : 0u;
     p.inv_spp = (job->spp & (job->spp - 1)) == 0 ? 1.0 / job->spp : 0.0;
+    p.colmap = job->spp >= 8 ? render_column_order(job->width) : nullptr;
     std::vector<uint32_t> g = job->generator && job->generator_dims
                                   ? std::vector<uint32_t>(job->generator,
                                                           job->generator + job->generator_dims)

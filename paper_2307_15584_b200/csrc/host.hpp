@@ -142,6 +142,8 @@ DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor, uint32_t min_
                        uint32_t max_entries = kDigitTableMax, bool with_quotients = false);
 // floor(2^64 / b^D) for D = 0..32 (0 where b^D >= 2^32), on the current device
 const uint64_t* pow_magic(uint32_t b);
+// k_render's column order for an image `width` wide (kernels_render.cu).
+const uint32_t* render_column_order(uint32_t width);
 std::vector<RadicalDim> radical_dims(uint32_t dims, uint32_t first_prime, qmc_radical_scramble sc,
                                      const uint32_t* factors, std::vector<uint32_t>& sigma_pool,
                                      std::vector<size_t>& sigma_off);

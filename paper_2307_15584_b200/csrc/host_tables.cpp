@@ -5,6 +5,7 @@
 #include "host.hpp"
 
 #include <cstdlib>
+#include <cmath>
 #include <map>
 #include <sstream>
 #include <tuple>
@@ -321,6 +322,40 @@ DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor, uint32_t min_
     }
     return {static_cast<const uint32_t*>(slot.t.get()), slot.group,
             static_cast<const uint32_t*>(slot.qx.get())};
+}
+
+// Column order of k_render's warps at spp >= 8: the columns whose pixel
+// footprints keep one sine quadrant of sin(8 pi x) with an even quadrant
+// count first, then those with an odd count, then the few that cross a
+// quadrant boundary — so nearly every warp of 32 consecutive entries shares
+// its quadrant parity and takes the specialised loop. The order only decides
+// which thread renders which pixel; every pixel's value is unchanged. The
+// classification restates sin_fixed_quadrant (device.cuh).
+const uint32_t* render_column_order(uint32_t width)
+{
+    static std::mutex mu;
+    static std::map<std::pair<int, uint32_t>, DevPtr> cache;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(mu);
+    auto& slot = cache[{dev, width}];
+    if (!slot) {
+        const SceneConsts c = make_scene_consts();
+        const double inv_w = 1.0 / width;
+        std::vector<uint32_t> cls[3];
+        for (uint32_t px = 0; px < width; ++px) {
+            const double t0 = px * inv_w * c.k8pi * c.two_over_pi;
+            const double t1 = (px + 1.0) * inv_w * c.k8pi * c.two_over_pi;
+            const double n = std::rint(t0);
+            const bool fixed = t0 > n - 0.5 + 1e-9 && t1 < n + 0.5 - 1e-9;
+            cls[fixed ? static_cast<int64_t>(n) & 1 : 2].push_back(px);
+        }
+        std::vector<uint32_t> order;
+        order.reserve(width);
+        for (const auto& v : cls)
+            order.insert(order.end(), v.begin(), v.end());
+        slot = dev_upload(order.data(), order.size() * 4);
+    }
+    return static_cast<const uint32_t*>(slot.get());
 }
 
 const uint64_t* pow_magic(uint32_t b)

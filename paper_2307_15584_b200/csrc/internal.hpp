@@ -74,6 +74,7 @@ struct RenderParams {
     Div32 divw;                   // exact division by width (width >= 2)
     uint32_t small_band;          // rows * width < 2^32: 32-bit pixel indexing
     double inv_spp;               // 1 / spp when spp is a power of two (exact), else 0
+    const uint32_t* colmap;       // device, k_render's column order at spp >= 8 (or null)
 };
 
 // Per-stream (one pixel context) parameters for qmc_stream_fill kinds that

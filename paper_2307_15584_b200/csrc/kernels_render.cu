@@ -152,7 +152,9 @@ __device__ __forceinline__ void sobol_direct2(uint32_t i, const RenderParams& p,
 // scene_value at sample i of the pixel (render.cpp:61-68): the two fp32
 // sample components, the sample point ((px + u) / W, (py + v) / H) in FP64
 // and the integrand. sob0/sob1: the Sobol' value of index i (KIND 0).
-template <uint32_t KIND, bool DISC_TEST = true, bool FIXED_Q = false, bool SMEM_T3 = false>
+// UQ >= 0: the warp shares qx and qy, UQ = their parities (scene_value_uq).
+template <uint32_t KIND, bool DISC_TEST = true, bool FIXED_Q = false, bool SMEM_T3 = false,
+          int UQ = -1>
 __device__ __forceinline__ double pixel_sample(uint32_t i, const PixelState& s,
                                                const RenderParams& p, double fx, double fy,
                                                const double2* s_poly, uint32_t sob0,
@@ -163,9 +165,12 @@ __device__ __forceinline__ double pixel_sample(uint32_t i, const PixelState& s,
     sample2<KIND, SMEM_T3>(i, s, p, a, b, sob0, sob1, SMEM_T3 ? s_tab3 : p.tab3);
     const double u = static_cast<double>(map_u32(a));
     const double v = static_cast<double>(map_u32(b));
-    return scene_value<true, DISC_TEST, FIXED_Q>(__dmul_rn(__dadd_rn(fx, u), p.inv_w),
-                                                 __dmul_rn(__dadd_rn(fy, v), p.inv_h), p.sc,
-                                                 s_poly, inside_px, qx, qy);
+    const double x = __dmul_rn(__dadd_rn(fx, u), p.inv_w);
+    const double y = __dmul_rn(__dadd_rn(fy, v), p.inv_h);
+    if constexpr (UQ >= 0)
+        return scene_value_uq<UQ, DISC_TEST>(x, y, p.sc, inside_px, qx, qy);
+    else
+        return scene_value<true, DISC_TEST, FIXED_Q>(x, y, p.sc, s_poly, inside_px, qx, qy);
 }
 
 // render.cpp:72-78: llround(f * 2^32), the int accumulator's term.
@@ -194,7 +199,7 @@ __device__ __forceinline__ float finish_int(long long isum, uint32_t spp, double
 }
 
 // The sequential per-pixel sample loop of k_render (render.cpp:61-78).
-template <uint32_t KIND, uint32_t ACCUM, bool DISC_TEST, bool FIXED_Q>
+template <uint32_t KIND, uint32_t ACCUM, bool DISC_TEST, bool FIXED_Q, int UQ = -1>
 __device__ __forceinline__ float render_pixel(const PixelState& s, const RenderParams& p,
                                               double fx, double fy, const double2* s_poly,
                                               const uint32_t* sob_d, bool inside_px, int qx,
@@ -208,7 +213,7 @@ __device__ __forceinline__ float render_pixel(const PixelState& s, const RenderP
     auto run = [&](uint32_t i0, uint32_t i1, auto big) {
 #pragma unroll 2
         for (uint32_t i = i0; i < i1; ++i) {
-            const double f = pixel_sample<KIND, DISC_TEST, FIXED_Q, kSmemT3>(
+            const double f = pixel_sample<KIND, DISC_TEST, FIXED_Q, kSmemT3, UQ>(
                 i, s, p, fx, fy, s_poly, sob0, sob1, inside_px, qx, qy, s_tab3);
             if (ACCUM != 0)
                 isum += int_term(f);
@@ -245,73 +250,160 @@ __device__ __forceinline__ float render_pixel(const PixelState& s, const RenderP
 template <uint32_t KIND>
 constexpr bool kLowSppStride = KIND == 0 || KIND == 1 || KIND == 3;
 
-template <uint32_t KIND, uint32_t ACCUM>
-__global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __restrict__ out)
+// Per-warp classification of k_render's pixels (spp >= 8). Thread q takes
+// the pixel in row q / W of the band and column colmap[q % W] (host::
+// render_column_order groups the columns by sine-quadrant parity, so nearly
+// every warp is uniform below); o is that pixel's offset in the band.
+// valid: the lane has a pixel; every vote is over the whole warp and counts
+// valid lanes only, so all k_render modes classify every warp identically.
+struct WarpClass {
+    uint64_t o;
+    uint32_t px, py;
+    int qx, qy;     // the lane's fixed quadrant counts (when fixed)
+    bool inside;    // the lane's pixel lies inside the disc
+    bool test;      // some lane's footprint crosses the disc's edge
+    bool fixed;     // every lane keeps one sine quadrant per axis
+    bool uniform;   // fixed, and all lanes share the parities of qx and qy
+};
+
+__device__ __forceinline__ WarpClass classify_warp(bool valid, uint64_t q, const RenderParams& p)
 {
-    __shared__ double2 s_poly[8];
-    __shared__ uint32_t s_sob_d[KIND == 0 ? 64 : 1]; // sobol: prefix XORs of the columns
+    WarpClass c{};
+    int disc = kDiscOutside;
+    bool fixed = true;
+    if (valid) {
+        band_pixel(q, p, c.px, c.py);
+        c.o = q;
+        if (p.colmap) {
+            c.px = __ldg(p.colmap + c.px);
+            c.o = static_cast<uint64_t>(c.py - p.row_begin) * p.width + c.px;
+        }
+        const double fx = static_cast<double>(c.px), fy = static_cast<double>(c.py);
+        disc = disc_class(c.px, c.py, p.inv_w, p.inv_h, p.sc.disc_r2);
+        fixed = sin_fixed_quadrant(fx * p.inv_w, (fx + 1.0) * p.inv_w, p.sc, c.qx) &&
+                sin_fixed_quadrant(fy * p.inv_h, (fy + 1.0) * p.inv_h, p.sc, c.qy);
+    }
+    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+    c.inside = disc == kDiscInside;
+    c.test = __any_sync(0xffffffffu, disc == kDiscTest);
+    c.fixed = __all_sync(0xffffffffu, fixed);
+    const int par = (c.qx & 1) | (c.qy & 1) << 1;
+    const int lead = vmask ? __ffs(vmask) - 1 : 0;
+    const int par0 = __shfl_sync(0xffffffffu, par, lead);
+    c.uniform = vmask != 0 && c.fixed && __all_sync(0xffffffffu, !valid || par == par0);
+    return c;
+}
+
+// k_render. At spp >= 8 every warp is classified. With UQ, the warps whose
+// lanes share the quadrant parities per axis (uniform) run sine polynomials
+// specialised on those parities, with the coefficients in the constant bank
+// (scene_value_uq); every other warp (and every warp without UQ) runs the
+// per-lane quadrant / per-sample paths. Each pixel is rendered by one thread
+// in the reference's per-pixel sample order, so neither the column order
+// nor the path changes an output bit. UQ costs registers (the generic paths
+// and the specialised loops in one kernel), so render_kind launches the UQ
+// instance only at spp >= 8 and for the kinds where it measured faster.
+// Shared-memory tables of the render kernels: the Sobol' prefix XORs (KIND
+// 0), the phi_3 table (the Halton kinds) and the sine coefficients.
+template <uint32_t KIND>
+struct RenderSmem {
+    static constexpr bool kT3 = KIND == 1 || KIND == 3 || KIND == 6;
+    double2 poly[8];
+    uint32_t sob_d[KIND == 0 ? 64 : 1]; // sobol: prefix XORs of the columns
+    uint32_t tab3[kT3 ? 2187 : 1];      // halton kinds: 3^7 words
+};
+
+template <uint32_t KIND>
+__device__ __forceinline__ void stage_render_smem(RenderSmem<KIND>& sm, const RenderParams& p)
+{
     if (KIND == 0 && threadIdx.x < 64) {
         const uint32_t dim = threadIdx.x >> 5, c = threadIdx.x & 31u;
         uint32_t d = 0;
         for (uint32_t k = 0; k <= c; ++k)
             d ^= __ldg(p.cols2 + 52 * dim + k);
-        s_sob_d[threadIdx.x] = d;
+        sm.sob_d[threadIdx.x] = d;
     }
-    // halton kinds: the phi_3 table (3^7 words) staged in shared memory
-    constexpr bool kSmemT3 = KIND == 1 || KIND == 3 || KIND == 6;
-    __shared__ uint32_t s_tab3[kSmemT3 ? 2187 : 1];
-    if (kSmemT3)
+    if (RenderSmem<KIND>::kT3)
         for (uint32_t e = threadIdx.x; e < 2187; e += blockDim.x)
-            s_tab3[e] = __ldg(p.tab3 + e);
-    load_sin_poly(s_poly); // includes the barrier
+            sm.tab3[e] = __ldg(p.tab3 + e);
+    load_sin_poly(sm.poly); // includes the barrier
+}
+
+// spp < 8: too few samples to repay the per-warp classification. The kinds
+// that stage tables per CTA run a grid-stride loop (render_kind sizes the
+// grid to the resident CTAs) to spread the staging over many pixels.
+template <uint32_t KIND, uint32_t ACCUM>
+__global__ void __launch_bounds__(kBlock) k_render_low(RenderParams p, float* __restrict__ out)
+{
+    __shared__ RenderSmem<KIND> sm;
+    stage_render_smem(sm, p);
+    const uint64_t npix = static_cast<uint64_t>(p.row_end - p.row_begin) * p.width;
+    const uint64_t step = kLowSppStride<KIND> ? static_cast<uint64_t>(gridDim.x) * blockDim.x : npix;
+    for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < npix;
+         q += step) {
+        uint32_t px, py;
+        band_pixel(q, p, px, py);
+        const PixelState s = pixel_state<KIND>(px, py, p);
+        out[q] = render_pixel<KIND, ACCUM, true, false>(s, p, static_cast<double>(px),
+                                                         static_cast<double>(py), sm.poly, sm.sob_d,
+                                                         false, 0, 0, sm.tab3);
+    }
+}
+
+// spp >= 8. Every warp is classified (classify_warp). With UQ, the warps
+// whose lanes share the quadrant parities per axis (uniform) run sine
+// polynomials specialised on those parities, with the coefficients in the
+// constant bank (scene_value_uq); every other warp (and every warp without
+// UQ) runs the per-lane quadrant / per-sample paths. Each pixel is rendered
+// by one thread in the reference's per-pixel sample order, so neither the
+// column order nor the path changes an output bit. UQ costs registers (the
+// generic paths and the specialised loops share the kernel), so render_kind
+// launches the UQ instance only for the kinds where it measured faster.
+template <uint32_t KIND, uint32_t ACCUM, bool UQ>
+__global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __restrict__ out)
+{
     const uint64_t npix = static_cast<uint64_t>(p.row_end - p.row_begin) * p.width;
     const uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (kLowSppStride<KIND> && p.spp < 8) {
-        // too few samples to repay the per-pixel classification; a
-        // grid-stride loop (render_kind sizes the grid to the resident
-        // CTAs) spreads the CTA's table staging over many pixels
-        for (uint64_t qq = q; qq < npix; qq += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-            uint32_t px, py;
-            band_pixel(qq, p, px, py);
-            const PixelState s = pixel_state<KIND>(px, py, p);
-            out[qq] = render_pixel<KIND, ACCUM, true, false>(
-                s, p, static_cast<double>(px), static_cast<double>(py), s_poly, s_sob_d, false, 0,
-                0, s_tab3);
+    const bool valid = q < npix;
+    const WarpClass wc = classify_warp(valid, q, p);
+    __shared__ RenderSmem<KIND> sm;
+    stage_render_smem(sm, p);
+    if (!valid)
+        return;
+    const PixelState s = pixel_state<KIND>(wc.px, wc.py, p);
+    const double fx = static_cast<double>(wc.px), fy = static_cast<double>(wc.py);
+    const bool inside = wc.inside;
+    const int qx = wc.qx, qy = wc.qy;
+    float r;
+    if (UQ && wc.uniform) {
+        // four parities x disc test: warp-uniform choices
+#define QMC_UQ_CASE(U)                                                                             \
+    r = wc.test ? render_pixel<KIND, ACCUM, true, true, U>(s, p, fx, fy, sm.poly, sm.sob_d, false, \
+                                                           qx, qy, sm.tab3)                        \
+                : render_pixel<KIND, ACCUM, false, true, U>(s, p, fx, fy, sm.poly, sm.sob_d,       \
+                                                            inside, qx, qy, sm.tab3)
+        switch ((qx & 1) | (qy & 1) << 1) {
+        case 0: QMC_UQ_CASE(0); break;
+        case 1: QMC_UQ_CASE(1); break;
+        case 2: QMC_UQ_CASE(2); break;
+        default: QMC_UQ_CASE(3); break;
         }
-        return;
-    }
-    if (q >= npix)
-        return;
-    uint32_t px, py;
-    band_pixel(q, p, px, py);
-    const PixelState s = pixel_state<KIND>(px, py, p);
-    const double fx = static_cast<double>(px), fy = static_cast<double>(py);
-    if (p.spp < 8) { // too few samples to repay the per-pixel classification
-        out[q] = render_pixel<KIND, ACCUM, true, false>(s, p, fx, fy, s_poly, s_sob_d, false, 0,
-                                                         0, s_tab3);
-        return;
-    }
-    // warps with no pixel on the disc's edge skip the per-sample disc test;
-    // warps whose footprints each keep one sine quadrant per axis skip the
-    // per-sample quadrant count (both choices warp-uniform)
-    const int disc = disc_class(px, py, p.inv_w, p.inv_h, p.sc.disc_r2);
-    int qx, qy;
-    const bool fixed = sin_fixed_quadrant(fx * p.inv_w, (fx + 1.0) * p.inv_w, p.sc, qx) &&
-                       sin_fixed_quadrant(fy * p.inv_h, (fy + 1.0) * p.inv_h, p.sc, qy);
-    const unsigned mask = __activemask();
-    const bool test = __any_sync(mask, disc == kDiscTest);
-    const bool inside = disc == kDiscInside;
-    if (__all_sync(mask, fixed)) {
-        out[q] = test ? render_pixel<KIND, ACCUM, true, true>(s, p, fx, fy, s_poly, s_sob_d, false,
-                                                               qx, qy, s_tab3)
-                      : render_pixel<KIND, ACCUM, false, true>(s, p, fx, fy, s_poly, s_sob_d,
-                                                                inside, qx, qy, s_tab3);
+#undef QMC_UQ_CASE
+    } else if (wc.fixed) {
+        // warps with no pixel on the disc's edge skip the per-sample disc
+        // test; warps whose footprints each keep one sine quadrant per axis
+        // skip the per-sample quadrant count (both choices warp-uniform)
+        r = wc.test ? render_pixel<KIND, ACCUM, true, true>(s, p, fx, fy, sm.poly, sm.sob_d, false,
+                                                             qx, qy, sm.tab3)
+                    : render_pixel<KIND, ACCUM, false, true>(s, p, fx, fy, sm.poly, sm.sob_d,
+                                                              inside, qx, qy, sm.tab3);
     } else {
-        out[q] = test ? render_pixel<KIND, ACCUM, true, false>(s, p, fx, fy, s_poly, s_sob_d,
-                                                                false, 0, 0, s_tab3)
-                      : render_pixel<KIND, ACCUM, false, false>(s, p, fx, fy, s_poly, s_sob_d,
-                                                                 inside, 0, 0, s_tab3);
+        r = wc.test ? render_pixel<KIND, ACCUM, true, false>(s, p, fx, fy, sm.poly, sm.sob_d, false,
+                                                              0, 0, sm.tab3)
+                    : render_pixel<KIND, ACCUM, false, false>(s, p, fx, fy, sm.poly, sm.sob_d,
+                                                               inside, 0, 0, sm.tab3);
     }
+    out[wc.o] = r;
 }
 
 // Few pixels, many samples (npix < kWarpPixels, spp >= 64): one warp per
@@ -606,6 +698,11 @@ __global__ void k_scene_value(const double* __restrict__ xy, double* __restrict_
         out[k] = scene_value(xy[2 * k], xy[2 * k + 1]);
 }
 
+// The kinds whose k_render<.., true> measured faster (4K, 8-64 spp): sobol,
+// lattice, pixel-shifted / pixel-random lattice, sobol-xor-table. The
+// Halton kinds' phi_3 digit work needs the registers more: +8-16 % without.
+constexpr uint32_t kRenderUqKinds = 0xb5u;
+
 constexpr uint64_t kWarpPixels = 32768; // below this (and spp >= 64): warp per pixel
 
 template <uint32_t KIND>
@@ -621,12 +718,20 @@ cudaError_t render_kind(const RenderParams& p, uint32_t accum, float* out, cudaS
         return cudaGetLastError();
     }
     unsigned grid = static_cast<unsigned>((npix + kBlock - 1) / kBlock);
-    if (kLowSppStride<KIND> && p.spp < 8) // grid-stride: about one wave of resident CTAs
-        grid = std::min(grid, static_cast<unsigned>(sm_count()) * 8u);
+    if (p.spp < 8) {
+        if (kLowSppStride<KIND>) // grid-stride: about one wave of resident CTAs
+            grid = std::min(grid, static_cast<unsigned>(sm_count()) * 8u);
+        if (accum == 0)
+            k_render_low<KIND, 0><<<grid, kBlock, 0, s>>>(p, out);
+        else
+            k_render_low<KIND, 1><<<grid, kBlock, 0, s>>>(p, out);
+        return cudaGetLastError();
+    }
+    constexpr bool kUq = (kRenderUqKinds >> KIND) & 1u;
     if (accum == 0)
-        k_render<KIND, 0><<<grid, kBlock, 0, s>>>(p, out);
+        k_render<KIND, 0, kUq><<<grid, kBlock, 0, s>>>(p, out);
     else
-        k_render<KIND, 1><<<grid, kBlock, 0, s>>>(p, out);
+        k_render<KIND, 1, kUq><<<grid, kBlock, 0, s>>>(p, out);
     return cudaGetLastError();
 }
 

@@ -443,6 +443,32 @@ def test_render_bands_equal_full():
     np.testing.assert_array_equal(np.concatenate(bands), full)
 
 
+@pytest.mark.parametrize("kind", q.SAMPLER_KINDS)
+def test_render_ragged_columns_vs_reference(ref, kind):
+    """spp >= 8 renders through k_render's column order (columns grouped by
+    sine-quadrant parity, host::render_column_order) and its per-warp
+    classification: a width that is no multiple of 32 and crosses quadrant
+    boundaries mid-warp, int bit-identical, Kahan within 1e-6."""
+    w, h, spp = 333, 77, 16
+    for accum in ("int", "kahan"):
+        exp = np.zeros((h, w), np.float32)
+        assert ref.ref_render(w, h, spp, kind.encode(), accum.encode(), 0, 8, ptr(exp)) == 0
+        got = q.render(w, h, spp, kind=kind, accum=accum).cpu().numpy()
+        if accum == "int":
+            np.testing.assert_array_equal(got, exp)
+        else:
+            rel = np.abs(got.astype(np.float64) - exp) / np.maximum(np.abs(exp), 1e-30)
+            assert rel.max() <= 1e-6, rel.max()
+
+
+def test_render_bands_equal_full_classified():
+    """Row bands at spp >= 8 (the column-ordered kernel) tile the image."""
+    full = q.render(333, 77, 16).cpu().numpy()
+    bands = [q.render(333, 77, 16, rows=(r0, r1)).cpu().numpy()
+             for r0, r1 in [(0, 5), (5, 40), (40, 77)]]
+    np.testing.assert_array_equal(np.concatenate(bands), full)
+
+
 def test_render_seeded_sobol_vs_reference(ref):
     exp = np.zeros((32, 32), np.float32)
     assert ref.ref_render(32, 32, 8, b"sobol", b"int", 99, 4, ptr(exp)) == 0
