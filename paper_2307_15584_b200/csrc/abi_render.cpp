@@ -52,6 +52,7 @@ void resolve_render(const qmc_render_job* job, uint32_t row_begin, uint32_t row_
     p.small_band = static_cast<uint64_t>(row_end - row_begin) * job->width < (1ull << 32) ? 1u : 0u;
     p.inv_spp = (job->spp & (job->spp - 1)) == 0 ? 1.0 / job->spp : 0.0;
     p.colmap = job->spp >= 8 ? render_column_order(job->width) : nullptr;
+    p.q3 = render_phi3_quotients();
     std::vector<uint32_t> g = job->generator && job->generator_dims
                                   ? std::vector<uint32_t>(job->generator,
                                                           job->generator + job->generator_dims)
@@ -90,6 +91,8 @@ void resolve_render(const qmc_render_job* job, uint32_t row_begin, uint32_t row_
         p.stride = he.stride;
         p.crt_x = he.crt_x;
         p.crt_y = he.crt_y;
+        p.dlo3 = he.sx % 2187u;
+        p.dhi3 = he.sx / 2187u;
     }
     if (kind == QMC_KIND_SOBOL_XOR_TABLE) {
         uint32_t pc = 1;

@@ -144,6 +144,8 @@ DigitTable digit_table(uint32_t b, uint32_t mode, uint32_t factor, uint32_t min_
 const uint64_t* pow_magic(uint32_t b);
 // k_render's column order for an image `width` wide (kernels_render.cu).
 const uint32_t* render_column_order(uint32_t width);
+// phi_3 quotient tables of the render (kernels_render.cu, phi3_q).
+const uint32_t* render_phi3_quotients();
 std::vector<RadicalDim> radical_dims(uint32_t dims, uint32_t first_prime, qmc_radical_scramble sc,
                                      const uint32_t* factors, std::vector<uint32_t>& sigma_pool,
                                      std::vector<size_t>& sigma_off);

@@ -358,6 +358,29 @@ const uint32_t* render_column_order(uint32_t width)
     return static_cast<const uint32_t*>(slot.get());
 }
 
+// [floor(T[v] 2^32 / 3^7) | floor(T[v] 2^32 / 3^14)], v < 3^7, T[v] the
+// 7-digit base-3 reversal of v (kernels_render.cu, phi3_q).
+const uint32_t* render_phi3_quotients()
+{
+    static std::mutex mu;
+    static std::map<int, DevPtr> cache;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(mu);
+    auto& slot = cache[dev];
+    if (!slot) {
+        std::vector<uint32_t> q(2 * 2187);
+        for (uint32_t v = 0; v < 2187; ++v) {
+            uint32_t t = 0;
+            for (uint32_t k = 0, r = v; k < 7; ++k, r /= 3)
+                t = t * 3 + r % 3;
+            q[v] = static_cast<uint32_t>((static_cast<uint64_t>(t) << 32) / 2187u);
+            q[2187 + v] = static_cast<uint32_t>((static_cast<uint64_t>(t) << 32) / 4782969u);
+        }
+        slot = dev_upload(q.data(), q.size() * 4);
+    }
+    return static_cast<const uint32_t*>(slot.get());
+}
+
 const uint64_t* pow_magic(uint32_t b)
 {
     static std::mutex mu;

@@ -75,6 +75,8 @@ struct RenderParams {
     uint32_t small_band;          // rows * width < 2^32: 32-bit pixel indexing
     double inv_spp;               // 1 / spp when spp is a power of two (exact), else 0
     const uint32_t* colmap;       // device, k_render's column order at spp >= 8 (or null)
+    const uint32_t* q3;           // device, phi3_q's quotient tables (2 x 3^7 words)
+    uint32_t dlo3, dhi3;          // image-plane halton: scale_x = dhi3 * 3^7 + dlo3
 };
 
 // Per-stream (one pixel context) parameters for qmc_stream_fill kinds that

@@ -80,12 +80,38 @@ __device__ __forceinline__ uint32_t rad2(uint32_t i) { return brev32(i & 0x7ffff
 // Component j in {0,1} of sample i (SampleStream::sample, imageplane.cpp:
 // 427-461) at the integer stage, for the render's 2-dim streams.
 // SMEM_T3: t3 is a shared-memory copy of the 3^7-entry phi_3 table.
-template <uint32_t KIND, bool SMEM_T3 = false>
+// phi_3 (u32 fixed point) of n = hi * 3^7 + lo < 3^14 from the quotient
+// tables q3 = [floor(T[v] 2^32 / 3^7) | floor(T[v] 2^32 / 3^14)], T the
+// 7-digit reversal: phi_3(n) = floor(2^32 (T[lo] / 3^7 + T[hi] / 3^14)). With
+// S = q3[lo] + q3[3^7 + hi], the dropped fractions sum to F / 3^14 with
+// F < 2 * 3^14 < 2^32 and 3^14 (S + F / 3^14) = 2^32 (T[lo] 3^7 + T[hi]), so
+// F = -3^14 S mod 2^32 and phi_3(n) = S + (F >= 3^14) — the same value as
+// phi3_fixed's two-step branch (frac_div_magic of T[lo] 3^7 + T[hi]).
+// a_lo, a_hi: the shared-memory addresses of q3[lo] and q3[3^7 + hi].
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a)
+{
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a)); // read-only after staging
+    return v;
+}
+__device__ __forceinline__ uint32_t phi3_q(uint32_t a_lo, uint32_t a_hi)
+{
+    const uint32_t s = lds_u32(a_lo) + lds_u32(a_hi);
+    return s + (s * (0u - 4782969u) >= 4782969u ? 1u : 0u);
+}
+
+// INC3 (KIND 1 and 6): sob0 / sob1 carry the shared-memory addresses of
+// q3[lo] and q3[3^7 + hi] for the (lo, hi) base-3^7 digits of the phi_3
+// index, advanced by the caller.
+template <uint32_t KIND, bool SMEM_T3 = false, bool INC3 = false>
 __device__ __forceinline__ void sample2(uint32_t i, const PixelState& s, const RenderParams& p,
                                         uint32_t& x0, uint32_t& x1, uint32_t& sob0,
                                         uint32_t& sob1, const uint32_t* t3)
 {
-    if (KIND == 0) { // sobol: natural-order incremental, caller advances
+    if (INC3 && (KIND == 1 || KIND == 6)) {
+        x0 = KIND == 1 ? rad2(i) : rad2(s.ipx0 + i * p.scale_y);
+        x1 = phi3_q(sob0, sob1);
+    } else if (KIND == 0) { // sobol: natural-order incremental, caller advances
         x0 = sob0;
         x1 = sob1;
     } else if (KIND == 1) { // halton (plain)
@@ -154,7 +180,7 @@ __device__ __forceinline__ void sobol_direct2(uint32_t i, const RenderParams& p,
 // and the integrand. sob0/sob1: the Sobol' value of index i (KIND 0).
 // UQ >= 0: the warp shares qx and qy, UQ = their parities (scene_value_uq).
 template <uint32_t KIND, bool DISC_TEST = true, bool FIXED_Q = false, bool SMEM_T3 = false,
-          int UQ = -1>
+          int UQ = -1, bool INC3 = false>
 __device__ __forceinline__ double pixel_sample(uint32_t i, const PixelState& s,
                                                const RenderParams& p, double fx, double fy,
                                                const double2* s_poly, uint32_t sob0,
@@ -162,7 +188,7 @@ __device__ __forceinline__ double pixel_sample(uint32_t i, const PixelState& s,
                                                int qy = 0, const uint32_t* s_tab3 = nullptr)
 {
     uint32_t a, b;
-    sample2<KIND, SMEM_T3>(i, s, p, a, b, sob0, sob1, SMEM_T3 ? s_tab3 : p.tab3);
+    sample2<KIND, SMEM_T3, INC3>(i, s, p, a, b, sob0, sob1, SMEM_T3 || INC3 ? s_tab3 : p.tab3);
     const double u = static_cast<double>(map_u32(a));
     const double v = static_cast<double>(map_u32(b));
     const double x = __dmul_rn(__dadd_rn(fx, u), p.inv_w);
@@ -199,7 +225,10 @@ __device__ __forceinline__ float finish_int(long long isum, uint32_t spp, double
 }
 
 // The sequential per-pixel sample loop of k_render (render.cpp:61-78).
-template <uint32_t KIND, uint32_t ACCUM, bool DISC_TEST, bool FIXED_Q, int UQ = -1>
+// INC3: s_tab3 is the q3 quotient table and the phi_3 index advances as
+// base-3^7 digits (the caller checked that it stays below 3^14).
+template <uint32_t KIND, uint32_t ACCUM, bool DISC_TEST, bool FIXED_Q, int UQ = -1,
+          bool INC3 = false>
 __device__ __forceinline__ float render_pixel(const PixelState& s, const RenderParams& p,
                                               double fx, double fy, const double2* s_poly,
                                               const uint32_t* sob_d, bool inside_px, int qx,
@@ -207,13 +236,23 @@ __device__ __forceinline__ float render_pixel(const PixelState& s, const RenderP
 {
     constexpr bool kSmemT3 = KIND == 1 || KIND == 3 || KIND == 6;
     uint32_t sob0 = p.scr0, sob1 = p.scr1; // sobol index 0 value
+    uint32_t dlo = 0, dhi = 0, a_end = 0;
+    if (INC3) { // image-plane halton: n = ipy0 + i * scale_x; halton: n = i
+        const uint32_t n0 = KIND == 6 ? s.ipy0 : 0u;
+        const uint32_t hi = n0 / 2187u, base = static_cast<uint32_t>(__cvta_generic_to_shared(s_tab3));
+        sob0 = base + 4u * (n0 - 2187u * hi);
+        sob1 = base + 4u * (2187u + hi);
+        a_end = base + 4u * 2187u;
+        dlo = 4u * (KIND == 6 ? p.dlo3 : 1u);
+        dhi = 4u * (KIND == 6 ? p.dhi3 : 0u);
+    }
     double sum = 0.0, comp = 0.0;
     long long isum = 0;
     // BIG: Neumaier's |sum| >= |v| branch is known to hold
     auto run = [&](uint32_t i0, uint32_t i1, auto big) {
 #pragma unroll 2
         for (uint32_t i = i0; i < i1; ++i) {
-            const double f = pixel_sample<KIND, DISC_TEST, FIXED_Q, kSmemT3, UQ>(
+            const double f = pixel_sample<KIND, DISC_TEST, FIXED_Q, kSmemT3, UQ, INC3>(
                 i, s, p, fx, fy, s_poly, sob0, sob1, inside_px, qx, qy, s_tab3);
             if (ACCUM != 0)
                 isum += int_term(f);
@@ -221,7 +260,14 @@ __device__ __forceinline__ float render_pixel(const PixelState& s, const RenderP
                 neumaier_add_big(sum, comp, f);
             else
                 neumaier_add(sum, comp, f);
-            if (KIND == 0) { // x(i+1) = x(i) ^ D[ctz(i+1)], D[c] = C[0] ^ ... ^ C[c]
+            if (INC3) {
+                sob0 += dlo;
+                sob1 += dhi;
+                if (sob0 >= a_end) {
+                    sob0 -= 4u * 2187u;
+                    sob1 += 4u;
+                }
+            } else if (KIND == 0) { // x(i+1) = x(i) ^ D[ctz(i+1)], D[c] = C[0] ^ ... ^ C[c]
                 const uint32_t c = __ffs(static_cast<int>(i + 1)) - 1;
                 sob0 ^= sob_d[c];
                 sob1 ^= sob_d[32 + c];
@@ -305,17 +351,22 @@ __device__ __forceinline__ WarpClass classify_warp(bool valid, uint64_t q, const
 // instance only at spp >= 8 and for the kinds where it measured faster.
 // Shared-memory tables of the render kernels: the Sobol' prefix XORs (KIND
 // 0), the phi_3 table (the Halton kinds) and the sine coefficients.
-template <uint32_t KIND>
+template <uint32_t KIND, bool Q3 = false>
 struct RenderSmem {
     static constexpr bool kT3 = KIND == 1 || KIND == 3 || KIND == 6;
+    static constexpr bool kQ3 = Q3 && (KIND == 1 || KIND == 6); // k_render's INC3 kinds
     double2 poly[8];
     uint32_t sob_d[KIND == 0 ? 64 : 1]; // sobol: prefix XORs of the columns
     uint32_t tab3[kT3 ? 2187 : 1];      // halton kinds: 3^7 words
+    uint32_t q3[kQ3 ? 2 * 2187 : 1];    // phi3_q's quotient tables
 };
 
-template <uint32_t KIND>
-__device__ __forceinline__ void stage_render_smem(RenderSmem<KIND>& sm, const RenderParams& p)
+template <uint32_t KIND, bool Q3>
+__device__ __forceinline__ void stage_render_smem(RenderSmem<KIND, Q3>& sm, const RenderParams& p)
 {
+    if (RenderSmem<KIND, Q3>::kQ3)
+        for (uint32_t e = threadIdx.x; e < 2 * 2187; e += blockDim.x)
+            sm.q3[e] = __ldg(p.q3 + e);
     if (KIND == 0 && threadIdx.x < 64) {
         const uint32_t dim = threadIdx.x >> 5, c = threadIdx.x & 31u;
         uint32_t d = 0;
@@ -323,7 +374,7 @@ __device__ __forceinline__ void stage_render_smem(RenderSmem<KIND>& sm, const Re
             d ^= __ldg(p.cols2 + 52 * dim + k);
         sm.sob_d[threadIdx.x] = d;
     }
-    if (RenderSmem<KIND>::kT3)
+    if (RenderSmem<KIND, Q3>::kT3)
         for (uint32_t e = threadIdx.x; e < 2187; e += blockDim.x)
             sm.tab3[e] = __ldg(p.tab3 + e);
     load_sin_poly(sm.poly); // includes the barrier
@@ -359,22 +410,49 @@ __global__ void __launch_bounds__(kBlock) k_render_low(RenderParams p, float* __
 // column order nor the path changes an output bit. UQ costs registers (the
 // generic paths and the specialised loops share the kernel), so render_kind
 // launches the UQ instance only for the kinds where it measured faster.
-template <uint32_t KIND, uint32_t ACCUM, bool UQ>
-__global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __restrict__ out)
+template <uint32_t KIND, uint32_t ACCUM, bool UQ, bool Q3>
+__device__ __forceinline__ void render_classified(const WarpClass& wc,
+                                                  const RenderSmem<KIND, Q3>& sm,
+                                                  const RenderParams& p, float* __restrict__ out)
 {
-    const uint64_t npix = static_cast<uint64_t>(p.row_end - p.row_begin) * p.width;
-    const uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const bool valid = q < npix;
-    const WarpClass wc = classify_warp(valid, q, p);
-    __shared__ RenderSmem<KIND> sm;
-    stage_render_smem(sm, p);
-    if (!valid)
-        return;
     const PixelState s = pixel_state<KIND>(wc.px, wc.py, p);
     const double fx = static_cast<double>(wc.px), fy = static_cast<double>(wc.py);
     const bool inside = wc.inside;
     const int qx = wc.qx, qy = wc.qy;
     float r;
+    if constexpr (RenderSmem<KIND, Q3>::kQ3) {
+        // the phi_3 index of every sample below 3^14: the incremental
+        // quotient-table path (phi3_q), warp-uniform
+        const uint64_t nmax = (KIND == 6 ? static_cast<uint64_t>(s.ipy0) : 0ull) +
+                              static_cast<uint64_t>(p.spp - 1) * (KIND == 6 ? p.scale_x : 1u);
+        if (__all_sync(__activemask(), nmax < 4782969ull)) {
+            if (UQ && wc.uniform) {
+#define QMC_UQ3_CASE(U)                                                                            \
+    r = wc.test ? render_pixel<KIND, ACCUM, true, true, U, true>(s, p, fx, fy, sm.poly, sm.sob_d,  \
+                                                                 false, qx, qy, sm.q3)            \
+                : render_pixel<KIND, ACCUM, false, true, U, true>(s, p, fx, fy, sm.poly, sm.sob_d, \
+                                                                  inside, qx, qy, sm.q3)
+                switch ((qx & 1) | (qy & 1) << 1) {
+                case 0: QMC_UQ3_CASE(0); break;
+                case 1: QMC_UQ3_CASE(1); break;
+                case 2: QMC_UQ3_CASE(2); break;
+                default: QMC_UQ3_CASE(3); break;
+                }
+#undef QMC_UQ3_CASE
+            } else if (wc.fixed)
+                r = wc.test ? render_pixel<KIND, ACCUM, true, true, -1, true>(
+                                  s, p, fx, fy, sm.poly, sm.sob_d, false, qx, qy, sm.q3)
+                            : render_pixel<KIND, ACCUM, false, true, -1, true>(
+                                  s, p, fx, fy, sm.poly, sm.sob_d, inside, qx, qy, sm.q3);
+            else
+                r = wc.test ? render_pixel<KIND, ACCUM, true, false, -1, true>(
+                                  s, p, fx, fy, sm.poly, sm.sob_d, false, 0, 0, sm.q3)
+                            : render_pixel<KIND, ACCUM, false, false, -1, true>(
+                                  s, p, fx, fy, sm.poly, sm.sob_d, inside, 0, 0, sm.q3);
+            out[wc.o] = r;
+            return;
+        }
+    }
     if (UQ && wc.uniform) {
         // four parities x disc test: warp-uniform choices
 #define QMC_UQ_CASE(U)                                                                             \
@@ -404,6 +482,25 @@ __global__ void __launch_bounds__(kBlock) k_render(RenderParams p, float* __rest
                                                                inside, 0, 0, sm.tab3);
     }
     out[wc.o] = r;
+}
+
+// Q3: the incremental phi3_q path of the image-plane / plain Halton kinds
+// (17.5 KB of quotient tables per CTA: render_kind enables it from 32 spp,
+// where the per-CTA staging is repaid).
+#ifndef QMC_RENDER_Q3_MINB
+#define QMC_RENDER_Q3_MINB 0
+#endif
+template <uint32_t KIND, uint32_t ACCUM, bool UQ, bool Q3>
+__global__ void __launch_bounds__(kBlock, Q3 ? QMC_RENDER_Q3_MINB : 0)
+    k_render(RenderParams p, float* __restrict__ out)
+{
+    const uint64_t npix = static_cast<uint64_t>(p.row_end - p.row_begin) * p.width;
+    const uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const WarpClass wc = classify_warp(q < npix, q, p);
+    __shared__ RenderSmem<KIND, Q3> sm;
+    stage_render_smem(sm, p);
+    if (q < npix)
+        render_classified<KIND, ACCUM, UQ, Q3>(wc, sm, p, out);
 }
 
 // Few pixels, many samples (npix < kWarpPixels, spp >= 64): one warp per
@@ -701,7 +798,10 @@ __global__ void k_scene_value(const double* __restrict__ xy, double* __restrict_
 // The kinds whose k_render<.., true> measured faster (4K, 8-64 spp): sobol,
 // lattice, pixel-shifted / pixel-random lattice, sobol-xor-table. The
 // Halton kinds' phi_3 digit work needs the registers more: +8-16 % without.
-constexpr uint32_t kRenderUqKinds = 0xb5u;
+#ifndef QMC_RENDER_UQ_KINDS
+#define QMC_RENDER_UQ_KINDS 0xb5u
+#endif
+constexpr uint32_t kRenderUqKinds = QMC_RENDER_UQ_KINDS;
 
 constexpr uint64_t kWarpPixels = 32768; // below this (and spp >= 64): warp per pixel
 
@@ -728,10 +828,17 @@ cudaError_t render_kind(const RenderParams& p, uint32_t accum, float* out, cudaS
         return cudaGetLastError();
     }
     constexpr bool kUq = (kRenderUqKinds >> KIND) & 1u;
-    if (accum == 0)
-        k_render<KIND, 0, kUq><<<grid, kBlock, 0, s>>>(p, out);
-    else
-        k_render<KIND, 1, kUq><<<grid, kBlock, 0, s>>>(p, out);
+    constexpr bool kHasQ3 = KIND == 1 || KIND == 6;
+    if (kHasQ3 && p.spp >= 32) { // the phi3_q path, with the specialised sine loop
+        if (accum == 0)
+            k_render<KIND, 0, true, kHasQ3><<<grid, kBlock, 0, s>>>(p, out);
+        else
+            k_render<KIND, 1, true, kHasQ3><<<grid, kBlock, 0, s>>>(p, out);
+    } else if (accum == 0) {
+        k_render<KIND, 0, kUq, false><<<grid, kBlock, 0, s>>>(p, out);
+    } else {
+        k_render<KIND, 1, kUq, false><<<grid, kBlock, 0, s>>>(p, out);
+    }
     return cudaGetLastError();
 }
 
