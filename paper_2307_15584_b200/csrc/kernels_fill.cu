@@ -325,6 +325,198 @@ __global__ void __launch_bounds__(kBlock)
     }
 }
 
+// Work split of the slab kernels: warps come in groups of nslab, one per
+// slab, and a group walks one contiguous range of 32-point tiles. The
+// slabs of a row are thus written by sibling warps at about the same time,
+// so a 128-B line that a slab boundary splits (row pitches that are no
+// multiple of 128 B) is completed in L2 before it is evicted.
+__device__ __forceinline__ bool slab_tiles(uint32_t nslab, uint64_t tile0, uint64_t ntp,
+                                           uint64_t per_group, uint32_t& slab, uint64_t& t,
+                                           uint64_t& tend)
+{
+    const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t group = warp / nslab;
+    slab = static_cast<uint32_t>(warp - group * nslab);
+    t = tile0 + group * per_group;
+    tend = t + per_group < tile0 + ntp ? t + per_group : tile0 + ntp;
+    return t < tend;
+}
+
+// Wide rows (dims a multiple of DPL whose rows the fast kernels cannot
+// tile: dims > 256, or dims up to 256 not dividing 256 / 128): the row is
+// cut into slabs of 32 * DPL dims, and a warp walks one slab, one point per
+// step, each lane DPL consecutive dims, with k_sobol_fast's step-mask
+// recurrence (32 steps per tile, the step from point i to i + 1 flips the
+// columns 0 .. ctz(i + 1)). Every warp store is one 32 * DPL-word row
+// segment (256-bit or 128-bit per lane), so the stream is as dense as the
+// fast kernels' whatever the row length (work split: slab_tiles).
+template <int DPL, int MODE, bool U32OUT>
+__global__ void __launch_bounds__(kBlock)
+    k_sobol_slab(const uint32_t* __restrict__ colsT, const __grid_constant__ SmallArgs args,
+                 uint32_t dims, uint64_t first, uint64_t n, uint64_t tile0, uint64_t ntp,
+                 uint32_t nslab, uint64_t per_group, uint32_t* __restrict__ out)
+{
+    constexpr uint32_t kSlab = 32 * DPL;
+    const uint32_t lane = threadIdx.x & 31u;
+    uint64_t t, tend;
+    uint32_t slab;
+    if (!slab_tiles(nslab, tile0, ntp, per_group, slab, t, tend))
+        return;
+    {
+        const uint32_t j0 = slab * kSlab + lane * DPL; // this lane's first dimension
+        const bool mine = j0 < dims;                    // dims % DPL == 0: all DPL or none
+        const uint32_t* cols = colsT + (mine ? j0 : 0u);
+        uint32_t D[5][DPL], c[DPL], seed[DPL], xr[DPL], xp[DPL];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            load_cols<DPL>(cols + k * dims, c);
+#pragma unroll
+            for (int e = 0; e < DPL; ++e)
+                D[k][e] = k ? D[k - 1][e] ^ c[e] : c[e];
+        }
+#pragma unroll
+        for (int e = 0; e < DPL; ++e)
+            seed[e] = xr[e] = xp[e] = 0;
+        if (const uint32_t* words = small_a(args)) {
+            if (MODE == 2)
+                load_small<DPL>(words + (mine ? j0 : 0u), seed);
+            else
+                load_small<DPL>(words + (mine ? j0 : 0u), xr);
+        }
+        uint32_t omul[DPL], oadd[DPL];
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) {
+            omul[e] = (seed[e] >> 16) | 1u;
+            oadd[e] = seed[e] * omul[e];
+        }
+        for (uint64_t b = t; b; b &= b - 1) { // value of the tile base t << 5
+            load_cols<DPL>(cols + (5 + __ffsll(static_cast<long long>(b)) - 1) * dims, c);
+#pragma unroll
+            for (int e = 0; e < DPL; ++e)
+                xp[e] ^= c[e];
+        }
+        for (;;) {
+            const uint64_t p0 = t << 5;
+            uint32_t x[DPL], y[DPL];
+#pragma unroll
+            for (int e = 0; e < DPL; ++e)
+                x[e] = xp[e] ^ xr[e];
+            const bool full = p0 >= first && p0 + 32 <= first + n;
+            uint32_t* o = out + (p0 - first) * dims + j0;
+            auto group = [&](uint32_t v, auto check) {
+#pragma unroll
+                for (uint32_t w = 0; w < 8; ++w) {
+                    const uint32_t k = 8 * v + w;
+#pragma unroll
+                    for (int e = 0; e < DPL; ++e) {
+                        uint32_t val = x[e];
+                        if (MODE == 2)
+                            val = brev32(owen_lk_folded(val, omul[e], oadd[e]));
+                        y[e] = U32OUT ? val : map_bits(val);
+                    }
+                    if (mine && (!decltype(check)::value || (p0 + k) - first < n))
+                        store_vec<DPL>(o + static_cast<uint64_t>(k) * dims, y);
+                    if (w < 7) {
+#pragma unroll
+                        for (int e = 0; e < DPL; ++e)
+                            x[e] ^= D[ctz_const(w + 1)][e];
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e < DPL; ++e)
+                    x[e] ^= (v == 1) ? D[4][e] : D[3][e];
+            };
+            if (full) {
+#pragma unroll 1
+                for (uint32_t v = 0; v < 4; ++v)
+                    group(v, std::false_type{});
+            } else {
+#pragma unroll 1
+                for (uint32_t v = 0; v < 4; ++v)
+                    group(v, std::true_type{});
+            }
+            if (++t >= tend)
+                break;
+            const int cz = __ffsll(static_cast<long long>(t)) - 1; // tile t-1 -> t
+            for (int k = 0; k <= cz; ++k) {
+                load_cols<DPL>(cols + (5 + k) * dims, c);
+#pragma unroll
+                for (int e = 0; e < DPL; ++e)
+                    xp[e] ^= c[e];
+            }
+        }
+    }
+}
+
+// Wide lattice rows, the slab layout of k_sobol_slab with k_lattice_fast's
+// arithmetic at one point per step: brev(p0 + u) = brev(p0) + brev5(u) << 27
+// for the 32 points u of a tile (disjoint bits), so each value is x0 plus a
+// compile-time multiple of g << 27.
+template <int DPL, bool U32OUT>
+__global__ void __launch_bounds__(kBlock)
+    k_lattice_slab(const __grid_constant__ SmallArgs args, uint32_t dims, uint64_t first,
+                   uint64_t n, uint64_t tile0, uint64_t ntp, uint32_t nslab, uint64_t per_group,
+                   uint32_t* __restrict__ out)
+{
+    constexpr uint32_t kSlab = 32 * DPL;
+    const uint32_t lane = threadIdx.x & 31u;
+    uint64_t t, tend;
+    uint32_t slab;
+    if (!slab_tiles(nslab, tile0, ntp, per_group, slab, t, tend))
+        return;
+    {
+        const uint32_t j0 = slab * kSlab + lane * DPL;
+        const bool mine = j0 < dims; // dims % DPL == 0: all DPL or none
+        uint32_t gv[DPL], sv[DPL], G[DPL];
+        load_small<DPL>(small_a(args) + (mine ? j0 : 0u), gv);
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) {
+            sv[e] = 0;
+            G[e] = gv[e] << 27;
+        }
+        if (const uint32_t* shifts = small_b(args))
+            load_small<DPL>(shifts + (mine ? j0 : 0u), sv);
+        for (; t < tend; ++t) {
+            const uint64_t p0 = t << 5;
+            const uint32_t b = brev32(static_cast<uint32_t>(p0));
+            uint32_t x0[DPL], y[DPL];
+#pragma unroll
+            for (int e = 0; e < DPL; ++e)
+                x0[e] = b * gv[e] + sv[e];
+            const bool full = p0 >= first && p0 + 32 <= first + n;
+            uint32_t* o = out + (p0 - first) * dims + j0;
+            auto group = [&](uint32_t v, auto check) {
+                const uint32_t cv = ((v & 1u) << 1) | (v >> 1);
+                uint32_t xv[DPL];
+#pragma unroll
+                for (int e = 0; e < DPL; ++e)
+                    xv[e] = x0[e] + cv * G[e];
+#pragma unroll
+                for (uint32_t w = 0; w < 8; ++w) {
+                    const uint32_t k = 8 * v + w;
+                    const uint32_t cw = (((w & 1u) << 2) | (w & 2u) | (w >> 2)) << 2;
+#pragma unroll
+                    for (int e = 0; e < DPL; ++e) {
+                        const uint32_t xx = xv[e] + cw * G[e];
+                        y[e] = U32OUT ? xx : map_bits(xx);
+                    }
+                    if (mine && (!decltype(check)::value || (p0 + k) - first < n))
+                        store_vec<DPL>(o + static_cast<uint64_t>(k) * dims, y);
+                }
+            };
+            if (full) {
+#pragma unroll 1
+                for (uint32_t v = 0; v < 4; ++v)
+                    group(v, std::false_type{});
+            } else {
+#pragma unroll 1
+                for (uint32_t v = 0; v < 4; ++v)
+                    group(v, std::true_type{});
+            }
+        }
+    }
+}
+
 // Any dims whose tables fit shared memory (dims <= kElemMaxDims), element-
 // wise with no transpose: a CTA owns a contiguous range of output words,
 // walked in chunks of at most 1024 points. Word (p, j) is
@@ -1851,6 +2043,39 @@ bool launch_bulk_fill(const W& w, uint32_t dims, const FillRange& r, cudaStream_
     return true;
 }
 
+// Slab width per lane for the wide-row kernels: 8 dims (256-bit stores)
+// unless 4 leaves fewer idle lanes; 0 when the rows are not 16-B multiples.
+int slab_dpl(uint32_t dims, const FillRange& r)
+{
+    const uintptr_t a = reinterpret_cast<uintptr_t>(r.out);
+    const bool ok8 = dims % 8 == 0 && (a & 31u) == 0, ok4 = dims % 4 == 0 && (a & 15u) == 0;
+    if (ok8 && !(ok4 && (dims + 127) / 128 * 128 < (dims + 255) / 256 * 256))
+        return 8;
+    return ok4 ? 4 : 0;
+}
+
+// Grid of a slab kernel: groups of nslab warps (slab_tiles), as many groups
+// as the resident warps allow, each a contiguous range of 32-point tiles.
+template <class K, class... A>
+cudaError_t launch_slab(K kern, uint32_t dims, uint32_t slab, const FillRange& r, cudaStream_t s,
+                        A... pre)
+{
+    const uint64_t tile0 = r.first >> 5, tile1 = (r.first + r.n + 31) >> 5;
+    const uint64_t ntp = tile1 - tile0;
+    const uint32_t nslab = (dims + slab - 1) / slab;
+    const uint64_t max_warps =
+        static_cast<uint64_t>(sm_count()) * blocks_per_sm(kern) * (kBlock / 32);
+    uint64_t groups = max_warps / nslab;
+    groups = groups < 1 ? 1 : (groups < ntp ? groups : ntp);
+    const uint64_t per_group = (ntp + groups - 1) / groups;
+    const uint64_t used = (ntp + per_group - 1) / per_group;
+    const unsigned grid =
+        static_cast<unsigned>((used * nslab * 32 + kBlock - 1) / kBlock);
+    kern<<<grid, kBlock, 0, s>>>(pre..., dims, r.first, r.n, tile0, ntp, nslab, per_group,
+                                 static_cast<uint32_t*>(r.out));
+    return cudaGetLastError();
+}
+
 cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const SmallArgs& words,
                          uint32_t dims, int mode, bool u32, const FillRange& r, cudaStream_t s)
 {
@@ -1881,6 +2106,18 @@ cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const
                                 : launch_tiled(k_sobol_narrow<2, 2, false>, kLogTp2, r, s, cols, words))
                          : (u32 ? launch_tiled(k_sobol_narrow<2, 0, true>, kLogTp2, r, s, cols, words)
                                 : launch_tiled(k_sobol_narrow<2, 0, false>, kLogTp2, r, s, cols, words));
+    }
+    // wide rows: slabs of 32 * DPL dims (k_sobol_slab)
+    if (const int sdpl = dims > 64 ? slab_dpl(dims, r) : 0) {
+        if (sdpl == 8)
+            return mode == 2 ? (u32 ? launch_slab(k_sobol_slab<8, 2, true>, dims, 256, r, s, cols, words)
+                                    : launch_slab(k_sobol_slab<8, 2, false>, dims, 256, r, s, cols, words))
+                             : (u32 ? launch_slab(k_sobol_slab<8, 0, true>, dims, 256, r, s, cols, words)
+                                    : launch_slab(k_sobol_slab<8, 0, false>, dims, 256, r, s, cols, words));
+        return mode == 2 ? (u32 ? launch_slab(k_sobol_slab<4, 2, true>, dims, 128, r, s, cols, words)
+                                : launch_slab(k_sobol_slab<4, 2, false>, dims, 128, r, s, cols, words))
+                         : (u32 ? launch_slab(k_sobol_slab<4, 0, true>, dims, 128, r, s, cols, words)
+                                : launch_slab(k_sobol_slab<4, 0, false>, dims, 128, r, s, cols, words));
     }
     // one dimension per warp (k_tma for dims % 32 == 0, else k_runs for dims
     // <= 32) from a 32-aligned index; the few points before it go through
@@ -2024,6 +2261,11 @@ cudaError_t launch_lattice(const SmallArgs& args, uint32_t dims, bool u32, const
         return u32 ? launch_tiled(k_lattice_narrow<2, true>, 12, r, s, nullptr, args)
                    : launch_tiled(k_lattice_narrow<2, false>, 12, r, s, nullptr, args);
     }
+    if (const int sdpl = dims > 64 ? slab_dpl(dims, r) : 0) // wide rows (k_lattice_slab)
+        return sdpl == 8 ? (u32 ? launch_slab(k_lattice_slab<8, true>, dims, 256, r, s, args)
+                                : launch_slab(k_lattice_slab<8, false>, dims, 256, r, s, args))
+                         : (u32 ? launch_slab(k_lattice_slab<4, true>, dims, 128, r, s, args)
+                                : launch_slab(k_lattice_slab<4, false>, dims, 128, r, s, args));
     const Div32 d = dims >= 2 ? make_div32(dims) : Div32{0, 0};
     return launch_chunked(dims, r, [&](unsigned grid, uint64_t first, uint32_t elems, uint32_t* o) {
         k_lattice_generic<<<grid, kBlock, 0, s>>>(args, dims, d, first, elems, u32, o);

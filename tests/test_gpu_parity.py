@@ -263,8 +263,9 @@ def test_sobol_owen_vs_oracle(oracle, columns64, golden_arrays, mapv, dims):
 @pytest.mark.parametrize("scramble", ["none", "xor", "owen"])
 def test_sobol_walk_dims_vs_oracle(oracle, columns64, dims, scramble):
     """One dimension per warp (k_runs for dims <= 32, k_tma column blocks for
-    dims % 32 == 0): several sub-tiles per run, the 1024-index block steps,
-    an unaligned first (head through the element-wise path), a ragged end."""
+    dims % 32 == 0) and, for wider rows, the slab kernel (k_sobol_slab):
+    several sub-tiles per run, the 1024-index block steps, an unaligned first
+    (head through the element-wise path), a ragged end."""
     rng = np.random.default_rng(dims)
     if dims <= 64:
         cols = np.ascontiguousarray(columns64[:dims])
@@ -290,11 +291,12 @@ def test_sobol_walk_dims_vs_oracle(oracle, columns64, dims, scramble):
         np.testing.assert_array_equal(got, exp, err_msg=f"first={first}")
 
 
-@pytest.mark.parametrize("dims", [200, 700, 1000, 2500])
+@pytest.mark.parametrize("dims", [200, 700, 1000, 2500, 3000, 1001])
 @pytest.mark.parametrize("scramble", ["xor", "owen"])
 def test_sobol_many_dims_vs_oracle(oracle, dims, scramble):
     """Direction-number sets with hundreds to thousands of dimensions: the
-    1024-thread tiled path and, past what a tile holds, the per-element path."""
+    slab kernel (dims % 4 == 0) and, for the other widths, the 1024-thread
+    tiled path or, past what a tile holds, the per-element path."""
     rng = np.random.default_rng(dims)
     cols = rng.integers(0, 2**32, (dims, 52), dtype=np.uint64).astype(np.uint32)
     m = q.GeneratorMatrixSet.from_columns(cols)
@@ -336,17 +338,25 @@ def test_lattice_vs_golden(golden_arrays, golden, oracle):
     assert fnv(oracle, u32(f)) == golden["lattice_cp_f32_wrap_fnv"]
 
 
-@pytest.mark.parametrize("dims", [1, 2, 3, 4, 8, 16, 32, 64, 128])
+@pytest.mark.parametrize("dims", [1, 2, 3, 4, 8, 16, 32, 64, 128, 96, 100, 200, 1000, 3000])
 def test_lattice_dims_vs_oracle(oracle, dims):
+    """Fast tiles (dims dividing 256 / 128), narrow kernels, and the wide-row
+    slab kernel (dims > 64 otherwise, k_lattice_slab) across the 2^32 wrap."""
     rng = np.random.default_rng(dims)
     g = (rng.integers(0, 1 << 31, dims) * 2 + 1).astype(np.uint32)
     s = rng.integers(0, 1 << 32, dims, dtype=np.uint64).astype(np.uint32)
     first, n = (1 << 32) - 1000, 2100
     got = u32(q.lattice_fill(n, g, first=first, shifts=s, fixed=True)).reshape(n, dims)
+    cols = range(dims) if dims <= 200 else sorted(set(range(0, dims, 37)) | {dims - 1})
     for k in range(0, n, 13):
         i = (first + k) & 0xFFFFFFFF
-        for j in range(dims):
+        for j in cols:
             assert got[k, j] == oracle.qo_lattice_cp_fixed(i, int(g[j]), int(s[j]))
+    # float output of the same points: the bit-exact map of the integers
+    f = q.lattice_fill(n, g, first=first, shifts=s).cpu().numpy().reshape(n, dims)
+    for k in (0, 999, 1000, n - 1):
+        for j in cols:
+            assert f.view(np.uint32)[k, j] == oracle.qo_map_bits(int(got[k, j]))
 
 
 # ------------------------------------------------------- stream façade
