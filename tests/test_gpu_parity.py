@@ -192,10 +192,11 @@ def test_halton_fill_32_dims_small_and_ragged_vs_reference(ref):
             np.testing.assert_array_equal(f[:, j].view(np.uint32), mapped, err_msg=f"n={n} dim={j}")
 
 
-@pytest.mark.parametrize("dims", [64, 96, 256])
+@pytest.mark.parametrize("dims", [64, 96, 256, 36, 100, 300, 1000])
 def test_halton_fill_column_blocks_vs_reference(ref, dims):
-    """dims % 32 == 0 (k_halton_tma over 32-dimension column blocks: a CTA's
-    unit range crosses block boundaries, TMA boxes at column offset 32*cb)."""
+    """k_tma over 32-dimension column blocks (dims % 32 == 0, or dims % 4 == 0
+    with a partial last block that the tensor store clips): a CTA's unit
+    range crosses block boundaries, TMA boxes at column offset 32*cb."""
     n = 148 * 512 + 1000
     for first, mode in [(3486784401 - 20000, "linear"), (5, "faure")]:
         got = u32(q.halton_fill(n, dims, first=first, scramble=mode, fixed=True)).reshape(n, dims)
