@@ -162,6 +162,12 @@ __global__ void k_map_selfcheck(unsigned long long* count)
 template <int DPL>
 __device__ __forceinline__ void load_cols(const uint32_t* p, uint32_t (&v)[DPL])
 {
+    if constexpr (DPL < 4) { // the slab kernels' narrow lanes
+#pragma unroll
+        for (int e = 0; e < DPL; ++e)
+            v[e] = __ldg(p + e);
+        return;
+    }
 #pragma unroll
     for (int q = 0; q < DPL / 4; ++q) {
         const uint4 t = __ldg(reinterpret_cast<const uint4*>(p) + q);
@@ -197,6 +203,10 @@ __device__ __forceinline__ void store_vec(uint32_t* p, const uint32_t (&v)[DPL])
         asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]),
                      "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
                      : "memory");
+    } else if constexpr (DPL == 2) {
+        __stcs(reinterpret_cast<uint2*>(p), make_uint2(v[0], v[1]));
+    } else if constexpr (DPL == 1) {
+        __stcs(p, v[0]);
     } else {
         __stcs(reinterpret_cast<uint4*>(p), make_uint4(v[0], v[1], v[2], v[3]));
     }
@@ -2054,13 +2064,23 @@ bool launch_bulk_fill(const W& w, uint32_t dims, const FillRange& r, cudaStream_
 
 // Slab width per lane for the wide-row kernels: 8 dims (256-bit stores)
 // unless 4 leaves fewer idle lanes; 0 when the rows are not 16-B multiples.
-int slab_dpl(uint32_t dims, const FillRange& r)
+// narrow: also rows that are no multiple of 16 B (2 or 1 dims per lane).
+// Their row segments start mid-sector, so L2 merges partial sectors; that
+// measured 0.32-0.36 of the roofline at any width, better than the staged
+// per-dimension paths only for wide Sobol' rows (255 / 1001 / 2999 dims:
+// 0.13 / 0.15 / 0.05), worse at 65-127 dims (0.45 -> 0.27) and for the
+// lattice (0.76 -> 0.30).
+int slab_dpl(uint32_t dims, const FillRange& r, bool narrow = false)
 {
     const uintptr_t a = reinterpret_cast<uintptr_t>(r.out);
     const bool ok8 = dims % 8 == 0 && (a & 31u) == 0, ok4 = dims % 4 == 0 && (a & 15u) == 0;
     if (ok8 && !(ok4 && (dims + 127) / 128 * 128 < (dims + 255) / 256 * 256))
         return 8;
-    return ok4 ? 4 : 0;
+    if (ok4)
+        return 4;
+    if (!narrow)
+        return 0;
+    return dims % 2 == 0 && (a & 7u) == 0 ? 2 : 1;
 }
 
 // Grid of a slab kernel: groups of nslab warps (slab_tiles), as many groups
@@ -2117,16 +2137,26 @@ cudaError_t launch_sobol(const uint32_t* colsT, const uint32_t* colsT_rev, const
                                 : launch_tiled(k_sobol_narrow<2, 0, false>, kLogTp2, r, s, cols, words));
     }
     // wide rows: slabs of 32 * DPL dims (k_sobol_slab)
-    if (const int sdpl = dims > 64 ? slab_dpl(dims, r) : 0) {
+    if (const int sdpl = dims > 64 ? slab_dpl(dims, r, dims > 128) : 0) {
         if (sdpl == 8)
             return mode == 2 ? (u32 ? launch_slab(k_sobol_slab<8, 2, true>, dims, 256, r, s, cols, words)
                                     : launch_slab(k_sobol_slab<8, 2, false>, dims, 256, r, s, cols, words))
                              : (u32 ? launch_slab(k_sobol_slab<8, 0, true>, dims, 256, r, s, cols, words)
                                     : launch_slab(k_sobol_slab<8, 0, false>, dims, 256, r, s, cols, words));
-        return mode == 2 ? (u32 ? launch_slab(k_sobol_slab<4, 2, true>, dims, 128, r, s, cols, words)
-                                : launch_slab(k_sobol_slab<4, 2, false>, dims, 128, r, s, cols, words))
-                         : (u32 ? launch_slab(k_sobol_slab<4, 0, true>, dims, 128, r, s, cols, words)
-                                : launch_slab(k_sobol_slab<4, 0, false>, dims, 128, r, s, cols, words));
+        if (sdpl == 4)
+            return mode == 2 ? (u32 ? launch_slab(k_sobol_slab<4, 2, true>, dims, 128, r, s, cols, words)
+                                    : launch_slab(k_sobol_slab<4, 2, false>, dims, 128, r, s, cols, words))
+                             : (u32 ? launch_slab(k_sobol_slab<4, 0, true>, dims, 128, r, s, cols, words)
+                                    : launch_slab(k_sobol_slab<4, 0, false>, dims, 128, r, s, cols, words));
+        if (sdpl == 2)
+            return mode == 2 ? (u32 ? launch_slab(k_sobol_slab<2, 2, true>, dims, 64, r, s, cols, words)
+                                    : launch_slab(k_sobol_slab<2, 2, false>, dims, 64, r, s, cols, words))
+                             : (u32 ? launch_slab(k_sobol_slab<2, 0, true>, dims, 64, r, s, cols, words)
+                                    : launch_slab(k_sobol_slab<2, 0, false>, dims, 64, r, s, cols, words));
+        return mode == 2 ? (u32 ? launch_slab(k_sobol_slab<1, 2, true>, dims, 32, r, s, cols, words)
+                                : launch_slab(k_sobol_slab<1, 2, false>, dims, 32, r, s, cols, words))
+                         : (u32 ? launch_slab(k_sobol_slab<1, 0, true>, dims, 32, r, s, cols, words)
+                                : launch_slab(k_sobol_slab<1, 0, false>, dims, 32, r, s, cols, words));
     }
     // one dimension per warp (k_tma for dims % 32 == 0, else k_runs for dims
     // <= 32) from a 32-aligned index; the few points before it go through
@@ -2271,10 +2301,10 @@ cudaError_t launch_lattice(const SmallArgs& args, uint32_t dims, bool u32, const
                    : launch_tiled(k_lattice_narrow<2, false>, 12, r, s, nullptr, args);
     }
     if (const int sdpl = dims > 64 ? slab_dpl(dims, r) : 0) // wide rows (k_lattice_slab)
-        return sdpl == 8 ? (u32 ? launch_slab(k_lattice_slab<8, true>, dims, 256, r, s, args)
-                                : launch_slab(k_lattice_slab<8, false>, dims, 256, r, s, args))
-                         : (u32 ? launch_slab(k_lattice_slab<4, true>, dims, 128, r, s, args)
-                                : launch_slab(k_lattice_slab<4, false>, dims, 128, r, s, args));
+        return sdpl == 8   ? (u32 ? launch_slab(k_lattice_slab<8, true>, dims, 256, r, s, args)
+                                  : launch_slab(k_lattice_slab<8, false>, dims, 256, r, s, args))
+                           : (u32 ? launch_slab(k_lattice_slab<4, true>, dims, 128, r, s, args)
+                                  : launch_slab(k_lattice_slab<4, false>, dims, 128, r, s, args));
     const Div32 d = dims >= 2 ? make_div32(dims) : Div32{0, 0};
     return launch_chunked(dims, r, [&](unsigned grid, uint64_t first, uint32_t elems, uint32_t* o) {
         k_lattice_generic<<<grid, kBlock, 0, s>>>(args, dims, d, first, elems, u32, o);

@@ -292,12 +292,12 @@ def test_sobol_walk_dims_vs_oracle(oracle, columns64, dims, scramble):
         np.testing.assert_array_equal(got, exp, err_msg=f"first={first}")
 
 
-@pytest.mark.parametrize("dims", [200, 700, 1000, 2500, 3000, 1001])
+@pytest.mark.parametrize("dims", [200, 700, 1000, 2500, 3000, 1001, 255, 1002])
 @pytest.mark.parametrize("scramble", ["xor", "owen"])
 def test_sobol_many_dims_vs_oracle(oracle, dims, scramble):
     """Direction-number sets with hundreds to thousands of dimensions: the
-    slab kernel (dims % 4 == 0) and, for the other widths, the 1024-thread
-    tiled path or, past what a tile holds, the per-element path."""
+    slab kernel (4 or 8 dims per lane for dims % 4 == 0; 2 or 1 for the other
+    widths above 128, k_sobol_slab<2|1>) and the 1024-thread tiled path."""
     rng = np.random.default_rng(dims)
     cols = rng.integers(0, 2**32, (dims, 52), dtype=np.uint64).astype(np.uint32)
     m = q.GeneratorMatrixSet.from_columns(cols)
