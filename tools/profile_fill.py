@@ -39,8 +39,9 @@ elif a.config == "c1":
     n = 1 << 24
     out = torch.empty(n, dtype=torch.float32, device="cuda")
     fn = lambda: q.radical_inverse_fill(n, 0, out=out)  # noqa: E731
-elif a.config == "halton":
-    n, d = 1 << 24, 32
+elif a.config.startswith("halton"):  # halton (2^24 x 32) or halton<dims> (2^29 samples)
+    d = int(a.config[6:] or 32)
+    n = (1 << 24) if d == 32 else (1 << 29) // d
     out = torch.empty((n, d), dtype=torch.float32, device="cuda")
     fn = lambda: q.halton_fill(n, d, scramble="linear", out=out)  # noqa: E731
 elif a.config in ("sobolowen12", "sobolowen256"):
