@@ -720,7 +720,8 @@ def run_extra(q, stream, peak, args):
         rh = measure_fill("halton linear 2^24 x 32",
                           lambda: q.halton_fill(nh, 32, scramble="linear", out=oh), nh * 32, steps,
                           warm, peak, stream)
-        rh["roofline"]["bound"] = "hbm (issue-limited: quotient-table load + 3 integer ops + map per sample; TMA store)"
+        rh["roofline"]["bound"] = ("hbm (issue/latency-limited walk: two shared-memory table loads, "
+                                   "the carry add and the map per sample; TMA store; k_halton_lv)")
         res["halton_linear_2^24x32"] = rh
 
     def c3():

@@ -474,7 +474,7 @@ static void halton_fill_impl(uint64_t first, uint64_t n, uint32_t dims, uint32_t
     args.upload();
     const RadicalDim* rdev = args.at<RadicalDim>(off);
     place_fill(out, first, n, dims, s, [&](const FillRange& r, cudaStream_t st) {
-        return launch_halton(rdev, dims, u32, r, st);
+        return launch_halton(rdev, dims, u32, r, st, rd.data());
     });
 }
 

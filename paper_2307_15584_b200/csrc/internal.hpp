@@ -13,6 +13,9 @@ struct Div32 {
     uint32_t m, s;
 };
 
+#ifdef __CUDACC__
+__host__ __device__
+#endif
 inline Div32 make_div32(uint32_t d)
 {
     uint32_t l = 0;
@@ -162,8 +165,10 @@ cudaError_t launch_lattice(const SmallArgs& args, uint32_t dims, bool out_u32,
 cudaError_t launch_vdc(bool out_u32, const FillRange& r, cudaStream_t s);
 
 // rd: device RadicalDim[dims].
+// rd: device RadicalDim[dims]; rd_host: the same array on the host (or
+// null: the level-table fill is then not taken)
 cudaError_t launch_halton(const void* rd, uint32_t dims, bool out_u32, const FillRange& r,
-                          cudaStream_t s);
+                          cudaStream_t s, const void* rd_host = nullptr);
 
 cudaError_t launch_pixel_stream(const PixelStreamParams& p, bool out_u32, const FillRange& r,
                                 cudaStream_t s);

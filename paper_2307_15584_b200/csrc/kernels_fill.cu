@@ -1628,6 +1628,377 @@ __global__ void __launch_bounds__(1024, 1)
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// ---------------------------------------------------------------------------
+// Halton fill from on-chip level tables (dims % 32 == 0).
+//
+// The index i (mod prime_max_power) of a base-b dimension is split as
+// i = (H * G1 + l1) * G0 + l0 with G0 = b^d0 >= 32 and G1 = b^d1 <= G0
+// (lv_groups). With q0[l] = radical_inverse_fixed(l) for l < G0 (a
+// d0-digit reversal over G0) and W1 = radical_inverse_fixed(H * G1 + l1)
+// (the fixed-point inverse of the high part i / G0), the inverse of i is
+// exactly
+//     q0[l0] + floor(W1 / G0) + (r0 >= G0 - W1 mod G0),
+// r0 = -q0[l0] * G0 mod 2^32 (q0's dropped remainder, < G0): i's low d0
+// digits land on top of the reversal, 2^32 * RI(i) = 2^32 * T0 / G0 +
+// 2^32 * RI(i / G0) / G0, and the two fractional parts add up to < 2.
+// Every scramble maps digit 0 to 0 and uses one permutation for all digit
+// positions (radical.cpp:130-181), so the split holds for plain, linear and
+// Faure.
+//
+// Shared memory per dimension: the position table X[u] = {q0[u mod G0],
+// 8 * floor(u / G0)} for u < G0 + kLvRows (a lane's position u relative to
+// lane 0's G0-block runs past G0 within a sub-tile; the second word is the
+// byte offset of its record), and per walker group a record table R[l1] =
+// {floor(W1 / G0), 2^32 - (G0 - W1 mod G0)} for the G1 values of l1 of the
+// current H plus the first kLvNext of the next H, rebuilt (lv_compose from
+// q0 and one radical_inverse_fixed per G0 * G1 indices) when lane 0 enters
+// the next H. A sample is two conflict-free shared loads (X at consecutive
+// lanes, the record a broadcast), one address add, the carry add and the
+// map: no table stream from L2 (the k_tma walk's bound).
+//
+// Layout: 8 walker warps per group; warp k of a group owns the 4
+// consecutive dimensions 4k..4k+3 of the CTA's 32-dimension column block
+// and lane l the point l of each 32-point step, so a step is one STS.128
+// per lane into a sub-tile laid out as the output rows with the 128-B
+// swizzle (conflict-free: 8 lanes cover the 8 swizzled chunks). GROUPS
+// groups walk their own contiguous sub-tile ranges into their own rings;
+// one extra warp per group issues its cp.async.bulk.tensor stores and
+// releases each buffer as soon as its store has read it (a blocking
+// wait_group.read stalls the whole warp, so the groups do not share one). One CTA per SM; a
+// CTA stays in one column block (its tables).
+__host__ __device__ inline void lv_groups(uint32_t b, uint32_t& G0, uint32_t& G1)
+{
+    G0 = b;
+    while (G0 < 32)
+        G0 *= b;
+    G1 = b;
+    while (G1 * b <= G0 && G0 * G1 < 1024)
+        G1 *= b;
+}
+
+struct LvDim {
+    uint32_t G0, G1, G0G1, hmod; // hmod = prime_max_power / (G0 * G1)
+    uint32_t xoff, recoff;       // words: X in the table area, R in a group's area
+    Div32 dG0, dG1;
+};
+
+constexpr uint32_t kLvMaxBufs = 4;
+constexpr uint32_t kLvRows = 128; // points per sub-tile (4 warp steps)
+// records of the next H: a lane's record index runs up to l1 + (G0 - 1 +
+// 31 + 96) / G0 <= l1 + 4 within a sub-tile (G0 >= 32)
+constexpr uint32_t kLvNext = 5;
+
+__host__ __device__ inline uint32_t lv_xwords(uint32_t G0) { return 2 * (G0 + kLvRows); }
+__host__ __device__ inline uint32_t lv_rwords(uint32_t G1) { return 2 * (G1 + kLvNext); }
+
+__device__ __forceinline__ uint32_t lds32(uint32_t a)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
+__device__ __forceinline__ uint2 lds64(uint32_t a)
+{
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+
+__device__ __forceinline__ void sts64(uint32_t a, uint32_t x, uint32_t y)
+{
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y));
+}
+
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w)
+{
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z),
+                 "r"(w));
+}
+
+// radical_inverse_fixed(h * G + l) from Wc = radical_inverse_fixed(h), for
+// l < G <= G0 (X at shared address xa)
+__device__ __forceinline__ uint32_t lv_compose(uint32_t xa, uint32_t G, const Div32& dG,
+                                               uint32_t l, uint32_t Wc)
+{
+    const uint32_t q = lds32(xa + 8 * l);
+    const uint32_t r = q * (0u - G);
+    const uint32_t t = div32(Wc, dG);
+    return q + t + (r >= G - (Wc - t * G) ? 1u : 0u);
+}
+
+// Records of block H (l1 < G1) and of the first kLvNext values of l1 of the
+// block after it; W2 = radical_inverse_fixed(H), W2n = that of the next
+// block. Warp-collective.
+__device__ __forceinline__ void lv_fill_records(const LvDim& D, uint32_t xa, uint32_t reca,
+                                                uint32_t W2, uint32_t W2n, uint32_t lane)
+{
+    __syncwarp();
+    for (uint32_t l = lane; l < D.G1 + kLvNext; l += 32) {
+        const uint32_t W1 = l < D.G1 ? lv_compose(xa, D.G1, D.dG1, l, W2)
+                                     : lv_compose(xa, D.G1, D.dG1, l - D.G1, W2n);
+        const uint32_t qU = div32(W1, D.dG0);
+        sts64(reca + 8 * l, qU, 0u - (D.G0 - (W1 - qU * D.G0)));
+    }
+    __syncwarp();
+}
+
+// Walk state of a dimension that is not touched per sub-tile: the current
+// block H and radical_inverse_fixed of the next block (the next rebuild's W2).
+struct LvSlot {
+    uint32_t H, W2n, p0, pad; // p0: lane 0's position in the block at the last check
+};
+
+// Walk state in registers: a0 = X address of the lane's position, a1 = the
+// record address of lane 0's l1 (warp-uniform), p0 = lane 0's position in
+// its G0 * G1 block (warp-uniform).
+struct LvWalk {
+    uint32_t a0, a1, p0;
+};
+
+__device__ __noinline__ uint32_t lv_radical(uint32_t i, const RadicalDim& R)
+{
+    return radical_fixed(i, R);
+}
+
+// Start a walk at i0 (lane 0's index).
+__device__ __forceinline__ LvWalk lv_init(const LvDim& D, const RadicalDim& R, uint32_t xa,
+                                          uint32_t reca, LvSlot* slot, uint32_t i0, uint32_t lane)
+{
+    const uint32_t ir = i0 - div32(i0, R.divmp) * R.maxpow;
+    const uint32_t H = ir / D.G0G1, pos = ir - H * D.G0G1;
+    const uint32_t l1 = pos / D.G0;
+    const LvWalk w{xa + 8 * (pos - l1 * D.G0 + lane), reca + 8 * l1, pos};
+    const uint32_t Hn = H + 1 == D.hmod ? 0u : H + 1;
+    const uint32_t W2 = radical_fixed(H, R), W2n = radical_fixed(Hn, R);
+    lv_fill_records(D, xa, reca, W2, W2n, lane);
+    if (lane == 0)
+        *slot = LvSlot{H, W2n};
+    __syncwarp();
+    return w;
+}
+
+// radical_inverse_fixed(h) for h < prime_max_power from the shared q0 table
+// alone (no global loads): h's base-G0 groups, most significant first,
+// composed with lv_compose.
+__device__ __forceinline__ uint32_t lv_radical_q0(uint32_t h, const LvDim& D, uint32_t xa)
+{
+    uint32_t grp[6], m = 0; // G0 >= 32 and h < 2^32: at most 7 groups, the top one < 4
+    while (h >= D.G0 && m < 6) {
+        const uint32_t q = div32(h, D.dG0);
+        grp[m++] = h - q * D.G0;
+        h = q;
+    }
+    uint32_t W = lds32(xa + 8 * h); // q0[h], h < G0 (m < 6 always holds: G0^6 >= 2^30 * 32)
+    while (m > 0)
+        W = lv_compose(xa, D.G0, D.dG0, grp[--m], W);
+    return W;
+}
+
+// Lane 0 entered block H + 1: rebuild the records; the record address moves
+// back by G1 entries (the returned byte count).
+__device__ __forceinline__ uint32_t lv_next_block(const LvDim& D, uint32_t xa, uint32_t reca,
+                                                  LvSlot* slot, uint32_t lane)
+{
+    const LvSlot s = *slot;
+    const uint32_t H = s.H + 1 == D.hmod ? 0u : s.H + 1;
+    const uint32_t Hn = H + 1 == D.hmod ? 0u : H + 1;
+    const uint32_t W2n = lv_radical_q0(Hn, D, xa);
+    lv_fill_records(D, xa, reca, s.W2n, W2n, lane);
+    if (lane == 0)
+        *slot = LvSlot{H, W2n};
+    __syncwarp();
+    return 8 * D.G1;
+}
+
+template <bool U32OUT, int GROUPS>
+__global__ void __launch_bounds__(GROUPS * 288, 1)
+    k_halton_lv(const __grid_constant__ CUtensorMap tmap, const RadicalDim* __restrict__ rd,
+                uint32_t nbuf, uint32_t ctas_per_cb, uint32_t xw, uint32_t recw, uint64_t first,
+                uint64_t n, uint64_t nsub)
+{
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    __shared__ __align__(8) uint64_t bars[2 * GROUPS * kLvMaxBufs];
+    __shared__ LvDim desc[32];
+    __shared__ LvSlot slots[GROUPS * 32];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint32_t raw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    const uint32_t ring_bytes = GROUPS * nbuf * kLvRows * 128;
+    const uint32_t xs = base + ring_bytes;
+    const uint32_t recs = xs + xw * 4;
+    uint32_t* xg = reinterpret_cast<uint32_t*>(smem_raw + (xs - raw));
+    const uint32_t full0 = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
+    const uint32_t empty0 = full0 + 8 * GROUPS * kLvMaxBufs;
+    const uint32_t cb = blockIdx.x / ctas_per_cb, cta = blockIdx.x - cb * ctas_per_cb;
+    const RadicalDim* rdb = rd + cb * 32;
+    if (warp == 0) {
+        const RadicalDim& R = rdb[lane];
+        uint32_t G0, G1;
+        lv_groups(R.base, G0, G1);
+        uint32_t a = lv_xwords(G0), c = lv_rwords(G1); // inclusive prefix sums over the lanes
+        for (uint32_t o = 1; o < 32; o <<= 1) {
+            const uint32_t ya = __shfl_up_sync(~0u, a, o), yc = __shfl_up_sync(~0u, c, o);
+            if (lane >= o) {
+                a += ya;
+                c += yc;
+            }
+        }
+        desc[lane] = LvDim{G0, G1, G0 * G1, R.maxpow / (G0 * G1), a - lv_xwords(G0),
+                           c - lv_rwords(G1), make_div32(G0), make_div32(G1)};
+    }
+    if (threadIdx.x == 32) {
+        for (uint32_t b = 0; b < GROUPS * kLvMaxBufs; ++b) {
+            mbar_init(full0 + 8 * b, 8);
+            mbar_init(empty0 + 8 * b, 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    for (uint32_t j = 0; j < 32; ++j) { // X[u] = {q0[u mod G0], 8 * (u / G0)}
+        const uint32_t G0 = desc[j].G0, off = desc[j].xoff;
+        for (uint32_t u = threadIdx.x; u < G0 + kLvRows; u += blockDim.x) {
+            const uint32_t k = u / G0;
+            xg[off + 2 * u] = lv_radical(u - k * G0, rdb[j]);
+            xg[off + 2 * u + 1] = 8 * k;
+        }
+    }
+    __syncthreads();
+    const uint64_t s_beg = nsub * cta / ctas_per_cb, s_end = nsub * (cta + 1) / ctas_per_cb;
+    if (warp >= GROUPS * 8) { // warp 8 * GROUPS + g: lane 0 issues and releases group g's ring
+        if (lane != 0)
+            return;
+        const uint32_t g = warp - GROUPS * 8;
+        const uint64_t gb = s_beg + (s_end - s_beg) * g / GROUPS;
+        const uint64_t ge = s_beg + (s_end - s_beg) * (g + 1) / GROUPS;
+        uint32_t b = 0, ph = 0;
+        for (uint64_t s = gb; s < ge; ++s) {
+            mbar_wait(full0 + 8 * (g * kLvMaxBufs + b), ph);
+            const uint32_t buf = base + (g * nbuf + b) * kLvRows * 128;
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                             reinterpret_cast<uint64_t>(&tmap)),
+                         "r"(buf), "r"(cb * 32), "r"(static_cast<int32_t>(s * kLvRows))
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            // release the buffer as soon as the store has read it
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            mbar_arrive(empty0 + 8 * (g * kLvMaxBufs + b));
+            if (++b == nbuf) {
+                b = 0;
+                ph ^= 1u;
+            }
+        }
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        return;
+    }
+    const uint32_t g = warp >> 3, k = warp & 7u;
+    const uint64_t gb = s_beg + (s_end - s_beg) * g / GROUPS;
+    const uint64_t ge = s_beg + (s_end - s_beg) * (g + 1) / GROUPS;
+    const uint32_t reca0 = recs + g * recw * 4;
+    // row l of a sub-tile: row & 7 == lane & 7, so the swizzled 16-B chunk of
+    // dimensions 4k..4k+3 is fixed per lane
+    const uint32_t stoff = lane * 128 + ((k ^ (lane & 7u)) << 4);
+    // lane 0's X entry one sub-tile ahead, relative to this lane's address
+    const uint32_t ahead = 8 * kLvRows + 4 - 8 * lane;
+    uint32_t a0[4], a1[4], ng[4];
+    uint32_t nref = 0;  // sub-tiles until the first record rebuild of the 4 dims
+    uint32_t since = 0; // sub-tiles since slots[].p0 was written
+    bool live = false;
+    uint32_t b = 0, ph = 0; // ring slot and the parity of its uses
+    const uint32_t buf0 = base + g * nbuf * kLvRows * 128 + stoff;
+    uint32_t buf = buf0;
+    uint32_t i0 = static_cast<uint32_t>(first + gb * kLvRows);
+    const uint32_t cnt = static_cast<uint32_t>(ge - gb);
+    for (uint32_t u = 0; u < cnt; ++u, i0 += kLvRows) {
+        if (u >= nbuf)
+            mbar_wait(empty0 + 8 * (g * kLvMaxBufs + b), ph ^ 1u);
+        if (i0 > 0xffffffffu - (kLvRows - 1)) { // the sub-tile crosses the u32 index wrap
+            for (uint32_t st = 0; st < kLvRows; st += 32) {
+                uint32_t v[4];
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {
+                    const uint32_t x = lv_radical(i0 + st + lane, rdb[4 * k + d]);
+                    v[d] = U32OUT ? x : map_bits(x);
+                }
+                sts128(buf + st * 128, v[0], v[1], v[2], v[3]);
+            }
+            live = false;
+        } else {
+            if (!live || nref == 0) {
+                nref = 0xffffffffu;
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {
+                    const uint32_t j = 4 * k + d;
+                    const LvDim& D = desc[j];
+                    LvSlot* sl = &slots[g * 32 + j];
+                    uint32_t p0;
+                    if (!live) {
+                        const LvWalk w =
+                            lv_init(D, rdb[j], xs + 4 * D.xoff, reca0 + 4 * D.recoff, sl, i0, lane);
+                        a0[d] = w.a0;
+                        a1[d] = w.a1;
+                        p0 = w.p0;
+                        ng[d] = 0u - D.G0;
+                    } else {
+                        p0 = sl->p0 + since * kLvRows;
+                        if (p0 >= D.G0G1) { // lane 0 is in the next block
+                            p0 -= D.G0G1;
+                            a1[d] -= lv_next_block(D, xs + 4 * D.xoff, reca0 + 4 * D.recoff, sl,
+                                                   lane);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0)
+                        sl->p0 = p0;
+                    nref = min(nref, (D.G0G1 - p0 + kLvRows - 1) / kLvRows);
+                }
+                __syncwarp();
+                since = 0;
+                live = true;
+            }
+#pragma unroll
+            for (uint32_t st = 0; st < kLvRows / 32; ++st) {
+                uint32_t v[4];
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {
+                    const uint2 e = lds64(a0[d] + 256 * st);
+                    const uint2 rc = lds64(a1[d] + e.y);
+                    // q + qU + (r0 >= thr): the carry of r0 + (2^32 - thr)
+                    uint32_t x, dummy;
+                    asm("{\n\t"
+                        "add.cc.u32 %1, %2, %3;\n\t"
+                        "addc.u32 %0, %4, %5;\n\t}"
+                        : "=r"(x), "=r"(dummy)
+                        : "r"(e.x * ng[d]), "r"(rc.y), "r"(e.x), "r"(rc.x));
+                    v[d] = U32OUT ? x : map_bits(x);
+                }
+                sts128(buf + st * 4096, v[0], v[1], v[2], v[3]);
+            }
+            // next sub-tile: lane 0's position advances by kLvRows; fold the
+            // G0-blocks it passed (k8 / 8 of them) into the record address
+#pragma unroll
+            for (int d = 0; d < 4; ++d) {
+                const uint32_t k8 = lds32(a0[d] + ahead);
+                a0[d] += 8 * kLvRows;
+                a0[d] += k8 * ng[d];
+                a1[d] += k8;
+            }
+            --nref;
+            ++since;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0)
+            mbar_arrive(full0 + 8 * (g * kLvMaxBufs + b));
+        buf += kLvRows * 128;
+        if (++b == nbuf) {
+            b = 0;
+            ph ^= 1u;
+            buf = buf0;
+        }
+    }
+}
+
 // Odd dims <= 31: the padded sub-tile of k_runs has an odd row stride, so
 // with no padding at all (ld == dims) it is already conflict-free and laid
 // out exactly as the output — so each run keeps a ring of nbuf dense
@@ -1997,6 +2368,89 @@ bool launch_tma_fill(const W& w, uint32_t dims, const FillRange& r, cudaStream_t
     return true;
 }
 
+// Halton fills with dims % 32 == 0 from on-chip level tables (k_halton_lv);
+// false when the shape does not fit (the k_tma walk takes it then): out
+// 16-B aligned, n < 2^31, and every column block's X tables plus the
+// walker groups' record areas and rings within the opt-in shared memory.
+template <bool U32OUT>
+bool launch_halton_lv(const RadicalDim* rd, const RadicalDim* rd_host, uint32_t dims,
+                      const FillRange& r, cudaStream_t s, cudaError_t* err)
+{
+    if (!rd_host || dims % 32 != 0 || (reinterpret_cast<uintptr_t>(r.out) & 15u) != 0 ||
+        r.n >= (1ull << 31))
+        return false;
+    uint32_t xw = 0, recw = 0;
+    for (uint32_t cb = 0; cb < dims / 32; ++cb) {
+        uint32_t a = 0, c = 0;
+        for (uint32_t j = 0; j < 32; ++j) {
+            uint32_t G0, G1;
+            lv_groups(rd_host[cb * 32 + j].base, G0, G1);
+            if (rd_host[cb * 32 + j].maxpow % (G0 * G1) != 0)
+                return false;
+            a += lv_xwords(G0);
+            c += lv_rwords(G1);
+        }
+        xw = std::max(xw, a);
+        recw = std::max(recw, c);
+    }
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    constexpr uint32_t kRows = kLvRows;
+    // the most walker groups (latency hiding: the walk is issue / latency
+    // bound), then the deepest ring, that fit: 3 groups x 2 buffers at 32
+    // dimensions (measured: 2 groups x 3 buffers 1020, 3 x 2 1160 Gsamples/s)
+    int kGroups = 0;
+    uint32_t nbuf = 0;
+    auto need = [&](int gr, uint32_t nb) {
+        return 1024 + static_cast<size_t>(gr) * nb * kRows * 128 + static_cast<size_t>(xw) * 4 +
+               static_cast<size_t>(gr) * recw * 4 + 2 * gr * kLvMaxBufs * 8 + 32 * sizeof(LvDim) +
+               gr * 32 * sizeof(LvSlot);
+    };
+    for (int gr = 3; gr >= 2 && !kGroups; --gr)
+        for (uint32_t nb = 3; nb >= 2 && !kGroups; --nb)
+            if (need(gr, nb) <= static_cast<size_t>(optin)) {
+                kGroups = gr;
+                nbuf = nb;
+            }
+    if (!kGroups)
+        return false;
+    static PFN_cuTensorMapEncodeTiled encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+    }();
+    if (!encode)
+        return false;
+    CUtensorMap tmap;
+    const cuuint64_t gdim[2] = {dims, r.n};
+    const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(dims) * 4};
+    const cuuint32_t box[2] = {32, kRows};
+    const cuuint32_t estride[2] = {1, 1};
+    if (encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, r.out, gdim, gstride, box, estride,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    auto kern = kGroups == 3 ? k_halton_lv<U32OUT, 3> : k_halton_lv<U32OUT, 2>;
+    *err = allow_dynamic_smem(kern);
+    if (*err != cudaSuccess)
+        return true;
+    const uint64_t nsub = (r.n + kRows - 1) / kRows;
+    const uint32_t ncb = dims / 32;
+    const uint32_t per = static_cast<uint32_t>(std::max<uint64_t>(
+        1, std::min<uint64_t>(nsub, static_cast<uint64_t>(sm_count()) / ncb)));
+    const size_t dyn = need(kGroups, nbuf) - (2 * kGroups * kLvMaxBufs * 8 + 32 * sizeof(LvDim) +
+                                              kGroups * 32 * sizeof(LvSlot));
+    kern<<<ncb * per, kGroups * 288, dyn, s>>>(
+        tmap, rd, nbuf, per, xw, recw, r.first, r.n, nsub);
+    *err = cudaGetLastError();
+    return true;
+}
+
 // dims <= 32: one CTA per SM, runs x dims warps, sub-tiles sharing ~192 KB,
 // plus a 32-word scratch per warp
 template <class W, int DPW = 1>
@@ -2312,12 +2766,18 @@ cudaError_t launch_lattice(const SmallArgs& args, uint32_t dims, bool u32, const
 }
 
 cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRange& r,
-                          cudaStream_t s)
+                          cudaStream_t s, const void* rd_host)
 {
     if (r.n == 0)
         return cudaSuccess;
     const RadicalDim* rdv = static_cast<const RadicalDim*>(rd);
+    const RadicalDim* rdh = static_cast<const RadicalDim*>(rd_host);
     cudaError_t err = cudaSuccess;
+    // QMC_HALTON_NO_LV=1: the k_tma walk instead (A/B, tools/exp_halton_lv.py)
+    if (std::getenv("QMC_HALTON_NO_LV") == nullptr &&
+        (u32 ? launch_halton_lv<true>(rdv, rdh, dims, r, s, &err)
+             : launch_halton_lv<false>(rdv, rdh, dims, r, s, &err)))
+        return err;
     if (u32 ? launch_tma_fill(HaltonWalk<true>{rdv}, dims, r, s, &err, true)
             : launch_tma_fill(HaltonWalk<false>{rdv}, dims, r, s, &err, true))
         return err;

@@ -1506,6 +1506,29 @@ def test_halton_fill_q4_long_runs_vs_reference(ref, mode, first):
         np.testing.assert_array_equal(got[:, j], exp, err_msg=f"dim={j}")
 
 
+@pytest.mark.parametrize("mode", ["linear", "faure"])
+@pytest.mark.parametrize("first", [3486784401 - (1 << 22) + 5, 2**32 - (1 << 22) - 77])
+def test_halton_fill_level_tables_long_vs_reference(ref, mode, first):
+    """k_halton_lv (dims == 32, on-chip level tables): 2^23 + 333 points, so
+    every walker group crosses many G0 * G1 record blocks (record rebuilds
+    from the shared q0 table), the base-3 prime_max_power reduction, the
+    base-2 2^31 reduction, and the u32 index wrap (the per-sample sub-tile
+    and the re-initialised walk after it), u32 and f32 outputs."""
+    n, dims = (1 << 23) + 333, 32
+    got = u32(q.halton_fill(n, dims, first=first, scramble=mode, fixed=True)).reshape(n, dims)
+    f = q.halton_fill(n, dims, first=first, scramble=mode).cpu().numpy().reshape(n, dims)
+    for j in range(dims):
+        b = q.prime(j)
+        exp = np.zeros(n, np.uint32)
+        assert ref.ref_radical_fixed_fill(first & 0xFFFFFFFF, n, j, _MODE[mode],
+                                          b - 1 if (mode == "linear" and b > 2) else 1,
+                                          ptr(exp)) == 0
+        np.testing.assert_array_equal(got[:, j], exp, err_msg=f"dim={j}")
+        mapped = np.zeros(n, np.uint32)
+        ref.ref_map_bulk(ptr(exp), ptr(mapped), n)
+        np.testing.assert_array_equal(f[:, j].view(np.uint32), mapped, err_msg=f"f32 dim={j}")
+
+
 @pytest.mark.parametrize("dims", [64, 160])
 def test_halton_fill_q4_many_blocks_vs_reference(ref, dims):
     """Column blocks past the first (bases up to 941 at 160 dims, fill tables
