@@ -1746,7 +1746,9 @@ __device__ __forceinline__ void lv_fill_records(const LvDim& D, uint32_t xa, uin
 // Walk state of a dimension that is not touched per sub-tile: the current
 // block H and radical_inverse_fixed of the next block (the next rebuild's W2).
 struct LvSlot {
-    uint32_t H, W2n, p0, pad; // p0: lane 0's position in the block at the last check
+    // p0: lane 0's position in the block at the last check; W3 =
+    // radical_inverse_fixed(Hn / G0), Hn the next block
+    uint32_t H, W2n, p0, W3;
 };
 
 // Walk state in registers: a0 = X address of the lane's position, a1 = the
@@ -1773,7 +1775,7 @@ __device__ __forceinline__ LvWalk lv_init(const LvDim& D, const RadicalDim& R, u
     const uint32_t W2 = radical_fixed(H, R), W2n = radical_fixed(Hn, R);
     lv_fill_records(D, xa, reca, W2, W2n, lane);
     if (lane == 0)
-        *slot = LvSlot{H, W2n};
+        *slot = LvSlot{H, W2n, 0u, radical_fixed(Hn / D.G0, R)};
     __syncwarp();
     return w;
 }
@@ -1803,10 +1805,14 @@ __device__ __forceinline__ uint32_t lv_next_block(const LvDim& D, uint32_t xa, u
     const LvSlot s = *slot;
     const uint32_t H = s.H + 1 == D.hmod ? 0u : s.H + 1;
     const uint32_t Hn = H + 1 == D.hmod ? 0u : H + 1;
-    const uint32_t W2n = lv_radical_q0(Hn, D, xa);
+    // radical_inverse_fixed(Hn) = compose of Hn mod G0 over that of Hn / G0
+    // (cached; it changes once per G0 blocks)
+    const uint32_t hq = div32(Hn, D.dG0), m = Hn - hq * D.G0;
+    const uint32_t W3 = Hn == 0 ? 0u : (m == 0 ? lv_radical_q0(hq, D, xa) : s.W3);
+    const uint32_t W2n = lv_compose(xa, D.G0, D.dG0, m, W3);
     lv_fill_records(D, xa, reca, s.W2n, W2n, lane);
     if (lane == 0)
-        *slot = LvSlot{H, W2n};
+        *slot = LvSlot{H, W2n, 0u, W3};
     __syncwarp();
     return 8 * D.G1;
 }
