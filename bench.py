@@ -266,6 +266,20 @@ class CpuRef:
                 raise RuntimeError(self.lib.ref_last_error().decode())
         return time.perf_counter() - t0, sum(c for _, c in wins)
 
+    def halton_linear(self, total, n, dims, threads):
+        import numpy as np
+
+        from oracle import ptr
+
+        wins = windows(total, n)
+        out = np.empty((max(c for _, c in wins), dims), np.float32)
+        t0 = time.perf_counter()
+        for first, cnt in wins:
+            rc = self.lib.ref_halton_linear_fill(first, cnt, dims, ptr(out), threads)
+            if rc != 0:
+                raise RuntimeError(self.lib.ref_last_error().decode())
+        return time.perf_counter() - t0, sum(c for _, c in wins) * dims
+
     def lattice_cp(self, total, n, g, shifts, threads):
         import numpy as np
 
@@ -722,6 +736,9 @@ def run_extra(q, stream, peak, args):
                           warm, peak, stream)
         rh["roofline"]["bound"] = ("hbm (issue/latency-limited walk: two shared-memory table loads, "
                                    "the carry add and the map per sample; TMA store; k_halton_lv)")
+        rh["cpu_baseline"] = cpu("qmc::halton_point(i, 32, default_linear_factors(32)), "
+                                 "%d windows over [0, 2^24)" % CPU_WINDOWS,
+                                 lambda n, t: ref.halton_linear(nh, n, 32, t), nmax=nh)
         res["halton_linear_2^24x32"] = rh
 
     def c3():

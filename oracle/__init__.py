@@ -135,6 +135,7 @@ def load_ref():
         _sig(lib, "ref_integrate", i32, cstr, u32, u32, cstr, u64, cstr, u32, C.POINTER(f64))
         _sig(lib, "ref_integrate_sobol_text", i32, cstr, u32, cstr, u64, cstr, u32, C.POINTER(f64))
         _sig(lib, "ref_radical_fill", i32, u64, u64, u32, P, i32)
+        _sig(lib, "ref_halton_linear_fill", i32, u64, u64, u32, P, i32)
         _sig(lib, "ref_neumaier", f64, P, u64)
         _sig(lib, "ref_reduce_deterministic", f64, P, P, u64)
         _sig(lib, "ref_l2_star", i32, P, u64, u32, C.POINTER(f64))

@@ -454,6 +454,23 @@ int ref_radical_fill(std::uint64_t first, std::uint64_t n, std::uint32_t prime_i
         });
     });
 }
+// CPU linearly scrambled Halton points through the public API
+// (qmc::halton_point with qmc::default_linear_factors, radical.cpp:260-279)
+// on `threads` threads, rows of `dims` floats — the Halton fill's CPU baseline.
+int ref_halton_linear_fill(std::uint64_t first, std::uint64_t n, std::uint32_t dims, float* out,
+                           int threads)
+{
+    return guard([&] {
+        const std::vector<std::uint32_t> f = qmc::default_linear_factors(dims);
+        parallel_ranges(n, threads, [&](std::uint64_t b, std::uint64_t e) {
+            for (std::uint64_t k = b; k < e; ++k) {
+                const std::vector<float> x =
+                    qmc::halton_point(static_cast<std::uint32_t>(first + k), dims, f);
+                std::copy(x.begin(), x.end(), out + k * dims);
+            }
+        });
+    });
+}
 int ref_l2_star(const float* pts, std::uint64_t n, std::uint32_t dims, double* out)
 {
     return guard([&] {
