@@ -53,6 +53,7 @@ void resolve_render(const qmc_render_job* job, uint32_t row_begin, uint32_t row_
     p.inv_spp = (job->spp & (job->spp - 1)) == 0 ? 1.0 / job->spp : 0.0;
     p.colmap = job->spp >= 8 ? render_column_order(job->width) : nullptr;
     p.q3 = render_phi3_quotients();
+    p.t3q3 = render_t3q3();
     std::vector<uint32_t> g = job->generator && job->generator_dims
                                   ? std::vector<uint32_t>(job->generator,
                                                           job->generator + job->generator_dims)

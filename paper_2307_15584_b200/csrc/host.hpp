@@ -146,6 +146,8 @@ const uint64_t* pow_magic(uint32_t b);
 const uint32_t* render_column_order(uint32_t width);
 // phi_3 quotient tables of the render (kernels_render.cu, phi3_q).
 const uint32_t* render_phi3_quotients();
+constexpr uint32_t kRenderT3Q3Words = 2188 + 2 * 2187 + 2; // 16-B multiple
+const uint32_t* render_t3q3();
 std::vector<RadicalDim> radical_dims(uint32_t dims, uint32_t first_prime, qmc_radical_scramble sc,
                                      const uint32_t* factors, std::vector<uint32_t>& sigma_pool,
                                      std::vector<size_t>& sigma_off);

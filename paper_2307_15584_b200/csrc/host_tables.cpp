@@ -381,6 +381,28 @@ const uint32_t* render_phi3_quotients()
     return static_cast<const uint32_t*>(slot.get());
 }
 
+// The render's staged phi_3 tables in one 16-B padded device buffer, laid out
+// as k_render's shared copy (RenderSmem tab3 then q3): [T (3^7 words), 0,
+// QL (3^7), QH (3^7), 0, 0], so one cp.async.bulk copies them.
+const uint32_t* render_t3q3()
+{
+    static std::mutex mu;
+    static std::map<int, DevPtr> cache;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(mu);
+    auto& slot = cache[dev];
+    if (!slot) {
+        std::vector<uint32_t> z(kRenderT3Q3Words, 0u);
+        slot = dev_upload(z.data(), z.size() * 4);
+        cuda_ok(cudaMemcpy(slot.get(), digit_table(3, 0, 0).ptr, 2187 * 4, cudaMemcpyDeviceToDevice),
+                "cudaMemcpy D2D");
+        cuda_ok(cudaMemcpy(static_cast<uint32_t*>(slot.get()) + 2188, render_phi3_quotients(),
+                           2 * 2187 * 4, cudaMemcpyDeviceToDevice),
+                "cudaMemcpy D2D");
+    }
+    return static_cast<const uint32_t*>(slot.get());
+}
+
 const uint64_t* pow_magic(uint32_t b)
 {
     static std::mutex mu;

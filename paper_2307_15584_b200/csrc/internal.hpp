@@ -80,6 +80,7 @@ struct RenderParams {
     const uint32_t* colmap;       // device, k_render's column order at spp >= 8 (or null)
     const uint32_t* q3;           // device, phi3_q's quotient tables (2 x 3^7 words)
     uint32_t dlo3, dhi3;          // image-plane halton: scale_x = dhi3 * 3^7 + dlo3
+    const uint32_t* t3q3;         // device, tab3 | 0 | q3 | 0 0 (render_t3q3, 16-B padded)
 };
 
 // Per-stream (one pixel context) parameters for qmc_stream_fill kinds that

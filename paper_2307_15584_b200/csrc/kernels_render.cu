@@ -356,17 +356,34 @@ struct RenderSmem {
     static constexpr bool kT3 = KIND == 1 || KIND == 3 || KIND == 6;
     static constexpr bool kQ3 = Q3 && (KIND == 1 || KIND == 6); // k_render's INC3 kinds
     double2 poly[8];
-    uint32_t sob_d[KIND == 0 ? 64 : 1]; // sobol: prefix XORs of the columns
-    uint32_t tab3[kT3 ? 2187 : 1];      // halton kinds: 3^7 words
-    uint32_t q3[kQ3 ? 2 * 2187 : 1];    // phi3_q's quotient tables
+    uint32_t sob_d[KIND == 0 ? 64 : 4]; // sobol: prefix XORs of the columns
+    // halton kinds: 3^7 words (+1 pad), then phi3_q's quotient tables, laid
+    // out as the padded device buffer p.t3q3 so one bulk copy stages both
+    alignas(16) uint32_t tab3[kT3 ? 2188 : 4];
+    uint32_t q3[kQ3 ? 2 * 2187 + 2 : 4];
+    uint64_t bar;
 };
 
+// The phi_3 tables are staged by one cp.async.bulk (TMA) copy from thread 0
+// into the CTA's shared memory, completing on an mbarrier: no per-thread
+// load/store loop (image-plane Halton stages 26 KB per 128-pixel CTA).
 template <uint32_t KIND, bool Q3>
 __device__ __forceinline__ void stage_render_smem(RenderSmem<KIND, Q3>& sm, const RenderParams& p)
 {
-    if (RenderSmem<KIND, Q3>::kQ3)
-        for (uint32_t e = threadIdx.x; e < 2 * 2187; e += blockDim.x)
-            sm.q3[e] = __ldg(p.q3 + e);
+    using S = RenderSmem<KIND, Q3>;
+    const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&sm.bar));
+    if (S::kT3 && threadIdx.x == 0) {
+        constexpr uint32_t bytes = (S::kQ3 ? 2188 + 2 * 2187 + 2 : 2188) * 4;
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"(bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
+                     "%2, [%3];" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(sm.tab3))),
+                     "l"(p.t3q3), "r"(bytes), "r"(bar)
+                     : "memory");
+    }
     if (KIND == 0 && threadIdx.x < 64) {
         const uint32_t dim = threadIdx.x >> 5, c = threadIdx.x & 31u;
         uint32_t d = 0;
@@ -374,10 +391,18 @@ __device__ __forceinline__ void stage_render_smem(RenderSmem<KIND, Q3>& sm, cons
             d ^= __ldg(p.cols2 + 52 * dim + k);
         sm.sob_d[threadIdx.x] = d;
     }
-    if (RenderSmem<KIND, Q3>::kT3)
-        for (uint32_t e = threadIdx.x; e < 2187; e += blockDim.x)
-            sm.tab3[e] = __ldg(p.tab3 + e);
-    load_sin_poly(sm.poly); // includes the barrier
+    load_sin_poly(sm.poly); // includes the barrier (the mbarrier init is visible after it)
+    if (S::kT3) {
+        uint32_t ok;
+        do {
+            asm volatile("{\n\t.reg .pred p;\n\t"
+                         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+                         "selp.u32 %0, 1, 0, p;\n\t}"
+                         : "=r"(ok)
+                         : "r"(bar)
+                         : "memory");
+        } while (!ok);
+    }
 }
 
 // spp < 8: too few samples to repay the per-warp classification. The kinds

@@ -31,7 +31,8 @@ row = []
 for kind, spp, acc in [("pixel-shifted-lattice", 1, "kahan"), ("sobol", 1, "kahan"),
                        ("pixel-shifted-lattice", 16, "kahan"), ("pixel-shifted-lattice", 64, "kahan"),
                        ("pixel-shifted-lattice", 256, "kahan"), ("pixel-shifted-lattice", 64, "int"),
-                       ("image-plane-halton", 64, "kahan"), ("sobol", 64, "kahan")]:
+                       ("image-plane-halton", 64, "kahan"), ("image-plane-halton", 256, "kahan"),
+                       ("halton-hilbert", 64, "kahan"), ("halton", 64, "kahan"), ("sobol", 64, "kahan")]:
     row.append("%s/%d/%s=%s" % (kind[:5], spp, acc, t(lambda: q.render(3840, 2160, spp, kind=kind, accum=acc, out=img), 3840 * 2160 * spp)))
 print(os.path.basename(q.LIB_PATH), " ".join(row))
 im = q.render(3840, 2160, 64).cpu().numpy()
