@@ -103,12 +103,26 @@ __device__ __forceinline__ uint32_t phi3_q(uint32_t a_lo, uint32_t a_hi)
 // INC3 (KIND 1 and 6): sob0 / sob1 carry the shared-memory addresses of
 // q3[lo] and q3[3^7 + hi] for the (lo, hi) base-3^7 digits of the phi_3
 // index, advanced by the caller.
+// INC3 with KIND 3 (halton_hilbert, n = block + i up to 3^20): sob1 is the
+// shared-memory address of q3[lo] for n = H * 3^7 + lo and rec = {floor(W /
+// 3^7), 2^32 - (3^7 - W mod 3^7)} with W = phi_3(H): phi_3(n) = q3[lo] +
+// rec.x + (r >= 3^7 - W mod 3^7), r = -q3[lo] * 3^7 mod 2^32 (the split of
+// the level-table Halton fill, kernels_fill.cu k_halton_lv, with G0 = 3^7).
 template <uint32_t KIND, bool SMEM_T3 = false, bool INC3 = false>
 __device__ __forceinline__ void sample2(uint32_t i, const PixelState& s, const RenderParams& p,
                                         uint32_t& x0, uint32_t& x1, uint32_t& sob0,
-                                        uint32_t& sob1, const uint32_t* t3)
+                                        uint32_t& sob1, const uint32_t* t3, uint2 rec = {})
 {
-    if (INC3 && (KIND == 1 || KIND == 6)) {
+    if (INC3 && KIND == 3) {
+        x0 = rad2(static_cast<uint32_t>(s.block + i));
+        const uint32_t q = lds_u32(sob1);
+        uint32_t dummy;
+        asm("{\n\t"
+            "add.cc.u32 %1, %2, %3;\n\t"
+            "addc.u32 %0, %4, %5;\n\t}"
+            : "=r"(x1), "=r"(dummy)
+            : "r"(q * (0u - 2187u)), "r"(rec.y), "r"(q), "r"(rec.x));
+    } else if (INC3 && (KIND == 1 || KIND == 6)) {
         x0 = KIND == 1 ? rad2(i) : rad2(s.ipx0 + i * p.scale_y);
         x1 = phi3_q(sob0, sob1);
     } else if (KIND == 0) { // sobol: natural-order incremental, caller advances
@@ -185,10 +199,12 @@ __device__ __forceinline__ double pixel_sample(uint32_t i, const PixelState& s,
                                                const RenderParams& p, double fx, double fy,
                                                const double2* s_poly, uint32_t sob0,
                                                uint32_t sob1, bool inside_px = false, int qx = 0,
-                                               int qy = 0, const uint32_t* s_tab3 = nullptr)
+                                               int qy = 0, const uint32_t* s_tab3 = nullptr,
+                                               uint2 rec = {})
 {
     uint32_t a, b;
-    sample2<KIND, SMEM_T3, INC3>(i, s, p, a, b, sob0, sob1, SMEM_T3 || INC3 ? s_tab3 : p.tab3);
+    sample2<KIND, SMEM_T3, INC3>(i, s, p, a, b, sob0, sob1, SMEM_T3 || INC3 ? s_tab3 : p.tab3,
+                                 rec);
     const double u = static_cast<double>(map_u32(a));
     const double v = static_cast<double>(map_u32(b));
     const double x = __dmul_rn(__dadd_rn(fx, u), p.inv_w);
@@ -237,7 +253,22 @@ __device__ __forceinline__ float render_pixel(const PixelState& s, const RenderP
     constexpr bool kSmemT3 = KIND == 1 || KIND == 3 || KIND == 6;
     uint32_t sob0 = p.scr0, sob1 = p.scr1; // sobol index 0 value
     uint32_t dlo = 0, dhi = 0, a_end = 0;
-    if (INC3) { // image-plane halton: n = ipy0 + i * scale_x; halton: n = i
+    uint2 rec{}, rec2{}; // halton_hilbert: the records of H and H + 1
+    if (INC3 && KIND == 3) {
+        // n0 = the pixel's first index mod 3^20 (render_classified checked
+        // that its spp indices neither cross 3^20 nor wrap u32, spp <= 2187)
+        uint32_t n0 = static_cast<uint32_t>(s.block);
+        if (n0 >= 3486784401u)
+            n0 -= 3486784401u;
+        const uint32_t H = n0 / 2187u, base = static_cast<uint32_t>(__cvta_generic_to_shared(s_tab3));
+        sob1 = base + 4u * (n0 - 2187u * H);
+        a_end = base + 4u * 2187u;
+        const uint32_t* t7 = s_tab3 - 2188; // RenderSmem: tab3 (2188 words) precedes q3
+        const uint32_t W = phi3_fixed<true>(H, t7), W2 = phi3_fixed<true>(H + 1u, t7);
+        const uint32_t qw = W / 2187u, qw2 = W2 / 2187u;
+        rec = make_uint2(qw, 0u - (2187u - (W - 2187u * qw)));
+        rec2 = make_uint2(qw2, 0u - (2187u - (W2 - 2187u * qw2)));
+    } else if (INC3) { // image-plane halton: n = ipy0 + i * scale_x; halton: n = i
         const uint32_t n0 = KIND == 6 ? s.ipy0 : 0u;
         const uint32_t hi = n0 / 2187u, base = static_cast<uint32_t>(__cvta_generic_to_shared(s_tab3));
         sob0 = base + 4u * (n0 - 2187u * hi);
@@ -253,14 +284,20 @@ __device__ __forceinline__ float render_pixel(const PixelState& s, const RenderP
 #pragma unroll 2
         for (uint32_t i = i0; i < i1; ++i) {
             const double f = pixel_sample<KIND, DISC_TEST, FIXED_Q, kSmemT3, UQ, INC3>(
-                i, s, p, fx, fy, s_poly, sob0, sob1, inside_px, qx, qy, s_tab3);
+                i, s, p, fx, fy, s_poly, sob0, sob1, inside_px, qx, qy, s_tab3, rec);
             if (ACCUM != 0)
                 isum += int_term(f);
             else if (decltype(big)::value)
                 neumaier_add_big(sum, comp, f);
             else
                 neumaier_add(sum, comp, f);
-            if (INC3) {
+            if (INC3 && KIND == 3) {
+                sob1 += 4u;
+                if (sob1 >= a_end) {
+                    sob1 -= 4u * 2187u;
+                    rec = rec2;
+                }
+            } else if (INC3) {
                 sob0 += dlo;
                 sob1 += dhi;
                 if (sob0 >= a_end) {
@@ -354,7 +391,7 @@ __device__ __forceinline__ WarpClass classify_warp(bool valid, uint64_t q, const
 template <uint32_t KIND, bool Q3 = false>
 struct RenderSmem {
     static constexpr bool kT3 = KIND == 1 || KIND == 3 || KIND == 6;
-    static constexpr bool kQ3 = Q3 && (KIND == 1 || KIND == 6); // k_render's INC3 kinds
+    static constexpr bool kQ3 = Q3 && (KIND == 1 || KIND == 3 || KIND == 6); // k_render's INC3 kinds
     double2 poly[8];
     uint32_t sob_d[KIND == 0 ? 64 : 4]; // sobol: prefix XORs of the columns
     // halton kinds: 3^7 words (+1 pad), then phi3_q's quotient tables, laid
@@ -448,9 +485,16 @@ __device__ __forceinline__ void render_classified(const WarpClass& wc,
     if constexpr (RenderSmem<KIND, Q3>::kQ3) {
         // the phi_3 index of every sample below 3^14: the incremental
         // quotient-table path (phi3_q), warp-uniform
-        const uint64_t nmax = (KIND == 6 ? static_cast<uint64_t>(s.ipy0) : 0ull) +
-                              static_cast<uint64_t>(p.spp - 1) * (KIND == 6 ? p.scale_x : 1u);
-        if (__all_sync(__activemask(), nmax < 4782969ull)) {
+        bool inc;
+        if (KIND == 3) { // halton_hilbert: no 3^20 reduction or u32 wrap inside the pixel
+            const uint64_t g0 = static_cast<uint32_t>(s.block), g1 = g0 + (p.spp - 1);
+            inc = p.spp <= 2187u && (g0 < 3486784401ull ? g1 < 3486784401ull : g1 <= 0xffffffffull);
+        } else {
+            const uint64_t nmax = (KIND == 6 ? static_cast<uint64_t>(s.ipy0) : 0ull) +
+                                  static_cast<uint64_t>(p.spp - 1) * (KIND == 6 ? p.scale_x : 1u);
+            inc = nmax < 4782969ull;
+        }
+        if (__all_sync(__activemask(), inc)) {
             if (UQ && wc.uniform) {
 #define QMC_UQ3_CASE(U)                                                                            \
     r = wc.test ? render_pixel<KIND, ACCUM, true, true, U, true>(s, p, fx, fy, sm.poly, sm.sob_d,  \
@@ -853,7 +897,7 @@ cudaError_t render_kind(const RenderParams& p, uint32_t accum, float* out, cudaS
         return cudaGetLastError();
     }
     constexpr bool kUq = (kRenderUqKinds >> KIND) & 1u;
-    constexpr bool kHasQ3 = KIND == 1 || KIND == 6;
+    constexpr bool kHasQ3 = KIND == 1 || KIND == 3 || KIND == 6;
     if (kHasQ3 && p.spp >= 32) { // the phi3_q path, with the specialised sine loop
         if (accum == 0)
             k_render<KIND, 0, true, kHasQ3><<<grid, kBlock, 0, s>>>(p, out);
