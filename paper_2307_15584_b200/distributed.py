@@ -84,6 +84,12 @@ def gather_bands(band: torch.Tensor, height: int, width: int, group=None) -> tor
     world = dist.get_world_size(group)
     bands = row_bands(height, world)
     rows = max(r1 - r0 for r0, r1 in bands)
+    if all(r1 - r0 == rows for r0, r1 in bands):
+        # equal bands (height divisible by the world size, e.g. 2160 rows on
+        # 1/2/4/8 GPUs): the collective writes the image itself, no pad or cat
+        full = torch.empty((height, width), dtype=band.dtype, device=band.device)
+        dist.all_gather_into_tensor(full, band.contiguous(), group=group)
+        return full
     pad = torch.zeros((rows, width), dtype=band.dtype, device=band.device)
     pad[: band.shape[0]] = band
     full = torch.empty((world * rows, width), dtype=band.dtype, device=band.device)
