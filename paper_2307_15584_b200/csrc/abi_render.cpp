@@ -92,6 +92,7 @@ void resolve_render(const qmc_render_job* job, uint32_t row_begin, uint32_t row_
         p.stride = he.stride;
         p.crt_x = he.crt_x;
         p.crt_y = he.crt_y;
+        p.stride_magic = p.stride >= 2 && p.stride < (1ull << 32) ? ~0ull / p.stride : 0;
         p.dlo3 = he.sx % 2187u;
         p.dhi3 = he.sx / 2187u;
     }

@@ -68,6 +68,7 @@ struct RenderParams {
     // image-plane Halton (imageplane.cpp:80-106)
     uint32_t scale_x, scale_y, exp_x, exp_y;
     uint64_t stride, crt_x, crt_y;
+    uint64_t stride_magic;    // floor((2^64 - 1) / stride) when stride < 2^32, else 0
     const uint32_t* cols2;    // device, [2][52] MSB-aligned columns (sobol)
     const uint32_t* xor_reorder;  // device, 128*128 (sobol_xor_table)
     const uint32_t* xor_scramble; // device, 128*128*2

@@ -41,11 +41,34 @@ __device__ __forceinline__ uint64_t digit_reverse(uint64_t v, uint32_t base, uin
     return r;
 }
 
-// imageplane.cpp:100-106: CRT combination of the reversed digits
+// a mod m for a < 2^64 and m < 2^32 with mg = floor((2^64 - 1) / m): the
+// multiply-high quotient is at most two low
+__device__ __forceinline__ uint64_t mod_by_magic(uint64_t a, uint64_t m, uint64_t mg)
+{
+    uint64_t r = a - __umul64hi(a, mg) * m;
+    r = r >= m ? r - m : r;
+    return r >= m ? r - m : r;
+}
+
+// imageplane.cpp:100-106: CRT combination of the reversed digits. mg: the
+// magic of a stride below 2^32 (every image up to 2^16 x 3^10 pixels, 4K
+// included), else 0 and the plain 64-bit remainders
 __device__ __forceinline__ uint64_t halton_offset(uint32_t px, uint32_t py, uint32_t exp_x,
                                                   uint32_t exp_y, uint64_t stride, uint64_t crt_x,
-                                                  uint64_t crt_y)
+                                                  uint64_t crt_y, uint64_t mg)
 {
+    if (mg != 0) {
+        const uint64_t r2 = exp_x == 0 ? 0 : __brevll(px) >> (64 - exp_x);
+        uint32_t r3 = 0, v = py;
+        for (uint32_t k = 0; k < exp_y; ++k) { // digit_reverse(py, 3, exp_y) in 32 bits
+            const uint32_t q = __umulhi(v, 0xaaaaaaabu) >> 1;
+            r3 = r3 * 3u + (v - 3u * q);
+            v = q;
+        }
+        const uint64_t s = mod_by_magic(r2 * crt_x, stride, mg) +
+                           mod_by_magic(static_cast<uint64_t>(r3) * crt_y, stride, mg);
+        return s >= stride ? s - stride : s;
+    }
     // digit_reverse(px, 2, exp_x) = the exp_x low bits of px mirrored
     const uint64_t r2 = exp_x == 0 ? 0 : __brevll(px) >> (64 - exp_x);
     const uint64_t r3 = digit_reverse(py, 3, exp_y);
@@ -66,7 +89,7 @@ __device__ __forceinline__ PixelState pixel_state(uint32_t px, uint32_t py, cons
         s.block = hilbert_index(px, py, p.order) * p.spp;
     if (KIND == 6) {
         const uint64_t off =
-            halton_offset(px, py, p.exp_x, p.exp_y, p.stride, p.crt_x, p.crt_y);
+            halton_offset(px, py, p.exp_x, p.exp_y, p.stride, p.crt_x, p.crt_y, p.stride_magic);
         s.ipx0 = static_cast<uint32_t>(off >> p.exp_x);
         s.ipy0 = static_cast<uint32_t>(off / p.scale_y);
     }
@@ -769,7 +792,7 @@ __global__ void __launch_bounds__(256)
     if (KIND == 3)
         block = hilbert_index(p.px, p.py, p.order) * p.spp;
     if (KIND == 6) {
-        off = halton_offset(p.px, p.py, p.exp_x, p.exp_y, p.stride, p.crt_x, p.crt_y);
+        off = halton_offset(p.px, p.py, p.exp_x, p.exp_y, p.stride, p.crt_x, p.crt_y, 0);
         ipx0 = static_cast<uint32_t>(off >> p.exp_x);
         ipy0 = static_cast<uint32_t>(off / p.scale_y);
     }

@@ -59,6 +59,9 @@ elif a.config == "integrate":
 elif a.config == "c5iph":
     out = torch.empty((2160, 3840), dtype=torch.float32, device="cuda")
     fn = lambda: q.render(3840, 2160, 64, kind="image-plane-halton", out=out)  # noqa: E731
+elif a.config == "c5hh":
+    out = torch.empty((2160, 3840), dtype=torch.float32, device="cuda")
+    fn = lambda: q.render(3840, 2160, 64, kind="halton-hilbert", out=out)  # noqa: E731
 elif a.config.startswith("c5"):
     spp = int(a.config[2:] or 64)
     out = torch.empty((2160, 3840), dtype=torch.float32, device="cuda")
