@@ -8,6 +8,8 @@ import torch  # noqa: E402
 
 import paper_2307_15584_b200 as q  # noqa: E402
 
+if len(sys.argv) > 1:  # an alternative libqmcgpu.so (A/B)
+    q.LIB_PATH = os.path.abspath(sys.argv[1])
 n, d = 1 << 26, 8
 for kind in ["sobol", "halton", "lattice", "pixel-shifted-lattice"]:
     kw = {"generator": q.lfsr_generator_vector(0xACE1, d)} if "lattice" in kind else {}
@@ -15,7 +17,7 @@ for kind in ["sobol", "halton", "lattice", "pixel-shifted-lattice"]:
         kw.update(pixel=(5, 9), order=12)
     for f in ["product-sine", "product-poly"]:
         fn = lambda: q.integrate(kind, f, n, d, "kahan", **kw)  # noqa: E731
-        fn()
+        est = fn()
         fn()
         ts = []
         for _ in range(7):
@@ -24,4 +26,5 @@ for kind in ["sobol", "halton", "lattice", "pixel-shifted-lattice"]:
             fn()
             ts.append(time.perf_counter() - t0)
         ts.sort()
-        print("%-22s %-13s %.1f Gsamples/s" % (kind, f, n * d / ts[3] / 1e9))
+        print("%-22s %-13s %.1f Gsamples/s  estimate %r" % (kind, f, n * d / ts[3] / 1e9,
+                                                            getattr(est, "estimate", est)))
