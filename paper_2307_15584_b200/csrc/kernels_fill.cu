@@ -1705,6 +1705,16 @@ __device__ __forceinline__ uint2 lds64(uint32_t a)
     return v;
 }
 
+// Non-volatile shared load for tables that do not change while they are
+// read (the walk's X and record loads between rebuilds): the scheduler may
+// hoist the next step's loads above this step's math and store.
+__device__ __forceinline__ uint2 lds64_ro(uint32_t a)
+{
+    uint2 v;
+    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+
 __device__ __forceinline__ void sts64(uint32_t a, uint32_t x, uint32_t y)
 {
     asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y));
@@ -1966,26 +1976,50 @@ __global__ void __launch_bounds__(GROUPS * (32 / DPW + 1) * 32, 1)
                 since = 0;
                 live = true;
             }
+            // software-pipelined: step st + 1's table loads are issued before
+            // step st's math and store (ptxas does not move shared loads above
+            // the sub-tile stores, which it cannot tell apart from the tables)
+            uint2 e[DPW], rc[DPW];
+#pragma unroll
+            for (int d = 0; d < DPW; ++d)
+                e[d] = lds64_ro(a0[d]);
+#pragma unroll
+            for (int d = 0; d < DPW; ++d)
+                rc[d] = lds64_ro(a1[d] + e[d].y);
 #pragma unroll
             for (uint32_t st = 0; st < kLvRows / 32; ++st) {
+                uint2 en[DPW], rn[DPW];
+                if (st + 1 < kLvRows / 32) {
+#pragma unroll
+                    for (int d = 0; d < DPW; ++d)
+                        en[d] = lds64_ro(a0[d] + 256 * (st + 1));
+#pragma unroll
+                    for (int d = 0; d < DPW; ++d)
+                        rn[d] = lds64_ro(a1[d] + en[d].y);
+                }
                 uint32_t v[DPW];
 #pragma unroll
                 for (int d = 0; d < DPW; ++d) {
-                    const uint2 e = lds64(a0[d] + 256 * st);
-                    const uint2 rc = lds64(a1[d] + e.y);
                     // q + qU + (r0 >= thr): the carry of r0 + (2^32 - thr)
                     uint32_t x, dummy;
                     asm("{\n\t"
                         "add.cc.u32 %1, %2, %3;\n\t"
                         "addc.u32 %0, %4, %5;\n\t}"
                         : "=r"(x), "=r"(dummy)
-                        : "r"(e.x * ng[d]), "r"(rc.y), "r"(e.x), "r"(rc.x));
+                        : "r"(e[d].x * ng[d]), "r"(rc[d].y), "r"(e[d].x), "r"(rc[d].x));
                     v[d] = U32OUT ? x : map_bits(x);
                 }
 #pragma unroll
                 for (int cc = 0; cc < DPW / 4; ++cc)
                     sts128((buf ^ (cc << 4)) + st * 4096, v[4 * cc], v[4 * cc + 1], v[4 * cc + 2],
                            v[4 * cc + 3]);
+                if (st + 1 < kLvRows / 32) {
+#pragma unroll
+                    for (int d = 0; d < DPW; ++d) {
+                        e[d] = en[d];
+                        rc[d] = rn[d];
+                    }
+                }
             }
             // next sub-tile: lane 0's position advances by kLvRows; fold the
             // G0-blocks it passed (k8 / 8 of them) into the record address
