@@ -81,7 +81,11 @@ __device__ __forceinline__ bool factor(float xs, double& v, const SceneConsts& s
 // order, so the chunk partial is bit-identical to chunk_sum_kahan
 // (quality.cpp:180-194); (int) the llround(v*2^32) terms are exactly
 // associative, so the CTA reduces them in any order (quality.cpp:196-210).
-template <uint32_t KIND, uint32_t FN, uint32_t ACCUM>
+// SMALL (Sobol', dims <= kSmallDims): the per-thread Sobol' state is indexed
+// with compile-time dimension numbers (unrolled, guarded loops), so it stays
+// in registers instead of local memory.
+constexpr uint32_t kSmallDims = 8;
+template <uint32_t KIND, uint32_t FN, uint32_t ACCUM, bool SMALL = false>
 __global__ void __launch_bounds__(ChunkShape<KIND>::kBlock)
     k_integrate(IntegrateParams p, double* __restrict__ partial,
                 unsigned long long* __restrict__ isum, unsigned long long* __restrict__ bad)
@@ -120,7 +124,7 @@ __global__ void __launch_bounds__(ChunkShape<KIND>::kBlock)
 
     // Sobol' state: x(begin + t + B m) = XB ^ X(t) ^ X(B m); m advances
     // with x ^= E[ctz(m+1)].
-    uint32_t sob[kStateDims];
+    uint32_t sob[SMALL ? kSmallDims : kStateDims];
     if (KIND == 0) {
         for (uint32_t j = t; j < sdims; j += kBlock) {
             uint32_t x = p.words ? p.words[j] : 0u;
@@ -136,12 +140,24 @@ __global__ void __launch_bounds__(ChunkShape<KIND>::kBlock)
             }
         }
         __syncthreads();
-        for (uint32_t j = 0; j < sdims; ++j) {
-            uint32_t x = XB[j];
-            for (uint32_t k = 0; k < kLogBlock; ++k)
-                if ((t >> k) & 1u)
-                    x ^= __ldg(p.colsT + k * p.mdims + j);
-            sob[j] = x;
+        if (SMALL) {
+#pragma unroll
+            for (uint32_t j = 0; j < kSmallDims; ++j)
+                if (j < sdims) {
+                    uint32_t x = XB[j];
+                    for (uint32_t k = 0; k < kLogBlock; ++k)
+                        if ((t >> k) & 1u)
+                            x ^= __ldg(p.colsT + k * p.mdims + j);
+                    sob[j] = x;
+                }
+        } else {
+            for (uint32_t j = 0; j < sdims; ++j) {
+                uint32_t x = XB[j];
+                for (uint32_t k = 0; k < kLogBlock; ++k)
+                    if ((t >> k) & 1u)
+                        x ^= __ldg(p.colsT + k * p.mdims + j);
+                sob[j] = x;
+            }
         }
     }
 
@@ -189,6 +205,12 @@ __global__ void __launch_bounds__(ChunkShape<KIND>::kBlock)
             const uint32_t i = static_cast<uint32_t>(idx);
             double v = 1.0;
             bool alive = true;
+            if (KIND == 0 && SMALL) {
+#pragma unroll
+                for (uint32_t j = 0; j < kSmallDims; ++j)
+                    if (j < dims && alive)
+                        alive = factor<FN>(map_u32(sob[j]), v, p.sc);
+            } else
             for (uint32_t j = 0; j < dims && alive; ++j) {
                 uint32_t x;
                 if (KIND == 0)
@@ -235,8 +257,15 @@ __global__ void __launch_bounds__(ChunkShape<KIND>::kBlock)
         }
         if (KIND == 0 && m + 1 < kSteps) {
             const uint32_t c = __ffs(static_cast<int>(m + 1)) - 1;
-            for (uint32_t j = 0; j < sdims; ++j)
-                sob[j] ^= E[c][j];
+            if (SMALL) {
+#pragma unroll
+                for (uint32_t j = 0; j < kSmallDims; ++j)
+                    if (j < sdims)
+                        sob[j] ^= E[c][j];
+            } else {
+                for (uint32_t j = 0; j < sdims; ++j)
+                    sob[j] ^= E[c][j];
+            }
         }
     }
     (void)finite;
@@ -273,6 +302,8 @@ cudaError_t integrate_kind_fn(const IntegrateParams& p, uint32_t accum, double* 
         return cudaErrorInvalidValue;
     const unsigned grid = static_cast<unsigned>(p.nchunks);
     auto kern = accum == 0 ? k_integrate<KIND, FN, 0> : k_integrate<KIND, FN, 1>;
+    if (KIND == 0 && p.fdims <= kSmallDims)
+        kern = accum == 0 ? k_integrate<KIND, FN, 0, KIND == 0> : k_integrate<KIND, FN, 1, KIND == 0>;
     kern<<<grid, ChunkShape<KIND>::kBlock, 0, s>>>(p, partial, isum, bad);
     return cudaGetLastError();
 }
