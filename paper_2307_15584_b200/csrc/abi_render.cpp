@@ -1,6 +1,7 @@
 // abi_render.cpp — the fused per-pixel render of the C ABI (render.cpp:58-143
 // on the device): qmc_render, the sample-partitioned qmc_render_partial /
 // qmc_render_finalize, and qmc_scene_value.
+#include <cstdlib>
 #include "objects.hpp"
 
 #include <string>
@@ -15,6 +16,9 @@ extern "C" {
 // ------------------------------------------------------------------ render
 
 namespace {
+
+// row bands of a host-image render (D2H of band b overlaps the render of b+1)
+constexpr uint32_t kRenderHostBands = 8;
 
 // render() validation and defaults (render.cpp:83-106) resolved into the
 // kernel parameters; owns the XOR tables view for the call.
@@ -137,8 +141,42 @@ qmc_status qmc_render(const qmc_render_job* job, uint32_t row_begin, uint32_t ro
         }
         float* d = nullptr;
         cuda_ok(cudaMallocAsync(&d, rr.npix * 4, s), "cudaMallocAsync");
-        cuda_ok(launch_render(rr.p, job->kind, job->accum, d, s), "launch_render");
-        cuda_ok(cudaMemcpyAsync(out, d, rr.npix * 4, cudaMemcpyDeviceToHost, s), "D2H");
+        // Host image: render in row bands and copy each band to the host on
+        // a second stream while the next band renders, so the D2H (PCIe)
+        // overlaps the render instead of following it. Small images: one band.
+        const uint32_t rows = row_end - row_begin;
+        const char* env = std::getenv("QMC_RENDER_BANDS");
+        const uint32_t want = env ? static_cast<uint32_t>(std::atoi(env)) : kRenderHostBands;
+        const uint32_t nb = rr.npix >= (1ull << 20) ? std::max(1u, std::min(want, rows)) : 1u;
+        if (nb == 1) {
+            cuda_ok(launch_render(rr.p, job->kind, job->accum, d, s), "launch_render");
+            cuda_ok(cudaMemcpyAsync(out, d, rr.npix * 4, cudaMemcpyDeviceToHost, s), "D2H");
+        } else {
+            cudaStream_t c = nullptr;
+            cuda_ok(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking), "cudaStreamCreate");
+            std::vector<cudaEvent_t> ev(nb + 1, nullptr);
+            for (auto& e : ev)
+                cuda_ok(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+            for (uint32_t b = 0; b < nb; ++b) {
+                const uint32_t rb = row_begin + static_cast<uint32_t>(uint64_t(rows) * b / nb);
+                const uint32_t re = row_begin + static_cast<uint32_t>(uint64_t(rows) * (b + 1) / nb);
+                RenderParams pb = rr.p;
+                pb.row_begin = rb;
+                pb.row_end = re;
+                const uint64_t off = static_cast<uint64_t>(rb - row_begin) * job->width;
+                const uint64_t cnt = static_cast<uint64_t>(re - rb) * job->width;
+                cuda_ok(launch_render(pb, job->kind, job->accum, d + off, s), "launch_render");
+                cuda_ok(cudaEventRecord(ev[b], s), "cudaEventRecord");
+                cuda_ok(cudaStreamWaitEvent(c, ev[b], 0), "cudaStreamWaitEvent");
+                cuda_ok(cudaMemcpyAsync(out + off, d + off, cnt * 4, cudaMemcpyDeviceToHost, c),
+                        "D2H");
+            }
+            cuda_ok(cudaEventRecord(ev[nb], c), "cudaEventRecord");
+            cuda_ok(cudaStreamWaitEvent(s, ev[nb], 0), "cudaStreamWaitEvent"); // before the free
+            for (auto& e : ev)
+                cudaEventDestroy(e);
+            cudaStreamDestroy(c);
+        }
         cudaFreeAsync(d, s);
         cuda_ok(cudaStreamSynchronize(s), "sync");
     });

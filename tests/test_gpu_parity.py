@@ -1506,6 +1506,20 @@ def test_halton_fill_q4_long_runs_vs_reference(ref, mode, first):
         np.testing.assert_array_equal(got[:, j], exp, err_msg=f"dim={j}")
 
 
+@pytest.mark.parametrize("kind", ["pixel-shifted-lattice", "image-plane-halton"])
+def test_render_host_image_bands_equal_device(kind):
+    """qmc_render into host memory renders in row bands whose D2H copies
+    overlap the next band's render (>= 2^20 pixels): the host image equals
+    the device render bit for bit, for the whole image and for a row range
+    that does not split evenly into the bands."""
+    import numpy as np
+    for rows in [(0, 2160), (7, 2001)]:
+        dev = q.render(3840, 2160, 16, kind=kind, rows=rows).cpu().numpy()
+        host = np.empty_like(dev)
+        q.render(3840, 2160, 16, kind=kind, rows=rows, out=host)
+        np.testing.assert_array_equal(host.view(np.uint32), dev.view(np.uint32))
+
+
 @pytest.mark.parametrize("mode", ["linear", "faure"])
 @pytest.mark.parametrize("first", [3486784401 - (1 << 22) + 5, 2**32 - (1 << 22) - 77])
 def test_halton_fill_level_tables_long_vs_reference(ref, mode, first):
