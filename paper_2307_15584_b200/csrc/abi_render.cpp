@@ -152,11 +152,25 @@ qmc_status qmc_render(const qmc_render_job* job, uint32_t row_begin, uint32_t ro
             cuda_ok(launch_render(rr.p, job->kind, job->accum, d, s), "launch_render");
             cuda_ok(cudaMemcpyAsync(out, d, rr.npix * 4, cudaMemcpyDeviceToHost, s), "D2H");
         } else {
-            cudaStream_t c = nullptr;
-            cuda_ok(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking), "cudaStreamCreate");
-            std::vector<cudaEvent_t> ev(nb + 1, nullptr);
-            for (auto& e : ev)
+            // the copy stream and events die with the call, also on an error
+            struct Side {
+                cudaStream_t c = nullptr;
+                std::vector<cudaEvent_t> ev;
+                ~Side()
+                {
+                    for (cudaEvent_t e : ev)
+                        if (e)
+                            cudaEventDestroy(e);
+                    if (c)
+                        cudaStreamDestroy(c);
+                }
+            } side;
+            side.ev.assign(nb + 1, nullptr);
+            cuda_ok(cudaStreamCreateWithFlags(&side.c, cudaStreamNonBlocking), "cudaStreamCreate");
+            for (auto& e : side.ev)
                 cuda_ok(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+            const cudaStream_t c = side.c;
+            std::vector<cudaEvent_t>& ev = side.ev;
             for (uint32_t b = 0; b < nb; ++b) {
                 const uint32_t rb = row_begin + static_cast<uint32_t>(uint64_t(rows) * b / nb);
                 const uint32_t re = row_begin + static_cast<uint32_t>(uint64_t(rows) * (b + 1) / nb);
@@ -173,9 +187,6 @@ qmc_status qmc_render(const qmc_render_job* job, uint32_t row_begin, uint32_t ro
             }
             cuda_ok(cudaEventRecord(ev[nb], c), "cudaEventRecord");
             cuda_ok(cudaStreamWaitEvent(s, ev[nb], 0), "cudaStreamWaitEvent"); // before the free
-            for (auto& e : ev)
-                cudaEventDestroy(e);
-            cudaStreamDestroy(c);
         }
         cudaFreeAsync(d, s);
         cuda_ok(cudaStreamSynchronize(s), "sync");
