@@ -145,7 +145,7 @@ qmc_status qmc_render(const qmc_render_job* job, uint32_t row_begin, uint32_t ro
         // a second stream while the next band renders, so the D2H (PCIe)
         // overlaps the render instead of following it. Small images: one band.
         const uint32_t rows = row_end - row_begin;
-        const char* env = std::getenv("QMC_RENDER_BANDS");
+        const char* env = std::getenv("QMC_RENDER_BANDS"); // A/B: tools/exp_render_e2e.py
         const uint32_t want = env ? static_cast<uint32_t>(std::atoi(env)) : kRenderHostBands;
         const uint32_t nb = rr.npix >= (1ull << 20) ? std::max(1u, std::min(want, rows)) : 1u;
         if (nb == 1) {
