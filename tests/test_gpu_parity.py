@@ -1225,6 +1225,23 @@ def test_fills_misaligned_outputs(shift):
         assert bool((head == 0x5A5A5A5A).all()) and bool((tail == 0x5A5A5A5A).all()), dims
 
 
+def test_render_tables_and_host_bands_write_exactly_their_range():
+    """spp >= 32 renders of the Halton kinds (phi_3 tables bulk-copied per
+    CTA, halton-hilbert's record split) and a host image above 2^20 pixels
+    (row bands, D2H overlapped) write only their rows: canaries intact."""
+    for kind in ("image-plane-halton", "halton", "halton-hilbert"):
+        buf, mid = _guarded(50 * 96)
+        q.render(96, 80, 64, kind=kind, rows=(13, 63), out=mid.view(torch.float32))
+        torch.cuda.synchronize()
+        assert _canaries_intact(buf), kind
+    rows, w = (3, 1103), 1000
+    host = np.full((rows[1] - rows[0]) * w + 2 * GUARD, 0x5A5A5A5A, np.uint32)
+    q.render(w, 1110, 4, rows=rows, out=host[GUARD:-GUARD].view(np.float32).reshape(-1, w))
+    assert (host[:GUARD] == 0x5A5A5A5A).all() and (host[-GUARD:] == 0x5A5A5A5A).all()
+    dev = q.render(w, 1110, 4, rows=rows).cpu().numpy()
+    np.testing.assert_array_equal(host[GUARD:-GUARD], dev.view(np.uint32).ravel())
+
+
 def test_render_and_streams_write_exactly_their_range():
     for kind in q.SAMPLER_KINDS:
         buf, mid = _guarded(23 * 37)

@@ -44,6 +44,13 @@ for kind in q.SAMPLER_KINDS:
         q.integrate(kind, "product-sine", 5000, 3, stream_dims=3, **kw) if kind != "halton-hilbert" else None
     acc = q.render_partial(37, 23, 5, 1, 2, kind=kind)
     q.render_finalize(acc, 5)
+# spp >= 32: the phi_3 tables bulk-copied per CTA (image-plane Halton,
+# halton, halton-hilbert incremental path); a host image above 2^20 pixels
+# (banded render with overlapped D2H)
+for kind in ("image-plane-halton", "halton", "halton-hilbert", "pixel-shifted-lattice"):
+    q.render(96, 80, 64, kind=kind)
+host = np.empty((1100, 1000), np.float32)
+q.render(1000, 1100, 8, out=host)
 pts = q.sobol_fill(300, 5).contiguous()
 q.l2_star_discrepancy(pts)
 q.min_toroidal_distance(pts)
