@@ -1225,6 +1225,22 @@ def test_fills_misaligned_outputs(shift):
         assert bool((head == 0x5A5A5A5A).all()) and bool((tail == 0x5A5A5A5A).all()), dims
 
 
+def test_halton_level_table_fill_writes_exactly_its_range():
+    """k_halton_lv with every CTA's three walker groups busy over several
+    ring rounds and a partial last sub-tile: canaries intact, and the u32 and
+    f32 outputs agree through the map."""
+    n, dims = 148 * 128 * 3 * 5 + 77, 32
+    for first in (0, 3486784401 - 50000, (1 << 32) - 60000):
+        buf, mid = _guarded(n * dims)
+        q.halton_fill(n, dims, first=first, scramble="linear", fixed=True, out=mid)
+        torch.cuda.synchronize()
+        assert _canaries_intact(buf), first
+        f = q.halton_fill(n, dims, first=first, scramble="linear")
+        np.testing.assert_array_equal(
+            f.cpu().numpy().view(np.uint32).ravel(),
+            q.map_u32_to_unifloat(mid.view(torch.int32)).cpu().numpy().view(np.uint32).ravel())
+
+
 def test_render_tables_and_host_bands_write_exactly_their_range():
     """spp >= 32 renders of the Halton kinds (phi_3 tables bulk-copied per
     CTA, halton-hilbert's record split) and a host image above 2^20 pixels
