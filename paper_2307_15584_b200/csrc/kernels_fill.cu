@@ -1650,22 +1650,22 @@ __global__ void __launch_bounds__(1024, 1)
 // lane 0's G0-block runs past G0 within a sub-tile; the second word is the
 // byte offset of its record), and per walker group a record table R[l1] =
 // {floor(W1 / G0), 2^32 - (G0 - W1 mod G0)} for the G1 values of l1 of the
-// current H plus the first kLvNext of the next H, rebuilt (lv_compose from
-// q0 and one radical_inverse_fixed per G0 * G1 indices) when lane 0 enters
-// the next H. A sample is two conflict-free shared loads (X at consecutive
+// current H plus the first kLvNext of the next H, rebuilt from q0 alone
+// (lv_compose; the next block's inverse composes over a cached high part)
+// when lane 0 enters the next H. A sample is two conflict-free shared loads (X at consecutive
 // lanes, the record a broadcast), one address add, the carry add and the
 // map: no table stream from L2 (the k_tma walk's bound).
 //
-// Layout: 8 walker warps per group; warp k of a group owns the 4
-// consecutive dimensions 4k..4k+3 of the CTA's 32-dimension column block
+// Layout: 32 / DPW walker warps per group (DPW = 4); warp k of a group owns
+// the DPW consecutive dimensions DPW*k.. of the CTA's 32-dimension column block
 // and lane l the point l of each 32-point step, so a step is one STS.128
 // per lane into a sub-tile laid out as the output rows with the 128-B
 // swizzle (conflict-free: 8 lanes cover the 8 swizzled chunks). GROUPS
 // groups walk their own contiguous sub-tile ranges into their own rings;
 // one extra warp per group issues its cp.async.bulk.tensor stores and
 // releases each buffer as soon as its store has read it (a blocking
-// wait_group.read stalls the whole warp, so the groups do not share one). One CTA per SM; a
-// CTA stays in one column block (its tables).
+// wait_group.read stalls the whole warp, so the groups do not share one).
+// One CTA per SM; a CTA stays in one column block (its tables).
 __host__ __device__ inline void lv_groups(uint32_t b, uint32_t& G0, uint32_t& G1)
 {
     G0 = b;
