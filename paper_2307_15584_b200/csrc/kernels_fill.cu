@@ -1552,7 +1552,8 @@ __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity)
 template <class W>
 __global__ void __launch_bounds__(1024, 1)
     k_tma(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ W w, uint32_t rows,
-          uint32_t nbuf, uint32_t ncb, uint32_t dims, uint64_t first, uint64_t n, uint64_t nsub)
+          uint32_t nbuf, uint32_t ncb, uint32_t dims, uint64_t first, uint64_t n, uint64_t nsub,
+          uint32_t cb0)
 {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t bars[16];
@@ -1580,8 +1581,11 @@ __global__ void __launch_bounds__(1024, 1)
     typename W::State st;
     w.reset(st);
     uint32_t b = 0, k = 0;
+    // column blocks cb0 .. cb0 + ncb - 1 (the ones before cb0 went to the
+    // level-table fill)
     uint32_t cb = static_cast<uint32_t>(u0 / nsub);
     uint64_t s = u0 - static_cast<uint64_t>(cb) * nsub;
+    cb += cb0;
     for (uint64_t u = u0; u < u1; ++u, ++s) {
         if (s == nsub) { // next column block: other dimensions, fresh walk
             s = 0;
@@ -2371,7 +2375,7 @@ cudaError_t launch_map_selfcheck(unsigned long long* count, cudaStream_t s)
 // TMA: dims % 32 == 0, out 16-B aligned, n < 2^31; returns false otherwise.
 template <class W>
 bool launch_tma_fill(const W& w, uint32_t dims, const FillRange& r, cudaStream_t s,
-                     cudaError_t* err, bool partial_blocks = false)
+                     cudaError_t* err, bool partial_blocks = false, uint32_t cb0 = 0)
 {
     // partial_blocks: wide rows of whole 16-B units (dims > 256, dims % 4 ==
     // 0) also go here, the last 32-dim column block partial (the tensor
@@ -2407,10 +2411,10 @@ bool launch_tma_fill(const W& w, uint32_t dims, const FillRange& r, cudaStream_t
     if (*err != cudaSuccess)
         return true;
     const uint64_t nsub = (r.n + kRows - 1) / kRows;
-    const uint32_t ncb = (dims + 31) / 32;
+    const uint32_t ncb = (dims + 31) / 32 - cb0;
     const unsigned grid = static_cast<unsigned>(
         std::min<uint64_t>(nsub * ncb, static_cast<uint64_t>(sm_count())));
-    k_tma<W><<<grid, 1024, smem, s>>>(tmap, w, kRows, kBufs, ncb, dims, r.first, r.n, nsub);
+    k_tma<W><<<grid, 1024, smem, s>>>(tmap, w, kRows, kBufs, ncb, dims, r.first, r.n, nsub, cb0);
     *err = cudaGetLastError();
     return true;
 }
@@ -2421,39 +2425,48 @@ bool launch_tma_fill(const W& w, uint32_t dims, const FillRange& r, cudaStream_t
 // walker groups' record areas and rings within the opt-in shared memory.
 template <bool U32OUT>
 bool launch_halton_lv(const RadicalDim* rd, const RadicalDim* rd_host, uint32_t dims,
-                      const FillRange& r, cudaStream_t s, cudaError_t* err)
+                      const FillRange& r, cudaStream_t s, cudaError_t* err, uint32_t* nblocks)
 {
     if (!rd_host || dims % 32 != 0 || (reinterpret_cast<uintptr_t>(r.out) & 15u) != 0 ||
         r.n >= (1ull << 31))
         return false;
-    uint32_t xw = 0, recw = 0;
-    for (uint32_t cb = 0; cb < dims / 32; ++cb) {
-        uint32_t a = 0, c = 0;
-        for (uint32_t j = 0; j < 32; ++j) {
-            uint32_t G0, G1;
-            lv_groups(rd_host[cb * 32 + j].base, G0, G1);
-            if (rd_host[cb * 32 + j].maxpow % (G0 * G1) != 0)
-                return false;
-            a += lv_xwords(G0);
-            c += lv_rwords(G1);
-        }
-        xw = std::max(xw, a);
-        recw = std::max(recw, c);
-    }
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     constexpr uint32_t kRows = kLvRows;
+    auto need_w = [&](int gr, uint32_t nb, uint32_t x, uint32_t rw) {
+        return 1024 + static_cast<size_t>(gr) * nb * kRows * 128 + static_cast<size_t>(x) * 4 +
+               static_cast<size_t>(gr) * rw * 4 + 2 * gr * kLvMaxBufs * 8 + 32 * sizeof(LvDim) +
+               gr * 32 * sizeof(LvSlot);
+    };
+    // the leading column blocks whose tables fit (the small primes: at 32
+    // dimensions the whole row; wider rows hand the rest to the k_tma walk)
+    uint32_t xw = 0, recw = 0, nfit = 0;
+    for (uint32_t cb = 0; cb < dims / 32; ++cb) {
+        uint32_t a = 0, c = 0;
+        bool ok = true;
+        for (uint32_t j = 0; j < 32; ++j) {
+            uint32_t G0, G1;
+            lv_groups(rd_host[cb * 32 + j].base, G0, G1);
+            ok = ok && rd_host[cb * 32 + j].maxpow % (G0 * G1) == 0;
+            a += lv_xwords(G0);
+            c += lv_rwords(G1);
+        }
+        const uint32_t nx = std::max(xw, a), nr = std::max(recw, c);
+        if (!ok || need_w(3, 2, nx, nr) > static_cast<size_t>(optin))
+            break;
+        xw = nx;
+        recw = nr;
+        ++nfit;
+    }
+    if (nfit == 0)
+        return false;
     // the most walker groups (latency hiding: the walk is issue / latency
     // bound), then the deepest ring, that fit: 3 groups x 2 buffers at 32
     // dimensions (measured: 2 groups x 3 buffers 1020, 3 x 2 1160 Gsamples/s)
     int kGroups = 0;
     uint32_t nbuf = 0;
-    auto need = [&](int gr, uint32_t nb) {
-        return 1024 + static_cast<size_t>(gr) * nb * kRows * 128 + static_cast<size_t>(xw) * 4 +
-               static_cast<size_t>(gr) * recw * 4 + 2 * gr * kLvMaxBufs * 8 + 32 * sizeof(LvDim) +
-               gr * 32 * sizeof(LvSlot);
-    };
+    auto need = [&](int gr, uint32_t nb) { return need_w(gr, nb, xw, recw); };
     for (int gr = 3; gr >= 2 && !kGroups; --gr)
         for (uint32_t nb = 3; nb >= 2 && !kGroups; --nb)
             if (need(gr, nb) <= static_cast<size_t>(optin)) {
@@ -2490,7 +2503,8 @@ bool launch_halton_lv(const RadicalDim* rd, const RadicalDim* rd_host, uint32_t 
     if (*err != cudaSuccess)
         return true;
     const uint64_t nsub = (r.n + kRows - 1) / kRows;
-    const uint32_t ncb = dims / 32;
+    const uint32_t ncb = nfit;
+    *nblocks = nfit;
     const uint32_t per = static_cast<uint32_t>(std::max<uint64_t>(
         1, std::min<uint64_t>(nsub, static_cast<uint64_t>(sm_count()) / ncb)));
     const size_t dyn = need(kGroups, nbuf) - (2 * kGroups * kLvMaxBufs * 8 + 32 * sizeof(LvDim) +
@@ -2824,10 +2838,18 @@ cudaError_t launch_halton(const void* rd, uint32_t dims, bool u32, const FillRan
     const RadicalDim* rdh = static_cast<const RadicalDim*>(rd_host);
     cudaError_t err = cudaSuccess;
     // QMC_HALTON_NO_LV=1: the k_tma walk instead (A/B, tools/exp_halton_lv.py)
+    uint32_t lv_blocks = 0;
     if (std::getenv("QMC_HALTON_NO_LV") == nullptr &&
-        (u32 ? launch_halton_lv<true>(rdv, rdh, dims, r, s, &err)
-             : launch_halton_lv<false>(rdv, rdh, dims, r, s, &err)))
-        return err;
+        (u32 ? launch_halton_lv<true>(rdv, rdh, dims, r, s, &err, &lv_blocks)
+             : launch_halton_lv<false>(rdv, rdh, dims, r, s, &err, &lv_blocks))) {
+        if (err != cudaSuccess || lv_blocks == dims / 32)
+            return err;
+        // the wider column blocks (larger primes) on the k_tma walk
+        if (u32 ? launch_tma_fill(HaltonWalk<true>{rdv}, dims, r, s, &err, false, lv_blocks)
+                : launch_tma_fill(HaltonWalk<false>{rdv}, dims, r, s, &err, false, lv_blocks))
+            return err;
+        return cudaErrorNotSupported;
+    }
     if (u32 ? launch_tma_fill(HaltonWalk<true>{rdv}, dims, r, s, &err, true)
             : launch_tma_fill(HaltonWalk<false>{rdv}, dims, r, s, &err, true))
         return err;
