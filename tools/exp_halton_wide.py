@@ -6,6 +6,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2307_15584_b200 as q
 
+if len(sys.argv) > 1:  # an alternative libqmcgpu.so (A/B)
+    q.LIB_PATH = os.path.abspath(sys.argv[1])
+
 
 def t(fn, samples, k=7):
     for _ in range(2):
